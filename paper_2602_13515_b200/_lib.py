@@ -1,0 +1,125 @@
+"""ctypes binding of ``libspa2.so`` (the C ABI declared in ``include/spa2.h``).
+
+The library is built in-tree by ``__graft_entry__.build()`` (``make -C csrc``) and loaded
+from this directory.  There is no fallback: if the library or a CUDA device is missing,
+every operator raises.  Status codes map to the exceptions the reference raises
+(``ValueError`` / ``FloatingPointError``, numerics.py:17-32) or ``RuntimeError`` for CUDA
+failures.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+import threading
+
+import torch
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libspa2.so")
+HEADER_PATH = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "spa2.h")
+
+SPA2_OK = 0
+SPA2_ERR_VALUE = -1
+SPA2_ERR_NONFINITE = -2
+SPA2_ERR_UNSUPPORTED = -3
+SPA2_ERR_CUDA = -4
+
+DTYPE_CODES = {torch.bfloat16: 0, torch.float16: 1, torch.float32: 2, torch.float64: 3}
+
+
+class View(ctypes.Structure):
+    """``spa2_view``: base pointer + element strides of the B, H, N axes."""
+
+    _fields_ = [("ptr", ctypes.c_void_p), ("sb", ctypes.c_int64), ("sh", ctypes.c_int64), ("sn", ctypes.c_int64)]
+
+
+_P = ctypes.c_void_p
+_I64 = ctypes.c_int64
+_I32 = ctypes.c_int
+_F32 = ctypes.c_float
+_F64 = ctypes.c_double
+
+SIGNATURES = {
+    "spa2_version": ([], ctypes.c_char_p),
+    "spa2_last_error": ([], ctypes.c_char_p),
+    "spa2_device_supported": ([_I32], _I32),
+    "spa2_pooled_map": ([View, View, _I32, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P, _P, _P], _I32),
+    "spa2_select": ([_P, _I64, _I64, _I64, _F64, _P, _P, _P], _I32),
+    "spa2_build_lists": ([_P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P], _I32),
+    "spa2_fwd": ([View, View, View, View, _P, _I32, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P, _P, _F32, _P, _P],
+                 _I32),
+    "spa2_bwd": ([View, View, View, View, View, _P, _P, View, View, View, _I32, _I64, _I64, _I64, _I64, _I64, _I64,
+                  _P, _P, _P, _P, _P, _P, _F32, _P], _I32),
+    "spa2_probe_gemm": ([_P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _P], _I32),
+}
+
+_lock = threading.Lock()
+_lib = None
+_checked_devices: set[int] = set()
+
+
+def header_symbols() -> list[str]:
+    """Every function the public header declares."""
+    with open(HEADER_PATH) as f:
+        text = f.read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w[\w\s\*]*?\b(spa2_\w+)\s*\(", text, flags=re.M)))
+
+
+def load() -> ctypes.CDLL:
+    """Load (once) and type the shared library.  Raises if it has not been built."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise RuntimeError(
+                    f"libspa2.so not found at {LIB_PATH}; build it with `python -c 'import __graft_entry__ as g; "
+                    "g.build()'` (there is no CPU fallback)")
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, (args, res) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.argtypes = args
+                fn.restype = res
+            _lib = lib
+    return _lib
+
+
+def last_error() -> str:
+    return load().spa2_last_error().decode(errors="replace")
+
+
+def check(rc: int, what: str) -> None:
+    if rc == SPA2_OK:
+        return
+    msg = f"{what}: {last_error()}"
+    if rc in (SPA2_ERR_VALUE, SPA2_ERR_UNSUPPORTED):
+        raise ValueError(msg)
+    if rc == SPA2_ERR_NONFINITE:
+        raise FloatingPointError(msg)
+    raise RuntimeError(msg)
+
+
+def require_device(device: torch.device) -> None:
+    """Fail loudly unless ``device`` is a CUDA sm_100 GPU (no CPU fallback exists)."""
+    if device.type != "cuda":
+        raise RuntimeError("paper_2602_13515_b200 runs on CUDA (B200, sm_100a) only; got device " + str(device))
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    if idx not in _checked_devices:
+        check(load().spa2_device_supported(idx), "device check")
+        _checked_devices.add(idx)
+
+
+def stream_of(t: torch.Tensor) -> int:
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def ptr(t: torch.Tensor | None):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def view4(t: torch.Tensor) -> View:
+    """``spa2_view`` of a [B, H, N, d] tensor whose last axis is contiguous."""
+    if t.dim() != 4 or (t.stride(3) != 1 and t.shape[3] > 1):
+        raise ValueError(f"expected a [B,H,N,d] tensor with contiguous last axis, got {tuple(t.shape)} "
+                         f"strides {t.stride()}")
+    return View(t.data_ptr(), t.stride(0), t.stride(1), t.stride(2))

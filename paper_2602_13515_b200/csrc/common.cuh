@@ -1,0 +1,52 @@
+// common.cuh — error plumbing and small helpers shared by every libspa2 translation unit.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "../../include/spa2.h"
+
+namespace spa2 {
+
+void set_error(const char* fmt, ...);
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace spa2
+
+#define SPA2_REQUIRE(cond, status, ...)      \
+  do {                                       \
+    if (!(cond)) {                           \
+      ::spa2::set_error(__VA_ARGS__);        \
+      return (status);                       \
+    }                                        \
+  } while (0)
+
+#define SPA2_CUDA_TRY(call)                                                              \
+  do {                                                                                   \
+    cudaError_t err_ = (call);                                                           \
+    if (err_ != cudaSuccess) {                                                           \
+      ::spa2::set_error("%s failed: %s (%s:%d)", #call, cudaGetErrorString(err_), __FILE__, \
+                        __LINE__);                                                       \
+      return SPA2_ERR_CUDA;                                                              \
+    }                                                                                    \
+  } while (0)
+
+#define SPA2_LAUNCH_CHECK() SPA2_CUDA_TRY(cudaPeekAtLastError())
+
+// ---- element loads as double / float ------------------------------------------------
+template <typename T>
+__device__ __forceinline__ double to_f64(T x);
+template <>
+__device__ __forceinline__ double to_f64<double>(double x) { return x; }
+template <>
+__device__ __forceinline__ double to_f64<float>(float x) { return (double)x; }
+template <>
+__device__ __forceinline__ double to_f64<__nv_bfloat16>(__nv_bfloat16 x) {
+  return (double)__bfloat162float(x);
+}
+template <>
+__device__ __forceinline__ double to_f64<__half>(__half x) { return (double)__half2float(x); }

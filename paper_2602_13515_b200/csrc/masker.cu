@@ -1,0 +1,514 @@
+// masker.cu — K1 pooled map, K2 select, K3 block lists (CUDA cores, HBM/L2-bound).
+//
+// Reference stages replaced (paths under /root/reference/pkg/src/sparseattn_lab):
+//   K1  numerics.block_mean_pool (numerics.py:55-65), masker.pooled_map (masker.py:100-110),
+//       numerics.softmax_rows (numerics.py:46-52)
+//   K2  masker._descending_order .. hybrid_mask (masker.py:113-146)
+//   K3  the row-major kept-block iteration of attention.py:97/151-157 and its KV-major
+//       transpose for the backward.
+//
+// Everything after the bf16 load is IEEE float64, so the pooled map agrees with the
+// reference to ~1e-16 relative and the block selection is bit-exact for a given map.
+#include <math.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace spa2 {
+namespace {
+
+constexpr int kPoolThreads = 256;
+
+// ---------------------------------------------------------------------------------------
+// K1a: block-mean pooling of Q (by b_q) and K (by b_kv) in float64.
+// One CTA per (b, h, block).  Thread (r, g) sums rows r, r+R, ... of column group g
+// (8 columns with 16-byte loads when VEC, else 1 column), then the R partial sums of a
+// column are added in a fixed order — deterministic, not order-matched to numpy's
+// reduceat (the difference is last-bit, far below the 1e-12 the reference promises).
+// ---------------------------------------------------------------------------------------
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(kPoolThreads) k_pool(spa2_view q, spa2_view k, int H, int N, int d,
+                                                       int b_q, int b_kv, int T_m, int T_n, int64_t BH,
+                                                       double* __restrict__ qbar,
+                                                       double* __restrict__ kbar,
+                                                       int32_t* __restrict__ nonfinite) {
+  extern __shared__ double red[];  // [R][d]
+  constexpr int CPT = VEC ? (16 / (int)sizeof(T) < 8 ? 16 / (int)sizeof(T) : 8) : 1;
+  const int64_t g = blockIdx.x;
+  const bool is_q = g < BH * T_m;
+  const int64_t gl = is_q ? g : g - BH * T_m;
+  const int nblk = is_q ? T_m : T_n;
+  const int64_t bh = gl / nblk;
+  const int blk = (int)(gl % nblk);
+  const int bsz = is_q ? b_q : b_kv;
+  const spa2_view vw = is_q ? q : k;
+  const int64_t bi = bh / H, hi = bh % H;
+  const int row0 = blk * bsz;
+  const int rows = min(bsz, N - row0);
+  const T* base = reinterpret_cast<const T*>(vw.ptr) + bi * vw.sb + hi * vw.sh + (int64_t)row0 * vw.sn;
+
+  const int cpr = d / CPT;            // threads per row
+  const int R = kPoolThreads / cpr;   // rows in flight
+  const int r = threadIdx.x / cpr;
+  const int cg = threadIdx.x % cpr;
+  double acc[CPT];
+#pragma unroll
+  for (int e = 0; e < CPT; ++e) acc[e] = 0.0;
+  bool bad = false;
+  if (r < R) {
+    for (int row = r; row < rows; row += R) {
+      const T* p = base + (int64_t)row * vw.sn + cg * CPT;
+      if constexpr (VEC) {
+        T vals[CPT];
+        *reinterpret_cast<uint4*>(vals) = *reinterpret_cast<const uint4*>(p);
+#pragma unroll
+        for (int e = 0; e < CPT; ++e) {
+          double x = to_f64<T>(vals[e]);
+          bad |= !isfinite(x);
+          acc[e] += x;
+        }
+      } else {
+        double x = to_f64<T>(p[0]);
+        bad |= !isfinite(x);
+        acc[0] += x;
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < CPT; ++e) red[r * d + cg * CPT + e] = acc[e];
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0 && nonfinite != nullptr) atomicOr(nonfinite, 1);
+  double* out = (is_q ? qbar : kbar) + (bh * nblk + blk) * (int64_t)d;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    double s = 0.0;
+    for (int rr = 0; rr < R; ++rr) s += red[rr * d + c];
+    out[c] = s / (double)rows;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// K1b: scores S = Q̄ K̄ᵀ / √d in float64 (written into `probs`), 32x64 tiles, k-chunks of 16.
+// ---------------------------------------------------------------------------------------
+constexpr int kSTI = 32, kSTJ = 64, kSTK = 16;
+
+__global__ void __launch_bounds__(256) k_scores(const double* __restrict__ qbar,
+                                                const double* __restrict__ kbar, int T_m, int T_n,
+                                                int d, double sqrt_d, double* __restrict__ s_out) {
+  __shared__ double sq[kSTK][kSTI + 1];
+  __shared__ double sk[kSTK][kSTJ + 1];
+  const int64_t bh = blockIdx.z;
+  const int i0 = blockIdx.y * kSTI, j0 = blockIdx.x * kSTJ;
+  const double* qb = qbar + bh * (int64_t)T_m * d;
+  const double* kb = kbar + bh * (int64_t)T_n * d;
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;  // 16 x 16 threads; 2 rows x 4 cols each
+  double acc[2][4] = {};
+  for (int c0 = 0; c0 < d; c0 += kSTK) {
+    for (int e = threadIdx.x; e < kSTI * kSTK; e += 256) {
+      int ii = e / kSTK, cc = e % kSTK;
+      int i = i0 + ii, c = c0 + cc;
+      sq[cc][ii] = (i < T_m && c < d) ? qb[(int64_t)i * d + c] : 0.0;
+    }
+    for (int e = threadIdx.x; e < kSTJ * kSTK; e += 256) {
+      int jj = e / kSTK, cc = e % kSTK;
+      int j = j0 + jj, c = c0 + cc;
+      sk[cc][jj] = (j < T_n && c < d) ? kb[(int64_t)j * d + c] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int cc = 0; cc < kSTK; ++cc) {
+      double a0 = sq[cc][ty * 2], a1 = sq[cc][ty * 2 + 1];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        double bv = sk[cc][tx * 4 + u];
+        acc[0][u] = fma(a0, bv, acc[0][u]);
+        acc[1][u] = fma(a1, bv, acc[1][u]);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+    int i = i0 + ty * 2 + a;
+    if (i >= T_m) continue;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      int j = j0 + tx * 4 + u;
+      if (j < T_n) s_out[(bh * T_m + i) * (int64_t)T_n + j] = acc[a][u] / sqrt_d;
+    }
+  }
+}
+
+// K1c: in-place row softmax with max subtraction (numerics.py:46-52). One warp per row.
+__global__ void k_softmax_rows(double* __restrict__ p, int64_t rows, int T_n) {
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (row >= rows) return;
+  double* x = p + row * (int64_t)T_n;
+  double m = -INFINITY;
+  for (int j = lane; j < T_n; j += 32) m = fmax(m, x[j]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  double s = 0.0;
+  for (int j = lane; j < T_n; j += 32) {
+    double e = exp(x[j] - m);
+    x[j] = e;
+    s += e;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  for (int j = lane; j < T_n; j += 32) x[j] = x[j] / s;
+}
+
+// ---------------------------------------------------------------------------------------
+// K2: per-row selection.  One warp per row: bitonic sort of (value, column) pairs in
+// shared memory into the reference's stable descending order (masker.py:113-115: larger
+// value first, equal values by ascending column), then the hybrid count
+//   kept = min(max(K, cnt_p), T_n),  cnt_p = searchsorted_left(cumsum(sorted), thr) + 1
+// with the cumsum evaluated strictly sequentially in float64 exactly like np.cumsum.
+// For non-negative rows the running sum is monotone, so a linear scan that stops at the
+// first prefix >= thr equals numpy's binary search; if a row has a negative entry the
+// full cumsum is built and numpy's left binary search is replayed step for step.
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ bool goes_before(double va, int ca, double vb, int cb) {
+  return va > vb || (va == vb && ca < cb);
+}
+
+__global__ void k_select(const double* __restrict__ probs, int64_t rows, int T_n, int T_pad,
+                         int k_count, double thr, int use_p, uint8_t* __restrict__ keep,
+                         int32_t* __restrict__ counts) {
+  extern __shared__ unsigned char smem_raw[];
+  const int warps = blockDim.x / 32;
+  const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+  double* vals = reinterpret_cast<double*>(smem_raw) + (int64_t)w * T_pad;
+  int* cols = reinterpret_cast<int*>(reinterpret_cast<double*>(smem_raw) + (int64_t)warps * T_pad) +
+              (int64_t)w * T_pad;
+  const int64_t row = (int64_t)blockIdx.x * warps + w;
+  if (row >= rows) return;
+  const double* x = probs + row * (int64_t)T_n;
+  bool neg = false;
+  for (int t = lane; t < T_pad; t += 32) {
+    if (t < T_n) {
+      double v = x[t];
+      neg |= v < 0.0;
+      vals[t] = v;
+      cols[t] = t;
+    } else {
+      vals[t] = -INFINITY;
+      cols[t] = 0x7fffffff;
+    }
+  }
+  neg = __any_sync(0xffffffffu, neg);
+  __syncwarp();
+  for (int size = 2; size <= T_pad; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = lane; t < (T_pad >> 1); t += 32) {
+        int i = 2 * t - (t & (stride - 1));
+        int j = i + stride;
+        bool up = (i & size) == 0;
+        double vi = vals[i], vj = vals[j];
+        int ci = cols[i], cj = cols[j];
+        if (goes_before(vj, cj, vi, ci) == up) {
+          vals[i] = vj; vals[j] = vi;
+          cols[i] = cj; cols[j] = ci;
+        }
+      }
+      __syncwarp();
+    }
+  }
+  int kept = 0;
+  if (lane == 0) {
+    int cnt_p = 1;
+    if (use_p) {
+      if (!neg) {
+        double run = 0.0;
+        int t = 0;
+        for (; t < T_n; ++t) {
+          run = (t == 0) ? vals[0] : run + vals[t];
+          if (run >= thr) break;
+        }
+        cnt_p = t + 1;
+      } else {
+        double run = 0.0;
+        for (int t = 0; t < T_n; ++t) {
+          run = (t == 0) ? vals[0] : run + vals[t];
+          vals[t] = run;  // sorted values are no longer needed
+        }
+        int lo = 0, hi = T_n;  // numpy npy_binsearch (side='left'), single key
+        while (lo < hi) {
+          int mid = lo + ((hi - lo) >> 1);
+          if (vals[mid] < thr) lo = mid + 1; else hi = mid;
+        }
+        cnt_p = lo + 1;
+      }
+    }
+    kept = min(max(k_count, cnt_p), T_n);
+  }
+  kept = __shfl_sync(0xffffffffu, kept, 0);
+  uint8_t* out = keep + row * (int64_t)T_n;
+  for (int t = lane; t < T_n; t += 32) out[t] = 0;
+  __syncwarp();
+  for (int t = lane; t < kept; t += 32) out[cols[t]] = 1;
+  if (lane == 0 && counts != nullptr) counts[row] = kept;
+}
+
+// ---------------------------------------------------------------------------------------
+// K3: block lists.
+// ---------------------------------------------------------------------------------------
+__global__ void k_row_counts(const uint8_t* __restrict__ keep, int64_t nrows, int T_n,
+                             int32_t* __restrict__ row_cnt) {
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (row >= nrows) return;
+  int c = 0;
+  for (int j = lane; j < T_n; j += 32) c += keep[row * T_n + j] != 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0) row_cnt[row] = c;
+}
+
+__global__ void k_col_counts(const uint8_t* __restrict__ keep, int64_t bh, int T_m, int T_n,
+                             int32_t* __restrict__ col_cnt) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= bh * T_n) return;
+  const int64_t h = g / T_n;
+  const int j = (int)(g % T_n);
+  const uint8_t* base = keep + h * (int64_t)T_m * T_n + j;
+  int c = 0;
+  for (int i = 0; i < T_m; ++i) c += base[(int64_t)i * T_n] != 0;
+  col_cnt[g] = c;
+}
+
+constexpr int kScanThreads = 1024;
+
+// Exclusive scan of in[0..n) into out[0..n], out[n] = total, by one CTA.
+__device__ void cta_exclusive_scan(const int32_t* in, int32_t* out, int64_t n, int32_t* sh) {
+  const int tid = threadIdx.x;
+  const int64_t per = (n + kScanThreads - 1) / kScanThreads;
+  const int64_t beg = min((int64_t)tid * per, n), end = min(beg + per, n);
+  int32_t local = 0;
+  for (int64_t i = beg; i < end; ++i) local += in[i];
+  sh[tid] = local;
+  __syncthreads();
+  for (int off = 1; off < kScanThreads; off <<= 1) {  // Hillis-Steele inclusive scan
+    int32_t v = tid >= off ? sh[tid - off] : 0;
+    __syncthreads();
+    sh[tid] += v;
+    __syncthreads();
+  }
+  int32_t run = sh[tid] - local;
+  for (int64_t i = beg; i < end; ++i) {
+    int32_t c = in[i];
+    out[i] = run;
+    run += c;
+  }
+  if (tid == kScanThreads - 1) out[n] = sh[tid];
+  __syncthreads();
+}
+
+// Longest-first order: counting sort of ids by descending count (counts in [0, maxc]).
+__device__ void cta_order_desc(const int32_t* cnt, int64_t n, int maxc, int32_t* order,
+                               int32_t* bins, int32_t* sh) {
+  for (int c = threadIdx.x; c <= maxc; c += kScanThreads) bins[c] = 0;
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < n; i += kScanThreads) atomicAdd(&bins[maxc - cnt[i]], 1);
+  __syncthreads();
+  // bins (indexed by maxc - count, i.e. descending count) -> exclusive starts, in place
+  const int nb = maxc + 1;
+  const int per = (nb + kScanThreads - 1) / kScanThreads;
+  const int beg = min((int)threadIdx.x * per, nb), end = min(beg + per, nb);
+  int32_t local = 0;
+  for (int b = beg; b < end; ++b) local += bins[b];
+  sh[threadIdx.x] = local;
+  __syncthreads();
+  for (int off = 1; off < kScanThreads; off <<= 1) {
+    int32_t v = threadIdx.x >= off ? sh[threadIdx.x - off] : 0;
+    __syncthreads();
+    sh[threadIdx.x] += v;
+    __syncthreads();
+  }
+  int32_t run = sh[threadIdx.x] - local;
+  for (int b = beg; b < end; ++b) {
+    int32_t c = bins[b];
+    bins[b] = run;
+    run += c;
+  }
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < n; i += kScanThreads) {
+    int pos = atomicAdd(&bins[maxc - cnt[i]], 1);
+    order[pos] = (int32_t)i;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_orders(const int32_t* __restrict__ row_cnt,
+                                                              const int32_t* __restrict__ col_cnt,
+                                                              int64_t nrows, int64_t ncols, int T_m,
+                                                              int T_n, int32_t* row_ptr,
+                                                              int32_t* col_ptr, int32_t* row_order,
+                                                              int32_t* col_order) {
+  extern __shared__ int32_t sh_scan[];  // [kScanThreads] + bins[max(T_m,T_n)+1]
+  int32_t* bins = sh_scan + kScanThreads;
+  cta_exclusive_scan(row_cnt, row_ptr, nrows, sh_scan);
+  cta_exclusive_scan(col_cnt, col_ptr, ncols, sh_scan);
+  cta_order_desc(row_cnt, nrows, T_n, row_order, bins, sh_scan);
+  cta_order_desc(col_cnt, ncols, T_m, col_order, bins, sh_scan);
+}
+
+__global__ void k_fill_rows(const uint8_t* __restrict__ keep, int64_t nrows, int T_n,
+                            const int32_t* __restrict__ row_ptr, int32_t* __restrict__ row_idx) {
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (row >= nrows) return;
+  int base = row_ptr[row];
+  for (int j0 = 0; j0 < T_n; j0 += 32) {
+    int j = j0 + lane;
+    bool f = j < T_n && keep[row * T_n + j] != 0;
+    unsigned m = __ballot_sync(0xffffffffu, f);
+    if (f) row_idx[base + __popc(m & ((1u << lane) - 1u))] = j;
+    base += __popc(m);
+  }
+}
+
+__global__ void k_fill_cols(const uint8_t* __restrict__ keep, int64_t bh, int T_m, int T_n,
+                            const int32_t* __restrict__ col_ptr, int32_t* __restrict__ col_idx) {
+  const int64_t g = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (g >= bh * T_n) return;
+  const int64_t h = g / T_n;
+  const int j = (int)(g % T_n);
+  const uint8_t* base_p = keep + h * (int64_t)T_m * T_n + j;
+  int base = col_ptr[g];
+  for (int i0 = 0; i0 < T_m; i0 += 32) {
+    int i = i0 + lane;
+    bool f = i < T_m && base_p[(int64_t)i * T_n] != 0;
+    unsigned m = __ballot_sync(0xffffffffu, f);
+    if (f) col_idx[base + __popc(m & ((1u << lane) - 1u))] = i;
+    base += __popc(m);
+  }
+}
+
+template <typename T>
+int launch_pool(spa2_view q, spa2_view k, int64_t B, int64_t H, int64_t N, int64_t d, int64_t b_q,
+                int64_t b_kv, int64_t T_m, int64_t T_n, double* qbar, double* kbar,
+                int32_t* nonfinite, cudaStream_t st) {
+  const int64_t BH = B * H;
+  const int cpt_vec = 16 / (int)sizeof(T) < 8 ? 16 / (int)sizeof(T) : 8;
+  auto aligned = [&](const spa2_view& v) {
+    return ((uintptr_t)v.ptr % 16 == 0) && (v.sb % cpt_vec == 0) && (v.sh % cpt_vec == 0) &&
+           (v.sn % cpt_vec == 0);
+  };
+  const bool vec = (d % cpt_vec == 0) && aligned(q) && aligned(k) && (d / cpt_vec) <= kPoolThreads;
+  const int cpt = vec ? cpt_vec : 1;
+  SPA2_REQUIRE(d / cpt <= kPoolThreads, SPA2_ERR_UNSUPPORTED,
+               "pooled_map: d=%lld too large for the pooling kernel", (long long)d);
+  const int R = kPoolThreads / (int)(d / cpt);
+  const size_t smem = (size_t)R * d * sizeof(double);
+  const int64_t grid = BH * (T_m + T_n);
+  SPA2_REQUIRE(grid < (1ll << 31), SPA2_ERR_UNSUPPORTED, "pooled_map: grid too large");
+  if (vec) {
+    auto kern = k_pool<T, true>;
+    if (smem > 48 * 1024) SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)grid, kPoolThreads, smem, st>>>(q, k, (int)H, (int)N, (int)d, (int)b_q, (int)b_kv,
+                                                      (int)T_m, (int)T_n, BH, qbar, kbar, nonfinite);
+  } else {
+    auto kern = k_pool<T, false>;
+    if (smem > 48 * 1024) SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)grid, kPoolThreads, smem, st>>>(q, k, (int)H, (int)N, (int)d, (int)b_q, (int)b_kv,
+                                                      (int)T_m, (int)T_n, BH, qbar, kbar, nonfinite);
+  }
+  SPA2_LAUNCH_CHECK();
+  return SPA2_OK;
+}
+
+}  // namespace
+}  // namespace spa2
+
+using namespace spa2;
+
+extern "C" int spa2_pooled_map(spa2_view q, spa2_view k, int dtype, int64_t B, int64_t H, int64_t N,
+                               int64_t d, int64_t b_q, int64_t b_kv, double* probs,
+                               double* workspace, int32_t* nonfinite, void* stream) {
+  SPA2_REQUIRE(B >= 1 && H >= 1 && N >= 1 && d >= 1, SPA2_ERR_VALUE,
+               "pooled_map: bad shape B=%lld H=%lld N=%lld d=%lld", (long long)B, (long long)H,
+               (long long)N, (long long)d);
+  SPA2_REQUIRE(b_q >= 1 && b_kv >= 1, SPA2_ERR_VALUE, "block sizes must be >= 1: b_q=%lld, b_kv=%lld",
+               (long long)b_q, (long long)b_kv);
+  SPA2_REQUIRE(q.ptr && k.ptr && probs && workspace, SPA2_ERR_VALUE, "pooled_map: null pointer");
+  SPA2_REQUIRE(N < (1ll << 31), SPA2_ERR_UNSUPPORTED, "pooled_map: N too large");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t T_m = ceil_div(N, b_q), T_n = ceil_div(N, b_kv), BH = B * H;
+  double* qbar = workspace;
+  double* kbar = workspace + BH * T_m * d;
+  int rc;
+  switch (dtype) {
+    case SPA2_BF16: rc = launch_pool<__nv_bfloat16>(q, k, B, H, N, d, b_q, b_kv, T_m, T_n, qbar, kbar, nonfinite, st); break;
+    case SPA2_F16: rc = launch_pool<__half>(q, k, B, H, N, d, b_q, b_kv, T_m, T_n, qbar, kbar, nonfinite, st); break;
+    case SPA2_F32: rc = launch_pool<float>(q, k, B, H, N, d, b_q, b_kv, T_m, T_n, qbar, kbar, nonfinite, st); break;
+    case SPA2_F64: rc = launch_pool<double>(q, k, B, H, N, d, b_q, b_kv, T_m, T_n, qbar, kbar, nonfinite, st); break;
+    default: SPA2_REQUIRE(false, SPA2_ERR_UNSUPPORTED, "pooled_map: unsupported dtype %d", dtype);
+  }
+  if (rc != SPA2_OK) return rc;
+  dim3 grid((unsigned)ceil_div(T_n, kSTJ), (unsigned)ceil_div(T_m, kSTI), (unsigned)BH);
+  k_scores<<<grid, 256, 0, st>>>(qbar, kbar, (int)T_m, (int)T_n, (int)d, sqrt((double)d), probs);
+  SPA2_LAUNCH_CHECK();
+  const int64_t rows = BH * T_m;
+  k_softmax_rows<<<(unsigned)ceil_div(rows, 8), 256, 0, st>>>(probs, rows, (int)T_n);
+  SPA2_LAUNCH_CHECK();
+  return SPA2_OK;
+}
+
+extern "C" int spa2_select(const double* probs, int64_t rows, int64_t t_n, int64_t k_count,
+                           double p_threshold, uint8_t* keep, int32_t* counts, void* stream) {
+  SPA2_REQUIRE(rows >= 1 && t_n >= 1, SPA2_ERR_VALUE, "select: empty map (%lld x %lld)",
+               (long long)rows, (long long)t_n);
+  SPA2_REQUIRE(k_count >= 1, SPA2_ERR_VALUE, "select: k_count must be >= 1");
+  SPA2_REQUIRE(probs && keep, SPA2_ERR_VALUE, "select: null pointer");
+  SPA2_REQUIRE(!isnan(p_threshold), SPA2_ERR_VALUE, "select: p_threshold is NaN");
+  int t_pad = 1;
+  while (t_pad < t_n) t_pad <<= 1;
+  if (t_pad < 32) t_pad = 32;
+  const size_t per_warp = (size_t)t_pad * (sizeof(double) + sizeof(int));
+  SPA2_REQUIRE(per_warp <= 200 * 1024, SPA2_ERR_UNSUPPORTED, "select: T_n=%lld exceeds 16384",
+               (long long)t_n);
+  int warps = (int)std::min<size_t>(8, std::max<size_t>(1, (48 * 1024) / per_warp));
+  const size_t smem = per_warp * warps;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (smem > 48 * 1024)
+    SPA2_CUDA_TRY(cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int use_p = isinf(p_threshold) && p_threshold < 0 ? 0 : 1;
+  const int kk = (int)std::min<int64_t>(k_count, t_n);
+  k_select<<<(unsigned)ceil_div(rows, warps), warps * 32, smem, st>>>(
+      probs, rows, (int)t_n, t_pad, kk, p_threshold, use_p, keep, counts);
+  SPA2_LAUNCH_CHECK();
+  return SPA2_OK;
+}
+
+extern "C" int spa2_build_lists(const uint8_t* keep, int64_t bh, int64_t t_m, int64_t t_n,
+                                int32_t* row_ptr, int32_t* row_idx, int32_t* col_ptr,
+                                int32_t* col_idx, int32_t* row_order, int32_t* col_order,
+                                int32_t* scratch, void* stream) {
+  SPA2_REQUIRE(bh >= 1 && t_m >= 1 && t_n >= 1, SPA2_ERR_VALUE, "build_lists: empty grid");
+  SPA2_REQUIRE(keep && row_ptr && row_idx && col_ptr && col_idx && row_order && col_order && scratch,
+               SPA2_ERR_VALUE, "build_lists: null pointer");
+  SPA2_REQUIRE(bh * t_m * t_n < (1ll << 31), SPA2_ERR_UNSUPPORTED, "build_lists: grid too large");
+  SPA2_REQUIRE(std::max(t_m, t_n) <= 32768, SPA2_ERR_UNSUPPORTED, "build_lists: T_m/T_n > 32768");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t nrows = bh * t_m, ncols = bh * t_n;
+  int32_t* col_cnt = scratch;          // [ncols]
+  int32_t* row_cnt = scratch + ncols;  // [nrows]
+  k_row_counts<<<(unsigned)ceil_div(nrows, 8), 256, 0, st>>>(keep, nrows, (int)t_n, row_cnt);
+  SPA2_LAUNCH_CHECK();
+  k_col_counts<<<(unsigned)ceil_div(ncols, 256), 256, 0, st>>>(keep, bh, (int)t_m, (int)t_n, col_cnt);
+  SPA2_LAUNCH_CHECK();
+  const size_t smem = (kScanThreads + std::max(t_m, t_n) + 1) * sizeof(int32_t);
+  if (smem > 48 * 1024)
+    SPA2_CUDA_TRY(cudaFuncSetAttribute(k_scan_orders, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_scan_orders<<<1, kScanThreads, smem, st>>>(row_cnt, col_cnt, nrows, ncols, (int)t_m, (int)t_n,
+                                               row_ptr, col_ptr, row_order, col_order);
+  SPA2_LAUNCH_CHECK();
+  k_fill_rows<<<(unsigned)ceil_div(nrows, 8), 256, 0, st>>>(keep, nrows, (int)t_n, row_ptr, row_idx);
+  SPA2_LAUNCH_CHECK();
+  k_fill_cols<<<(unsigned)ceil_div(ncols, 8), 256, 0, st>>>(keep, bh, (int)t_m, (int)t_n, col_ptr, col_idx);
+  SPA2_LAUNCH_CHECK();
+  return SPA2_OK;
+}

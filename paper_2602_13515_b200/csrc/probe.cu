@@ -1,0 +1,123 @@
+// probe.cu — a one-CTA tcgen05 GEMM that exercises exactly the operand layouts, UMMA
+// descriptors, TMA swizzle and TMEM read-back the attention kernels rely on.  It is a
+// diagnostic entry point (spa2_probe_gemm) used by the GPU tests to validate those
+// building blocks in isolation before they are trusted inside the fused kernels.
+#include "common.cuh"
+#include "ptx.cuh"
+#include "tma_host.h"
+
+namespace spa2 {
+namespace {
+
+using namespace ptx;
+
+// Stage a row-major [R][C] bf16 matrix into SWIZZLE_128B column chunks with generic stores.
+__device__ void stage_generic(uint8_t* dst, const __nv_bfloat16* src, int R, int C) {
+  const int units_per_row = C / 8;
+  for (int e = threadIdx.x; e < R * units_per_row; e += blockDim.x) {
+    const int r = e / units_per_row, u = e % units_per_row;
+    const uint4 v = *reinterpret_cast<const uint4*>(src + (int64_t)r * C + u * 8);
+    const uint32_t addr = smem_u32(dst) + (uint32_t)((u / 8) * R * 128) + sw128_offset(r, u % 8);
+    st_shared_v4(addr, v.x, v.y, v.z, v.w);
+  }
+}
+
+// Descriptor for the k-step `ks` (16 deep) of an operand stored as described in ptx.cuh.
+__device__ uint64_t operand_desc(uint32_t base, bool mn_major, int R, int ks) {
+  if (!mn_major) {
+    const int k0 = ks * 16;
+    return sw128_desc(base + (uint32_t)((k0 / 64) * R * 128 + (k0 % 64) * 2), 16, 1024);
+  }
+  return sw128_desc(base + (uint32_t)(ks * 16 * 128), (uint32_t)(R * 128), 1024);
+}
+
+__global__ void __launch_bounds__(128) k_probe(const __nv_bfloat16* a, const __nv_bfloat16* b, float* d, int M,
+                                               int N, int K, int a_mn, int b_mn, int use_tma,
+                                               const __grid_constant__ CUtensorMap ta,
+                                               const __grid_constant__ CUtensorMap tb) {
+  extern __shared__ uint8_t smem_dyn[];
+  __shared__ uint64_t bar_load, bar_mma;
+  __shared__ uint32_t tmem_base;
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+  uint8_t* sa = base;
+  uint8_t* sb = base + 32768;
+  const int Ra = a_mn ? K : M, Ca = a_mn ? M : K;
+  const int Rb = b_mn ? K : N, Cb = b_mn ? N : K;
+  if (warp_id() == 0) tmem_alloc(&tmem_base, 128);
+  if (threadIdx.x == 32) {
+    mbar_init(&bar_load, 1);
+    mbar_init(&bar_mma, 1);
+    fence_mbar_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tmem_base;
+  if (use_tma) {
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(&bar_load, (uint32_t)((Ra * Ca + Rb * Cb) * 2));
+      for (int c = 0; c < Ca / 64; ++c) tma_load_2d(sa + c * Ra * 128, &ta, &bar_load, c * 64, 0);
+      for (int c = 0; c < Cb / 64; ++c) tma_load_2d(sb + c * Rb * 128, &tb, &bar_load, c * 64, 0);
+    }
+    mbar_wait(&bar_load, 0);
+  } else {
+    stage_generic(sa, a, Ra, Ca);
+    stage_generic(sb, b, Rb, Cb);
+    fence_proxy_async_smem();
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    tc_fence_after();
+    const uint32_t idesc = idesc_bf16(M, N, a_mn != 0, b_mn != 0);
+    for (int ks = 0; ks < K / 16; ++ks) {
+      mma_bf16(tbase, operand_desc(smem_u32(sa), a_mn, Ra, ks), operand_desc(smem_u32(sb), b_mn, Rb, ks), idesc,
+               ks > 0 ? 1u : 0u);
+    }
+    mma_commit(&bar_mma);
+  }
+  __syncwarp();
+  mbar_wait(&bar_mma, 0);
+  tc_fence_after();
+  const int w = warp_id(), l = lane_id();
+  for (int c0 = 0; c0 < N; c0 += 16) {
+    uint32_t r[16];
+    tmem_ld16(tbase + ((uint32_t)(32 * w) << 16) + (uint32_t)c0, r);
+    int m = -1;
+    if (M == 128) m = 32 * w + l;
+    else if (l < 16) m = 16 * w + l;
+    if (m >= 0)
+      for (int e = 0; e < 16; ++e) d[(int64_t)m * N + c0 + e] = __uint_as_float(r[e]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp_id() == 0) tmem_dealloc(tbase, 128);
+}
+
+}  // namespace
+}  // namespace spa2
+
+using namespace spa2;
+
+extern "C" int spa2_probe_gemm(const void* a, const void* b, float* d, int m, int n, int k, int a_mn, int b_mn,
+                               int use_tma, void* stream) {
+  SPA2_REQUIRE(m == 64 || m == 128, SPA2_ERR_UNSUPPORTED, "probe: m must be 64 or 128");
+  SPA2_REQUIRE(n == 64 || n == 128, SPA2_ERR_UNSUPPORTED, "probe: n must be 64 or 128");
+  SPA2_REQUIRE(k == 64 || k == 128, SPA2_ERR_UNSUPPORTED, "probe: k must be 64 or 128");
+  CUtensorMap ta, tb;
+  memset(&ta, 0, sizeof(ta));
+  memset(&tb, 0, sizeof(tb));
+  if (use_tma) {
+    const int Ra = a_mn ? k : m, Ca = a_mn ? m : k;
+    const int Rb = b_mn ? k : n, Cb = b_mn ? n : k;
+    int rc = make_tma_bf16_2d(&ta, a, Ca, Ra, Ca, 64, Ra);
+    if (rc) return rc;
+    rc = make_tma_bf16_2d(&tb, b, Cb, Rb, Cb, 64, Rb);
+    if (rc) return rc;
+  }
+  const size_t smem = 65536 + 1024;
+  SPA2_CUDA_TRY(cudaFuncSetAttribute(k_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_probe<<<1, 128, smem, (cudaStream_t)stream>>>((const __nv_bfloat16*)a, (const __nv_bfloat16*)b, d, m, n, k,
+                                                  a_mn, b_mn, use_tma, ta, tb);
+  SPA2_LAUNCH_CHECK();
+  return SPA2_OK;
+}

@@ -1,0 +1,14 @@
+// tma_host.h — host-side TMA descriptor encoding (bf16, SWIZZLE_128B, zero OOB fill).
+#pragma once
+#include <cuda.h>
+#include <stdint.h>
+
+namespace spa2 {
+// 4-D map over a [dims[3]][dims[2]][dims[1]][dims[0]] bf16 tensor with element strides
+// strides_elems = {axis1, axis2, axis3} (axis 0 is contiguous).
+int make_tma_bf16_4d(CUtensorMap* map, const void* base, const uint64_t dims[4], const uint64_t strides_elems[3],
+                     const uint32_t box[4]);
+// 2-D map over a row-major [rows][cols] bf16 matrix.
+int make_tma_bf16_2d(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint64_t row_stride_elems,
+                     uint32_t box_cols, uint32_t box_rows);
+}  // namespace spa2

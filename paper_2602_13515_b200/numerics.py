@@ -1,0 +1,73 @@
+"""Input coercion at the reference-facing boundary.
+
+The reference coerces every input to a C-contiguous float64 numpy array and raises
+``ShapeError`` (a ``ValueError``) on a wrong rank (numerics.py:17-26).  This module does
+the B200 equivalent: inputs become CUDA tensors viewed as [B, H, N, d] (rank 2 = the
+reference's single-head [N, d]; rank 4 = the batched extension), and results go back in
+the caller's container (numpy in -> numpy float64 out, torch in -> torch out).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+
+
+class ShapeError(ValueError):
+    """Operand dimensions are incompatible (numerics.py:17-18)."""
+
+
+def num_blocks(n: int, block: int) -> int:
+    """ceil(n / block) (numerics.py:68-69)."""
+    return -(-n // block)
+
+
+@dataclass(frozen=True)
+class Boundary:
+    """How the caller handed us a tensor, so results can be returned the same way."""
+
+    rank: int
+    numpy: bool
+    device: torch.device
+
+
+def current_device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2602_13515_b200 requires a CUDA device (B200, sm_100a); none is visible")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def to_device4(x, dtype: torch.dtype | None, name: str, device: torch.device | None = None):
+    """Return (tensor [B,H,N,d] on CUDA, Boundary).  ``dtype=None`` keeps a floating dtype."""
+    is_np = not isinstance(x, torch.Tensor)
+    t = torch.as_tensor(np.asarray(x)) if is_np else x
+    if t.dim() not in (2, 4):
+        raise ShapeError(f"{name}: expected rank 2 [N,d] or rank 4 [B,H,N,d], got rank {t.dim()} "
+                         f"with shape {tuple(t.shape)}")
+    if t.shape[-1] < 1 or t.shape[-2] < 1:
+        raise ShapeError(f"{name}: empty tensor {tuple(t.shape)}")
+    if device is None:
+        device = t.device if t.is_cuda else current_device()
+    _lib.require_device(device)
+    want = dtype if dtype is not None else (t.dtype if t.dtype in _lib.DTYPE_CODES else torch.float64)
+    t = t.to(device=device, dtype=want, non_blocking=True)
+    if t.stride(-1) != 1:
+        t = t.contiguous()
+    rank = t.dim()
+    if rank == 2:
+        t = t.view(1, 1, *t.shape) if t.is_contiguous() else t.contiguous().view(1, 1, *t.shape)
+    return t, Boundary(rank=rank, numpy=is_np, device=device)
+
+
+def from_device(t: torch.Tensor, b: Boundary, rows_dims: int = 2):
+    """Undo ``to_device4``'s batching for an output whose trailing ``rows_dims`` axes are
+    per-head (e.g. 2 for [N,d], 1 for lse [N])."""
+    if b.rank == 2:
+        t = t.reshape(t.shape[-rows_dims:])
+    if b.numpy:
+        return t.detach().to(torch.float64).cpu().numpy()
+    return t

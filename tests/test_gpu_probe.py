@@ -1,0 +1,32 @@
+"""tcgen05 building blocks on hardware: one-CTA MMA through the exact shared-memory
+layouts (K-major / MN-major SWIZZLE_128B), UMMA descriptors, TMA staging and TMEM
+read-back (M = 64 and 128 layouts) that the attention kernels are built from."""
+
+import itertools
+
+import pytest
+import torch
+
+from paper_2602_13515_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("m,n,k", [(128, 64, 128), (128, 128, 64), (64, 64, 128), (128, 128, 128), (64, 128, 64)])
+@pytest.mark.parametrize("a_mn,b_mn", list(itertools.product((0, 1), repeat=2)))
+@pytest.mark.parametrize("use_tma", [0, 1])
+def test_probe_gemm(m, n, k, a_mn, b_mn, use_tma):
+    g = torch.Generator(device="cuda").manual_seed(m * 7 + n * 3 + k + a_mn * 11 + b_mn * 13 + use_tma)
+    a = torch.randn(m, k, device="cuda", generator=g).to(torch.bfloat16)
+    b = torch.randn(n, k, device="cuda", generator=g).to(torch.bfloat16)
+    a_store = a.t().contiguous() if a_mn else a.contiguous()
+    b_store = b.t().contiguous() if b_mn else b.contiguous()
+    d = torch.full((m, n), float("nan"), device="cuda", dtype=torch.float32)
+    lib = _lib.load()
+    rc = lib.spa2_probe_gemm(_lib.ptr(a_store), _lib.ptr(b_store), _lib.ptr(d), m, n, k, a_mn, b_mn, use_tma,
+                             torch.cuda.current_stream().cuda_stream)
+    _lib.check(rc, "probe")
+    torch.cuda.synchronize()
+    want = a.float() @ b.float().t()
+    err = (d - want).abs().max().item()
+    assert err <= 1e-3 * max(1.0, want.abs().max().item()), (m, n, k, a_mn, b_mn, use_tma, err)
