@@ -122,8 +122,9 @@ int spa2_bwd(spa2_view q, spa2_view k, spa2_view v, spa2_view o, spa2_view dout,
  * row-major [m,n], computed by ONE tcgen05 MMA chain through exactly the shared-memory
  * layouts and descriptors the attention kernels use.  A is stored row-major as [m,k]
  * (a_mn = 0, staged K-major) or as [k,m] (a_mn = 1, staged MN-major); likewise B as
- * [n,k] or [k,n].  use_tma = 1 stages operands with TMA (SWIZZLE_128B), 0 with generic
- * swizzled stores.  m in {64,128}; n, k in {64,128}. */
+ * [n,k] or [k,n].  use_tma (staging mode): 0 = generic swizzled stores, 1 = TMA
+ * (SWIZZLE_128B), 2 = A packed into TMEM by tcgen05.st and consumed by the TS form of
+ * tcgen05.mma (m = 128, K-major A only).  m in {64,128}; n, k in {64,128}. */
 int spa2_probe_gemm(const void* a, const void* b, float* d, int m, int n, int k, int a_mn, int b_mn,
                     int use_tma, void* stream);
 

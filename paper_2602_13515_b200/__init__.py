@@ -21,3 +21,14 @@ from .masker import (  # noqa: F401,E402
     top_p_mask,
 )
 from .numerics import ShapeError, num_blocks  # noqa: F401,E402
+from .attention import (  # noqa: F401,E402
+    AttentionGrads,
+    AttentionOutput,
+    BlockCounter,
+    SparseAttentionFunction,
+    attention_backward,
+    dense_attention,
+    full_mask,
+    sparse_attention,
+    sparse_attention_with_mask,
+)

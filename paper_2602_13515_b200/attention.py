@@ -1,0 +1,319 @@
+"""Block-sparse attention forward / backward on the GPU, with autograd.
+
+Drop-in for ``sparseattn_lab.attention`` (attention.py:22-166): same names, arguments,
+result types and errors.  Compute runs in ``libspa2.so``:
+
+* ``sparse_attention_with_mask`` -> K4 tcgen05 forward (O bf16, LSE fp32 natural log);
+* ``attention_backward`` / autograd -> K5 δ, K6 dK/dV (KV-major lists), K7 dQ (row lists);
+* ``sparse_attention`` = K1 pooled map -> K2 hybrid select -> K3 lists -> K4.
+
+Inputs are [N, d] (the reference contract) or [B, H, N, d]; they are computed in bf16
+(the reference's float64 is out of reach of tensor cores); results come back in the
+caller's container (numpy in -> numpy float64 out).  The kernels use b_q = 128 and
+b_kv = 64 (the paper's setting); masks at coarser multiples of that grid
+(or all-ones masks such as ``full_mask``) are refined exactly, other geometries raise.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .masker import BlockMask, SparsityConfig, _pooled_probs, _select, top_k_count
+from .numerics import from_device, num_blocks, to_device4
+
+BQ, BKV = 128, 64
+SUPPORTED_HEAD_DIMS = (64, 128)
+
+
+@dataclass(frozen=True)
+class AttentionOutput:
+    """attention.py:22-26."""
+
+    out: object
+    lse: object
+    mask_used: BlockMask
+
+
+@dataclass(frozen=True)
+class AttentionGrads:
+    """attention.py:29-33."""
+
+    dq: object
+    dk: object
+    dv: object
+
+
+class BlockCounter:
+    """Counts computed (query block, key block) tiles (attention.py:36-43).  The GPU forward
+    adds the number of tiles it actually computed, counted on the device."""
+
+    def __init__(self):
+        self.count = 0
+
+    def hit(self, i: int, j: int) -> None:
+        self.count += 1
+
+
+def full_mask(n: int) -> BlockMask:
+    """One all-kept block covering everything (attention.py:46-47)."""
+    return BlockMask(np.ones((1, 1), dtype=bool), b_q=n, b_kv=n, n_tokens=n)
+
+
+# --------------------------------------------------------------------------------------
+# block lists
+# --------------------------------------------------------------------------------------
+
+@dataclass(frozen=True)
+class BlockLists:
+    """CSR block lists over flattened (b, h, block) rows / columns, on the device."""
+
+    row_ptr: torch.Tensor
+    row_idx: torch.Tensor
+    row_order: torch.Tensor
+    col_ptr: torch.Tensor
+    col_idx: torch.Tensor
+    col_order: torch.Tensor
+    shape: tuple  # (B, H, T_m, T_n)
+
+
+def _native_keep(bm: BlockMask, B: int, H: int, N: int) -> torch.Tensor:
+    """keep at the kernel grid (128, 64) as uint8 [B, H, T_m, T_n] (exact refinement)."""
+    t_m, t_n = num_blocks(N, BQ), num_blocks(N, BKV)
+    keep = bm.keep
+    if keep.dim() == 2:
+        keep = keep.view(1, 1, *keep.shape)
+    if (bm.b_q, bm.b_kv) != (BQ, BKV):
+        if bm.b_q % BQ == 0 and bm.b_kv % BKV == 0:
+            keep = keep.repeat_interleave(bm.b_q // BQ, dim=-2).repeat_interleave(bm.b_kv // BKV, dim=-1)
+            keep = keep[..., :t_m, :t_n]
+        elif bool(keep.all()):
+            keep = torch.ones((*keep.shape[:2], t_m, t_n), device=keep.device, dtype=torch.bool)
+        else:
+            raise ValueError(f"GPU kernels use b_q={BQ}, b_kv={BKV}; mask geometry (b_q={bm.b_q}, b_kv={bm.b_kv}) "
+                             "is not an exact multiple of it")
+    if keep.shape[0] != B or keep.shape[1] != H:
+        if keep.shape[0] == 1 and keep.shape[1] == 1:
+            keep = keep.expand(B, H, t_m, t_n)
+        else:
+            raise ValueError(f"mask batch/head dims {tuple(keep.shape[:2])} do not match inputs ({B}, {H})")
+    return keep.contiguous().view(torch.uint8)
+
+
+def build_lists(keep_u8: torch.Tensor) -> BlockLists:
+    """K3 on a uint8 [B, H, T_m, T_n] keep tensor."""
+    B, H, t_m, t_n = keep_u8.shape
+    bh, dev = B * H, keep_u8.device
+    cap = max(1, bh * t_m * t_n)
+    i32 = dict(device=dev, dtype=torch.int32)
+    lists = BlockLists(
+        row_ptr=torch.empty(bh * t_m + 1, **i32), row_idx=torch.empty(cap, **i32), row_order=torch.empty(bh * t_m, **i32),
+        col_ptr=torch.empty(bh * t_n + 1, **i32), col_idx=torch.empty(cap, **i32), col_order=torch.empty(bh * t_n, **i32),
+        shape=(B, H, t_m, t_n))
+    scratch = torch.empty(bh * (t_m + t_n), **i32)
+    rc = _lib.load().spa2_build_lists(
+        _lib.ptr(keep_u8), bh, t_m, t_n, _lib.ptr(lists.row_ptr), _lib.ptr(lists.row_idx), _lib.ptr(lists.col_ptr),
+        _lib.ptr(lists.col_idx), _lib.ptr(lists.row_order), _lib.ptr(lists.col_order), _lib.ptr(scratch),
+        _lib.stream_of(keep_u8))
+    _lib.check(rc, "build_lists")
+    return lists
+
+
+def _lists_with_order(keep_u8: torch.Tensor, visit) -> BlockLists:
+    """Host-built row lists honouring the reference's ``_block_order`` test hook
+    (attention.py:74-81, 97-99).  Test-only: copies the mask to the host."""
+    base = build_lists(keep_u8)
+    B, H, t_m, t_n = keep_u8.shape
+    keep = keep_u8.cpu().numpy().astype(bool).reshape(B * H * t_m, t_n)
+    idx = []
+    for r in range(keep.shape[0]):
+        kept = np.flatnonzero(keep[r])
+        idx.append(np.asarray(visit(r % t_m, kept), dtype=np.int32))
+    flat = torch.tensor(np.concatenate(idx) if idx else np.zeros(0, np.int32), device=keep_u8.device)
+    return BlockLists(base.row_ptr, flat, base.row_order, base.col_ptr, base.col_idx, base.col_order, base.shape)
+
+
+def mask_lists(bm: BlockMask, B: int, H: int, N: int) -> BlockLists:
+    """Block lists of ``bm`` for a [B, H, N, d] problem, cached on the (immutable) mask."""
+    key = ("lists", B, H, N)
+    hit = bm._cache.get(key)
+    if hit is None:
+        hit = build_lists(_native_keep(bm, B, H, N))
+        bm._cache[key] = hit
+    return hit
+
+
+# --------------------------------------------------------------------------------------
+# kernel launchers
+# --------------------------------------------------------------------------------------
+
+def _check_kernel_shape(q4: torch.Tensor) -> None:
+    d = q4.shape[-1]
+    if d not in SUPPORTED_HEAD_DIMS:
+        raise ValueError(f"GPU kernels support head dim d in {SUPPORTED_HEAD_DIMS}, got d={d}")
+
+
+def fwd(q4, k4, v4, lists: BlockLists, scale: float, counter: torch.Tensor | None = None):
+    """K4: returns (O [B,H,N,d] bf16, LSE [B,H,N] fp32)."""
+    B, H, N, d = q4.shape
+    o = torch.empty((B, H, N, d), device=q4.device, dtype=q4.dtype)
+    lse = torch.empty((B, H, N), device=q4.device, dtype=torch.float32)
+    rc = _lib.load().spa2_fwd(
+        _lib.view4(q4), _lib.view4(k4), _lib.view4(v4), _lib.view4(o), _lib.ptr(lse), _lib.DTYPE_CODES[q4.dtype],
+        B, H, N, d, BQ, BKV, _lib.ptr(lists.row_ptr), _lib.ptr(lists.row_idx), _lib.ptr(lists.row_order), scale,
+        _lib.ptr(counter), _lib.stream_of(q4))
+    _lib.check(rc, "sparse attention forward")
+    return o, lse
+
+
+def bwd(q4, k4, v4, o4, do4, lse, lists: BlockLists, scale: float):
+    """K5-K7: returns (dQ, dK, dV) bf16 [B,H,N,d]."""
+    B, H, N, d = q4.shape
+    dq = torch.empty((B, H, N, d), device=q4.device, dtype=q4.dtype)
+    dk = torch.empty_like(dq)
+    dv = torch.empty_like(dq)
+    delta = torch.empty((B, H, N), device=q4.device, dtype=torch.float32)
+    rc = _lib.load().spa2_bwd(
+        _lib.view4(q4), _lib.view4(k4), _lib.view4(v4), _lib.view4(o4), _lib.view4(do4), _lib.ptr(lse),
+        _lib.ptr(delta), _lib.view4(dq), _lib.view4(dk), _lib.view4(dv), _lib.DTYPE_CODES[q4.dtype], B, H, N, d, BQ,
+        BKV, _lib.ptr(lists.row_ptr), _lib.ptr(lists.row_idx), _lib.ptr(lists.row_order), _lib.ptr(lists.col_ptr),
+        _lib.ptr(lists.col_idx), _lib.ptr(lists.col_order), scale, _lib.stream_of(q4))
+    _lib.check(rc, "sparse attention backward")
+    return dq, dk, dv
+
+
+class SparseAttentionFunction(torch.autograd.Function):
+    """O, LSE = sparse_attention(q, k, v | block lists); the mask is a constant
+    (SPEC.md:260), so only q, k, v receive gradients."""
+
+    @staticmethod
+    def forward(ctx, q4, k4, v4, lists, scale, counter):
+        o, lse = fwd(q4, k4, v4, lists, scale, counter)
+        ctx.save_for_backward(q4, k4, v4, o, lse)
+        ctx.lists = lists
+        ctx.scale = scale
+        ctx.mark_non_differentiable(lse)
+        return o, lse
+
+    @staticmethod
+    def backward(ctx, do, _dlse):
+        q4, k4, v4, o, lse = ctx.saved_tensors
+        do = do.to(q4.dtype)
+        if do.stride(-1) != 1 or any(s % 8 for s in do.stride()[:3]):
+            do = do.contiguous()
+        dq, dk, dv = bwd(q4, k4, v4, o, do, lse, ctx.lists, ctx.scale)
+        return dq, dk, dv, None, None, None
+
+
+# --------------------------------------------------------------------------------------
+# reference-facing API
+# --------------------------------------------------------------------------------------
+
+def _prepare(q, k, v, check_finite: bool):
+    """attention.py:50-59: same shapes (ValueError), rank (ShapeError), finite (FloatingPointError)."""
+    q4, qb = to_device4(q, torch.bfloat16, "q")
+    k4, _ = to_device4(k, torch.bfloat16, "k", device=qb.device)
+    v4, _ = to_device4(v, torch.bfloat16, "v", device=qb.device)
+    if not (q4.shape == k4.shape == v4.shape):
+        raise ValueError(f"q/k/v shapes differ: {tuple(q4.shape)}, {tuple(k4.shape)}, {tuple(v4.shape)}")
+    _check_kernel_shape(q4)
+    q4, k4, v4 = (_tma_ready(t) for t in (q4, k4, v4))
+    if check_finite:
+        for name, t in (("q", q4), ("k", k4), ("v", v4)):
+            if not bool(torch.isfinite(t).all()):
+                raise FloatingPointError(f"non-finite values in {name}")
+    return q4, k4, v4, qb
+
+
+def _tma_ready(t: torch.Tensor) -> torch.Tensor:
+    """TMA needs 16-byte aligned base and strides that are multiples of 8 elements."""
+    if t.data_ptr() % 16 or any(s % 8 for s in t.stride()[:3]):
+        return t.contiguous()
+    return t
+
+
+def _run(q4, k4, v4, bm: BlockMask, qb, counter, visit=None) -> AttentionOutput:
+    B, H, N, d = q4.shape
+    if bm.n_tokens != N:
+        raise ValueError(f"mask built for {bm.n_tokens} tokens, inputs have {N}")
+    lists = mask_lists(bm, B, H, N) if visit is None else _lists_with_order(_native_keep(bm, B, H, N), visit)
+    ctr = torch.zeros((1,), device=q4.device, dtype=torch.int64) if counter is not None else None
+    o, lse = SparseAttentionFunction.apply(q4, k4, v4, lists, 1.0 / math.sqrt(d), ctr)
+    if counter is not None:
+        counter.count += int(ctr.item())
+    return AttentionOutput(out=from_device(o, qb), lse=from_device(lse, qb, 1), mask_used=bm)
+
+
+def sparse_attention_with_mask(q, k, v, bm: BlockMask, counter: BlockCounter | None = None, _block_order=None,
+                               *, check_finite: bool = True) -> AttentionOutput:
+    """Tiled attention restricted to ``bm``'s kept blocks (attention.py:73-114).
+
+    ``out`` is differentiable w.r.t. torch inputs.  ``_block_order(i, kept)`` may permute
+    the visit order of each row (the reference's test hook); the result does not depend
+    on it beyond float rounding.  ``check_finite=False`` skips the NaN/Inf scan (and its
+    host sync) that mirrors the reference's ``ensure_finite``.
+    """
+    q4, k4, v4, qb = _prepare(q, k, v, check_finite)
+    return _run(q4, k4, v4, bm, qb, counter, _block_order)
+
+
+def _hybrid_mask_device(q4, k4, cfg: SparsityConfig, check_finite: bool) -> BlockMask:
+    probs, flag = _pooled_probs(q4, k4, cfg.b_q, cfg.b_kv, check_finite)
+    if flag is not None and int(flag.item()) != 0:
+        raise FloatingPointError("non-finite values in q or k")
+    keep, _ = _select(probs, top_k_count(cfg.k_frac, probs.shape[-1]), cfg.p_frac)
+    if q4.shape[0] == 1 and q4.shape[1] == 1:
+        keep = keep[0, 0]
+    return BlockMask._trusted(keep, cfg.b_q, cfg.b_kv, q4.shape[2])
+
+
+def sparse_attention(q, k, v, cfg: SparsityConfig, counter: BlockCounter | None = None, *,
+                     check_finite: bool = True) -> AttentionOutput:
+    """Derive the hybrid mask from the current q/k, then run the kernel (attention.py:117-125).
+    The mask is rebuilt on every call; nothing is cached across steps."""
+    q4, k4, v4, qb = _prepare(q, k, v, check_finite=False)
+    if check_finite and not bool(torch.isfinite(v4).all()):
+        raise FloatingPointError("non-finite values in v")
+    bm = _hybrid_mask_device(q4, k4, cfg, check_finite)
+    return _run(q4, k4, v4, bm, qb, counter)
+
+
+def dense_attention(q, k, v, *, check_finite: bool = True) -> AttentionOutput:
+    """Full softmax attention (attention.py:62-70), computed by the same kernels with every
+    block kept; ``mask_used`` is ``full_mask(N)`` as in the reference."""
+    q4, k4, v4, qb = _prepare(q, k, v, check_finite)
+    N = q4.shape[2]
+    res = _run(q4, k4, v4, full_mask(N), qb, None)
+    return res
+
+
+def attention_backward(q, k, v, bm: BlockMask, d_out, *, check_finite: bool = True) -> AttentionGrads:
+    """Gradients of the masked attention output with the mask held constant
+    (attention.py:128-166).  Like the reference it recomputes the forward for O and LSE."""
+    q4, k4, v4, qb = _prepare(q, k, v, check_finite)
+    do4, _ = to_device4(d_out, torch.bfloat16, "d_out", device=qb.device)
+    if do4.shape != q4.shape:
+        raise ValueError(f"d_out shape {tuple(do4.shape)} != q shape {tuple(q4.shape)}")
+    do4 = _tma_ready(do4)
+    if check_finite and not bool(torch.isfinite(do4).all()):
+        raise FloatingPointError("non-finite values in d_out")
+    B, H, N, d = q4.shape
+    if bm.n_tokens != N:
+        raise ValueError(f"mask built for {bm.n_tokens} tokens, inputs have {N}")
+    lists = mask_lists(bm, B, H, N)
+    scale = 1.0 / math.sqrt(d)
+    with torch.no_grad():
+        o, lse = fwd(q4, k4, v4, lists, scale)
+        dq, dk, dv = bwd(q4, k4, v4, o, do4, lse, lists, scale)
+    return AttentionGrads(dq=from_device(dq, qb), dk=from_device(dk, qb), dv=from_device(dv, qb))
+
+
+__all__ = [
+    "AttentionOutput", "AttentionGrads", "BlockCounter", "BlockLists", "full_mask", "dense_attention",
+    "sparse_attention", "sparse_attention_with_mask", "attention_backward", "SparseAttentionFunction",
+    "build_lists", "mask_lists",
+]

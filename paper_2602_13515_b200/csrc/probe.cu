@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(128) k_probe(const __nv_bfloat16* a, const __n
   uint8_t* sb = base + 32768;
   const int Ra = a_mn ? K : M, Ca = a_mn ? M : K;
   const int Rb = b_mn ? K : N, Cb = b_mn ? N : K;
-  if (warp_id() == 0) tmem_alloc(&tmem_base, 128);
+  if (warp_id() == 0) tmem_alloc(&tmem_base, 256);
   if (threadIdx.x == 32) {
     mbar_init(&bar_load, 1);
     mbar_init(&bar_mma, 1);
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(128) k_probe(const __nv_bfloat16* a, const __n
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = tmem_base;
-  if (use_tma) {
+  if (use_tma == 1) {
     if (threadIdx.x == 0) {
       mbar_expect_tx(&bar_load, (uint32_t)((Ra * Ca + Rb * Cb) * 2));
       for (int c = 0; c < Ca / 64; ++c) tma_load_2d(sa + c * Ra * 128, &ta, &bar_load, c * 64, 0);
@@ -61,17 +61,34 @@ __global__ void __launch_bounds__(128) k_probe(const __nv_bfloat16* a, const __n
     }
     mbar_wait(&bar_load, 0);
   } else {
-    stage_generic(sa, a, Ra, Ca);
+    if (use_tma == 2) {
+      // A -> TMEM columns [128, 128 + K/2): thread row m packs its K bf16 values in pairs
+      const int m = 32 * (int)warp_id() + (int)lane_id();
+      for (int c0 = 0; c0 < K / 2; c0 += 32) {
+        uint32_t r[32];
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(a + (int64_t)m * K) + c0;
+        for (int e = 0; e < 32; ++e) r[e] = src[e];
+        tmem_st32(tbase + ((uint32_t)(32 * warp_id()) << 16) + 128u + (uint32_t)c0, r);
+      }
+      tmem_st_wait();
+    } else {
+      stage_generic(sa, a, Ra, Ca);
+    }
     stage_generic(sb, b, Rb, Cb);
     fence_proxy_async_smem();
+    tc_fence_before();
     __syncthreads();
   }
   if (threadIdx.x == 0) {
     tc_fence_after();
     const uint32_t idesc = idesc_bf16(M, N, a_mn != 0, b_mn != 0);
     for (int ks = 0; ks < K / 16; ++ks) {
-      mma_bf16(tbase, operand_desc(smem_u32(sa), a_mn, Ra, ks), operand_desc(smem_u32(sb), b_mn, Rb, ks), idesc,
-               ks > 0 ? 1u : 0u);
+      if (use_tma == 2)
+        mma_bf16_ts(tbase, tbase + 128u + (uint32_t)(ks * 8), operand_desc(smem_u32(sb), b_mn, Rb, ks), idesc,
+                    ks > 0 ? 1u : 0u);
+      else
+        mma_bf16(tbase, operand_desc(smem_u32(sa), a_mn, Ra, ks), operand_desc(smem_u32(sb), b_mn, Rb, ks), idesc,
+                 ks > 0 ? 1u : 0u);
     }
     mma_commit(&bar_mma);
   }
@@ -90,7 +107,7 @@ __global__ void __launch_bounds__(128) k_probe(const __nv_bfloat16* a, const __n
   }
   tc_fence_before();
   __syncthreads();
-  if (warp_id() == 0) tmem_dealloc(tbase, 128);
+  if (warp_id() == 0) tmem_dealloc(tbase, 256);
 }
 
 }  // namespace
@@ -103,10 +120,12 @@ extern "C" int spa2_probe_gemm(const void* a, const void* b, float* d, int m, in
   SPA2_REQUIRE(m == 64 || m == 128, SPA2_ERR_UNSUPPORTED, "probe: m must be 64 or 128");
   SPA2_REQUIRE(n == 64 || n == 128, SPA2_ERR_UNSUPPORTED, "probe: n must be 64 or 128");
   SPA2_REQUIRE(k == 64 || k == 128, SPA2_ERR_UNSUPPORTED, "probe: k must be 64 or 128");
+  SPA2_REQUIRE(use_tma >= 0 && use_tma <= 2, SPA2_ERR_VALUE, "probe: mode must be 0, 1 or 2");
+  SPA2_REQUIRE(use_tma != 2 || (m == 128 && a_mn == 0), SPA2_ERR_UNSUPPORTED, "probe: TMEM A needs m=128, K-major");
   CUtensorMap ta, tb;
   memset(&ta, 0, sizeof(ta));
   memset(&tb, 0, sizeof(tb));
-  if (use_tma) {
+  if (use_tma == 1) {
     const int Ra = a_mn ? k : m, Ca = a_mn ? m : k;
     const int Rb = b_mn ? k : n, Cb = b_mn ? n : k;
     int rc = make_tma_bf16_2d(&ta, a, Ca, Ra, Ca, 64, Ra);
