@@ -43,7 +43,7 @@ struct FwdCfg {
   static constexpr int OFF_V = OFF_K + NS * KV_BYTES;
   static constexpr int OFF_P = OFF_V + NS * KV_BYTES;
   static constexpr int OFF_BAR = OFF_P + P_BYTES;
-  static constexpr int NUM_BARS = 1 + 4 * NS + 2 + 1 + 1;
+  static constexpr int NUM_BARS = 1 + 4 * NS + 2 + 2 + 1 + 1;
   static constexpr int SMEM_USED = OFF_BAR + NUM_BARS * 8 + 16;
   // never let a third CTA share the SM's 512 TMEM columns
   static constexpr int SMEM = SMEM_USED < 80 * 1024 ? 80 * 1024 : SMEM_USED;
@@ -76,9 +76,10 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
   uint64_t* v_full = k_empty + NS;
   uint64_t* v_empty = v_full + NS;
   uint64_t* s_full = v_empty + NS;  // [2]
-  uint64_t* p_full = s_full + 2;
-  uint64_t* o_done = p_full + 1;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_done + 1);
+  uint64_t* p_full = s_full + 2;  // [2]: softmax warps may drift by one block, so one per parity
+  uint64_t* o_done = p_full + 2;   // one completion per PV MMA group
+  uint64_t* o_final = o_done + 1;  // the last PV group (unambiguous single phase)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_final + 1);
 
   const int warp = (int)warp_id(), lane = (int)lane_id();
   const int w = p.row_order ? p.row_order[blockIdx.x] : (int)blockIdx.x;
@@ -99,8 +100,10 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
     }
     mbar_init(&s_full[0], 1);
     mbar_init(&s_full[1], 1);
-    mbar_init(p_full, 128);
+    mbar_init(&p_full[0], 128);
+    mbar_init(&p_full[1], 128);
     mbar_init(o_done, 1);
+    mbar_init(o_final, 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tmem_holder, 256);
@@ -175,7 +178,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
         if (t >= 1) {
           const int u = t - 1;
           const int s = u % NS;
-          mbar_wait(p_full, (uint32_t)u & 1u);
+          mbar_wait(&p_full[u & 1], (uint32_t)(u >> 1) & 1u);
           mbar_wait(&v_full[s], (uint32_t)(u / NS) & 1u);
           tc_fence_after();
           const uint32_t sV = smem_u32(smem + C::OFF_V + s * C::KV_BYTES);
@@ -192,6 +195,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
           }
           mma_commit(o_done);
           mma_commit(&v_empty[s]);
+          if (u == n - 1) mma_commit(o_final);
         }
       }
     }
@@ -225,8 +229,10 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
       bool waited = false;
       if (t == 0) {
         m = mx;
-      } else if (mx > m + kRescaleThreshold) {
-        const float alpha = ex2(m - mx);
+      } else if (__any_sync(0xffffffffu, mx > m + kRescaleThreshold)) {
+        // warp-uniform: tcgen05.ld/st are warp-collective (.sync.aligned)
+        const float m_new = fmaxf(m, mx);
+        const float alpha = ex2(m - m_new);
         mbar_wait(o_done, (uint32_t)(t - 1) & 1u);  // PV_{t-1} has landed in O
         waited = true;
         tc_fence_after();
@@ -240,7 +246,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
         }
         tmem_st_wait();
         l *= alpha;
-        m = mx;
+        m = m_new;
       }
       const float neg_m = -m;
       uint32_t pk[32];
@@ -266,10 +272,10 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
         fence_proxy_async_smem();
       }
       tc_fence_before();
-      mbar_arrive(p_full);
+      mbar_arrive(&p_full[t & 1]);
     }
     // ---------------- epilogue ----------------
-    mbar_wait(o_done, (uint32_t)(n - 1) & 1u);
+    mbar_wait(o_final, 0);
     tc_fence_after();
     const float inv_l = 1.f / l;
     uint8_t* sO = smem + C::OFF_Q;  // Q is dead: every MMA has completed
