@@ -12,3 +12,10 @@ int make_tma_bf16_4d(CUtensorMap* map, const void* base, const uint64_t dims[4],
 int make_tma_bf16_2d(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint64_t row_stride_elems,
                      uint32_t box_cols, uint32_t box_rows);
 }  // namespace spa2
+
+#include "../../include/spa2.h"
+namespace spa2 {
+// Map over a [B,H,N,d] bf16 view with a (64 x rows) box — the operand tiles of the
+// attention kernels (defined in fwd.cu).
+int make_qkv_map(CUtensorMap* m, const spa2_view& v, int64_t B, int64_t H, int64_t N, int64_t d, int rows);
+}  // namespace spa2
