@@ -117,6 +117,21 @@ int spa2_bwd(spa2_view q, spa2_view k, spa2_view v, spa2_view o, spa2_view dout,
              const int32_t* row_idx, const int32_t* row_order, const int32_t* col_ptr,
              const int32_t* col_idx, const int32_t* col_order, float scale, void* stream);
 
+/* The three launches spa2_bwd makes, individually (same arguments; used to time each).
+ * K5: delta = rowsum(dout ∘ o) (attention.py:149).
+ * K7: dq over the row lists (the dq term of attention.py:164).
+ * K6: dk, dv over the column lists (attention.py:162, 165). */
+int spa2_bwd_delta(spa2_view o, spa2_view dout, float* delta, int dtype, int64_t B, int64_t H,
+                   int64_t N, int64_t d, void* stream);
+int spa2_bwd_dq(spa2_view q, spa2_view k, spa2_view v, spa2_view dout, const float* lse,
+                const float* delta, spa2_view dq, int dtype, int64_t B, int64_t H, int64_t N,
+                int64_t d, int64_t b_q, int64_t b_kv, const int32_t* row_ptr, const int32_t* row_idx,
+                const int32_t* row_order, float scale, void* stream);
+int spa2_bwd_dkdv(spa2_view q, spa2_view k, spa2_view v, spa2_view dout, const float* lse,
+                  const float* delta, spa2_view dk, spa2_view dv, int dtype, int64_t B, int64_t H,
+                  int64_t N, int64_t d, int64_t b_q, int64_t b_kv, const int32_t* col_ptr,
+                  const int32_t* col_idx, const int32_t* col_order, float scale, void* stream);
+
 /* ---- diagnostics -------------------------------------------------------------------
  * tcgen05 probe (test-only): D = A·Bᵀ with logical A [m,k], B [n,k] (bf16), D fp32
  * row-major [m,n], computed by ONE tcgen05 MMA chain through exactly the shared-memory

@@ -44,6 +44,7 @@ def sparse_forward(q, k, v, keep, b_q: int, b_kv: int, visit=None):
     q, k, v = _f64(q), _f64(k), _f64(v)
     keep = np.asarray(keep, dtype=bool)
     n, d = q.shape
+    n_kv = k.shape[0]  # == n for the reference contract; bench samples pass a q slice
     scale = 1.0 / math.sqrt(d)
     out = np.empty((n, v.shape[1]))
     lse = np.empty(n)
@@ -58,7 +59,7 @@ def sparse_forward(q, k, v, keep, b_q: int, b_kv: int, visit=None):
         if visit is not None:
             cols = visit(i, cols)
         for j in cols:
-            kv = slice(j * b_kv, min((j + 1) * b_kv, n))
+            kv = slice(j * b_kv, min((j + 1) * b_kv, n_kv))
             visited += 1
             s = (qi @ k[kv].T) * scale
             m_next = np.maximum(m, s.max(axis=1))
@@ -85,6 +86,7 @@ def attention_backward(q, k, v, keep, b_q: int, b_kv: int, d_out):
     keep = np.asarray(keep, dtype=bool)
     out, lse, _ = sparse_forward(q, k, v, keep, b_q, b_kv)
     n, d = q.shape
+    n_kv = k.shape[0]
     scale = 1.0 / math.sqrt(d)
     dq = np.zeros_like(q)
     dk = np.zeros_like(k)
@@ -94,7 +96,7 @@ def attention_backward(q, k, v, keep, b_q: int, b_kv: int, d_out):
         rows = slice(i * b_q, min((i + 1) * b_q, n))
         qi, doi = q[rows], d_out[rows]
         for j in np.flatnonzero(keep[i]):
-            kv = slice(j * b_kv, min((j + 1) * b_kv, n))
+            kv = slice(j * b_kv, min((j + 1) * b_kv, n_kv))
             p = np.exp((qi @ k[kv].T) * scale - lse[rows][:, None])
             dv[kv] += p.T @ doi
             ds = p * (doi @ v[kv].T - delta[rows][:, None])

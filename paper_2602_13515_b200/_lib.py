@@ -51,8 +51,54 @@ SIGNATURES = {
                  _I32),
     "spa2_bwd": ([View, View, View, View, View, _P, _P, View, View, View, _I32, _I64, _I64, _I64, _I64, _I64, _I64,
                   _P, _P, _P, _P, _P, _P, _F32, _P], _I32),
+    "spa2_bwd_delta": ([View, View, _P, _I32, _I64, _I64, _I64, _I64, _P], _I32),
+    "spa2_bwd_dq": ([View, View, View, View, _P, _P, View, _I32, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P, _P, _F32,
+                     _P], _I32),
+    "spa2_bwd_dkdv": ([View, View, View, View, _P, _P, View, View, _I32, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P,
+                       _P, _F32, _P], _I32),
     "spa2_probe_gemm": ([_P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _P], _I32),
 }
+
+# Kernels each entry point launches (for the bench's gpu_launches accounting).
+KERNELS_PER_CALL = {"spa2_pooled_map": 3, "spa2_select": 1, "spa2_build_lists": 5, "spa2_fwd": 1,
+                    "spa2_bwd_delta": 1, "spa2_bwd_dq": 1, "spa2_bwd_dkdv": 1, "spa2_bwd": 3}
+
+
+class LaunchStats:
+    """Counts kernels launched through the hot-path entry points, and optionally times
+    chosen entry points with CUDA events on the launching stream."""
+
+    def __init__(self):
+        self.launches = 0
+        self.timing = None  # dict name -> list[(start_event, end_event)] while enabled
+
+    def begin(self, name: str, stream):
+        self.launches += KERNELS_PER_CALL.get(name, 0)
+        if self.timing is not None and name in self.timing:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(stream)
+            return ev
+        return None
+
+    def end(self, name: str, start, stream):
+        if start is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(stream)
+            self.timing[name].append((start, ev))
+
+
+STATS = LaunchStats()
+
+
+def call(name: str, *args, stream_obj=None):
+    """Invoke entry point ``name`` (its last argument is the stream handle)."""
+    start = STATS.begin(name, stream_obj) if stream_obj is not None else None
+    if stream_obj is None:
+        STATS.launches += KERNELS_PER_CALL.get(name, 0)
+    rc = getattr(load(), name)(*args)
+    if start is not None:
+        STATS.end(name, start, stream_obj)
+    check(rc, name)
 
 _lock = threading.Lock()
 _lib = None

@@ -115,11 +115,10 @@ def build_lists(keep_u8: torch.Tensor) -> BlockLists:
         col_ptr=torch.empty(bh * t_n + 1, **i32), col_idx=torch.empty(cap, **i32), col_order=torch.empty(bh * t_n, **i32),
         shape=(B, H, t_m, t_n))
     scratch = torch.empty(bh * (t_m + t_n), **i32)
-    rc = _lib.load().spa2_build_lists(
-        _lib.ptr(keep_u8), bh, t_m, t_n, _lib.ptr(lists.row_ptr), _lib.ptr(lists.row_idx), _lib.ptr(lists.col_ptr),
-        _lib.ptr(lists.col_idx), _lib.ptr(lists.row_order), _lib.ptr(lists.col_order), _lib.ptr(scratch),
-        _lib.stream_of(keep_u8))
-    _lib.check(rc, "build_lists")
+    st = torch.cuda.current_stream(dev)
+    _lib.call("spa2_build_lists", _lib.ptr(keep_u8), bh, t_m, t_n, _lib.ptr(lists.row_ptr), _lib.ptr(lists.row_idx),
+              _lib.ptr(lists.col_ptr), _lib.ptr(lists.col_idx), _lib.ptr(lists.row_order), _lib.ptr(lists.col_order),
+              _lib.ptr(scratch), st.cuda_stream, stream_obj=st)
     return lists
 
 
@@ -162,11 +161,10 @@ def fwd(q4, k4, v4, lists: BlockLists, scale: float, counter: torch.Tensor | Non
     B, H, N, d = q4.shape
     o = torch.empty((B, H, N, d), device=q4.device, dtype=q4.dtype)
     lse = torch.empty((B, H, N), device=q4.device, dtype=torch.float32)
-    rc = _lib.load().spa2_fwd(
-        _lib.view4(q4), _lib.view4(k4), _lib.view4(v4), _lib.view4(o), _lib.ptr(lse), _lib.DTYPE_CODES[q4.dtype],
-        B, H, N, d, BQ, BKV, _lib.ptr(lists.row_ptr), _lib.ptr(lists.row_idx), _lib.ptr(lists.row_order), scale,
-        _lib.ptr(counter), _lib.stream_of(q4))
-    _lib.check(rc, "sparse attention forward")
+    st = torch.cuda.current_stream(q4.device)
+    _lib.call("spa2_fwd", _lib.view4(q4), _lib.view4(k4), _lib.view4(v4), _lib.view4(o), _lib.ptr(lse),
+              _lib.DTYPE_CODES[q4.dtype], B, H, N, d, BQ, BKV, _lib.ptr(lists.row_ptr), _lib.ptr(lists.row_idx),
+              _lib.ptr(lists.row_order), scale, _lib.ptr(counter), st.cuda_stream, stream_obj=st)
     return o, lse
 
 
@@ -177,12 +175,16 @@ def bwd(q4, k4, v4, o4, do4, lse, lists: BlockLists, scale: float):
     dk = torch.empty_like(dq)
     dv = torch.empty_like(dq)
     delta = torch.empty((B, H, N), device=q4.device, dtype=torch.float32)
-    rc = _lib.load().spa2_bwd(
-        _lib.view4(q4), _lib.view4(k4), _lib.view4(v4), _lib.view4(o4), _lib.view4(do4), _lib.ptr(lse),
-        _lib.ptr(delta), _lib.view4(dq), _lib.view4(dk), _lib.view4(dv), _lib.DTYPE_CODES[q4.dtype], B, H, N, d, BQ,
-        BKV, _lib.ptr(lists.row_ptr), _lib.ptr(lists.row_idx), _lib.ptr(lists.row_order), _lib.ptr(lists.col_ptr),
-        _lib.ptr(lists.col_idx), _lib.ptr(lists.col_order), scale, _lib.stream_of(q4))
-    _lib.check(rc, "sparse attention backward")
+    st = torch.cuda.current_stream(q4.device)
+    dt = _lib.DTYPE_CODES[q4.dtype]
+    _lib.call("spa2_bwd_delta", _lib.view4(o4), _lib.view4(do4), _lib.ptr(delta), dt, B, H, N, d, st.cuda_stream,
+              stream_obj=st)
+    _lib.call("spa2_bwd_dq", _lib.view4(q4), _lib.view4(k4), _lib.view4(v4), _lib.view4(do4), _lib.ptr(lse),
+              _lib.ptr(delta), _lib.view4(dq), dt, B, H, N, d, BQ, BKV, _lib.ptr(lists.row_ptr),
+              _lib.ptr(lists.row_idx), _lib.ptr(lists.row_order), scale, st.cuda_stream, stream_obj=st)
+    _lib.call("spa2_bwd_dkdv", _lib.view4(q4), _lib.view4(k4), _lib.view4(v4), _lib.view4(do4), _lib.ptr(lse),
+              _lib.ptr(delta), _lib.view4(dk), _lib.view4(dv), dt, B, H, N, d, BQ, BKV, _lib.ptr(lists.col_ptr),
+              _lib.ptr(lists.col_idx), _lib.ptr(lists.col_order), scale, st.cuda_stream, stream_obj=st)
     return dq, dk, dv
 
 

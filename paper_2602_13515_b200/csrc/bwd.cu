@@ -546,28 +546,25 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tmem_dealloc(tbase, 512);
 }
 
+struct BwdMaps {
+  CUtensorMap q, k, v, dout, out0, out1;
+};
+
+// which: 0 = dq kernel (out0 = dq), 1 = dk/dv kernel (out0 = dk, out1 = dv)
 template <int HD>
-int launch_bwd(const spa2_view& q, const spa2_view& k, const spa2_view& v, const spa2_view& o, const spa2_view& dout,
-               const float* lse, float* delta, const spa2_view& dq, const spa2_view& dk, const spa2_view& dv,
-               int64_t B, int64_t H, int64_t N, const int32_t* row_ptr, const int32_t* row_idx,
-               const int32_t* row_order, const int32_t* col_ptr, const int32_t* col_idx, const int32_t* col_order,
-               float scale, cudaStream_t st) {
+int launch_attn_bwd(int which, const spa2_view& q, const spa2_view& k, const spa2_view& v, const spa2_view& dout,
+                    const float* lse, const float* delta, const spa2_view& out0, const spa2_view* out1, int64_t B,
+                    int64_t H, int64_t N, const int32_t* ptr, const int32_t* idx, const int32_t* order, float scale,
+                    cudaStream_t st) {
   const int64_t T_m = ceil_div(N, BQ), T_n = ceil_div(N, BKV);
-  CUtensorMap tq, tk, tv, tdo, tdq, tdk, tdv;
+  BwdMaps m;
   int rc;
-  if ((rc = make_qkv_map(&tq, q, B, H, N, HD, BQ))) return rc;
-  if ((rc = make_qkv_map(&tdo, dout, B, H, N, HD, BQ))) return rc;
-  if ((rc = make_qkv_map(&tk, k, B, H, N, HD, BKV))) return rc;
-  if ((rc = make_qkv_map(&tv, v, B, H, N, HD, BKV))) return rc;
-  if ((rc = make_qkv_map(&tdq, dq, B, H, N, HD, BQ))) return rc;
-  if ((rc = make_qkv_map(&tdk, dk, B, H, N, HD, BKV))) return rc;
-  if ((rc = make_qkv_map(&tdv, dv, B, H, N, HD, BKV))) return rc;
-
-  const int64_t rows = B * H * N;
-  constexpr int RPC = 256 / (HD / 8);
-  k_delta<HD><<<(unsigned)ceil_div(rows, RPC), 256, 0, st>>>(o, dout, delta, (int)H, (int)N, rows);
-  SPA2_LAUNCH_CHECK();
-
+  if ((rc = make_qkv_map(&m.q, q, B, H, N, HD, BQ))) return rc;
+  if ((rc = make_qkv_map(&m.dout, dout, B, H, N, HD, BQ))) return rc;
+  if ((rc = make_qkv_map(&m.k, k, B, H, N, HD, BKV))) return rc;
+  if ((rc = make_qkv_map(&m.v, v, B, H, N, HD, BKV))) return rc;
+  if ((rc = make_qkv_map(&m.out0, out0, B, H, N, HD, which == 0 ? BQ : BKV))) return rc;
+  if (which == 1 && (rc = make_qkv_map(&m.out1, *out1, B, H, N, HD, BKV))) return rc;
   BwdParams prm{};
   prm.H = (int)H;
   prm.N = (int)N;
@@ -577,32 +574,38 @@ int launch_bwd(const spa2_view& q, const spa2_view& k, const spa2_view& v, const
   prm.delta = delta;
   prm.scale = scale;
   prm.sl2 = scale * kLog2e;
-
-  prm.ptr = row_ptr;
-  prm.idx = row_idx;
-  prm.order = row_order;
-  prm.out0 = (__nv_bfloat16*)dq.ptr;
-  prm.o0_sb = dq.sb, prm.o0_sh = dq.sh, prm.o0_sn = dq.sn;
-  {
+  prm.ptr = ptr;
+  prm.idx = idx;
+  prm.order = order;
+  prm.out0 = (__nv_bfloat16*)out0.ptr;
+  prm.o0_sb = out0.sb, prm.o0_sh = out0.sh, prm.o0_sn = out0.sn;
+  if (which == 0) {
     auto kern = k_dq<HD>;
     SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DqCfg<HD>::SMEM));
-    kern<<<(unsigned)(B * H * T_m), kThreads, DqCfg<HD>::SMEM, st>>>(tq, tk, tv, tdo, tdq, prm);
-    SPA2_LAUNCH_CHECK();
-  }
-  prm.ptr = col_ptr;
-  prm.idx = col_idx;
-  prm.order = col_order;
-  prm.out0 = (__nv_bfloat16*)dk.ptr;
-  prm.o0_sb = dk.sb, prm.o0_sh = dk.sh, prm.o0_sn = dk.sn;
-  prm.out1 = (__nv_bfloat16*)dv.ptr;
-  prm.o1_sb = dv.sb, prm.o1_sh = dv.sh, prm.o1_sn = dv.sn;
-  {
+    kern<<<(unsigned)(B * H * T_m), kThreads, DqCfg<HD>::SMEM, st>>>(m.q, m.k, m.v, m.dout, m.out0, prm);
+  } else {
+    prm.out1 = (__nv_bfloat16*)out1->ptr;
+    prm.o1_sb = out1->sb, prm.o1_sh = out1->sh, prm.o1_sn = out1->sn;
     auto kern = k_dkdv<HD>;
     SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvCfg<HD>::SMEM));
-    kern<<<(unsigned)(B * H * T_n), kThreads, DkvCfg<HD>::SMEM, st>>>(tq, tk, tv, tdo, tdk, tdv, prm);
-    SPA2_LAUNCH_CHECK();
+    kern<<<(unsigned)(B * H * T_n), kThreads, DkvCfg<HD>::SMEM, st>>>(m.q, m.k, m.v, m.dout, m.out0, m.out1, prm);
   }
+  SPA2_LAUNCH_CHECK();
   return SPA2_OK;
+}
+
+int check_bwd_args(int dtype, int64_t B, int64_t H, int64_t N, int64_t d, int64_t b_q, int64_t b_kv) {
+  SPA2_REQUIRE(dtype == SPA2_BF16, SPA2_ERR_UNSUPPORTED, "bwd: only bf16 operands are supported");
+  SPA2_REQUIRE(d == 64 || d == 128, SPA2_ERR_UNSUPPORTED, "bwd: head dim %lld not in {64, 128}", (long long)d);
+  SPA2_REQUIRE(b_q == BQ && b_kv == BKV, SPA2_ERR_UNSUPPORTED, "bwd: block sizes (%lld, %lld) != (128, 64)",
+               (long long)b_q, (long long)b_kv);
+  SPA2_REQUIRE(B >= 1 && H >= 1 && N >= 1, SPA2_ERR_VALUE, "bwd: empty problem");
+  SPA2_REQUIRE(N < (1ll << 31) && B * H * ceil_div(N, BKV) < (1ll << 31), SPA2_ERR_UNSUPPORTED, "bwd: too large");
+  return SPA2_OK;
+}
+
+bool al16(const spa2_view& x) {
+  return ((uintptr_t)x.ptr % 16 == 0) && x.sb % 8 == 0 && x.sh % 8 == 0 && x.sn % 8 == 0;
 }
 
 }  // namespace
@@ -610,28 +613,63 @@ int launch_bwd(const spa2_view& q, const spa2_view& k, const spa2_view& v, const
 
 using namespace spa2;
 
+extern "C" int spa2_bwd_delta(spa2_view o, spa2_view dout, float* delta, int dtype, int64_t B, int64_t H,
+                              int64_t N, int64_t d, void* stream) {
+  int rc;
+  if ((rc = check_bwd_args(dtype, B, H, N, d, BQ, BKV))) return rc;
+  SPA2_REQUIRE(o.ptr && dout.ptr && delta, SPA2_ERR_VALUE, "bwd_delta: null pointer");
+  SPA2_REQUIRE(al16(o) && al16(dout), SPA2_ERR_UNSUPPORTED, "bwd_delta: o/dout must be 16-byte aligned, strides % 8");
+  const int64_t rows = B * H * N;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (d == 128)
+    k_delta<128><<<(unsigned)ceil_div(rows, 16), 256, 0, st>>>(o, dout, delta, (int)H, (int)N, rows);
+  else
+    k_delta<64><<<(unsigned)ceil_div(rows, 32), 256, 0, st>>>(o, dout, delta, (int)H, (int)N, rows);
+  SPA2_LAUNCH_CHECK();
+  return SPA2_OK;
+}
+
+extern "C" int spa2_bwd_dq(spa2_view q, spa2_view k, spa2_view v, spa2_view dout, const float* lse, const float* delta,
+                           spa2_view dq, int dtype, int64_t B, int64_t H, int64_t N, int64_t d, int64_t b_q,
+                           int64_t b_kv, const int32_t* row_ptr, const int32_t* row_idx, const int32_t* row_order,
+                           float scale, void* stream) {
+  int rc;
+  if ((rc = check_bwd_args(dtype, B, H, N, d, b_q, b_kv))) return rc;
+  SPA2_REQUIRE(q.ptr && k.ptr && v.ptr && dout.ptr && lse && delta && dq.ptr && row_ptr && row_idx, SPA2_ERR_VALUE,
+               "bwd_dq: null pointer");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (d == 128)
+    return launch_attn_bwd<128>(0, q, k, v, dout, lse, delta, dq, nullptr, B, H, N, row_ptr, row_idx, row_order,
+                                scale, st);
+  return launch_attn_bwd<64>(0, q, k, v, dout, lse, delta, dq, nullptr, B, H, N, row_ptr, row_idx, row_order, scale,
+                             st);
+}
+
+extern "C" int spa2_bwd_dkdv(spa2_view q, spa2_view k, spa2_view v, spa2_view dout, const float* lse,
+                             const float* delta, spa2_view dk, spa2_view dv, int dtype, int64_t B, int64_t H,
+                             int64_t N, int64_t d, int64_t b_q, int64_t b_kv, const int32_t* col_ptr,
+                             const int32_t* col_idx, const int32_t* col_order, float scale, void* stream) {
+  int rc;
+  if ((rc = check_bwd_args(dtype, B, H, N, d, b_q, b_kv))) return rc;
+  SPA2_REQUIRE(q.ptr && k.ptr && v.ptr && dout.ptr && lse && delta && dk.ptr && dv.ptr && col_ptr && col_idx,
+               SPA2_ERR_VALUE, "bwd_dkdv: null pointer");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (d == 128)
+    return launch_attn_bwd<128>(1, q, k, v, dout, lse, delta, dk, &dv, B, H, N, col_ptr, col_idx, col_order, scale,
+                                st);
+  return launch_attn_bwd<64>(1, q, k, v, dout, lse, delta, dk, &dv, B, H, N, col_ptr, col_idx, col_order, scale, st);
+}
+
 extern "C" int spa2_bwd(spa2_view q, spa2_view k, spa2_view v, spa2_view o, spa2_view dout, const float* lse,
                         float* delta, spa2_view dq, spa2_view dk, spa2_view dv, int dtype, int64_t B, int64_t H,
                         int64_t N, int64_t d, int64_t b_q, int64_t b_kv, const int32_t* row_ptr,
                         const int32_t* row_idx, const int32_t* row_order, const int32_t* col_ptr,
                         const int32_t* col_idx, const int32_t* col_order, float scale, void* stream) {
-  SPA2_REQUIRE(dtype == SPA2_BF16, SPA2_ERR_UNSUPPORTED, "bwd: only bf16 operands are supported");
-  SPA2_REQUIRE(d == 64 || d == 128, SPA2_ERR_UNSUPPORTED, "bwd: head dim %lld not in {64, 128}", (long long)d);
-  SPA2_REQUIRE(b_q == BQ && b_kv == BKV, SPA2_ERR_UNSUPPORTED, "bwd: block sizes (%lld, %lld) != (128, 64)",
-               (long long)b_q, (long long)b_kv);
-  SPA2_REQUIRE(B >= 1 && H >= 1 && N >= 1, SPA2_ERR_VALUE, "bwd: empty problem");
-  SPA2_REQUIRE(N < (1ll << 31) && B * H * ceil_div(N, BKV) < (1ll << 31), SPA2_ERR_UNSUPPORTED, "bwd: too large");
-  SPA2_REQUIRE(q.ptr && k.ptr && v.ptr && o.ptr && dout.ptr && lse && delta && dq.ptr && dk.ptr && dv.ptr && row_ptr &&
-                   row_idx && col_ptr && col_idx,
-               SPA2_ERR_VALUE, "bwd: null pointer");
-  auto al16 = [](const spa2_view& x) {
-    return ((uintptr_t)x.ptr % 16 == 0) && x.sb % 8 == 0 && x.sh % 8 == 0 && x.sn % 8 == 0;
-  };
-  SPA2_REQUIRE(al16(o) && al16(dout), SPA2_ERR_UNSUPPORTED, "bwd: o/dout must be 16-byte aligned with strides % 8");
-  cudaStream_t st = (cudaStream_t)stream;
-  if (d == 128)
-    return launch_bwd<128>(q, k, v, o, dout, lse, delta, dq, dk, dv, B, H, N, row_ptr, row_idx, row_order, col_ptr,
-                           col_idx, col_order, scale, st);
-  return launch_bwd<64>(q, k, v, o, dout, lse, delta, dq, dk, dv, B, H, N, row_ptr, row_idx, row_order, col_ptr,
-                        col_idx, col_order, scale, st);
+  int rc;
+  if ((rc = spa2_bwd_delta(o, dout, delta, dtype, B, H, N, d, stream))) return rc;
+  if ((rc = spa2_bwd_dq(q, k, v, dout, lse, delta, dq, dtype, B, H, N, d, b_q, b_kv, row_ptr, row_idx, row_order,
+                        scale, stream)))
+    return rc;
+  return spa2_bwd_dkdv(q, k, v, dout, lse, delta, dk, dv, dtype, B, H, N, d, b_q, b_kv, col_ptr, col_idx, col_order,
+                       scale, stream);
 }

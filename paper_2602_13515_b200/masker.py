@@ -166,10 +166,9 @@ def _pooled_probs(qt: torch.Tensor, kt: torch.Tensor, b_q: int, b_kv: int, check
     probs = torch.empty((B, H, t_m, t_n), device=qt.device, dtype=torch.float64)
     work = torch.empty((B * H * (t_m + t_n) * d,), device=qt.device, dtype=torch.float64)
     flag = torch.zeros((1,), device=qt.device, dtype=torch.int32) if check_finite else None
-    lib = _lib.load()
-    rc = lib.spa2_pooled_map(_lib.view4(qt), _lib.view4(kt), _lib.DTYPE_CODES[qt.dtype], B, H, N, d, b_q, b_kv,
-                             _lib.ptr(probs), _lib.ptr(work), _lib.ptr(flag), _lib.stream_of(qt))
-    _lib.check(rc, "pooled_map")
+    st = torch.cuda.current_stream(qt.device)
+    _lib.call("spa2_pooled_map", _lib.view4(qt), _lib.view4(kt), _lib.DTYPE_CODES[qt.dtype], B, H, N, d, b_q, b_kv,
+              _lib.ptr(probs), _lib.ptr(work), _lib.ptr(flag), st.cuda_stream, stream_obj=st)
     return probs, flag
 
 
@@ -188,9 +187,9 @@ def _select(probs: torch.Tensor, k_count: int, p_frac: float | None) -> tuple[to
     keep = torch.empty(probs.shape, device=probs.device, dtype=torch.bool)
     counts = torch.empty(probs.shape[:-1], device=probs.device, dtype=torch.int32)
     thr = (p_frac - P_SLACK) if p_frac is not None else -math.inf
-    rc = _lib.load().spa2_select(_lib.ptr(probs), rows, t_n, k_count, thr, _lib.ptr(keep), _lib.ptr(counts),
-                                 _lib.stream_of(probs))
-    _lib.check(rc, "select")
+    st = torch.cuda.current_stream(probs.device)
+    _lib.call("spa2_select", _lib.ptr(probs), rows, t_n, k_count, thr, _lib.ptr(keep), _lib.ptr(counts),
+              st.cuda_stream, stream_obj=st)
     return keep, counts
 
 
