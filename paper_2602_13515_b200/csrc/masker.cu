@@ -57,18 +57,34 @@ __global__ void __launch_bounds__(kPoolThreads) k_pool(spa2_view q, spa2_view k,
   for (int e = 0; e < CPT; ++e) acc[e] = 0.0;
   bool bad = false;
   if (r < R) {
-    for (int row = r; row < rows; row += R) {
-      const T* p = base + (int64_t)row * vw.sn + cg * CPT;
-      if constexpr (VEC) {
-        T vals[CPT];
-        *reinterpret_cast<uint4*>(vals) = *reinterpret_cast<const uint4*>(p);
+    if constexpr (VEC) {
+      // issue up to 8 independent 16-byte loads before consuming any (memory-level parallelism)
+      constexpr int U = 8;
+      for (int row0 = r; row0 < rows; row0 += R * U) {
+        uint4 buf[U];
 #pragma unroll
-        for (int e = 0; e < CPT; ++e) {
-          double x = to_f64<T>(vals[e]);
-          bad |= !isfinite(x);
-          acc[e] += x;
+        for (int u = 0; u < U; ++u) {
+          const int row = row0 + u * R;
+          if (row < rows)
+            buf[u] = __ldg(reinterpret_cast<const uint4*>(base + (int64_t)row * vw.sn + cg * CPT));
         }
-      } else {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (row0 + u * R < rows) {
+            const T* vals = reinterpret_cast<const T*>(&buf[u]);
+#pragma unroll
+            for (int e = 0; e < CPT; ++e) {
+              double x = to_f64<T>(vals[e]);
+              bad |= !isfinite(x);
+              acc[e] += x;
+            }
+          }
+        }
+      }
+    }
+    for (int row = r; !VEC && row < rows; row += R) {
+      const T* p = base + (int64_t)row * vw.sn + cg * CPT;
+      {
         double x = to_f64<T>(p[0]);
         bad |= !isfinite(x);
         acc[0] += x;
@@ -87,53 +103,52 @@ __global__ void __launch_bounds__(kPoolThreads) k_pool(spa2_view q, spa2_view k,
 }
 
 // ---------------------------------------------------------------------------------------
-// K1b: scores S = Q̄ K̄ᵀ / √d in float64 (written into `probs`), 32x64 tiles, k-chunks of 16.
-// ---------------------------------------------------------------------------------------
-constexpr int kSTI = 32, kSTJ = 64, kSTK = 16;
+// K1b: scores S = Q̄ K̄ᵀ / √d in float64 (written into `probs`).  64x64 output tiles, 256
+// threads x (4x4) register blocking, k-chunks of 8 staged transposed in shared memory.
+constexpr int kSTI = 64, kSTJ = 64, kSTK = 8, kSTP = kSTI + 2;
 
 __global__ void __launch_bounds__(256) k_scores(const double* __restrict__ qbar,
                                                 const double* __restrict__ kbar, int T_m, int T_n,
                                                 int d, double sqrt_d, double* __restrict__ s_out) {
-  __shared__ double sq[kSTK][kSTI + 1];
-  __shared__ double sk[kSTK][kSTJ + 1];
+  __shared__ __align__(16) double sq[kSTK][kSTP];
+  __shared__ __align__(16) double sk[kSTK][kSTP];
   const int64_t bh = blockIdx.z;
   const int i0 = blockIdx.y * kSTI, j0 = blockIdx.x * kSTJ;
   const double* qb = qbar + bh * (int64_t)T_m * d;
   const double* kb = kbar + bh * (int64_t)T_n * d;
-  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;  // 16 x 16 threads; 2 rows x 4 cols each
-  double acc[2][4] = {};
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;  // 4 rows (ty) x 4 cols (tx) each
+  double acc[4][4] = {};
   for (int c0 = 0; c0 < d; c0 += kSTK) {
     for (int e = threadIdx.x; e < kSTI * kSTK; e += 256) {
-      int ii = e / kSTK, cc = e % kSTK;
-      int i = i0 + ii, c = c0 + cc;
+      const int ii = e / kSTK, cc = e % kSTK;
+      const int i = i0 + ii, j = j0 + ii, c = c0 + cc;
       sq[cc][ii] = (i < T_m && c < d) ? qb[(int64_t)i * d + c] : 0.0;
-    }
-    for (int e = threadIdx.x; e < kSTJ * kSTK; e += 256) {
-      int jj = e / kSTK, cc = e % kSTK;
-      int j = j0 + jj, c = c0 + cc;
-      sk[cc][jj] = (j < T_n && c < d) ? kb[(int64_t)j * d + c] : 0.0;
+      sk[cc][ii] = (j < T_n && c < d) ? kb[(int64_t)j * d + c] : 0.0;
     }
     __syncthreads();
 #pragma unroll
     for (int cc = 0; cc < kSTK; ++cc) {
-      double a0 = sq[cc][ty * 2], a1 = sq[cc][ty * 2 + 1];
+      const double2 a01 = *reinterpret_cast<const double2*>(&sq[cc][4 * ty]);
+      const double2 a23 = *reinterpret_cast<const double2*>(&sq[cc][4 * ty + 2]);
+      const double2 b01 = *reinterpret_cast<const double2*>(&sk[cc][4 * tx]);
+      const double2 b23 = *reinterpret_cast<const double2*>(&sk[cc][4 * tx + 2]);
+      const double a[4] = {a01.x, a01.y, a23.x, a23.y};
+      const double b[4] = {b01.x, b01.y, b23.x, b23.y};
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        double bv = sk[cc][tx * 4 + u];
-        acc[0][u] = fma(a0, bv, acc[0][u]);
-        acc[1][u] = fma(a1, bv, acc[1][u]);
-      }
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[x][y] = fma(a[x], b[y], acc[x][y]);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int a = 0; a < 2; ++a) {
-    int i = i0 + ty * 2 + a;
+  for (int x = 0; x < 4; ++x) {
+    const int i = i0 + 4 * ty + x;
     if (i >= T_m) continue;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      int j = j0 + tx * 4 + u;
-      if (j < T_n) s_out[(bh * T_m + i) * (int64_t)T_n + j] = acc[a][u] / sqrt_d;
+    for (int y = 0; y < 4; ++y) {
+      const int j = j0 + 4 * tx + y;
+      if (j < T_n) s_out[(bh * T_m + i) * (int64_t)T_n + j] = acc[x][y] / sqrt_d;
     }
   }
 }
@@ -305,9 +320,12 @@ __device__ void cta_exclusive_scan(const int32_t* in, int32_t* out, int64_t n, i
   __syncthreads();
 }
 
-// Longest-first order: counting sort of ids by descending count (counts in [0, maxc]).
+// Longest-first order: counting sort of ids base..base+n-1 by descending count (counts in
+// [0, maxc]); ids are written to order[base ...].
 __device__ void cta_order_desc(const int32_t* cnt, int64_t n, int maxc, int32_t* order,
-                               int32_t* bins, int32_t* sh) {
+                               int32_t* bins, int32_t* sh, int64_t base) {
+  cnt += base;
+  order += base;
   for (int c = threadIdx.x; c <= maxc; c += kScanThreads) bins[c] = 0;
   __syncthreads();
   for (int64_t i = threadIdx.x; i < n; i += kScanThreads) atomicAdd(&bins[maxc - cnt[i]], 1);
@@ -335,23 +353,32 @@ __device__ void cta_order_desc(const int32_t* cnt, int64_t n, int maxc, int32_t*
   __syncthreads();
   for (int64_t i = threadIdx.x; i < n; i += kScanThreads) {
     int pos = atomicAdd(&bins[maxc - cnt[i]], 1);
-    order[pos] = (int32_t)i;
+    order[pos] = (int32_t)(base + i);
   }
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kScanThreads) k_scan_orders(const int32_t* __restrict__ row_cnt,
-                                                              const int32_t* __restrict__ col_cnt,
-                                                              int64_t nrows, int64_t ncols, int T_m,
-                                                              int T_n, int32_t* row_ptr,
-                                                              int32_t* col_ptr, int32_t* row_order,
-                                                              int32_t* col_order) {
-  extern __shared__ int32_t sh_scan[];  // [kScanThreads] + bins[max(T_m,T_n)+1]
-  int32_t* bins = sh_scan + kScanThreads;
+__global__ void __launch_bounds__(kScanThreads) k_scan(const int32_t* __restrict__ row_cnt,
+                                                       const int32_t* __restrict__ col_cnt, int64_t nrows,
+                                                       int64_t ncols, int32_t* row_ptr, int32_t* col_ptr) {
+  __shared__ int32_t sh_scan[kScanThreads];
   cta_exclusive_scan(row_cnt, row_ptr, nrows, sh_scan);
   cta_exclusive_scan(col_cnt, col_ptr, ncols, sh_scan);
-  cta_order_desc(row_cnt, nrows, T_n, row_order, bins, sh_scan);
-  cta_order_desc(col_cnt, ncols, T_m, col_order, bins, sh_scan);
+}
+
+// Launch orders: head-major (so one or two heads' K/V or Q/dO stay resident in the 126 MB
+// L2 while their blocks are processed) and longest-first within each head (load balance).
+// blockIdx.x = (b, h); blockIdx.y = 0 rows, 1 columns.
+__global__ void __launch_bounds__(kScanThreads) k_orders(const int32_t* __restrict__ row_cnt,
+                                                         const int32_t* __restrict__ col_cnt, int T_m, int T_n,
+                                                         int32_t* row_order, int32_t* col_order) {
+  extern __shared__ int32_t sh_ord[];  // [kScanThreads] + bins[max(T_m,T_n)+1]
+  int32_t* bins = sh_ord + kScanThreads;
+  const int64_t bh = blockIdx.x;
+  if (blockIdx.y == 0)
+    cta_order_desc(row_cnt, T_m, T_n, row_order, bins, sh_ord, bh * T_m);
+  else
+    cta_order_desc(col_cnt, T_n, T_m, col_order, bins, sh_ord, bh * T_n);
 }
 
 __global__ void k_fill_rows(const uint8_t* __restrict__ keep, int64_t nrows, int T_n,
@@ -500,11 +527,13 @@ extern "C" int spa2_build_lists(const uint8_t* keep, int64_t bh, int64_t t_m, in
   SPA2_LAUNCH_CHECK();
   k_col_counts<<<(unsigned)ceil_div(ncols, 256), 256, 0, st>>>(keep, bh, (int)t_m, (int)t_n, col_cnt);
   SPA2_LAUNCH_CHECK();
+  k_scan<<<1, kScanThreads, 0, st>>>(row_cnt, col_cnt, nrows, ncols, row_ptr, col_ptr);
+  SPA2_LAUNCH_CHECK();
   const size_t smem = (kScanThreads + std::max(t_m, t_n) + 1) * sizeof(int32_t);
   if (smem > 48 * 1024)
-    SPA2_CUDA_TRY(cudaFuncSetAttribute(k_scan_orders, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_scan_orders<<<1, kScanThreads, smem, st>>>(row_cnt, col_cnt, nrows, ncols, (int)t_m, (int)t_n,
-                                               row_ptr, col_ptr, row_order, col_order);
+    SPA2_CUDA_TRY(cudaFuncSetAttribute(k_orders, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_orders<<<dim3((unsigned)bh, 2), kScanThreads, smem, st>>>(row_cnt, col_cnt, (int)t_m, (int)t_n, row_order,
+                                                               col_order);
   SPA2_LAUNCH_CHECK();
   k_fill_rows<<<(unsigned)ceil_div(nrows, 8), 256, 0, st>>>(keep, nrows, (int)t_n, row_ptr, row_idx);
   SPA2_LAUNCH_CHECK();

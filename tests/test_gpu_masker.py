@@ -198,8 +198,12 @@ def test_build_lists(bh, t_m, t_n, density):
     for c in range(bh * t_n):
         assert np.array_equal(col_idx[col_ptr[c]:col_ptr[c + 1]], np.flatnonzero(cols[c]))
     rc, cc = np.diff(row_ptr), np.diff(col_ptr)
-    assert sorted(row_order.tolist()) == list(range(bh * t_m)) and np.all(np.diff(rc[row_order]) <= 0)
-    assert sorted(col_order.tolist()) == list(range(bh * t_n)) and np.all(np.diff(cc[col_order]) <= 0)
+    # launch orders: head-major (L2 residency), longest-first inside each head
+    for order, cnt, per in ((row_order, rc, t_m), (col_order, cc, t_n)):
+        assert sorted(order.tolist()) == list(range(bh * per))
+        for h in range(bh):
+            seg = order[h * per:(h + 1) * per]
+            assert np.all(seg // per == h) and np.all(np.diff(cnt[seg]) <= 0)
 
 
 def test_public_names():
