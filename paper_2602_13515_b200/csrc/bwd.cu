@@ -4,19 +4,27 @@
 // (i, j) pairs row-major and accumulates into dq/dk/dv; here every accumulator lives in
 // TMEM of exactly one CTA, so the result is deterministic and needs no atomics:
 //   K5  δ_i = rowsum(dO ∘ O)                                          (attention.py:149)
-//   K7  one CTA per query block i, over its row list j:
+//   K7  work item = query block i, tiles = its row list j:
 //         S = Q_i K_jᵀ, dP = dO_i V_jᵀ  ->  dS = P ∘ (dP − δ), P = exp2(S·c − LSE·log2e)
 //         dQ_i += dS K_j                   (dS packed bf16 into TMEM = TS-MMA A operand)
-//   K6  one CTA per key block j, over the transposed (column) list i:
+//   K6  work item = key block j, tiles = its column list i:
 //         same S, dP, P, dS (written bf16 into swizzled smem), then with the accumulators
 //         kept TRANSPOSED so every MMA has M = 128:
 //         dVᵀ += dO_iᵀ P    (M = d, N = 64, K = 128; both operands MN-major in smem)
 //         dKᵀ += Q_iᵀ dS
+// Both kernels are persistent (one CTA per SM walking a head-major, longest-first work
+// list) and warp-specialised with 10 warps:
+//   warp 0 TMA producer (runs ahead across work items), warp 1 tcgen05.mma issuer (issues
+//   S/dP of tile g before the accumulate MMAs of tile g-1, also across items), warps 2-5
+//   elementwise (one TMEM lane = one row per thread), warps 6-9 epilogue (TMEM -> smem ->
+//   TMA store) overlapping the next item.  TMEM: S[2] | dP[2] | accumulator[2] = 512 cols.
 // The query-block-major and key-block-major passes both recompute S and dP (7 MMAs per
 // kept tile instead of 5) in exchange for zero global reductions.
 // Key blocks no query keeps get exact zeros (attention.py:152-157: dropped blocks
-// contribute nothing).
+// contribute nothing); so do query blocks with empty lists.
 #include <math.h>
+
+#include <algorithm>
 
 #include "common.cuh"
 #include "ptx.cuh"
@@ -29,23 +37,39 @@ using namespace ptx;
 
 constexpr int BQ = 128;
 constexpr int BKV = 64;
-constexpr int kThreads = 192;
+constexpr int kThreads = 320;  // 10 warps
+constexpr int kEpiTid0 = 192;  // first epilogue thread (warp 6)
 constexpr float kLog2e = 1.4426950408889634f;
 
 struct BwdParams {
   int H, N, T_m, T_n;
+  int num_items;
   const int32_t* ptr;    // row_ptr (dq) / col_ptr (dkdv)
   const int32_t* idx;    // row_idx / col_idx
-  const int32_t* order;  // longest-first launch order
+  const int32_t* order;  // head-major, longest-first work order
   const float* lse;      // natural log, [B*H, N]
   const float* delta;    // [B*H, N]
   float scale;           // 1/sqrt(d)
   float sl2;             // scale * log2(e)
-  __nv_bfloat16* out0;   // dq (K7) / dk (K6), used for empty lists
+  __nv_bfloat16* out0;   // dq (K7) / dk (K6), for empty lists
   int64_t o0_sb, o0_sh, o0_sn;
   __nv_bfloat16* out1;   // dv (K6)
   int64_t o1_sb, o1_sh, o1_sn;
 };
+
+struct Item {
+  int bh, blk, beg, n;
+};
+
+__device__ __forceinline__ Item get_item(const BwdParams& p, int wi, int nblk) {
+  const int w = p.order ? p.order[wi] : wi;
+  Item m;
+  m.bh = w / nblk;
+  m.blk = w % nblk;
+  m.beg = p.ptr[w];
+  m.n = p.ptr[w + 1] - m.beg;
+  return m;
+}
 
 // ---------------------------------------------------------------------------------------
 // K5: δ = rowsum(dO ∘ O) in fp32.  HD/8 threads per row, 16-byte loads.
@@ -82,21 +106,20 @@ __global__ void __launch_bounds__(256) k_delta(spa2_view o, spa2_view dout, floa
 }
 
 // ---------------------------------------------------------------------------------------
-// K7: dQ, one CTA per query block.
+// K7: dQ.  Work item = query block; tiles = kept key blocks.
 // ---------------------------------------------------------------------------------------
 template <int HD>
 struct DqCfg {
   static constexpr int NSK = 3, NSV = 2;
   static constexpr int Q_BYTES = BQ * HD * 2;
   static constexpr int KV_BYTES = BKV * HD * 2;
-  static constexpr int OFF_Q = 0;
-  static constexpr int OFF_DO = Q_BYTES;
-  static constexpr int OFF_K = 2 * Q_BYTES;
+  static constexpr int OFF_QDO = 0;  // [2 item stages][Q | dO]
+  static constexpr int OFF_K = 4 * Q_BYTES;
   static constexpr int OFF_V = OFF_K + NSK * KV_BYTES;
   static constexpr int OFF_BAR = OFF_V + NSV * KV_BYTES;
-  static constexpr int NUM_BARS = 1 + 2 * NSK + 2 * NSV + 2 + 2 + 1 + 1;
+  static constexpr int NUM_BARS = 4 + 2 * NSK + 2 * NSV + 2 + 2 + 1 + 4;
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;
-  static constexpr uint32_t S_COL = 0, DP_COL = 128, DQ_COL = 256;
+  static constexpr uint32_t S_COL = 0, DP_COL = 128, ACC_COL = 256;
 };
 
 template <int HD>
@@ -105,44 +128,42 @@ __global__ void __launch_bounds__(kThreads, 1)
          const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
          const __grid_constant__ CUtensorMap tmDQ, const BwdParams p) {
   using C = DqCfg<HD>;
+  constexpr int NSK = C::NSK, NSV = C::NSV;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
-  uint64_t* qdo_full = bars;
-  uint64_t* k_full = qdo_full + 1;
-  uint64_t* k_empty = k_full + C::NSK;
-  uint64_t* v_full = k_empty + C::NSK;
-  uint64_t* v_empty = v_full + C::NSV;
-  uint64_t* s_full = v_empty + C::NSV;  // [2]  S and dP of block t landed
-  uint64_t* ds_full = s_full + 2;       // [2]  dS of block t packed into TMEM
+  uint64_t* qdo_full = bars;            // [2]
+  uint64_t* qdo_empty = qdo_full + 2;   // [2]
+  uint64_t* k_full = qdo_empty + 2;     // [NSK]
+  uint64_t* k_empty = k_full + NSK;     // [NSK]
+  uint64_t* v_full = k_empty + NSK;     // [NSV]
+  uint64_t* v_empty = v_full + NSV;     // [NSV]
+  uint64_t* s_full = v_empty + NSV;     // [2] S and dP of tile g landed
+  uint64_t* ds_full = s_full + 2;       // [2] dS of tile g packed into TMEM
   uint64_t* dq_done = ds_full + 2;      // one completion per dQ MMA group
-  uint64_t* dq_final = dq_done + 1;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(dq_final + 1);
+  uint64_t* acc_full = dq_done + 1;     // [2]
+  uint64_t* acc_empty = acc_full + 2;   // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = (int)warp_id(), lane = (int)lane_id();
-  const int w = p.order ? p.order[blockIdx.x] : (int)blockIdx.x;
-  const int bh = w / p.T_m, qi = w % p.T_m;
-  const int hh = bh % p.H, bb = bh / p.H;
-  const int beg = p.ptr[w];
-  const int n = p.ptr[w + 1] - beg;
-  const int32_t* list = p.idx + beg;
-
   if (threadIdx.x == 0) {
     if (smem_u32(smem) & 1023u) __trap();
-    mbar_init(qdo_full, 1);
-    for (int s = 0; s < C::NSK; ++s) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&qdo_full[s], 1);
+      mbar_init(&qdo_empty[s], 1);
+      mbar_init(&s_full[s], 1);
+      mbar_init(&ds_full[s], 128);
+      mbar_init(&acc_full[s], 1);
+      mbar_init(&acc_empty[s], 128);
+    }
+    for (int s = 0; s < NSK; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
     }
-    for (int s = 0; s < C::NSV; ++s) {
+    for (int s = 0; s < NSV; ++s) {
       mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&s_full[b], 1);
-      mbar_init(&ds_full[b], 128);
-    }
     mbar_init(dq_done, 1);
-    mbar_init(dq_final, 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tmem_holder, 512);
@@ -151,155 +172,205 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tbase = *tmem_holder;
 
-  if (n == 0) {
-    if (warp >= 2) {
-      const int tok = qi * BQ + (warp & 3) * 32 + lane;
-      if (tok < p.N) {
-        __nv_bfloat16* o = p.out0 + bb * p.o0_sb + hh * p.o0_sh + (int64_t)tok * p.o0_sn;
-        for (int c = 0; c < HD; ++c) o[c] = __float2bfloat16(0.f);
-      }
-    }
-  } else if (warp == 0) {
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
     if (elect_one()) {
       tma_prefetch(&tmQ);
       tma_prefetch(&tmDO);
       tma_prefetch(&tmK);
       tma_prefetch(&tmV);
-      mbar_expect_tx(qdo_full, 2 * C::Q_BYTES);
+      int it = 0, g = 0;
+      for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
+        const Item m = get_item(p, wi, p.T_m);
+        if (m.n == 0) continue;
+        const int hh = m.bh % p.H, bb = m.bh / p.H;
+        const int st = it & 1;
+        if (it >= 2) mbar_wait(&qdo_empty[st], ((uint32_t)(it >> 1) + 1u) & 1u);
+        mbar_expect_tx(&qdo_full[st], 2 * C::Q_BYTES);
+        uint8_t* sq = smem + C::OFF_QDO + st * 2 * C::Q_BYTES;
 #pragma unroll
-      for (int c = 0; c < HD / 64; ++c) {
-        tma_load_4d(smem + C::OFF_Q + c * BQ * 128, &tmQ, qdo_full, c * 64, qi * BQ, hh, bb);
-        tma_load_4d(smem + C::OFF_DO + c * BQ * 128, &tmDO, qdo_full, c * 64, qi * BQ, hh, bb);
-      }
-      for (int t = 0; t < n; ++t) {
-        const int j = list[t];
-        const int sk = t % C::NSK, sv = t % C::NSV;
-        if (t >= C::NSK) mbar_wait(&k_empty[sk], ((uint32_t)(t / C::NSK) & 1u) ^ 1u);
-        mbar_expect_tx(&k_full[sk], C::KV_BYTES);
+        for (int c = 0; c < HD / 64; ++c) {
+          tma_load_4d(sq + c * BQ * 128, &tmQ, &qdo_full[st], c * 64, m.blk * BQ, hh, bb);
+          tma_load_4d(sq + C::Q_BYTES + c * BQ * 128, &tmDO, &qdo_full[st], c * 64, m.blk * BQ, hh, bb);
+        }
+        for (int t = 0; t < m.n; ++t, ++g) {
+          const int j = p.idx[m.beg + t];
+          const int sk = g % NSK, sv = g % NSV;
+          if (g >= NSK) mbar_wait(&k_empty[sk], ((uint32_t)(g / NSK) + 1u) & 1u);
+          mbar_expect_tx(&k_full[sk], C::KV_BYTES);
 #pragma unroll
-        for (int c = 0; c < HD / 64; ++c)
-          tma_load_4d(smem + C::OFF_K + sk * C::KV_BYTES + c * BKV * 128, &tmK, &k_full[sk], c * 64, j * BKV, hh, bb);
-        if (t >= C::NSV) mbar_wait(&v_empty[sv], ((uint32_t)(t / C::NSV) & 1u) ^ 1u);
-        mbar_expect_tx(&v_full[sv], C::KV_BYTES);
+          for (int c = 0; c < HD / 64; ++c)
+            tma_load_4d(smem + C::OFF_K + sk * C::KV_BYTES + c * BKV * 128, &tmK, &k_full[sk], c * 64, j * BKV, hh,
+                        bb);
+          if (g >= NSV) mbar_wait(&v_empty[sv], ((uint32_t)(g / NSV) + 1u) & 1u);
+          mbar_expect_tx(&v_full[sv], C::KV_BYTES);
 #pragma unroll
-        for (int c = 0; c < HD / 64; ++c)
-          tma_load_4d(smem + C::OFF_V + sv * C::KV_BYTES + c * BKV * 128, &tmV, &v_full[sv], c * 64, j * BKV, hh, bb);
+          for (int c = 0; c < HD / 64; ++c)
+            tma_load_4d(smem + C::OFF_V + sv * C::KV_BYTES + c * BKV * 128, &tmV, &v_full[sv], c * 64, j * BKV, hh,
+                        bb);
+        }
+        ++it;
       }
     }
   } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
     if (elect_one()) {
       constexpr uint32_t idS = idesc_bf16(BQ, BKV, false, false);
       constexpr uint32_t idQ = idesc_bf16(BQ, HD, false, true);
-      const uint32_t sQ = smem_u32(smem + C::OFF_Q), sDO = smem_u32(smem + C::OFF_DO);
-      mbar_wait(qdo_full, 0);
-      for (int t = 0; t <= n; ++t) {
-        if (t < n) {
-          const uint32_t b = (uint32_t)(t & 1);
-          if (t >= 2) mbar_wait(dq_done, (uint32_t)(t - 2) & 1u);  // dS_{t-2} lives in S[b]
-          const int sk = t % C::NSK, sv = t % C::NSV;
-          mbar_wait(&k_full[sk], (uint32_t)(t / C::NSK) & 1u);
+      struct Pend {
+        int g, it, sk;
+        bool first, last, valid;
+      } pd{0, 0, 0, false, false, false};
+      auto issue_dq = [&](const Pend& q) {
+        const uint32_t acc = tbase + C::ACC_COL + (uint32_t)((q.it & 1) * 128);
+        if (q.first && q.it >= 2) mbar_wait(&acc_empty[q.it & 1], ((uint32_t)(q.it >> 1) + 1u) & 1u);
+        mbar_wait(&ds_full[q.g & 1], (uint32_t)(q.g >> 1) & 1u);
+        tc_fence_after();
+        const uint32_t sK = smem_u32(smem + C::OFF_K + q.sk * C::KV_BYTES);
+#pragma unroll
+        for (int ks = 0; ks < BKV / 16; ++ks)
+          mma_bf16_ts(acc, tbase + C::S_COL + (uint32_t)((q.g & 1) * 64 + ks * 8),
+                      sw128_desc(sK + (uint32_t)(ks * 2048), BKV * 128, 1024), idQ, (!q.first || ks > 0) ? 1u : 0u);
+        mma_commit(dq_done);
+        mma_commit(&k_empty[q.sk]);
+        if (q.last) mma_commit(&acc_full[q.it & 1]);
+      };
+      int it = 0, g = 0;
+      for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
+        const Item m = get_item(p, wi, p.T_m);
+        if (m.n == 0) continue;
+        const int st = it & 1;
+        mbar_wait(&qdo_full[st], (uint32_t)(it >> 1) & 1u);
+        tc_fence_after();
+        const uint32_t sQ = smem_u32(smem + C::OFF_QDO + st * 2 * C::Q_BYTES);
+        const uint32_t sDO = sQ + C::Q_BYTES;
+        for (int t = 0; t < m.n; ++t, ++g) {
+          const uint32_t b = (uint32_t)(g & 1);
+          const int sk = g % NSK, sv = g % NSV;
+          if (g >= 2) mbar_wait(dq_done, (uint32_t)(g - 2) & 1u);  // dS_{g-2} lives in S[b]
+          mbar_wait(&k_full[sk], (uint32_t)(g / NSK) & 1u);
           tc_fence_after();
           const uint32_t sK = smem_u32(smem + C::OFF_K + sk * C::KV_BYTES);
 #pragma unroll
           for (int ks = 0; ks < HD / 16; ++ks) {
-            const uint32_t ko = (uint32_t)((ks * 16 / 64) * BQ * 128 + (ks * 16 % 64) * 2);
-            const uint32_t kko = (uint32_t)((ks * 16 / 64) * BKV * 128 + (ks * 16 % 64) * 2);
-            mma_bf16(tbase + C::S_COL + b * 64, sw128_desc(sQ + ko, 16, 1024), sw128_desc(sK + kko, 16, 1024), idS,
+            const uint32_t qo = (uint32_t)((ks * 16 / 64) * BQ * 128 + (ks * 16 % 64) * 2);
+            const uint32_t ko = (uint32_t)((ks * 16 / 64) * BKV * 128 + (ks * 16 % 64) * 2);
+            mma_bf16(tbase + C::S_COL + b * 64, sw128_desc(sQ + qo, 16, 1024), sw128_desc(sK + ko, 16, 1024), idS,
                      ks > 0 ? 1u : 0u);
           }
-          mbar_wait(&v_full[sv], (uint32_t)(t / C::NSV) & 1u);
+          mbar_wait(&v_full[sv], (uint32_t)(g / NSV) & 1u);
           tc_fence_after();
           const uint32_t sV = smem_u32(smem + C::OFF_V + sv * C::KV_BYTES);
 #pragma unroll
           for (int ks = 0; ks < HD / 16; ++ks) {
-            const uint32_t ko = (uint32_t)((ks * 16 / 64) * BQ * 128 + (ks * 16 % 64) * 2);
-            const uint32_t vko = (uint32_t)((ks * 16 / 64) * BKV * 128 + (ks * 16 % 64) * 2);
-            mma_bf16(tbase + C::DP_COL + b * 64, sw128_desc(sDO + ko, 16, 1024), sw128_desc(sV + vko, 16, 1024), idS,
+            const uint32_t qo = (uint32_t)((ks * 16 / 64) * BQ * 128 + (ks * 16 % 64) * 2);
+            const uint32_t vo = (uint32_t)((ks * 16 / 64) * BKV * 128 + (ks * 16 % 64) * 2);
+            mma_bf16(tbase + C::DP_COL + b * 64, sw128_desc(sDO + qo, 16, 1024), sw128_desc(sV + vo, 16, 1024), idS,
                      ks > 0 ? 1u : 0u);
           }
           mma_commit(&s_full[b]);
           mma_commit(&v_empty[sv]);
+          if (pd.valid) issue_dq(pd);
+          pd = Pend{g, it, sk, t == 0, t == m.n - 1, true};
         }
-        if (t >= 1) {
-          const int u = t - 1;
-          const uint32_t b = (uint32_t)(u & 1);
-          const int sk = u % C::NSK;
-          mbar_wait(&ds_full[b], (uint32_t)(u >> 1) & 1u);
-          tc_fence_after();
-          const uint32_t sK = smem_u32(smem + C::OFF_K + sk * C::KV_BYTES);
-#pragma unroll
-          for (int ks = 0; ks < BKV / 16; ++ks)
-            mma_bf16_ts(tbase + C::DQ_COL, tbase + C::S_COL + b * 64 + (uint32_t)(ks * 8),
-                        sw128_desc(sK + (uint32_t)(ks * 2048), BKV * 128, 1024), idQ, (u > 0 || ks > 0) ? 1u : 0u);
-          mma_commit(dq_done);
-          mma_commit(&k_empty[sk]);
-          if (u == n - 1) mma_commit(dq_final);
-        }
+        ++it;
       }
+      if (pd.valid) issue_dq(pd);
     }
     __syncwarp();
-  } else {
+  } else if (warp < 6) {
+    // ---------------- dS warps (2..5) ----------------
     const int q4 = warp & 3;
     const int row = q4 * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
-    const int tok = qi * BQ + row;
-    const bool valid = tok < p.N;
-    const float lse2 = valid ? p.lse[(int64_t)bh * p.N + tok] * kLog2e : INFINITY;
-    const float dlt = valid ? p.delta[(int64_t)bh * p.N + tok] : 0.f;
     const int kv_tail = p.N - (p.T_n - 1) * BKV;
     const float sl2 = p.sl2;
-    for (int t = 0; t < n; ++t) {
-      const uint32_t b = (uint32_t)(t & 1);
-      const bool tail = list[t] == p.T_n - 1 && kv_tail < BKV;
-      mbar_wait(&s_full[b], (uint32_t)(t >> 1) & 1u);
-      tc_fence_after();
+    int g = 0;
+    for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
+      const Item m = get_item(p, wi, p.T_m);
+      if (m.n == 0) continue;
+      const int tok = m.blk * BQ + row;
+      const bool valid = tok < p.N;
+      const float lse2 = valid ? p.lse[(int64_t)m.bh * p.N + tok] * kLog2e : INFINITY;
+      const float dlt = valid ? p.delta[(int64_t)m.bh * p.N + tok] : 0.f;
+      for (int t = 0; t < m.n; ++t, ++g) {
+        const uint32_t b = (uint32_t)(g & 1);
+        const bool tail = p.idx[m.beg + t] == p.T_n - 1 && kv_tail < BKV;
+        mbar_wait(&s_full[b], (uint32_t)(g >> 1) & 1u);
+        tc_fence_after();
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        uint32_t sr[32], dr[32];
-        tmem_ld32(tbase + lane_off + C::S_COL + b * 64 + (uint32_t)(32 * h), sr);
-        tmem_ld32(tbase + lane_off + C::DP_COL + b * 64 + (uint32_t)(32 * h), dr);
+        for (int h = 0; h < 2; ++h) {
+          uint32_t sr[32], dr[32];
+          tmem_ld32(tbase + lane_off + C::S_COL + b * 64 + (uint32_t)(32 * h), sr);
+          tmem_ld32(tbase + lane_off + C::DP_COL + b * 64 + (uint32_t)(32 * h), dr);
+          uint32_t pk[16];
+#pragma unroll
+          for (int c = 0; c < 16; ++c) {
+            float p0 = ex2(fmaf(__uint_as_float(sr[2 * c]), sl2, -lse2));
+            float p1 = ex2(fmaf(__uint_as_float(sr[2 * c + 1]), sl2, -lse2));
+            if (tail) {
+              if (32 * h + 2 * c >= kv_tail) p0 = 0.f;
+              if (32 * h + 2 * c + 1 >= kv_tail) p1 = 0.f;
+            }
+            pk[c] = pack_bf16(p0 * (__uint_as_float(dr[2 * c]) - dlt), p1 * (__uint_as_float(dr[2 * c + 1]) - dlt));
+          }
+          tmem_st16(tbase + lane_off + C::S_COL + b * 64 + (uint32_t)(16 * h), pk);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&ds_full[b]);
+      }
+    }
+  } else {
+    // ---------------- epilogue warps (6..9) ----------------
+    const int q4 = warp & 3;
+    const int row = q4 * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    int it = 0;
+    for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
+      const Item m = get_item(p, wi, p.T_m);
+      const int hh = m.bh % p.H, bb = m.bh / p.H;
+      if (m.n == 0) {
+        const int tok = m.blk * BQ + row;
+        if (tok < p.N) {
+          __nv_bfloat16* o = p.out0 + bb * p.o0_sb + hh * p.o0_sh + (int64_t)tok * p.o0_sn;
+          for (int c = 0; c < HD; ++c) o[c] = __float2bfloat16(0.f);
+        }
+        continue;
+      }
+      const int st = it & 1;
+      mbar_wait(&acc_full[st], (uint32_t)(it >> 1) & 1u);
+      tc_fence_after();
+      uint8_t* sOut = smem + C::OFF_QDO + st * 2 * C::Q_BYTES;  // Q of this item is dead
+      fence_proxy_async_smem();
+#pragma unroll 1
+      for (int c0 = 0; c0 < HD; c0 += 32) {
+        uint32_t o[32];
+        tmem_ld32(tbase + lane_off + C::ACC_COL + (uint32_t)(st * 128 + c0), o);
         uint32_t pk[16];
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          float p0 = ex2(fmaf(__uint_as_float(sr[2 * c]), sl2, -lse2));
-          float p1 = ex2(fmaf(__uint_as_float(sr[2 * c + 1]), sl2, -lse2));
-          if (tail) {
-            if (32 * h + 2 * c >= kv_tail) p0 = 0.f;
-            if (32 * h + 2 * c + 1 >= kv_tail) p1 = 0.f;
-          }
-          pk[c] = pack_bf16(p0 * (__uint_as_float(dr[2 * c]) - dlt), p1 * (__uint_as_float(dr[2 * c + 1]) - dlt));
-        }
-        tmem_st16(tbase + lane_off + C::S_COL + b * 64 + (uint32_t)(16 * h), pk);
+        for (int c = 0; c < 16; ++c)
+          pk[c] = pack_bf16(__uint_as_float(o[2 * c]) * p.scale, __uint_as_float(o[2 * c + 1]) * p.scale);
+        const uint32_t base = smem_u32(sOut + (c0 / 64) * BQ * 128);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          st_shared_v4(base + sw128_offset((uint32_t)row, (uint32_t)((c0 % 64) / 8 + u)), pk[4 * u], pk[4 * u + 1],
+                       pk[4 * u + 2], pk[4 * u + 3]);
       }
-      tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(&ds_full[b]);
-    }
-    mbar_wait(dq_final, 0);
-    tc_fence_after();
-    uint8_t* sOut = smem + C::OFF_Q;  // every MMA is done: Q is dead
-#pragma unroll 1
-    for (int c0 = 0; c0 < HD; c0 += 32) {
-      uint32_t o[32];
-      tmem_ld32(tbase + lane_off + C::DQ_COL + (uint32_t)c0, o);
-      uint32_t pk[16];
+      mbar_arrive(&acc_empty[st]);
+      fence_proxy_async_smem();
+      named_bar_sync(1, 128);
+      if (threadIdx.x == kEpiTid0) {
 #pragma unroll
-      for (int c = 0; c < 16; ++c)
-        pk[c] = pack_bf16(__uint_as_float(o[2 * c]) * p.scale, __uint_as_float(o[2 * c + 1]) * p.scale);
-      const uint32_t base = smem_u32(sOut + (c0 / 64) * BQ * 128);
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        st_shared_v4(base + sw128_offset((uint32_t)row, (uint32_t)((c0 % 64) / 8 + u)), pk[4 * u], pk[4 * u + 1],
-                     pk[4 * u + 2], pk[4 * u + 3]);
+        for (int c = 0; c < HD / 64; ++c) tma_store_4d(&tmDQ, sOut + c * BQ * 128, c * 64, m.blk * BQ, hh, bb);
+        tma_store_commit();
+        tma_store_wait_read();
+        mbar_arrive(&qdo_empty[st]);
+      }
+      ++it;
     }
-    fence_proxy_async_smem();
-    named_bar_sync(1, 128);
-    if (threadIdx.x == 64) {
-#pragma unroll
-      for (int c = 0; c < HD / 64; ++c) tma_store_4d(&tmDQ, sOut + c * BQ * 128, c * 64, qi * BQ, hh, bb);
-      tma_store_commit();
-      tma_store_wait_all();
-    }
+    if (threadIdx.x == kEpiTid0) tma_store_wait_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -307,7 +378,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ---------------------------------------------------------------------------------------
-// K6: dK and dV, one CTA per key block, accumulators transposed (lanes = head dim).
+// K6: dK and dV.  Work item = key block; tiles = query blocks keeping it.  Accumulators
+// transposed (TMEM lanes = head dim).
 // ---------------------------------------------------------------------------------------
 template <int HD>
 struct DkvCfg {
@@ -315,16 +387,14 @@ struct DkvCfg {
   static constexpr int KV_BYTES = BKV * HD * 2;
   static constexpr int Q_BYTES = BQ * HD * 2;
   static constexpr int PB = BQ * BKV * 2;
-  static constexpr int OFF_K = 0;
-  static constexpr int OFF_V = KV_BYTES;
-  static constexpr int OFF_Q = 2 * KV_BYTES;
-  static constexpr int OFF_DO = OFF_Q + NS * Q_BYTES;
-  static constexpr int OFF_P = OFF_DO + NS * Q_BYTES;
+  static constexpr int OFF_KV = 0;  // [2 item stages][K | V]
+  static constexpr int OFF_QDO = 4 * KV_BYTES;
+  static constexpr int OFF_P = OFF_QDO + NS * 2 * Q_BYTES;
   static constexpr int OFF_DS = OFF_P + PB;
   static constexpr int OFF_BAR = OFF_DS + PB;
-  static constexpr int NUM_BARS = 1 + 2 * NS + 2 + 2 + 1 + 1;
+  static constexpr int NUM_BARS = 4 + 2 * NS + 2 + 2 + 1 + 4;
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;
-  static constexpr uint32_t S_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 320;
+  static constexpr uint32_t S_COL = 0, DP_COL = 128, ACC_COL = 256;  // acc a: dV at +a*128, dK at +a*128+64
 };
 
 template <int HD>
@@ -336,36 +406,33 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int NS = C::NS;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
-  uint64_t* kv_full = bars;
-  uint64_t* qdo_full = kv_full + 1;
-  uint64_t* qdo_empty = qdo_full + NS;
+  uint64_t* kv_full = bars;             // [2]
+  uint64_t* kv_empty = kv_full + 2;     // [2]
+  uint64_t* qdo_full = kv_empty + 2;    // [NS]
+  uint64_t* qdo_empty = qdo_full + NS;  // [NS]
   uint64_t* sdp_full = qdo_empty + NS;  // [2]
   uint64_t* pds_full = sdp_full + 2;    // [2]
   uint64_t* pds_free = pds_full + 2;    // one completion per dV/dK MMA group
-  uint64_t* acc_final = pds_free + 1;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_final + 1);
+  uint64_t* acc_full = pds_free + 1;    // [2]
+  uint64_t* acc_empty = acc_full + 2;   // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = (int)warp_id(), lane = (int)lane_id();
-  const int w = p.order ? p.order[blockIdx.x] : (int)blockIdx.x;
-  const int bh = w / p.T_n, kj = w % p.T_n;
-  const int hh = bh % p.H, bb = bh / p.H;
-  const int beg = p.ptr[w];
-  const int n = p.ptr[w + 1] - beg;
-  const int32_t* list = p.idx + beg;
-
   if (threadIdx.x == 0) {
     if (smem_u32(smem) & 1023u) __trap();
-    mbar_init(kv_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+      mbar_init(&sdp_full[s], 1);
+      mbar_init(&pds_full[s], 128);
+      mbar_init(&acc_full[s], 1);
+      mbar_init(&acc_empty[s], 128);
+    }
     for (int s = 0; s < NS; ++s) {
       mbar_init(&qdo_full[s], 1);
       mbar_init(&qdo_empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&sdp_full[b], 1);
-      mbar_init(&pds_full[b], 128);
-    }
     mbar_init(pds_free, 1);
-    mbar_init(acc_final, 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tmem_holder, 512);
@@ -374,57 +441,91 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tbase = *tmem_holder;
 
-  if (n == 0) {
-    // no query block keeps this key block: its dK and dV rows are exactly zero
-    if (warp >= 2) {
-      for (int e = threadIdx.x - 64; e < BKV * HD; e += 128) {
-        const int r = e / HD, c = e % HD;
-        const int tok = kj * BKV + r;
-        if (tok < p.N) {
-          p.out0[bb * p.o0_sb + hh * p.o0_sh + (int64_t)tok * p.o0_sn + c] = __float2bfloat16(0.f);
-          p.out1[bb * p.o1_sb + hh * p.o1_sh + (int64_t)tok * p.o1_sn + c] = __float2bfloat16(0.f);
-        }
-      }
-    }
-  } else if (warp == 0) {
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
     if (elect_one()) {
       tma_prefetch(&tmQ);
       tma_prefetch(&tmDO);
       tma_prefetch(&tmK);
       tma_prefetch(&tmV);
-      mbar_expect_tx(kv_full, 2 * C::KV_BYTES);
-#pragma unroll
-      for (int c = 0; c < HD / 64; ++c) {
-        tma_load_4d(smem + C::OFF_K + c * BKV * 128, &tmK, kv_full, c * 64, kj * BKV, hh, bb);
-        tma_load_4d(smem + C::OFF_V + c * BKV * 128, &tmV, kv_full, c * 64, kj * BKV, hh, bb);
-      }
-      for (int t = 0; t < n; ++t) {
-        const int i = list[t];
-        const int s = t % NS;
-        if (t >= NS) mbar_wait(&qdo_empty[s], ((uint32_t)(t / NS) & 1u) ^ 1u);
-        mbar_expect_tx(&qdo_full[s], 2 * C::Q_BYTES);
+      int it = 0, g = 0;
+      for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
+        const Item m = get_item(p, wi, p.T_n);
+        if (m.n == 0) continue;
+        const int hh = m.bh % p.H, bb = m.bh / p.H;
+        const int st = it & 1;
+        if (it >= 2) mbar_wait(&kv_empty[st], ((uint32_t)(it >> 1) + 1u) & 1u);
+        mbar_expect_tx(&kv_full[st], 2 * C::KV_BYTES);
+        uint8_t* skv = smem + C::OFF_KV + st * 2 * C::KV_BYTES;
 #pragma unroll
         for (int c = 0; c < HD / 64; ++c) {
-          tma_load_4d(smem + C::OFF_Q + s * C::Q_BYTES + c * BQ * 128, &tmQ, &qdo_full[s], c * 64, i * BQ, hh, bb);
-          tma_load_4d(smem + C::OFF_DO + s * C::Q_BYTES + c * BQ * 128, &tmDO, &qdo_full[s], c * 64, i * BQ, hh, bb);
+          tma_load_4d(skv + c * BKV * 128, &tmK, &kv_full[st], c * 64, m.blk * BKV, hh, bb);
+          tma_load_4d(skv + C::KV_BYTES + c * BKV * 128, &tmV, &kv_full[st], c * 64, m.blk * BKV, hh, bb);
         }
+        for (int t = 0; t < m.n; ++t, ++g) {
+          const int i = p.idx[m.beg + t];
+          const int s = g % NS;
+          if (g >= NS) mbar_wait(&qdo_empty[s], ((uint32_t)(g / NS) + 1u) & 1u);
+          mbar_expect_tx(&qdo_full[s], 2 * C::Q_BYTES);
+          uint8_t* sq = smem + C::OFF_QDO + s * 2 * C::Q_BYTES;
+#pragma unroll
+          for (int c = 0; c < HD / 64; ++c) {
+            tma_load_4d(sq + c * BQ * 128, &tmQ, &qdo_full[s], c * 64, i * BQ, hh, bb);
+            tma_load_4d(sq + C::Q_BYTES + c * BQ * 128, &tmDO, &qdo_full[s], c * 64, i * BQ, hh, bb);
+          }
+        }
+        ++it;
       }
     }
   } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
     if (elect_one()) {
       constexpr uint32_t idS = idesc_bf16(BQ, BKV, false, false);
       constexpr uint32_t idT = idesc_bf16(HD, BKV, true, true);
-      const uint32_t sK = smem_u32(smem + C::OFF_K), sV = smem_u32(smem + C::OFF_V);
       const uint32_t sP = smem_u32(smem + C::OFF_P), sDS = smem_u32(smem + C::OFF_DS);
-      mbar_wait(kv_full, 0);
-      for (int t = 0; t <= n; ++t) {
-        if (t < n) {
-          const uint32_t b = (uint32_t)(t & 1);
-          const int s = t % NS;
-          mbar_wait(&qdo_full[s], (uint32_t)(t / NS) & 1u);
+      struct Pend {
+        int g, it, s;
+        bool first, last, valid;
+      } pd{0, 0, 0, false, false, false};
+      auto issue_dvdk = [&](const Pend& q) {
+        const uint32_t acc = tbase + C::ACC_COL + (uint32_t)((q.it & 1) * 128);
+        if (q.first && q.it >= 2) mbar_wait(&acc_empty[q.it & 1], ((uint32_t)(q.it >> 1) + 1u) & 1u);
+        mbar_wait(&pds_full[q.g & 1], (uint32_t)(q.g >> 1) & 1u);
+        tc_fence_after();
+        const uint32_t sQ = smem_u32(smem + C::OFF_QDO + q.s * 2 * C::Q_BYTES);
+        const uint32_t sDO = sQ + C::Q_BYTES;
+#pragma unroll
+        for (int ks = 0; ks < BQ / 16; ++ks) {
+          const uint32_t ro = (uint32_t)(ks * 2048);
+          mma_bf16(acc, sw128_desc(sDO + ro, BQ * 128, 1024), sw128_desc(sP + ro, BQ * 128, 1024), idT,
+                   (!q.first || ks > 0) ? 1u : 0u);
+        }
+#pragma unroll
+        for (int ks = 0; ks < BQ / 16; ++ks) {
+          const uint32_t ro = (uint32_t)(ks * 2048);
+          mma_bf16(acc + 64, sw128_desc(sQ + ro, BQ * 128, 1024), sw128_desc(sDS + ro, BQ * 128, 1024), idT,
+                   (!q.first || ks > 0) ? 1u : 0u);
+        }
+        mma_commit(pds_free);
+        mma_commit(&qdo_empty[q.s]);
+        if (q.last) mma_commit(&acc_full[q.it & 1]);
+      };
+      int it = 0, g = 0;
+      for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
+        const Item m = get_item(p, wi, p.T_n);
+        if (m.n == 0) continue;
+        const int st = it & 1;
+        mbar_wait(&kv_full[st], (uint32_t)(it >> 1) & 1u);
+        tc_fence_after();
+        const uint32_t sK = smem_u32(smem + C::OFF_KV + st * 2 * C::KV_BYTES);
+        const uint32_t sV = sK + C::KV_BYTES;
+        for (int t = 0; t < m.n; ++t, ++g) {
+          const uint32_t b = (uint32_t)(g & 1);
+          const int s = g % NS;
+          mbar_wait(&qdo_full[s], (uint32_t)(g / NS) & 1u);
           tc_fence_after();
-          const uint32_t sQ = smem_u32(smem + C::OFF_Q + s * C::Q_BYTES);
-          const uint32_t sDO = smem_u32(smem + C::OFF_DO + s * C::Q_BYTES);
+          const uint32_t sQ = smem_u32(smem + C::OFF_QDO + s * 2 * C::Q_BYTES);
+          const uint32_t sDO = sQ + C::Q_BYTES;
 #pragma unroll
           for (int ks = 0; ks < HD / 16; ++ks) {
             const uint32_t qo = (uint32_t)((ks * 16 / 64) * BQ * 128 + (ks * 16 % 64) * 2);
@@ -440,110 +541,134 @@ __global__ void __launch_bounds__(kThreads, 1)
                      ks > 0 ? 1u : 0u);
           }
           mma_commit(&sdp_full[b]);
+          if (pd.valid) issue_dvdk(pd);
+          pd = Pend{g, it, s, t == 0, t == m.n - 1, true};
         }
-        if (t >= 1) {
-          const int u = t - 1;
-          const uint32_t b = (uint32_t)(u & 1);
-          const int s = u % NS;
-          mbar_wait(&pds_full[b], (uint32_t)(u >> 1) & 1u);
-          tc_fence_after();
-          const uint32_t sQ = smem_u32(smem + C::OFF_Q + s * C::Q_BYTES);
-          const uint32_t sDO = smem_u32(smem + C::OFF_DO + s * C::Q_BYTES);
-#pragma unroll
-          for (int ks = 0; ks < BQ / 16; ++ks) {
-            const uint32_t ro = (uint32_t)(ks * 2048);
-            mma_bf16(tbase + C::DV_COL, sw128_desc(sDO + ro, BQ * 128, 1024), sw128_desc(sP + ro, BQ * 128, 1024), idT,
-                     (u > 0 || ks > 0) ? 1u : 0u);
-          }
-#pragma unroll
-          for (int ks = 0; ks < BQ / 16; ++ks) {
-            const uint32_t ro = (uint32_t)(ks * 2048);
-            mma_bf16(tbase + C::DK_COL, sw128_desc(sQ + ro, BQ * 128, 1024), sw128_desc(sDS + ro, BQ * 128, 1024), idT,
-                     (u > 0 || ks > 0) ? 1u : 0u);
-          }
-          mma_commit(pds_free);
-          mma_commit(&qdo_empty[s]);
-          if (u == n - 1) mma_commit(acc_final);
-        }
+        ++it;
       }
+      if (pd.valid) issue_dvdk(pd);
     }
     __syncwarp();
-  } else {
+  } else if (warp < 6) {
+    // ---------------- P / dS warps (2..5) ----------------
     const int q4 = warp & 3;
     const int row = q4 * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
     const float sl2 = p.sl2;
     const uint32_t sP = smem_u32(smem + C::OFF_P), sDS = smem_u32(smem + C::OFF_DS);
-    for (int t = 0; t < n; ++t) {
-      const uint32_t b = (uint32_t)(t & 1);
-      const int tok = list[t] * BQ + row;
-      const bool valid = tok < p.N;
-      const float lse2 = valid ? p.lse[(int64_t)bh * p.N + tok] * kLog2e : INFINITY;
-      const float dlt = valid ? p.delta[(int64_t)bh * p.N + tok] : 0.f;
-      mbar_wait(&sdp_full[b], (uint32_t)(t >> 1) & 1u);
-      tc_fence_after();
-      if (t >= 1) mbar_wait(pds_free, (uint32_t)(t - 1) & 1u);  // dV/dK MMAs of t-1 done with sP/sDS
+    int g = 0;
+    for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
+      const Item m = get_item(p, wi, p.T_n);
+      if (m.n == 0) continue;
+      for (int t = 0; t < m.n; ++t, ++g) {
+        const uint32_t b = (uint32_t)(g & 1);
+        const int tok = p.idx[m.beg + t] * BQ + row;
+        const bool valid = tok < p.N;
+        const float lse2 = valid ? p.lse[(int64_t)m.bh * p.N + tok] * kLog2e : INFINITY;
+        const float dlt = valid ? p.delta[(int64_t)m.bh * p.N + tok] : 0.f;
+        mbar_wait(&sdp_full[b], (uint32_t)(g >> 1) & 1u);
+        tc_fence_after();
+        if (g >= 1) mbar_wait(pds_free, (uint32_t)(g - 1) & 1u);  // dV/dK MMAs of tile g-1 done with sP/sDS
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        uint32_t sr[32], dr[32];
-        tmem_ld32(tbase + lane_off + C::S_COL + b * 64 + (uint32_t)(32 * h), sr);
-        tmem_ld32(tbase + lane_off + C::DP_COL + b * 64 + (uint32_t)(32 * h), dr);
-        uint32_t pp[16], pd[16];
+        for (int h = 0; h < 2; ++h) {
+          uint32_t sr[32], dr[32];
+          tmem_ld32(tbase + lane_off + C::S_COL + b * 64 + (uint32_t)(32 * h), sr);
+          tmem_ld32(tbase + lane_off + C::DP_COL + b * 64 + (uint32_t)(32 * h), dr);
+          uint32_t pp[16], pd[16];
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          const float p0 = ex2(fmaf(__uint_as_float(sr[2 * c]), sl2, -lse2));
-          const float p1 = ex2(fmaf(__uint_as_float(sr[2 * c + 1]), sl2, -lse2));
-          pp[c] = pack_bf16(p0, p1);
-          pd[c] = pack_bf16(p0 * (__uint_as_float(dr[2 * c]) - dlt), p1 * (__uint_as_float(dr[2 * c + 1]) - dlt));
+          for (int c = 0; c < 16; ++c) {
+            const float p0 = ex2(fmaf(__uint_as_float(sr[2 * c]), sl2, -lse2));
+            const float p1 = ex2(fmaf(__uint_as_float(sr[2 * c + 1]), sl2, -lse2));
+            pp[c] = pack_bf16(p0, p1);
+            pd[c] = pack_bf16(p0 * (__uint_as_float(dr[2 * c]) - dlt), p1 * (__uint_as_float(dr[2 * c + 1]) - dlt));
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t off = sw128_offset((uint32_t)row, (uint32_t)(4 * h + u));
+            st_shared_v4(sP + off, pp[4 * u], pp[4 * u + 1], pp[4 * u + 2], pp[4 * u + 3]);
+            st_shared_v4(sDS + off, pd[4 * u], pd[4 * u + 1], pd[4 * u + 2], pd[4 * u + 3]);
+          }
         }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const uint32_t off = sw128_offset((uint32_t)row, (uint32_t)(4 * h + u));
-          st_shared_v4(sP + off, pp[4 * u], pp[4 * u + 1], pp[4 * u + 2], pp[4 * u + 3]);
-          st_shared_v4(sDS + off, pd[4 * u], pd[4 * u + 1], pd[4 * u + 2], pd[4 * u + 3]);
-        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        mbar_arrive(&pds_full[b]);
       }
-      fence_proxy_async_smem();
-      tc_fence_before();
-      mbar_arrive(&pds_full[b]);
     }
-    // ---- epilogue: TMEM (lanes = head dim, columns = key rows) -> smem [key][d] -> TMA ----
-    mbar_wait(acc_final, 0);
-    tc_fence_after();
-    const int dim = (HD == 128) ? row : 16 * q4 + lane;  // M=64 accumulators use lanes 0-15 per quarter
+  } else {
+    // ---------------- epilogue warps (6..9) ----------------
+    const int q4 = warp & 3;
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    const int dim = (HD == 128) ? q4 * 32 + lane : 16 * q4 + lane;  // M=64 accumulators: lanes 0-15 per quarter
     const bool own = (HD == 128) || lane < 16;
-    uint8_t* sdK = smem + C::OFF_K;  // K_j / V_j are dead: every MMA has completed
-    uint8_t* sdV = smem + C::OFF_V;
+    int it = 0;
+    for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
+      const Item m = get_item(p, wi, p.T_n);
+      const int hh = m.bh % p.H, bb = m.bh / p.H;
+      if (m.n == 0) {
+        // no query block keeps this key block: its dK and dV rows are exactly zero
+        for (int e = threadIdx.x - kEpiTid0; e < BKV * HD; e += 128) {
+          const int r = e / HD, c = e % HD;
+          const int tok = m.blk * BKV + r;
+          if (tok < p.N) {
+            p.out0[bb * p.o0_sb + hh * p.o0_sh + (int64_t)tok * p.o0_sn + c] = __float2bfloat16(0.f);
+            p.out1[bb * p.o1_sb + hh * p.o1_sh + (int64_t)tok * p.o1_sn + c] = __float2bfloat16(0.f);
+          }
+        }
+        continue;
+      }
+      const int st = it & 1;
+      mbar_wait(&acc_full[st], (uint32_t)(it >> 1) & 1u);
+      tc_fence_after();
+      uint8_t* sdK = smem + C::OFF_KV + st * 2 * C::KV_BYTES;  // K_j / V_j of this item are dead
+      uint8_t* sdV = sdK + C::KV_BYTES;
+      fence_proxy_async_smem();
 #pragma unroll 1
-    for (int which = 0; which < 2; ++which) {
-      uint32_t r[64];
-      tmem_ld64(tbase + lane_off + (which ? C::DK_COL : C::DV_COL), r);
-      const float mul = which ? p.scale : 1.f;
-      const uint32_t base = smem_u32(which ? sdK : sdV) + (uint32_t)((dim / 64) * BKV * 128);
-      if (own) {
+      for (int which = 0; which < 2; ++which) {
+        uint32_t r[64];
+        tmem_ld64(tbase + lane_off + C::ACC_COL + (uint32_t)(st * 128 + (which ? 64 : 0)), r);
+        const float mul = which ? p.scale : 1.f;
+        const uint32_t base = smem_u32(which ? sdK : sdV) + (uint32_t)((dim / 64) * BKV * 128);
+        if (own) {
 #pragma unroll
-        for (int kv = 0; kv < BKV; ++kv) {
-          const __nv_bfloat16 v = __float2bfloat16(__uint_as_float(r[kv]) * mul);
-          st_shared_b16(base + sw128_offset((uint32_t)kv, (uint32_t)((dim % 64) / 8)) + (uint32_t)((dim % 8) * 2),
-                        *reinterpret_cast<const uint16_t*>(&v));
+          for (int kv = 0; kv < BKV; ++kv) {
+            const __nv_bfloat16 v = __float2bfloat16(__uint_as_float(r[kv]) * mul);
+            st_shared_b16(base + sw128_offset((uint32_t)kv, (uint32_t)((dim % 64) / 8)) + (uint32_t)((dim % 8) * 2),
+                          *reinterpret_cast<const uint16_t*>(&v));
+          }
         }
       }
-    }
-    fence_proxy_async_smem();
-    named_bar_sync(1, 128);
-    if (threadIdx.x == 64) {
+      tc_fence_before();
+      mbar_arrive(&acc_empty[st]);
+      fence_proxy_async_smem();
+      named_bar_sync(1, 128);
+      if (threadIdx.x == kEpiTid0) {
 #pragma unroll
-      for (int c = 0; c < HD / 64; ++c) {
-        tma_store_4d(&tmDK, sdK + c * BKV * 128, c * 64, kj * BKV, hh, bb);
-        tma_store_4d(&tmDV, sdV + c * BKV * 128, c * 64, kj * BKV, hh, bb);
+        for (int c = 0; c < HD / 64; ++c) {
+          tma_store_4d(&tmDK, sdK + c * BKV * 128, c * 64, m.blk * BKV, hh, bb);
+          tma_store_4d(&tmDV, sdV + c * BKV * 128, c * 64, m.blk * BKV, hh, bb);
+        }
+        tma_store_commit();
+        tma_store_wait_read();
+        mbar_arrive(&kv_empty[st]);
       }
-      tma_store_commit();
-      tma_store_wait_all();
+      ++it;
     }
+    if (threadIdx.x == kEpiTid0) tma_store_wait_all();
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tbase, 512);
+}
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
 }
 
 struct BwdMaps {
@@ -579,16 +704,18 @@ int launch_attn_bwd(int which, const spa2_view& q, const spa2_view& k, const spa
   prm.order = order;
   prm.out0 = (__nv_bfloat16*)out0.ptr;
   prm.o0_sb = out0.sb, prm.o0_sh = out0.sh, prm.o0_sn = out0.sn;
+  prm.num_items = (int)(B * H * (which == 0 ? T_m : T_n));
+  const unsigned grid = (unsigned)std::min<int64_t>(prm.num_items, num_sms());
   if (which == 0) {
     auto kern = k_dq<HD>;
     SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DqCfg<HD>::SMEM));
-    kern<<<(unsigned)(B * H * T_m), kThreads, DqCfg<HD>::SMEM, st>>>(m.q, m.k, m.v, m.dout, m.out0, prm);
+    kern<<<grid, kThreads, DqCfg<HD>::SMEM, st>>>(m.q, m.k, m.v, m.dout, m.out0, prm);
   } else {
     prm.out1 = (__nv_bfloat16*)out1->ptr;
     prm.o1_sb = out1->sb, prm.o1_sh = out1->sh, prm.o1_sn = out1->sn;
     auto kern = k_dkdv<HD>;
     SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvCfg<HD>::SMEM));
-    kern<<<(unsigned)(B * H * T_n), kThreads, DkvCfg<HD>::SMEM, st>>>(m.q, m.k, m.v, m.dout, m.out0, m.out1, prm);
+    kern<<<grid, kThreads, DkvCfg<HD>::SMEM, st>>>(m.q, m.k, m.v, m.dout, m.out0, m.out1, prm);
   }
   SPA2_LAUNCH_CHECK();
   return SPA2_OK;
@@ -612,7 +739,6 @@ bool al16(const spa2_view& x) {
 }  // namespace spa2
 
 using namespace spa2;
-
 extern "C" int spa2_bwd_delta(spa2_view o, spa2_view dout, float* delta, int dtype, int64_t B, int64_t H,
                               int64_t N, int64_t d, void* stream) {
   int rc;
