@@ -387,12 +387,11 @@ struct DkvCfg {
   static constexpr int KV_BYTES = BKV * HD * 2;
   static constexpr int Q_BYTES = BQ * HD * 2;
   static constexpr int PB = BQ * BKV * 2;
-  static constexpr int OFF_KV = 0;  // [2 item stages][K | V]
-  static constexpr int OFF_QDO = 4 * KV_BYTES;
-  static constexpr int OFF_P = OFF_QDO + NS * 2 * Q_BYTES;
-  static constexpr int OFF_DS = OFF_P + PB;
-  static constexpr int OFF_BAR = OFF_DS + PB;
-  static constexpr int NUM_BARS = 4 + 2 * NS + 2 + 2 + 1 + 4;
+  static constexpr int OFF_KV = 0;                          // [K | V] of the current item
+  static constexpr int OFF_QDO = 2 * KV_BYTES;              // [NS stages][Q | dO]
+  static constexpr int OFF_PDS = OFF_QDO + NS * 2 * Q_BYTES;  // [2 buffers][P | dS]
+  static constexpr int OFF_BAR = OFF_PDS + 2 * 2 * PB;
+  static constexpr int NUM_BARS = 2 + 2 * NS + 2 + 2 + 2 + 4;
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr uint32_t S_COL = 0, DP_COL = 128, ACC_COL = 256;  // acc a: dV at +a*128, dK at +a*128+64
 };
@@ -400,31 +399,31 @@ struct DkvCfg {
 template <int HD>
 __global__ void __launch_bounds__(kThreads, 1)
     k_dkdv(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-           const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
-           const __grid_constant__ CUtensorMap tmDK, const __grid_constant__ CUtensorMap tmDV, const BwdParams p) {
+           const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO, const BwdParams p) {
   using C = DkvCfg<HD>;
   constexpr int NS = C::NS;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
-  uint64_t* kv_full = bars;             // [2]
-  uint64_t* kv_empty = kv_full + 2;     // [2]
-  uint64_t* qdo_full = kv_empty + 2;    // [NS]
+  uint64_t* kv_full = bars;             // K/V of item `it` landed
+  uint64_t* kv_empty = kv_full + 1;     // last S/dP MMA of item `it` done: K/V slot reusable
+  uint64_t* qdo_full = kv_empty + 1;    // [NS]
   uint64_t* qdo_empty = qdo_full + NS;  // [NS]
   uint64_t* sdp_full = qdo_empty + NS;  // [2]
-  uint64_t* pds_full = sdp_full + 2;    // [2]
-  uint64_t* pds_free = pds_full + 2;    // one completion per dV/dK MMA group
-  uint64_t* acc_full = pds_free + 1;    // [2]
+  uint64_t* pds_full = sdp_full + 2;    // [2] P/dS buffer b written
+  uint64_t* pds_free = pds_full + 2;    // [2] dV/dK MMAs reading buffer b done
+  uint64_t* acc_full = pds_free + 2;    // [2]
   uint64_t* acc_empty = acc_full + 2;   // [2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = (int)warp_id(), lane = (int)lane_id();
   if (threadIdx.x == 0) {
     if (smem_u32(smem) & 1023u) __trap();
+    mbar_init(kv_full, 1);
+    mbar_init(kv_empty, 1);
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&kv_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
       mbar_init(&sdp_full[s], 1);
       mbar_init(&pds_full[s], 128);
+      mbar_init(&pds_free[s], 1);
       mbar_init(&acc_full[s], 1);
       mbar_init(&acc_empty[s], 128);
     }
@@ -432,7 +431,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&qdo_full[s], 1);
       mbar_init(&qdo_empty[s], 1);
     }
-    mbar_init(pds_free, 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tmem_holder, 512);
@@ -453,14 +451,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const Item m = get_item(p, wi, p.T_n);
         if (m.n == 0) continue;
         const int hh = m.bh % p.H, bb = m.bh / p.H;
-        const int st = it & 1;
-        if (it >= 2) mbar_wait(&kv_empty[st], ((uint32_t)(it >> 1) + 1u) & 1u);
-        mbar_expect_tx(&kv_full[st], 2 * C::KV_BYTES);
-        uint8_t* skv = smem + C::OFF_KV + st * 2 * C::KV_BYTES;
+        if (it >= 1) mbar_wait(kv_empty, (uint32_t)(it - 1) & 1u);
+        mbar_expect_tx(kv_full, 2 * C::KV_BYTES);
 #pragma unroll
         for (int c = 0; c < HD / 64; ++c) {
-          tma_load_4d(skv + c * BKV * 128, &tmK, &kv_full[st], c * 64, m.blk * BKV, hh, bb);
-          tma_load_4d(skv + C::KV_BYTES + c * BKV * 128, &tmV, &kv_full[st], c * 64, m.blk * BKV, hh, bb);
+          tma_load_4d(smem + C::OFF_KV + c * BKV * 128, &tmK, kv_full, c * 64, m.blk * BKV, hh, bb);
+          tma_load_4d(smem + C::OFF_KV + C::KV_BYTES + c * BKV * 128, &tmV, kv_full, c * 64, m.blk * BKV, hh, bb);
         }
         for (int t = 0; t < m.n; ++t, ++g) {
           const int i = p.idx[m.beg + t];
@@ -482,18 +478,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (elect_one()) {
       constexpr uint32_t idS = idesc_bf16(BQ, BKV, false, false);
       constexpr uint32_t idT = idesc_bf16(HD, BKV, true, true);
-      const uint32_t sP = smem_u32(smem + C::OFF_P), sDS = smem_u32(smem + C::OFF_DS);
+      const uint32_t sK = smem_u32(smem + C::OFF_KV), sV = sK + C::KV_BYTES;
       struct Pend {
         int g, it, s;
         bool first, last, valid;
       } pd{0, 0, 0, false, false, false};
       auto issue_dvdk = [&](const Pend& q) {
         const uint32_t acc = tbase + C::ACC_COL + (uint32_t)((q.it & 1) * 128);
+        const int pb = q.g & 1;
         if (q.first && q.it >= 2) mbar_wait(&acc_empty[q.it & 1], ((uint32_t)(q.it >> 1) + 1u) & 1u);
-        mbar_wait(&pds_full[q.g & 1], (uint32_t)(q.g >> 1) & 1u);
+        mbar_wait(&pds_full[pb], (uint32_t)(q.g >> 1) & 1u);
         tc_fence_after();
         const uint32_t sQ = smem_u32(smem + C::OFF_QDO + q.s * 2 * C::Q_BYTES);
         const uint32_t sDO = sQ + C::Q_BYTES;
+        const uint32_t sP = smem_u32(smem + C::OFF_PDS + pb * 2 * C::PB), sDS = sP + C::PB;
 #pragma unroll
         for (int ks = 0; ks < BQ / 16; ++ks) {
           const uint32_t ro = (uint32_t)(ks * 2048);
@@ -506,7 +504,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mma_bf16(acc + 64, sw128_desc(sQ + ro, BQ * 128, 1024), sw128_desc(sDS + ro, BQ * 128, 1024), idT,
                    (!q.first || ks > 0) ? 1u : 0u);
         }
-        mma_commit(pds_free);
+        mma_commit(&pds_free[pb]);
         mma_commit(&qdo_empty[q.s]);
         if (q.last) mma_commit(&acc_full[q.it & 1]);
       };
@@ -514,11 +512,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
         const Item m = get_item(p, wi, p.T_n);
         if (m.n == 0) continue;
-        const int st = it & 1;
-        mbar_wait(&kv_full[st], (uint32_t)(it >> 1) & 1u);
+        mbar_wait(kv_full, (uint32_t)it & 1u);
         tc_fence_after();
-        const uint32_t sK = smem_u32(smem + C::OFF_KV + st * 2 * C::KV_BYTES);
-        const uint32_t sV = sK + C::KV_BYTES;
         for (int t = 0; t < m.n; ++t, ++g) {
           const uint32_t b = (uint32_t)(g & 1);
           const int s = g % NS;
@@ -541,6 +536,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                      ks > 0 ? 1u : 0u);
           }
           mma_commit(&sdp_full[b]);
+          if (t == m.n - 1) mma_commit(kv_empty);  // K_j / V_j are only read by S and dP
           if (pd.valid) issue_dvdk(pd);
           pd = Pend{g, it, s, t == 0, t == m.n - 1, true};
         }
@@ -555,20 +551,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = q4 * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
     const float sl2 = p.sl2;
-    const uint32_t sP = smem_u32(smem + C::OFF_P), sDS = smem_u32(smem + C::OFF_DS);
     int g = 0;
     for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
       const Item m = get_item(p, wi, p.T_n);
       if (m.n == 0) continue;
-      for (int t = 0; t < m.n; ++t, ++g) {
-        const uint32_t b = (uint32_t)(g & 1);
+      const int64_t rowbase = (int64_t)m.bh * p.N;
+      auto load_stats = [&](int t, float& lse2, float& dlt) {
         const int tok = p.idx[m.beg + t] * BQ + row;
         const bool valid = tok < p.N;
-        const float lse2 = valid ? p.lse[(int64_t)m.bh * p.N + tok] * kLog2e : INFINITY;
-        const float dlt = valid ? p.delta[(int64_t)m.bh * p.N + tok] : 0.f;
+        lse2 = valid ? __ldg(p.lse + rowbase + tok) * kLog2e : INFINITY;
+        dlt = valid ? __ldg(p.delta + rowbase + tok) : 0.f;
+      };
+      float lse2, dlt;
+      load_stats(0, lse2, dlt);
+      for (int t = 0; t < m.n; ++t, ++g) {
+        const uint32_t b = (uint32_t)(g & 1);
+        float lse2_n = 0.f, dlt_n = 0.f;
+        if (t + 1 < m.n) load_stats(t + 1, lse2_n, dlt_n);  // prefetch the next tile's row statistics
         mbar_wait(&sdp_full[b], (uint32_t)(g >> 1) & 1u);
         tc_fence_after();
-        if (g >= 1) mbar_wait(pds_free, (uint32_t)(g - 1) & 1u);  // dV/dK MMAs of tile g-1 done with sP/sDS
+        if (g >= 2) mbar_wait(&pds_free[b], ((uint32_t)(g >> 1) + 1u) & 1u);  // buffer b free (tile g-2 done)
+        const uint32_t sP = smem_u32(smem + C::OFF_PDS + (int)b * 2 * C::PB), sDS = sP + C::PB;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           uint32_t sr[32], dr[32];
@@ -592,10 +595,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         fence_proxy_async_smem();
         tc_fence_before();
         mbar_arrive(&pds_full[b]);
+        lse2 = lse2_n;
+        dlt = dlt_n;
       }
     }
   } else {
-    // ---------------- epilogue warps (6..9) ----------------
+    // ---------------- epilogue warps (6..9): TMEM -> registers -> coalesced global stores ----
     const int q4 = warp & 3;
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
     const int dim = (HD == 128) ? q4 * 32 + lane : 16 * q4 + lane;  // M=64 accumulators: lanes 0-15 per quarter
@@ -604,56 +609,37 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
       const Item m = get_item(p, wi, p.T_n);
       const int hh = m.bh % p.H, bb = m.bh / p.H;
+      __nv_bfloat16* dk = p.out0 + bb * p.o0_sb + hh * p.o0_sh + (int64_t)m.blk * BKV * p.o0_sn + dim;
+      __nv_bfloat16* dv = p.out1 + bb * p.o1_sb + hh * p.o1_sh + (int64_t)m.blk * BKV * p.o1_sn + dim;
+      const int rows = min(BKV, p.N - m.blk * BKV);
       if (m.n == 0) {
         // no query block keeps this key block: its dK and dV rows are exactly zero
-        for (int e = threadIdx.x - kEpiTid0; e < BKV * HD; e += 128) {
-          const int r = e / HD, c = e % HD;
-          const int tok = m.blk * BKV + r;
-          if (tok < p.N) {
-            p.out0[bb * p.o0_sb + hh * p.o0_sh + (int64_t)tok * p.o0_sn + c] = __float2bfloat16(0.f);
-            p.out1[bb * p.o1_sb + hh * p.o1_sh + (int64_t)tok * p.o1_sn + c] = __float2bfloat16(0.f);
+        if (own)
+          for (int r = 0; r < rows; ++r) {
+            dk[(int64_t)r * p.o0_sn] = __float2bfloat16(0.f);
+            dv[(int64_t)r * p.o1_sn] = __float2bfloat16(0.f);
           }
-        }
         continue;
       }
       const int st = it & 1;
       mbar_wait(&acc_full[st], (uint32_t)(it >> 1) & 1u);
       tc_fence_after();
-      uint8_t* sdK = smem + C::OFF_KV + st * 2 * C::KV_BYTES;  // K_j / V_j of this item are dead
-      uint8_t* sdV = sdK + C::KV_BYTES;
-      fence_proxy_async_smem();
-#pragma unroll 1
-      for (int which = 0; which < 2; ++which) {
-        uint32_t r[64];
-        tmem_ld64(tbase + lane_off + C::ACC_COL + (uint32_t)(st * 128 + (which ? 64 : 0)), r);
-        const float mul = which ? p.scale : 1.f;
-        const uint32_t base = smem_u32(which ? sdK : sdV) + (uint32_t)((dim / 64) * BKV * 128);
-        if (own) {
+      uint32_t rv[64], rk[64];
+      tmem_ld64(tbase + lane_off + C::ACC_COL + (uint32_t)(st * 128), rv);
+      tmem_ld64(tbase + lane_off + C::ACC_COL + (uint32_t)(st * 128 + 64), rk);
+      tc_fence_before();
+      mbar_arrive(&acc_empty[st]);  // accumulators are in registers: TMEM set reusable
+      if (own) {
 #pragma unroll
-          for (int kv = 0; kv < BKV; ++kv) {
-            const __nv_bfloat16 v = __float2bfloat16(__uint_as_float(r[kv]) * mul);
-            st_shared_b16(base + sw128_offset((uint32_t)kv, (uint32_t)((dim % 64) / 8)) + (uint32_t)((dim % 8) * 2),
-                          *reinterpret_cast<const uint16_t*>(&v));
+        for (int r = 0; r < BKV; ++r) {
+          if (r < rows) {
+            dv[(int64_t)r * p.o1_sn] = __float2bfloat16(__uint_as_float(rv[r]));
+            dk[(int64_t)r * p.o0_sn] = __float2bfloat16(__uint_as_float(rk[r]) * p.scale);
           }
         }
       }
-      tc_fence_before();
-      mbar_arrive(&acc_empty[st]);
-      fence_proxy_async_smem();
-      named_bar_sync(1, 128);
-      if (threadIdx.x == kEpiTid0) {
-#pragma unroll
-        for (int c = 0; c < HD / 64; ++c) {
-          tma_store_4d(&tmDK, sdK + c * BKV * 128, c * 64, m.blk * BKV, hh, bb);
-          tma_store_4d(&tmDV, sdV + c * BKV * 128, c * 64, m.blk * BKV, hh, bb);
-        }
-        tma_store_commit();
-        tma_store_wait_read();
-        mbar_arrive(&kv_empty[st]);
-      }
       ++it;
     }
-    if (threadIdx.x == kEpiTid0) tma_store_wait_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -688,8 +674,8 @@ int launch_attn_bwd(int which, const spa2_view& q, const spa2_view& k, const spa
   if ((rc = make_qkv_map(&m.dout, dout, B, H, N, HD, BQ))) return rc;
   if ((rc = make_qkv_map(&m.k, k, B, H, N, HD, BKV))) return rc;
   if ((rc = make_qkv_map(&m.v, v, B, H, N, HD, BKV))) return rc;
-  if ((rc = make_qkv_map(&m.out0, out0, B, H, N, HD, which == 0 ? BQ : BKV))) return rc;
-  if (which == 1 && (rc = make_qkv_map(&m.out1, *out1, B, H, N, HD, BKV))) return rc;
+  if (which == 0 && (rc = make_qkv_map(&m.out0, out0, B, H, N, HD, BQ))) return rc;
+
   BwdParams prm{};
   prm.H = (int)H;
   prm.N = (int)N;
@@ -715,7 +701,7 @@ int launch_attn_bwd(int which, const spa2_view& q, const spa2_view& k, const spa
     prm.o1_sb = out1->sb, prm.o1_sh = out1->sh, prm.o1_sn = out1->sn;
     auto kern = k_dkdv<HD>;
     SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvCfg<HD>::SMEM));
-    kern<<<grid, kThreads, DkvCfg<HD>::SMEM, st>>>(m.q, m.k, m.v, m.dout, m.out0, m.out1, prm);
+    kern<<<grid, kThreads, DkvCfg<HD>::SMEM, st>>>(m.q, m.k, m.v, m.dout, prm);
   }
   SPA2_LAUNCH_CHECK();
   return SPA2_OK;
