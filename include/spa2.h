@@ -143,6 +143,12 @@ int spa2_bwd_dkdv(spa2_view q, spa2_view k, spa2_view v, spa2_view dout, const f
 int spa2_probe_gemm(const void* a, const void* b, float* d, int m, int n, int k, int a_mn, int b_mn,
                     int use_tma, void* stream);
 
+/* tcgen05 issue-rate probe (diagnostic): `ctas` CTAs each issue reps*(k/16) dependent-free
+ * MMAs of shape m x n x 16 with the given operand layout (a_tmem = A from TMEM) and record
+ * the clock64 cycles of the whole chain in cycles[cta]. */
+int spa2_probe_mma_rate(int m, int n, int k, int a_mn, int b_mn, int a_tmem, int reps, int ctas,
+                        unsigned long long* cycles, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

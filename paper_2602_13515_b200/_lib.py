@@ -57,6 +57,7 @@ SIGNATURES = {
     "spa2_bwd_dkdv": ([View, View, View, View, _P, _P, View, View, _I32, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P,
                        _P, _F32, _P], _I32),
     "spa2_probe_gemm": ([_P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _P], _I32),
+    "spa2_probe_mma_rate": ([_I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P, _P], _I32),
 }
 
 # Kernels each entry point launches (for the bench's gpu_launches accounting).

@@ -140,3 +140,73 @@ extern "C" int spa2_probe_gemm(const void* a, const void* b, float* d, int m, in
   SPA2_LAUNCH_CHECK();
   return SPA2_OK;
 }
+
+// ---- tensor-pipe rate probe (diagnostic): cycles per tcgen05.mma for an operand layout ----
+namespace spa2 {
+namespace {
+__global__ void __launch_bounds__(128) k_mma_rate(int M, int N, int K, int a_mn, int b_mn, int a_tmem, int reps,
+                                                  unsigned long long* cycles) {
+  extern __shared__ uint8_t smem_dyn[];
+  __shared__ uint64_t bar_mma;
+  __shared__ uint32_t tmem_base;
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+  uint8_t* sa = base;
+  uint8_t* sb = base + 65536;
+  for (int i = threadIdx.x; i < 131072 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(base)[i] = make_uint4(0x3f803f80u, 0x3f803f80u, 0x3f803f80u, 0x3f803f80u);
+  const int Ra = a_mn ? K : M, Rb = b_mn ? K : N;
+  if (warp_id() == 0) tmem_alloc(&tmem_base, 512);
+  if (threadIdx.x == 32) {
+    mbar_init(&bar_mma, 1);
+    fence_mbar_init();
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tmem_base;
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = idesc_bf16(M, N, a_mn != 0, b_mn != 0);
+    uint64_t da[8], db[8];
+    uint32_t ta[8];
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      const int kk = ks % (K / 16);
+      da[ks] = operand_desc(smem_u32(sa), a_mn, Ra, kk);
+      db[ks] = operand_desc(smem_u32(sb), b_mn, Rb, kk);
+      ta[ks] = tbase + 256u + (uint32_t)(kk * 8);
+    }
+    const uint64_t t0 = clock64();
+    if (a_tmem) {
+      for (int r = 0; r < reps; ++r) {
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) mma_bf16_ts(tbase, ta[ks], db[ks], idesc, 1u);
+      }
+    } else {
+      for (int r = 0; r < reps; ++r) {
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) mma_bf16(tbase, da[ks], db[ks], idesc, 1u);
+      }
+    }
+    mma_commit(&bar_mma);
+    mbar_wait(&bar_mma, 0);
+    const uint64_t t1 = clock64();
+    cycles[blockIdx.x] = t1 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp_id() == 0) tmem_dealloc(tbase, 512);
+}
+}  // namespace
+}  // namespace spa2
+
+extern "C" int spa2_probe_mma_rate(int m, int n, int k, int a_mn, int b_mn, int a_tmem, int reps, int ctas,
+                                   unsigned long long* cycles, void* stream) {
+  SPA2_REQUIRE((m == 64 || m == 128) && (n == 64 || n == 128 || n == 256) && (k == 64 || k == 128), SPA2_ERR_UNSUPPORTED,
+               "mma_rate: unsupported shape");
+  const size_t smem = 131072 + 1024;
+  SPA2_CUDA_TRY(cudaFuncSetAttribute(k_mma_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_mma_rate<<<ctas, 128, smem, (cudaStream_t)stream>>>(m, n, k, a_mn, b_mn, a_tmem, reps, cycles);
+  SPA2_LAUNCH_CHECK();
+  return SPA2_OK;
+}
