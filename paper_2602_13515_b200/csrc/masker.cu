@@ -18,93 +18,76 @@
 namespace spa2 {
 namespace {
 
-constexpr int kPoolThreads = 256;
-
 // ---------------------------------------------------------------------------------------
 // K1a: block-mean pooling of Q (by b_q) and K (by b_kv) in float64.
-// One CTA per (b, h, block).  Thread (r, g) sums rows r, r+R, ... of column group g
-// (8 columns with 16-byte loads when VEC, else 1 column), then the R partial sums of a
-// column are added in a fixed order — deterministic, not order-matched to numpy's
-// reduceat (the difference is last-bit, far below the 1e-12 the reference promises).
+// One thread per (b, h, block, group of CPT columns): it walks the block's rows in order
+// and accumulates in float64 starting from the first row — the same left-to-right order
+// numpy's add.reduceat uses along axis 0 — then divides by the true row count
+// (numerics.py:62-65).  Rows are read 16 bytes at a time with 8 loads in flight.
 // ---------------------------------------------------------------------------------------
-template <typename T, bool VEC>
-__global__ void __launch_bounds__(kPoolThreads) k_pool(spa2_view q, spa2_view k, int H, int N, int d,
-                                                       int b_q, int b_kv, int T_m, int T_n, int64_t BH,
-                                                       double* __restrict__ qbar,
-                                                       double* __restrict__ kbar,
-                                                       int32_t* __restrict__ nonfinite) {
-  extern __shared__ double red[];  // [R][d]
-  constexpr int CPT = VEC ? (16 / (int)sizeof(T) < 8 ? 16 / (int)sizeof(T) : 8) : 1;
-  const int64_t g = blockIdx.x;
-  const bool is_q = g < BH * T_m;
-  const int64_t gl = is_q ? g : g - BH * T_m;
-  const int nblk = is_q ? T_m : T_n;
-  const int64_t bh = gl / nblk;
-  const int blk = (int)(gl % nblk);
-  const int bsz = is_q ? b_q : b_kv;
-  const spa2_view vw = is_q ? q : k;
-  const int64_t bi = bh / H, hi = bh % H;
-  const int row0 = blk * bsz;
-  const int rows = min(bsz, N - row0);
-  const T* base = reinterpret_cast<const T*>(vw.ptr) + bi * vw.sb + hi * vw.sh + (int64_t)row0 * vw.sn;
-
-  const int cpr = d / CPT;            // threads per row
-  const int R = kPoolThreads / cpr;   // rows in flight
-  const int r = threadIdx.x / cpr;
-  const int cg = threadIdx.x % cpr;
-  double acc[CPT];
-#pragma unroll
-  for (int e = 0; e < CPT; ++e) acc[e] = 0.0;
+template <typename T, int CPT>
+__global__ void __launch_bounds__(256) k_pool(spa2_view q, spa2_view k, int H, int N, int d, int b_q, int b_kv,
+                                              int T_m, int T_n, int64_t BH, double* __restrict__ qbar,
+                                              double* __restrict__ kbar, int32_t* __restrict__ nonfinite) {
+  const int cpr = d / CPT;  // threads per block row
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nq = BH * T_m * cpr, nk = BH * T_n * cpr;
   bool bad = false;
-  if (r < R) {
-    if constexpr (VEC) {
-      // issue up to 8 independent 16-byte loads before consuming any (memory-level parallelism)
-      constexpr int U = 8;
-      for (int row0 = r; row0 < rows; row0 += R * U) {
-        uint4 buf[U];
+  if (gid < nq + nk) {
+    const bool is_q = gid < nq;
+    const int64_t gl = is_q ? gid : gid - nq;
+    const int cg = (int)(gl % cpr);
+    const int64_t blk_g = gl / cpr;
+    const int nblk = is_q ? T_m : T_n;
+    const int64_t bh = blk_g / nblk;
+    const int blk = (int)(blk_g % nblk);
+    const int bsz = is_q ? b_q : b_kv;
+    const spa2_view vw = is_q ? q : k;
+    const int row0 = blk * bsz;
+    const int rows = min(bsz, N - row0);
+    const T* base = reinterpret_cast<const T*>(vw.ptr) + (bh / H) * vw.sb + (bh % H) * vw.sh +
+                    (int64_t)row0 * vw.sn + cg * CPT;
+    double acc[CPT];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int row = row0 + u * R;
-          if (row < rows)
-            buf[u] = __ldg(reinterpret_cast<const uint4*>(base + (int64_t)row * vw.sn + cg * CPT));
+    for (int e = 0; e < CPT; ++e) acc[e] = 0.0;
+    constexpr int U = 8;
+    for (int r0 = 0; r0 < rows; r0 += U) {
+      T buf[U][CPT];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (r0 + u < rows) {
+          const T* p = base + (int64_t)(r0 + u) * vw.sn;
+          if constexpr (CPT * sizeof(T) == 16) {
+            *reinterpret_cast<uint4*>(buf[u]) = __ldg(reinterpret_cast<const uint4*>(p));
+          } else {
+#pragma unroll
+            for (int e = 0; e < CPT; ++e) buf[u][e] = p[e];
+          }
         }
+      }
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (row0 + u * R < rows) {
-            const T* vals = reinterpret_cast<const T*>(&buf[u]);
+      for (int u = 0; u < U; ++u) {
+        if (r0 + u < rows) {
 #pragma unroll
-            for (int e = 0; e < CPT; ++e) {
-              double x = to_f64<T>(vals[e]);
-              bad |= !isfinite(x);
-              acc[e] += x;
-            }
+          for (int e = 0; e < CPT; ++e) {
+            const double x = to_f64<T>(buf[u][e]);
+            bad |= !isfinite(x);
+            acc[e] += x;
           }
         }
       }
     }
-    for (int row = r; !VEC && row < rows; row += R) {
-      const T* p = base + (int64_t)row * vw.sn + cg * CPT;
-      {
-        double x = to_f64<T>(p[0]);
-        bad |= !isfinite(x);
-        acc[0] += x;
-      }
-    }
+    double* out = (is_q ? qbar : kbar) + blk_g * (int64_t)d + cg * CPT;
 #pragma unroll
-    for (int e = 0; e < CPT; ++e) red[r * d + cg * CPT + e] = acc[e];
+    for (int e = 0; e < CPT; ++e) out[e] = acc[e] / (double)rows;
   }
-  if (__syncthreads_or(bad) && threadIdx.x == 0 && nonfinite != nullptr) atomicOr(nonfinite, 1);
-  double* out = (is_q ? qbar : kbar) + (bh * nblk + blk) * (int64_t)d;
-  for (int c = threadIdx.x; c < d; c += blockDim.x) {
-    double s = 0.0;
-    for (int rr = 0; rr < R; ++rr) s += red[rr * d + c];
-    out[c] = s / (double)rows;
-  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0 && nonfinite != nullptr) atomicOr(nonfinite, 1);
 }
 
 // ---------------------------------------------------------------------------------------
 // K1b: scores S = Q̄ K̄ᵀ / √d in float64 (written into `probs`).  64x64 output tiles, 256
 // threads x (4x4) register blocking, k-chunks of 8 staged transposed in shared memory.
+// ---------------------------------------------------------------------------------------
 constexpr int kSTI = 64, kSTJ = 64, kSTK = 8, kSTP = kSTI + 2;
 
 __global__ void __launch_bounds__(256) k_scores(const double* __restrict__ qbar,
@@ -175,9 +158,9 @@ __global__ void k_softmax_rows(double* __restrict__ p, int64_t rows, int T_n) {
 }
 
 // ---------------------------------------------------------------------------------------
-// K2: per-row selection.  One warp per row: bitonic sort of (value, column) pairs in
-// shared memory into the reference's stable descending order (masker.py:113-115: larger
-// value first, equal values by ascending column), then the hybrid count
+// K2: per-row selection.  One CTA per row: block-wide bitonic sort of (value, column)
+// pairs in shared memory into the reference's stable descending order (masker.py:113-115:
+// larger value first, equal values by ascending column), then the hybrid count
 //   kept = min(max(K, cnt_p), T_n),  cnt_p = searchsorted_left(cumsum(sorted), thr) + 1
 // with the cumsum evaluated strictly sequentially in float64 exactly like np.cumsum.
 // For non-negative rows the running sum is monotone, so a linear scan that stops at the
@@ -188,22 +171,20 @@ __device__ __forceinline__ bool goes_before(double va, int ca, double vb, int cb
   return va > vb || (va == vb && ca < cb);
 }
 
-__global__ void k_select(const double* __restrict__ probs, int64_t rows, int T_n, int T_pad,
-                         int k_count, double thr, int use_p, uint8_t* __restrict__ keep,
-                         int32_t* __restrict__ counts) {
+__global__ void k_select(const double* __restrict__ probs, int T_n, int T_pad, int k_count, double thr, int use_p,
+                         uint8_t* __restrict__ keep, int32_t* __restrict__ counts) {
   extern __shared__ unsigned char smem_raw[];
-  const int warps = blockDim.x / 32;
-  const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
-  double* vals = reinterpret_cast<double*>(smem_raw) + (int64_t)w * T_pad;
-  int* cols = reinterpret_cast<int*>(reinterpret_cast<double*>(smem_raw) + (int64_t)warps * T_pad) +
-              (int64_t)w * T_pad;
-  const int64_t row = (int64_t)blockIdx.x * warps + w;
-  if (row >= rows) return;
+  double* vals = reinterpret_cast<double*>(smem_raw);
+  int* cols = reinterpret_cast<int*>(vals + T_pad);
+  __shared__ int s_neg, s_kept;
+  const int64_t row = blockIdx.x;
   const double* x = probs + row * (int64_t)T_n;
+  if (threadIdx.x == 0) s_neg = 0;
+  __syncthreads();
   bool neg = false;
-  for (int t = lane; t < T_pad; t += 32) {
+  for (int t = threadIdx.x; t < T_pad; t += blockDim.x) {
     if (t < T_n) {
-      double v = x[t];
+      const double v = x[t];
       neg |= v < 0.0;
       vals[t] = v;
       cols[t] = t;
@@ -212,29 +193,30 @@ __global__ void k_select(const double* __restrict__ probs, int64_t rows, int T_n
       cols[t] = 0x7fffffff;
     }
   }
-  neg = __any_sync(0xffffffffu, neg);
-  __syncwarp();
+  if (neg) s_neg = 1;
+  __syncthreads();
   for (int size = 2; size <= T_pad; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int t = lane; t < (T_pad >> 1); t += 32) {
-        int i = 2 * t - (t & (stride - 1));
-        int j = i + stride;
-        bool up = (i & size) == 0;
-        double vi = vals[i], vj = vals[j];
-        int ci = cols[i], cj = cols[j];
+      for (int t = threadIdx.x; t < (T_pad >> 1); t += blockDim.x) {
+        const int i = 2 * t - (t & (stride - 1));
+        const int j = i + stride;
+        const bool up = (i & size) == 0;
+        const double vi = vals[i], vj = vals[j];
+        const int ci = cols[i], cj = cols[j];
         if (goes_before(vj, cj, vi, ci) == up) {
-          vals[i] = vj; vals[j] = vi;
-          cols[i] = cj; cols[j] = ci;
+          vals[i] = vj;
+          vals[j] = vi;
+          cols[i] = cj;
+          cols[j] = ci;
         }
       }
-      __syncwarp();
+      __syncthreads();
     }
   }
-  int kept = 0;
-  if (lane == 0) {
+  if (threadIdx.x == 0) {
     int cnt_p = 1;
     if (use_p) {
-      if (!neg) {
+      if (!s_neg) {
         double run = 0.0;
         int t = 0;
         for (; t < T_n; ++t) {
@@ -250,20 +232,21 @@ __global__ void k_select(const double* __restrict__ probs, int64_t rows, int T_n
         }
         int lo = 0, hi = T_n;  // numpy npy_binsearch (side='left'), single key
         while (lo < hi) {
-          int mid = lo + ((hi - lo) >> 1);
-          if (vals[mid] < thr) lo = mid + 1; else hi = mid;
+          const int mid = lo + ((hi - lo) >> 1);
+          if (vals[mid] < thr) lo = mid + 1;
+          else hi = mid;
         }
         cnt_p = lo + 1;
       }
     }
-    kept = min(max(k_count, cnt_p), T_n);
+    s_kept = min(max(k_count, cnt_p), T_n);
+    if (counts != nullptr) counts[row] = s_kept;
   }
-  kept = __shfl_sync(0xffffffffu, kept, 0);
   uint8_t* out = keep + row * (int64_t)T_n;
-  for (int t = lane; t < T_n; t += 32) out[t] = 0;
-  __syncwarp();
-  for (int t = lane; t < kept; t += 32) out[cols[t]] = 1;
-  if (lane == 0 && counts != nullptr) counts[row] = kept;
+  for (int t = threadIdx.x; t < T_n; t += blockDim.x) out[t] = 0;
+  __syncthreads();
+  const int kept = s_kept;
+  for (int t = threadIdx.x; t < kept; t += blockDim.x) out[cols[t]] = 1;
 }
 
 // ---------------------------------------------------------------------------------------
@@ -281,16 +264,62 @@ __global__ void k_row_counts(const uint8_t* __restrict__ keep, int64_t nrows, in
   if (lane == 0) row_cnt[row] = c;
 }
 
-__global__ void k_col_counts(const uint8_t* __restrict__ keep, int64_t bh, int T_m, int T_n,
-                             int32_t* __restrict__ col_cnt) {
-  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= bh * T_n) return;
-  const int64_t h = g / T_n;
-  const int j = (int)(g % T_n);
-  const uint8_t* base = keep + h * (int64_t)T_m * T_n + j;
+// Column counts and column lists: one CTA per (head, 32-column chunk); lane = column, the
+// 8 warps split the T_m rows into contiguous ranges (coalesced 32-byte row segments).
+constexpr int kColWarps = 8;
+
+__device__ __forceinline__ void col_range(int T_m, int w, int& r0, int& r1) {
+  const int per = (T_m + kColWarps - 1) / kColWarps;
+  r0 = min(w * per, T_m);
+  r1 = min(r0 + per, T_m);
+}
+
+__global__ void __launch_bounds__(kColWarps * 32) k_col_counts(const uint8_t* __restrict__ keep, int T_m, int T_n,
+                                                               int32_t* __restrict__ col_cnt) {
+  __shared__ int part[kColWarps][32];
+  const int64_t bh = blockIdx.y;
+  const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int j = blockIdx.x * 32 + lane;
+  int r0, r1;
+  col_range(T_m, w, r0, r1);
+  const uint8_t* base = keep + bh * (int64_t)T_m * T_n + j;
   int c = 0;
-  for (int i = 0; i < T_m; ++i) c += base[(int64_t)i * T_n] != 0;
-  col_cnt[g] = c;
+  if (j < T_n) {
+#pragma unroll 8
+    for (int i = r0; i < r1; ++i) c += base[(int64_t)i * T_n] != 0;
+  }
+  part[w][lane] = c;
+  __syncthreads();
+  if (w == 0 && j < T_n) {
+    int s = 0;
+#pragma unroll
+    for (int x = 0; x < kColWarps; ++x) s += part[x][lane];
+    col_cnt[bh * T_n + j] = s;
+  }
+}
+
+__global__ void __launch_bounds__(kColWarps * 32) k_fill_cols(const uint8_t* __restrict__ keep, int T_m, int T_n,
+                                                              const int32_t* __restrict__ col_ptr,
+                                                              int32_t* __restrict__ col_idx) {
+  __shared__ int part[kColWarps][32];
+  const int64_t bh = blockIdx.y;
+  const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int j = blockIdx.x * 32 + lane;
+  int r0, r1;
+  col_range(T_m, w, r0, r1);
+  const uint8_t* base = keep + bh * (int64_t)T_m * T_n + j;
+  int c = 0;
+  if (j < T_n) {
+#pragma unroll 8
+    for (int i = r0; i < r1; ++i) c += base[(int64_t)i * T_n] != 0;
+  }
+  part[w][lane] = c;
+  __syncthreads();
+  if (j >= T_n) return;
+  int off = col_ptr[bh * T_n + j];
+  for (int x = 0; x < w; ++x) off += part[x][lane];
+  for (int i = r0; i < r1; ++i)
+    if (base[(int64_t)i * T_n] != 0) col_idx[off++] = i;
 }
 
 constexpr int kScanThreads = 1024;
@@ -322,8 +351,8 @@ __device__ void cta_exclusive_scan(const int32_t* in, int32_t* out, int64_t n, i
 
 // Longest-first order: counting sort of ids base..base+n-1 by descending count (counts in
 // [0, maxc]); ids are written to order[base ...].
-__device__ void cta_order_desc(const int32_t* cnt, int64_t n, int maxc, int32_t* order,
-                               int32_t* bins, int32_t* sh, int64_t base) {
+__device__ void cta_order_desc(const int32_t* cnt, int64_t n, int maxc, int32_t* order, int32_t* bins, int32_t* sh,
+                               int64_t base) {
   cnt += base;
   order += base;
   for (int c = threadIdx.x; c <= maxc; c += kScanThreads) bins[c] = 0;
@@ -396,53 +425,25 @@ __global__ void k_fill_rows(const uint8_t* __restrict__ keep, int64_t nrows, int
   }
 }
 
-__global__ void k_fill_cols(const uint8_t* __restrict__ keep, int64_t bh, int T_m, int T_n,
-                            const int32_t* __restrict__ col_ptr, int32_t* __restrict__ col_idx) {
-  const int64_t g = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  const int lane = threadIdx.x % 32;
-  if (g >= bh * T_n) return;
-  const int64_t h = g / T_n;
-  const int j = (int)(g % T_n);
-  const uint8_t* base_p = keep + h * (int64_t)T_m * T_n + j;
-  int base = col_ptr[g];
-  for (int i0 = 0; i0 < T_m; i0 += 32) {
-    int i = i0 + lane;
-    bool f = i < T_m && base_p[(int64_t)i * T_n] != 0;
-    unsigned m = __ballot_sync(0xffffffffu, f);
-    if (f) col_idx[base + __popc(m & ((1u << lane) - 1u))] = i;
-    base += __popc(m);
-  }
-}
-
 template <typename T>
-int launch_pool(spa2_view q, spa2_view k, int64_t B, int64_t H, int64_t N, int64_t d, int64_t b_q,
-                int64_t b_kv, int64_t T_m, int64_t T_n, double* qbar, double* kbar,
-                int32_t* nonfinite, cudaStream_t st) {
+int launch_pool(spa2_view q, spa2_view k, int64_t B, int64_t H, int64_t N, int64_t d, int64_t b_q, int64_t b_kv,
+                int64_t T_m, int64_t T_n, double* qbar, double* kbar, int32_t* nonfinite, cudaStream_t st) {
   const int64_t BH = B * H;
-  const int cpt_vec = 16 / (int)sizeof(T) < 8 ? 16 / (int)sizeof(T) : 8;
+  constexpr int CV = 16 / (int)sizeof(T) < 8 ? 16 / (int)sizeof(T) : 8;
   auto aligned = [&](const spa2_view& v) {
-    return ((uintptr_t)v.ptr % 16 == 0) && (v.sb % cpt_vec == 0) && (v.sh % cpt_vec == 0) &&
-           (v.sn % cpt_vec == 0);
+    return ((uintptr_t)v.ptr % 16 == 0) && (v.sb % CV == 0) && (v.sh % CV == 0) && (v.sn % CV == 0);
   };
-  const bool vec = (d % cpt_vec == 0) && aligned(q) && aligned(k) && (d / cpt_vec) <= kPoolThreads;
-  const int cpt = vec ? cpt_vec : 1;
-  SPA2_REQUIRE(d / cpt <= kPoolThreads, SPA2_ERR_UNSUPPORTED,
-               "pooled_map: d=%lld too large for the pooling kernel", (long long)d);
-  const int R = kPoolThreads / (int)(d / cpt);
-  const size_t smem = (size_t)R * d * sizeof(double);
-  const int64_t grid = BH * (T_m + T_n);
-  SPA2_REQUIRE(grid < (1ll << 31), SPA2_ERR_UNSUPPORTED, "pooled_map: grid too large");
-  if (vec) {
-    auto kern = k_pool<T, true>;
-    if (smem > 48 * 1024) SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<(unsigned)grid, kPoolThreads, smem, st>>>(q, k, (int)H, (int)N, (int)d, (int)b_q, (int)b_kv,
-                                                      (int)T_m, (int)T_n, BH, qbar, kbar, nonfinite);
-  } else {
-    auto kern = k_pool<T, false>;
-    if (smem > 48 * 1024) SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<(unsigned)grid, kPoolThreads, smem, st>>>(q, k, (int)H, (int)N, (int)d, (int)b_q, (int)b_kv,
-                                                      (int)T_m, (int)T_n, BH, qbar, kbar, nonfinite);
-  }
+  const bool vec = (d % CV == 0) && aligned(q) && aligned(k);
+  const int cpt = vec ? CV : 1;
+  const int64_t threads = BH * (T_m + T_n) * (d / cpt);
+  SPA2_REQUIRE(threads < (1ll << 40), SPA2_ERR_UNSUPPORTED, "pooled_map: problem too large");
+  const unsigned grid = (unsigned)ceil_div(threads, 256);
+  if (vec)
+    k_pool<T, CV><<<grid, 256, 0, st>>>(q, k, (int)H, (int)N, (int)d, (int)b_q, (int)b_kv, (int)T_m, (int)T_n, BH,
+                                        qbar, kbar, nonfinite);
+  else
+    k_pool<T, 1><<<grid, 256, 0, st>>>(q, k, (int)H, (int)N, (int)d, (int)b_q, (int)b_kv, (int)T_m, (int)T_n, BH,
+                                       qbar, kbar, nonfinite);
   SPA2_LAUNCH_CHECK();
   return SPA2_OK;
 }
@@ -491,21 +492,18 @@ extern "C" int spa2_select(const double* probs, int64_t rows, int64_t t_n, int64
   SPA2_REQUIRE(k_count >= 1, SPA2_ERR_VALUE, "select: k_count must be >= 1");
   SPA2_REQUIRE(probs && keep, SPA2_ERR_VALUE, "select: null pointer");
   SPA2_REQUIRE(!isnan(p_threshold), SPA2_ERR_VALUE, "select: p_threshold is NaN");
-  int t_pad = 1;
+  SPA2_REQUIRE(rows < (1ll << 31), SPA2_ERR_UNSUPPORTED, "select: too many rows");
+  int t_pad = 2;
   while (t_pad < t_n) t_pad <<= 1;
-  if (t_pad < 32) t_pad = 32;
-  const size_t per_warp = (size_t)t_pad * (sizeof(double) + sizeof(int));
-  SPA2_REQUIRE(per_warp <= 200 * 1024, SPA2_ERR_UNSUPPORTED, "select: T_n=%lld exceeds 16384",
-               (long long)t_n);
-  int warps = (int)std::min<size_t>(8, std::max<size_t>(1, (48 * 1024) / per_warp));
-  const size_t smem = per_warp * warps;
+  const size_t smem = (size_t)t_pad * (sizeof(double) + sizeof(int));
+  SPA2_REQUIRE(smem <= 200 * 1024, SPA2_ERR_UNSUPPORTED, "select: T_n=%lld exceeds 16384", (long long)t_n);
   cudaStream_t st = (cudaStream_t)stream;
   if (smem > 48 * 1024)
     SPA2_CUDA_TRY(cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int use_p = isinf(p_threshold) && p_threshold < 0 ? 0 : 1;
   const int kk = (int)std::min<int64_t>(k_count, t_n);
-  k_select<<<(unsigned)ceil_div(rows, warps), warps * 32, smem, st>>>(
-      probs, rows, (int)t_n, t_pad, kk, p_threshold, use_p, keep, counts);
+  const int threads = std::max(32, std::min(1024, t_pad / 2));
+  k_select<<<(unsigned)rows, threads, smem, st>>>(probs, (int)t_n, t_pad, kk, p_threshold, use_p, keep, counts);
   SPA2_LAUNCH_CHECK();
   return SPA2_OK;
 }
@@ -518,14 +516,16 @@ extern "C" int spa2_build_lists(const uint8_t* keep, int64_t bh, int64_t t_m, in
   SPA2_REQUIRE(keep && row_ptr && row_idx && col_ptr && col_idx && row_order && col_order && scratch,
                SPA2_ERR_VALUE, "build_lists: null pointer");
   SPA2_REQUIRE(bh * t_m * t_n < (1ll << 31), SPA2_ERR_UNSUPPORTED, "build_lists: grid too large");
-  SPA2_REQUIRE(std::max(t_m, t_n) <= 32768, SPA2_ERR_UNSUPPORTED, "build_lists: T_m/T_n > 32768");
+  SPA2_REQUIRE(std::max(t_m, t_n) <= 32768 && bh < 65536, SPA2_ERR_UNSUPPORTED,
+               "build_lists: T_m/T_n > 32768 or B*H >= 65536");
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t nrows = bh * t_m, ncols = bh * t_n;
   int32_t* col_cnt = scratch;          // [ncols]
   int32_t* row_cnt = scratch + ncols;  // [nrows]
+  const dim3 cgrid((unsigned)ceil_div(t_n, 32), (unsigned)bh);
   k_row_counts<<<(unsigned)ceil_div(nrows, 8), 256, 0, st>>>(keep, nrows, (int)t_n, row_cnt);
   SPA2_LAUNCH_CHECK();
-  k_col_counts<<<(unsigned)ceil_div(ncols, 256), 256, 0, st>>>(keep, bh, (int)t_m, (int)t_n, col_cnt);
+  k_col_counts<<<cgrid, kColWarps * 32, 0, st>>>(keep, (int)t_m, (int)t_n, col_cnt);
   SPA2_LAUNCH_CHECK();
   k_scan<<<1, kScanThreads, 0, st>>>(row_cnt, col_cnt, nrows, ncols, row_ptr, col_ptr);
   SPA2_LAUNCH_CHECK();
@@ -537,7 +537,7 @@ extern "C" int spa2_build_lists(const uint8_t* keep, int64_t bh, int64_t t_m, in
   SPA2_LAUNCH_CHECK();
   k_fill_rows<<<(unsigned)ceil_div(nrows, 8), 256, 0, st>>>(keep, nrows, (int)t_n, row_ptr, row_idx);
   SPA2_LAUNCH_CHECK();
-  k_fill_cols<<<(unsigned)ceil_div(ncols, 8), 256, 0, st>>>(keep, bh, (int)t_m, (int)t_n, col_ptr, col_idx);
+  k_fill_cols<<<cgrid, kColWarps * 32, 0, st>>>(keep, (int)t_m, (int)t_n, col_ptr, col_idx);
   SPA2_LAUNCH_CHECK();
   return SPA2_OK;
 }
