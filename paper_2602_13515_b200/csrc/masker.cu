@@ -86,9 +86,9 @@ __global__ void __launch_bounds__(256) k_pool(spa2_view q, spa2_view k, int H, i
 
 // ---------------------------------------------------------------------------------------
 // K1b: scores S = Q̄ K̄ᵀ / √d in float64 (written into `probs`).  64x64 output tiles, 256
-// threads x (4x4) register blocking, k-chunks of 8 staged transposed in shared memory.
+// threads x (4x4) register blocking, k-chunks of 32 staged transposed in shared memory.
 // ---------------------------------------------------------------------------------------
-constexpr int kSTI = 64, kSTJ = 64, kSTK = 8, kSTP = kSTI + 2;
+constexpr int kSTI = 64, kSTJ = 64, kSTK = 32, kSTP = kSTI + 2;
 
 __global__ void __launch_bounds__(256) k_scores(const double* __restrict__ qbar,
                                                 const double* __restrict__ kbar, int T_m, int T_n,
@@ -171,43 +171,107 @@ __device__ __forceinline__ bool goes_before(double va, int ca, double vb, int cb
   return va > vb || (va == vb && ca < cb);
 }
 
-__global__ void k_select(const double* __restrict__ probs, int T_n, int T_pad, int k_count, double thr, int use_p,
-                         uint8_t* __restrict__ keep, int32_t* __restrict__ counts) {
-  extern __shared__ unsigned char smem_raw[];
-  double* vals = reinterpret_cast<double*>(smem_raw);
-  int* cols = reinterpret_cast<int*>(vals + T_pad);
-  __shared__ int s_neg, s_kept;
+constexpr int kSelThreads = 128;
+constexpr int kBuckets = 64;  // bucket 0: values >= 1, bucket b: [2^-b, 2^(1-b)), bucket 63: < 2^-62 (and 0)
+
+__device__ __forceinline__ int exp_bucket(double v) {
+  const int e = (int)((__double_as_longlong(v) >> 52) & 0x7FF);  // v >= 0
+  return min(kBuckets - 1, max(0, 1023 - e));
+}
+
+// One CTA per row.  (1) exponent histogram of the row (count and float64 mass per power-of-
+// two bucket); (2) walking buckets from the largest, the shortest bucket prefix holding at
+// least K entries and mass >= p + 1e-9 is a candidate set that is guaranteed to contain
+// the answer: entries outside it are strictly smaller than every candidate, and the exact
+// candidate mass exceeds the threshold by 1e-9, far above the rounding of a <=16384-term
+// float64 running sum, so the sequential cumsum reaches `thr` inside it; (3) only the
+// candidates are sorted (bitonic, shared memory) and scanned.  Rows with negative entries
+// (non-monotone cumsum) take every entry as a candidate.  Output is identical to sorting the
+// whole row.
+__global__ void __launch_bounds__(kSelThreads) k_select(const double* __restrict__ probs, int T_n, int k_count,
+                                                        double thr, int use_p, uint8_t* __restrict__ keep,
+                                                        int32_t* __restrict__ counts) {
+  extern __shared__ unsigned char smem_raw[];  // cand_v[T_pad] (double), cand_c[T_pad] (int)
+  __shared__ int h_cnt[kBuckets];
+  __shared__ double h_sum[kBuckets];
+  __shared__ int s_neg, s_bstar, s_npos, s_kept;
   const int64_t row = blockIdx.x;
   const double* x = probs + row * (int64_t)T_n;
-  if (threadIdx.x == 0) s_neg = 0;
+  for (int b = threadIdx.x; b < kBuckets; b += blockDim.x) {
+    h_cnt[b] = 0;
+    h_sum[b] = 0.0;
+  }
+  if (threadIdx.x == 0) {
+    s_neg = 0;
+    s_npos = 0;
+  }
   __syncthreads();
   bool neg = false;
-  for (int t = threadIdx.x; t < T_pad; t += blockDim.x) {
-    if (t < T_n) {
-      const double v = x[t];
-      neg |= v < 0.0;
-      vals[t] = v;
-      cols[t] = t;
+  for (int t = threadIdx.x; t < T_n; t += blockDim.x) {
+    const double v = x[t];
+    if (v < 0.0) {
+      neg = true;
     } else {
-      vals[t] = -INFINITY;
-      cols[t] = 0x7fffffff;
+      const int b = exp_bucket(v);
+      atomicAdd(&h_cnt[b], 1);
+      atomicAdd(&h_sum[b], v);
     }
   }
   if (neg) s_neg = 1;
   __syncthreads();
-  for (int size = 2; size <= T_pad; size <<= 1) {
+  if (threadIdx.x == 0) {
+    int bstar = kBuckets;  // kBuckets = "every entry"
+    if (!s_neg) {
+      int cnt = 0;
+      double mass = 0.0;
+      const double need = thr + 1e-9;
+      for (int b = 0; b < kBuckets; ++b) {
+        cnt += h_cnt[b];
+        mass += h_sum[b];
+        if (cnt >= k_count && (!use_p || mass >= need)) {
+          bstar = b;
+          break;
+        }
+      }
+    }
+    s_bstar = bstar;
+  }
+  __syncthreads();
+  const int bstar = s_bstar;
+  double* cv = reinterpret_cast<double*>(smem_raw);
+  int T_pad = 1;
+  while (T_pad < T_n) T_pad <<= 1;
+  int* cc = reinterpret_cast<int*>(cv + T_pad);
+  for (int t = threadIdx.x; t < T_n; t += blockDim.x) {
+    const double v = x[t];
+    if (bstar == kBuckets || (v >= 0.0 && exp_bucket(v) <= bstar)) {
+      const int pos = atomicAdd(&s_npos, 1);
+      cv[pos] = v;
+      cc[pos] = t;
+    }
+  }
+  __syncthreads();
+  const int C = s_npos;
+  int C_pad = 1;
+  while (C_pad < C) C_pad <<= 1;
+  for (int t = C + threadIdx.x; t < C_pad; t += blockDim.x) {
+    cv[t] = -INFINITY;
+    cc[t] = 0x7fffffff;
+  }
+  __syncthreads();
+  for (int size = 2; size <= C_pad; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int t = threadIdx.x; t < (T_pad >> 1); t += blockDim.x) {
+      for (int t = threadIdx.x; t < (C_pad >> 1); t += blockDim.x) {
         const int i = 2 * t - (t & (stride - 1));
         const int j = i + stride;
         const bool up = (i & size) == 0;
-        const double vi = vals[i], vj = vals[j];
-        const int ci = cols[i], cj = cols[j];
+        const double vi = cv[i], vj = cv[j];
+        const int ci = cc[i], cj = cc[j];
         if (goes_before(vj, cj, vi, ci) == up) {
-          vals[i] = vj;
-          vals[j] = vi;
-          cols[i] = cj;
-          cols[j] = ci;
+          cv[i] = vj;
+          cv[j] = vi;
+          cc[i] = cj;
+          cc[j] = ci;
         }
       }
       __syncthreads();
@@ -219,21 +283,21 @@ __global__ void k_select(const double* __restrict__ probs, int T_n, int T_pad, i
       if (!s_neg) {
         double run = 0.0;
         int t = 0;
-        for (; t < T_n; ++t) {
-          run = (t == 0) ? vals[0] : run + vals[t];
+        for (; t < C; ++t) {
+          run = (t == 0) ? cv[0] : run + cv[t];
           if (run >= thr) break;
         }
-        cnt_p = t + 1;
+        cnt_p = (t < C) ? t + 1 : T_n + 1;  // t == C only when every entry is a candidate
       } else {
         double run = 0.0;
         for (int t = 0; t < T_n; ++t) {
-          run = (t == 0) ? vals[0] : run + vals[t];
-          vals[t] = run;  // sorted values are no longer needed
+          run = (t == 0) ? cv[0] : run + cv[t];
+          cv[t] = run;  // sorted values are no longer needed
         }
         int lo = 0, hi = T_n;  // numpy npy_binsearch (side='left'), single key
         while (lo < hi) {
           const int mid = lo + ((hi - lo) >> 1);
-          if (vals[mid] < thr) lo = mid + 1;
+          if (cv[mid] < thr) lo = mid + 1;
           else hi = mid;
         }
         cnt_p = lo + 1;
@@ -246,7 +310,7 @@ __global__ void k_select(const double* __restrict__ probs, int T_n, int T_pad, i
   for (int t = threadIdx.x; t < T_n; t += blockDim.x) out[t] = 0;
   __syncthreads();
   const int kept = s_kept;
-  for (int t = threadIdx.x; t < kept; t += blockDim.x) out[cols[t]] = 1;
+  for (int t = threadIdx.x; t < kept; t += blockDim.x) out[cc[t]] = 1;
 }
 
 // ---------------------------------------------------------------------------------------
@@ -493,7 +557,7 @@ extern "C" int spa2_select(const double* probs, int64_t rows, int64_t t_n, int64
   SPA2_REQUIRE(probs && keep, SPA2_ERR_VALUE, "select: null pointer");
   SPA2_REQUIRE(!isnan(p_threshold), SPA2_ERR_VALUE, "select: p_threshold is NaN");
   SPA2_REQUIRE(rows < (1ll << 31), SPA2_ERR_UNSUPPORTED, "select: too many rows");
-  int t_pad = 2;
+  int t_pad = 1;
   while (t_pad < t_n) t_pad <<= 1;
   const size_t smem = (size_t)t_pad * (sizeof(double) + sizeof(int));
   SPA2_REQUIRE(smem <= 200 * 1024, SPA2_ERR_UNSUPPORTED, "select: T_n=%lld exceeds 16384", (long long)t_n);
@@ -502,8 +566,7 @@ extern "C" int spa2_select(const double* probs, int64_t rows, int64_t t_n, int64
     SPA2_CUDA_TRY(cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int use_p = isinf(p_threshold) && p_threshold < 0 ? 0 : 1;
   const int kk = (int)std::min<int64_t>(k_count, t_n);
-  const int threads = std::max(32, std::min(1024, t_pad / 2));
-  k_select<<<(unsigned)rows, threads, smem, st>>>(probs, (int)t_n, t_pad, kk, p_threshold, use_p, keep, counts);
+  k_select<<<(unsigned)rows, kSelThreads, smem, st>>>(probs, (int)t_n, kk, p_threshold, use_p, keep, counts);
   SPA2_LAUNCH_CHECK();
   return SPA2_OK;
 }
