@@ -12,6 +12,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -70,8 +71,22 @@ __global__ void __launch_bounds__(256) k_pool(spa2_view q, spa2_view k, int H, i
         if (r0 + u < rows) {
 #pragma unroll
           for (int e = 0; e < CPT; ++e) {
-            const double x = to_f64<T>(buf[u][e]);
-            bad |= !isfinite(x);
+            double x;
+            if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+              // exact bf16 -> f64 without the conversion pipe: rebias the exponent, move the
+              // 7-bit mantissa to the top of the 52-bit one; zeros/subnormals take the slow path
+              const uint32_t h = __bfloat16_as_ushort(buf[u][e]);
+              const uint32_t mag = h & 0x7FFFu;
+              bad |= (mag & 0x7F80u) == 0x7F80u;
+              if ((mag & 0x7F80u) != 0u)
+                x = __longlong_as_double((long long)(((uint64_t)(h & 0x8000u) << 48) |
+                                                     ((uint64_t)(mag + ((1023u - 127u) << 7)) << 45)));
+              else
+                x = (double)__bfloat162float(buf[u][e]);
+            } else {
+              x = to_f64<T>(buf[u][e]);
+              bad |= !isfinite(x);
+            }
             acc[e] += x;
           }
         }
@@ -172,20 +187,28 @@ __device__ __forceinline__ bool goes_before(double va, int ca, double vb, int cb
 }
 
 constexpr int kSelThreads = 128;
-constexpr int kBuckets = 64;  // bucket 0: values >= 1, bucket b: [2^-b, 2^(1-b)), bucket 63: < 2^-62 (and 0)
+constexpr int kBuckets = 256;  // 4 buckets per octave from 1 down to 2^-63; bucket 255 also holds 0
 
-__device__ __forceinline__ int exp_bucket(double v) {
-  const int e = (int)((__double_as_longlong(v) >> 52) & 0x7FF);  // v >= 0
-  return min(kBuckets - 1, max(0, 1023 - e));
+// Order-preserving bucket of a non-negative double: bucket 0 holds the largest values.
+__device__ __forceinline__ int value_bucket(double v) {
+  const long long bits = __double_as_longlong(v);
+  const int key = (int)((bits >> 50) & 0x1FFF);  // exponent (11 bits) and top 2 mantissa bits
+  return min(kBuckets - 1, max(0, ((1023 << 2) | 3) - key));
+}
+// Smallest value a bucket can hold (a lower bound used for the candidate mass).
+__device__ __forceinline__ double bucket_floor(int b) {
+  if (b >= kBuckets - 1) return 0.0;
+  const int key = ((1023 << 2) | 3) - b;
+  return ldexp(1.0 + 0.25 * (key & 3), (key >> 2) - 1023);
 }
 
-// One CTA per row.  (1) exponent histogram of the row (count and float64 mass per power-of-
-// two bucket); (2) walking buckets from the largest, the shortest bucket prefix holding at
-// least K entries and mass >= p + 1e-9 is a candidate set that is guaranteed to contain
-// the answer: entries outside it are strictly smaller than every candidate, and the exact
-// candidate mass exceeds the threshold by 1e-9, far above the rounding of a <=16384-term
-// float64 running sum, so the sequential cumsum reaches `thr` inside it; (3) only the
-// candidates are sorted (bitonic, shared memory) and scanned.  Rows with negative entries
+// One CTA per row.  (1) histogram of the row over order-preserving value buckets (4 per
+// octave); (2) walking buckets from the largest, the shortest bucket prefix holding at least
+// K entries whose mass LOWER BOUND (count x bucket floor) reaches p + 1e-9 is a candidate set
+// guaranteed to contain the answer: entries outside it are strictly smaller than every
+// candidate, and the candidates' exact mass exceeds the threshold by >= 1e-9, far above the
+// rounding of a <=16384-term float64 running sum, so the sequential cumsum reaches `thr`
+// inside it; (3) only the candidates are sorted (bitonic, shared memory) and scanned.  Rows with negative entries
 // (non-monotone cumsum) take every entry as a candidate.  Output is identical to sorting the
 // whole row.
 __global__ void __launch_bounds__(kSelThreads) k_select(const double* __restrict__ probs, int T_n, int k_count,
@@ -193,14 +216,10 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const double* __restrict
                                                         int32_t* __restrict__ counts) {
   extern __shared__ unsigned char smem_raw[];  // cand_v[T_pad] (double), cand_c[T_pad] (int)
   __shared__ int h_cnt[kBuckets];
-  __shared__ double h_sum[kBuckets];
   __shared__ int s_neg, s_bstar, s_npos, s_kept;
   const int64_t row = blockIdx.x;
   const double* x = probs + row * (int64_t)T_n;
-  for (int b = threadIdx.x; b < kBuckets; b += blockDim.x) {
-    h_cnt[b] = 0;
-    h_sum[b] = 0.0;
-  }
+  for (int b = threadIdx.x; b < kBuckets; b += blockDim.x) h_cnt[b] = 0;
   if (threadIdx.x == 0) {
     s_neg = 0;
     s_npos = 0;
@@ -212,9 +231,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const double* __restrict
     if (v < 0.0) {
       neg = true;
     } else {
-      const int b = exp_bucket(v);
-      atomicAdd(&h_cnt[b], 1);
-      atomicAdd(&h_sum[b], v);
+      atomicAdd(&h_cnt[value_bucket(v)], 1);
     }
   }
   if (neg) s_neg = 1;
@@ -227,7 +244,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const double* __restrict
       const double need = thr + 1e-9;
       for (int b = 0; b < kBuckets; ++b) {
         cnt += h_cnt[b];
-        mass += h_sum[b];
+        mass += h_cnt[b] * bucket_floor(b);
         if (cnt >= k_count && (!use_p || mass >= need)) {
           bstar = b;
           break;
@@ -244,7 +261,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const double* __restrict
   int* cc = reinterpret_cast<int*>(cv + T_pad);
   for (int t = threadIdx.x; t < T_n; t += blockDim.x) {
     const double v = x[t];
-    if (bstar == kBuckets || (v >= 0.0 && exp_bucket(v) <= bstar)) {
+    if (bstar == kBuckets || (v >= 0.0 && value_bucket(v) <= bstar)) {
       const int pos = atomicAdd(&s_npos, 1);
       cv[pos] = v;
       cc[pos] = t;
@@ -330,7 +347,7 @@ __global__ void k_row_counts(const uint8_t* __restrict__ keep, int64_t nrows, in
 
 // Column counts and column lists: one CTA per (head, 32-column chunk); lane = column, the
 // 8 warps split the T_m rows into contiguous ranges (coalesced 32-byte row segments).
-constexpr int kColWarps = 8;
+constexpr int kColWarps = 16;
 
 __device__ __forceinline__ void col_range(int T_m, int w, int& r0, int& r1) {
   const int per = (T_m + kColWarps - 1) / kColWarps;
@@ -382,35 +399,52 @@ __global__ void __launch_bounds__(kColWarps * 32) k_fill_cols(const uint8_t* __r
   if (j >= T_n) return;
   int off = col_ptr[bh * T_n + j];
   for (int x = 0; x < w; ++x) off += part[x][lane];
+#pragma unroll 8
   for (int i = r0; i < r1; ++i)
     if (base[(int64_t)i * T_n] != 0) col_idx[off++] = i;
 }
 
 constexpr int kScanThreads = 1024;
 
-// Exclusive scan of in[0..n) into out[0..n], out[n] = total, by one CTA.
+// Exclusive scan of in[0..n) into out[0..n], out[n] = total, by one CTA (warp-shuffle scan).
+__device__ int32_t cta_inclusive_scan_1024(int32_t v, int32_t* sh_warp) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += u;
+  }
+  if (lane == 31) sh_warp[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    int32_t t = sh_warp[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t u = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += u;
+    }
+    sh_warp[lane] = t;
+  }
+  __syncthreads();
+  const int32_t r = v + (w > 0 ? sh_warp[w - 1] : 0);
+  __syncthreads();
+  return r;
+}
+
 __device__ void cta_exclusive_scan(const int32_t* in, int32_t* out, int64_t n, int32_t* sh) {
   const int tid = threadIdx.x;
   const int64_t per = (n + kScanThreads - 1) / kScanThreads;
   const int64_t beg = min((int64_t)tid * per, n), end = min(beg + per, n);
   int32_t local = 0;
   for (int64_t i = beg; i < end; ++i) local += in[i];
-  sh[tid] = local;
-  __syncthreads();
-  for (int off = 1; off < kScanThreads; off <<= 1) {  // Hillis-Steele inclusive scan
-    int32_t v = tid >= off ? sh[tid - off] : 0;
-    __syncthreads();
-    sh[tid] += v;
-    __syncthreads();
-  }
-  int32_t run = sh[tid] - local;
+  const int32_t incl = cta_inclusive_scan_1024(local, sh);
+  int32_t run = incl - local;
   for (int64_t i = beg; i < end; ++i) {
-    int32_t c = in[i];
+    const int32_t c = in[i];
     out[i] = run;
     run += c;
   }
-  if (tid == kScanThreads - 1) out[n] = sh[tid];
-  __syncthreads();
+  if (tid == kScanThreads - 1) out[n] = incl;
 }
 
 // Longest-first order: counting sort of ids base..base+n-1 by descending count (counts in
@@ -429,15 +463,7 @@ __device__ void cta_order_desc(const int32_t* cnt, int64_t n, int maxc, int32_t*
   const int beg = min((int)threadIdx.x * per, nb), end = min(beg + per, nb);
   int32_t local = 0;
   for (int b = beg; b < end; ++b) local += bins[b];
-  sh[threadIdx.x] = local;
-  __syncthreads();
-  for (int off = 1; off < kScanThreads; off <<= 1) {
-    int32_t v = threadIdx.x >= off ? sh[threadIdx.x - off] : 0;
-    __syncthreads();
-    sh[threadIdx.x] += v;
-    __syncthreads();
-  }
-  int32_t run = sh[threadIdx.x] - local;
+  int32_t run = cta_inclusive_scan_1024(local, sh) - local;
   for (int b = beg; b < end; ++b) {
     int32_t c = bins[b];
     bins[b] = run;
