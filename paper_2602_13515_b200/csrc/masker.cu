@@ -73,16 +73,9 @@ __global__ void __launch_bounds__(256) k_pool(spa2_view q, spa2_view k, int H, i
           for (int e = 0; e < CPT; ++e) {
             double x;
             if constexpr (std::is_same<T, __nv_bfloat16>::value) {
-              // exact bf16 -> f64 without the conversion pipe: rebias the exponent, move the
-              // 7-bit mantissa to the top of the 52-bit one; zeros/subnormals take the slow path
-              const uint32_t h = __bfloat16_as_ushort(buf[u][e]);
-              const uint32_t mag = h & 0x7FFFu;
-              bad |= (mag & 0x7F80u) == 0x7F80u;
-              if ((mag & 0x7F80u) != 0u)
-                x = __longlong_as_double((long long)(((uint64_t)(h & 0x8000u) << 48) |
-                                                     ((uint64_t)(mag + ((1023u - 127u) << 7)) << 45)));
-              else
-                x = (double)__bfloat162float(buf[u][e]);
+              // non-finite test on the bf16 bits (exponent all ones) instead of on the double
+              bad |= (__bfloat16_as_ushort(buf[u][e]) & 0x7F80u) == 0x7F80u;
+              x = (double)__bfloat162float(buf[u][e]);
             } else {
               x = to_f64<T>(buf[u][e]);
               bad |= !isfinite(x);
