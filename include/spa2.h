@@ -149,6 +149,10 @@ int spa2_probe_gemm(const void* a, const void* b, float* d, int m, int n, int k,
 int spa2_probe_mma_rate(int m, int n, int k, int a_mn, int b_mn, int a_tmem, int reps, int ctas,
                         unsigned long long* cycles, void* stream);
 
+/* Diagnostic: record per-role pipeline events of CTA 0 of the next backward launches into a
+ * device buffer (u64[2 + 2*capacity], buf[0] must be zeroed by the caller); NULL disables. */
+int spa2_debug_trace(void* buf, int capacity);
+
 #ifdef __cplusplus
 }
 #endif

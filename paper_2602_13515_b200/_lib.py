@@ -58,6 +58,7 @@ SIGNATURES = {
                        _P, _F32, _P], _I32),
     "spa2_probe_gemm": ([_P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _P], _I32),
     "spa2_probe_mma_rate": ([_I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P, _P], _I32),
+    "spa2_debug_trace": ([_P, _I32], _I32),
 }
 
 # Kernels each entry point launches (for the bench's gpu_launches accounting).

@@ -55,6 +55,8 @@ struct BwdParams {
   int64_t o0_sb, o0_sh, o0_sn;
   __nv_bfloat16* out1;   // dv (K6)
   int64_t o1_sb, o1_sh, o1_sn;
+  unsigned long long* trace;  // diagnostic (spa2_debug_trace), normally null
+  int trace_cap;
 };
 
 struct Item {
@@ -461,7 +463,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int t = 0; t < m.n; ++t, ++g) {
           const int i = p.idx[m.beg + t];
           const int s = g % NS;
+          trace_ev(p.trace, p.trace_cap, 0, 1, g);
           if (g >= NS) mbar_wait(&qdo_empty[s], ((uint32_t)(g / NS) + 1u) & 1u);
+          trace_ev(p.trace, p.trace_cap, 0, 2, g);
           mbar_expect_tx(&qdo_full[s], 2 * C::Q_BYTES);
           uint8_t* sq = smem + C::OFF_QDO + s * 2 * C::Q_BYTES;
 #pragma unroll
@@ -487,7 +491,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t acc = tbase + C::ACC_COL + (uint32_t)((q.it & 1) * 128);
         const int pb = q.g & 1;
         if (q.first && q.it >= 2) mbar_wait(&acc_empty[q.it & 1], ((uint32_t)(q.it >> 1) + 1u) & 1u);
+        trace_ev(p.trace, p.trace_cap, 1, 3, q.g);
         mbar_wait(&pds_full[pb], (uint32_t)(q.g >> 1) & 1u);
+        trace_ev(p.trace, p.trace_cap, 1, 4, q.g);
         tc_fence_after();
         const uint32_t sQ = smem_u32(smem + C::OFF_QDO + q.s * 2 * C::Q_BYTES);
         const uint32_t sDO = sQ + C::Q_BYTES;
@@ -517,7 +523,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int t = 0; t < m.n; ++t, ++g) {
           const uint32_t b = (uint32_t)(g & 1);
           const int s = g % NS;
+          trace_ev(p.trace, p.trace_cap, 1, 1, g);
           mbar_wait(&qdo_full[s], (uint32_t)(g / NS) & 1u);
+          trace_ev(p.trace, p.trace_cap, 1, 2, g);
           tc_fence_after();
           const uint32_t sQ = smem_u32(smem + C::OFF_QDO + s * 2 * C::Q_BYTES);
           const uint32_t sDO = sQ + C::Q_BYTES;
@@ -568,9 +576,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t b = (uint32_t)(g & 1);
         float lse2_n = 0.f, dlt_n = 0.f;
         if (t + 1 < m.n) load_stats(t + 1, lse2_n, dlt_n);  // prefetch the next tile's row statistics
+        const bool tr = threadIdx.x == 64;
+        if (tr) trace_ev(p.trace, p.trace_cap, 2, 1, g);
         mbar_wait(&sdp_full[b], (uint32_t)(g >> 1) & 1u);
+        if (tr) trace_ev(p.trace, p.trace_cap, 2, 2, g);
         tc_fence_after();
         if (g >= 2) mbar_wait(&pds_free[b], ((uint32_t)(g >> 1) + 1u) & 1u);  // buffer b free (tile g-2 done)
+        if (tr) trace_ev(p.trace, p.trace_cap, 2, 3, g);
         const uint32_t sP = smem_u32(smem + C::OFF_PDS + (int)b * 2 * C::PB), sDS = sP + C::PB;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -595,6 +607,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         fence_proxy_async_smem();
         tc_fence_before();
         mbar_arrive(&pds_full[b]);
+        if (tr) trace_ev(p.trace, p.trace_cap, 2, 4, g);
         lse2 = lse2_n;
         dlt = dlt_n;
       }
@@ -622,7 +635,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         continue;
       }
       const int st = it & 1;
+      if (threadIdx.x == kEpiTid0) trace_ev(p.trace, p.trace_cap, 3, 1, it);
       mbar_wait(&acc_full[st], (uint32_t)(it >> 1) & 1u);
+      if (threadIdx.x == kEpiTid0) trace_ev(p.trace, p.trace_cap, 3, 2, it);
       tc_fence_after();
       uint32_t rv[64], rk[64];
       tmem_ld64(tbase + lane_off + C::ACC_COL + (uint32_t)(st * 128), rv);
@@ -638,6 +653,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      if (threadIdx.x == kEpiTid0) trace_ev(p.trace, p.trace_cap, 3, 3, it);
       ++it;
     }
   }
@@ -691,6 +707,8 @@ int launch_attn_bwd(int which, const spa2_view& q, const spa2_view& k, const spa
   prm.out0 = (__nv_bfloat16*)out0.ptr;
   prm.o0_sb = out0.sb, prm.o0_sh = out0.sh, prm.o0_sn = out0.sn;
   prm.num_items = (int)(B * H * (which == 0 ? T_m : T_n));
+  prm.trace = g_trace_buf;
+  prm.trace_cap = g_trace_cap;
   const unsigned grid = (unsigned)std::min<int64_t>(prm.num_items, num_sms());
   if (which == 0) {
     auto kern = k_dq<HD>;

@@ -12,6 +12,8 @@
 namespace spa2 {
 
 static thread_local char g_last_error[1024] = "";
+unsigned long long* g_trace_buf = nullptr;
+int g_trace_cap = 0;
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -83,5 +85,11 @@ extern "C" int spa2_device_supported(int device) {
   SPA2_CUDA_TRY(cudaGetDeviceProperties(&prop, device));
   SPA2_REQUIRE(prop.major == 10 && prop.minor == 0, SPA2_ERR_UNSUPPORTED,
                "device %d is sm_%d%d; libspa2 is built for sm_100a only", device, prop.major, prop.minor);
+  return SPA2_OK;
+}
+
+extern "C" int spa2_debug_trace(void* buf, int capacity) {
+  spa2::g_trace_buf = reinterpret_cast<unsigned long long*>(buf);
+  spa2::g_trace_cap = capacity;
   return SPA2_OK;
 }

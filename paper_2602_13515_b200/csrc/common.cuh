@@ -50,3 +50,19 @@ __device__ __forceinline__ double to_f64<__nv_bfloat16>(__nv_bfloat16 x) {
 }
 template <>
 __device__ __forceinline__ double to_f64<__half>(__half x) { return (double)__half2float(x); }
+
+// ---- diagnostic in-kernel trace (CTA 0 only; disabled unless spa2_debug_trace set a buffer) ----
+// buf[0] = event counter; events are (clock64, role<<48 | kind<<32 | index) pairs from buf[2].
+__device__ __forceinline__ void trace_ev(unsigned long long* buf, int cap, int role, int kind, int idx) {
+  if (buf == nullptr || blockIdx.x != 0) return;
+  const unsigned long long t = clock64();
+  const int i = atomicAdd(reinterpret_cast<int*>(buf), 1);
+  if (i < cap) {
+    buf[2 + 2 * i] = t;
+    buf[3 + 2 * i] = ((unsigned long long)role << 48) | ((unsigned long long)kind << 32) | (unsigned)idx;
+  }
+}
+namespace spa2 {
+extern unsigned long long* g_trace_buf;
+extern int g_trace_cap;
+}  // namespace spa2

@@ -1,0 +1,72 @@
+"""Pipeline trace of the dK/dV kernel (CTA 0) at the bench shape — diagnostic.
+
+    python tools/trace_bwd.py
+
+Roles/kinds recorded by the kernel (spa2_debug_trace):
+  producer 0: 1 before waiting for a free Q/dO stage, 2 after (loads issued next)
+  mma      1: 1 before waiting for Q/dO of tile g, 2 after (S/dP issued next),
+              3 before waiting for P/dS of tile g, 4 after (dV/dK issued next)
+  softmax  2: 1 before waiting for S/dP of tile g, 2 after, 3 P/dS buffer free, 4 P/dS written
+  epilog   3: 1 before waiting for the accumulators of item it, 2 after, 3 stores done
+"""
+import math
+import os
+import sys
+from collections import defaultdict
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2602_13515_b200 as spa  # noqa: E402
+from paper_2602_13515_b200 import _lib  # noqa: E402
+from paper_2602_13515_b200 import attention as at  # noqa: E402
+from paper_2602_13515_b200.synthetic import wan_like_qkv  # noqa: E402
+
+
+def main():
+    q, k, v = wan_like_qkv(1, 12, 32760, 128, 0.9, seed=0)
+    do = torch.randn_like(q)
+    cfg = spa.SparsityConfig(0.03, 0.2, 128, 64)
+    bm = at._hybrid_mask_device(q, k, cfg, False)
+    lists = at.mask_lists(bm, 1, 12, 32760)
+    scale = 1 / math.sqrt(128)
+    o, lse = at.fwd(q, k, v, lists, scale)
+    at.bwd(q, k, v, o, do, lse, lists, scale)
+    cap = 1 << 16
+    buf = torch.zeros(2 + 2 * cap, dtype=torch.int64, device="cuda")
+    _lib.load().spa2_debug_trace(_lib.ptr(buf), cap)
+    at.bwd(q, k, v, o, do, lse, lists, scale)
+    torch.cuda.synchronize()
+    _lib.load().spa2_debug_trace(None, 0)
+    n = min(int(buf[0].item()) & 0xFFFFFFFF, cap)
+    ev = buf[2:2 + 2 * n].view(n, 2).cpu().tolist()
+    t0 = min(e[0] for e in ev)
+    rec = defaultdict(dict)
+    for t, code in ev:
+        role, kind, idx = (code >> 48) & 0xFF, (code >> 32) & 0xFFFF, code & 0xFFFFFFFF
+        rec[(role, idx)][kind] = t - t0
+    tiles = sorted(i for (r, i) in rec if r == 2)
+    print(f"events {n}; tiles traced {len(tiles)}; span {max(e[0] for e in ev) - t0} cycles")
+    print(" g | sm_wait S/dP | sm_wait Pbuf | sm_compute | mma wait QdO | mma wait P/dS | prod wait")
+    agg = defaultdict(float)
+    for g in tiles[5:]:
+        s = rec[(2, g)]
+        m = rec.get((1, g), {})
+        pr = rec.get((0, g), {})
+        row = (s.get(2, 0) - s.get(1, 0), s.get(3, 0) - s.get(2, 0), s.get(4, 0) - s.get(3, 0),
+               m.get(2, 0) - m.get(1, 0), m.get(4, 0) - m.get(3, 0), pr.get(2, 0) - pr.get(1, 0))
+        for i, x in enumerate(row):
+            agg[i] += x
+        if g < 40:
+            print(f"{g:3d} | " + " | ".join(f"{x:12d}" for x in row))
+    cnt = max(1, len(tiles) - 5)
+    print("mean | " + " | ".join(f"{agg[i] / cnt:12.0f}" for i in range(6)))
+    # period between consecutive softmax completions
+    done = [rec[(2, g)].get(4, 0) for g in tiles]
+    per = [b - a for a, b in zip(done, done[1:])]
+    per.sort()
+    print("tile period cycles: median", per[len(per) // 2], "p10", per[len(per) // 10], "p90", per[9 * len(per) // 10])
+
+
+if __name__ == "__main__":
+    main()
