@@ -383,14 +383,55 @@ __global__ void __launch_bounds__(kThreads, 1)
 // K6: dK and dV.  Work item = key block; tiles = query blocks keeping it.  Accumulators
 // transposed (TMEM lanes = head dim).
 // ---------------------------------------------------------------------------------------
+// Work-list cursor shared by the roles of the persistent kernels: walks this CTA's items
+// (blockIdx.x, +gridDim.x, ...) skipping empty ones, one tile at a time.
+struct Cursor {
+  int wi, it, t, n, beg, bh, blk, g;
+  bool valid;
+};
+__device__ __forceinline__ void cursor_item(Cursor& c, const BwdParams& p, int nblk) {
+  for (;;) {
+    c.wi += gridDim.x;
+    if (c.wi >= p.num_items) {
+      c.valid = false;
+      return;
+    }
+    const Item m = get_item(p, c.wi, nblk);
+    if (m.n > 0) {
+      c.n = m.n;
+      c.beg = m.beg;
+      c.bh = m.bh;
+      c.blk = m.blk;
+      c.t = 0;
+      ++c.it;
+      c.valid = true;
+      return;
+    }
+  }
+}
+__device__ __forceinline__ void cursor_init(Cursor& c, const BwdParams& p, int nblk) {
+  c.wi = (int)blockIdx.x - (int)gridDim.x;
+  c.it = -1;
+  c.g = 0;
+  c.valid = false;
+  cursor_item(c, p, nblk);
+}
+__device__ __forceinline__ void cursor_next(Cursor& c, const BwdParams& p, int nblk) {
+  ++c.g;
+  if (++c.t >= c.n) cursor_item(c, p, nblk);
+}
+
+constexpr int kDkvThreads = 448;  // 14 warps: TMA, MMA, 8 elementwise, 4 epilogue
+constexpr int kDkvEpi0 = 320;     // first epilogue thread (warp 10)
+
 template <int HD>
 struct DkvCfg {
   static constexpr int NS = 2;
   static constexpr int KV_BYTES = BKV * HD * 2;
   static constexpr int Q_BYTES = BQ * HD * 2;
   static constexpr int PB = BQ * BKV * 2;
-  static constexpr int OFF_KV = 0;                          // [K | V] of the current item
-  static constexpr int OFF_QDO = 2 * KV_BYTES;              // [NS stages][Q | dO]
+  static constexpr int OFF_KV = 0;                            // [K | V] of the current item
+  static constexpr int OFF_QDO = 2 * KV_BYTES;                // [NS stages][Q | dO]
   static constexpr int OFF_PDS = OFF_QDO + NS * 2 * Q_BYTES;  // [2 buffers][P | dS]
   static constexpr int OFF_BAR = OFF_PDS + 2 * 2 * PB;
   static constexpr int NUM_BARS = 2 + 2 * NS + 2 + 2 + 2 + 4;
@@ -399,7 +440,7 @@ struct DkvCfg {
 };
 
 template <int HD>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kDkvThreads, 1)
     k_dkdv(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
            const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO, const BwdParams p) {
   using C = DkvCfg<HD>;
@@ -424,7 +465,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(kv_empty, 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&sdp_full[s], 1);
-      mbar_init(&pds_full[s], 128);
+      mbar_init(&pds_full[s], 256);
       mbar_init(&pds_free[s], 1);
       mbar_init(&acc_full[s], 1);
       mbar_init(&acc_empty[s], 128);
@@ -478,87 +519,109 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
+    // ---------------- MMA issuer: dataflow order ----------------
+    // Two streams of work: S/dP of tile gs (needs its Q/dO, and the S/dP buffer, i.e. at
+    // most one tile ahead of the dV/dK stream) and dV/dK of tile gd (needs its P/dS).
+    // Whichever is ready is issued, so dV/dK never waits behind the next tile's load.
     if (elect_one()) {
       constexpr uint32_t idS = idesc_bf16(BQ, BKV, false, false);
       constexpr uint32_t idT = idesc_bf16(HD, BKV, true, true);
       const uint32_t sK = smem_u32(smem + C::OFF_KV), sV = sK + C::KV_BYTES;
-      struct Pend {
-        int g, it, s;
-        bool first, last, valid;
-      } pd{0, 0, 0, false, false, false};
-      auto issue_dvdk = [&](const Pend& q) {
-        const uint32_t acc = tbase + C::ACC_COL + (uint32_t)((q.it & 1) * 128);
-        const int pb = q.g & 1;
-        if (q.first && q.it >= 2) mbar_wait(&acc_empty[q.it & 1], ((uint32_t)(q.it >> 1) + 1u) & 1u);
-        trace_ev(p.trace, p.trace_cap, 1, 3, q.g);
-        mbar_wait(&pds_full[pb], (uint32_t)(q.g >> 1) & 1u);
-        trace_ev(p.trace, p.trace_cap, 1, 4, q.g);
-        tc_fence_after();
-        const uint32_t sQ = smem_u32(smem + C::OFF_QDO + q.s * 2 * C::Q_BYTES);
-        const uint32_t sDO = sQ + C::Q_BYTES;
-        const uint32_t sP = smem_u32(smem + C::OFF_PDS + pb * 2 * C::PB), sDS = sP + C::PB;
-#pragma unroll
-        for (int ks = 0; ks < BQ / 16; ++ks) {
-          const uint32_t ro = (uint32_t)(ks * 2048);
-          mma_bf16(acc, sw128_desc(sDO + ro, BQ * 128, 1024), sw128_desc(sP + ro, BQ * 128, 1024), idT,
-                   (!q.first || ks > 0) ? 1u : 0u);
-        }
-#pragma unroll
-        for (int ks = 0; ks < BQ / 16; ++ks) {
-          const uint32_t ro = (uint32_t)(ks * 2048);
-          mma_bf16(acc + 64, sw128_desc(sQ + ro, BQ * 128, 1024), sw128_desc(sDS + ro, BQ * 128, 1024), idT,
-                   (!q.first || ks > 0) ? 1u : 0u);
-        }
-        mma_commit(&pds_free[pb]);
-        mma_commit(&qdo_empty[q.s]);
-        if (q.last) mma_commit(&acc_full[q.it & 1]);
-      };
-      int it = 0, g = 0;
-      for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
-        const Item m = get_item(p, wi, p.T_n);
-        if (m.n == 0) continue;
-        mbar_wait(kv_full, (uint32_t)it & 1u);
-        tc_fence_after();
-        for (int t = 0; t < m.n; ++t, ++g) {
-          const uint32_t b = (uint32_t)(g & 1);
-          const int s = g % NS;
-          trace_ev(p.trace, p.trace_cap, 1, 1, g);
-          mbar_wait(&qdo_full[s], (uint32_t)(g / NS) & 1u);
-          trace_ev(p.trace, p.trace_cap, 1, 2, g);
-          tc_fence_after();
-          const uint32_t sQ = smem_u32(smem + C::OFF_QDO + s * 2 * C::Q_BYTES);
-          const uint32_t sDO = sQ + C::Q_BYTES;
-#pragma unroll
-          for (int ks = 0; ks < HD / 16; ++ks) {
-            const uint32_t qo = (uint32_t)((ks * 16 / 64) * BQ * 128 + (ks * 16 % 64) * 2);
-            const uint32_t ko = (uint32_t)((ks * 16 / 64) * BKV * 128 + (ks * 16 % 64) * 2);
-            mma_bf16(tbase + C::S_COL + b * 64, sw128_desc(sQ + qo, 16, 1024), sw128_desc(sK + ko, 16, 1024), idS,
-                     ks > 0 ? 1u : 0u);
+      Cursor cs, cd;
+      cursor_init(cs, p, p.T_n);
+      cursor_init(cd, p, p.T_n);
+      int kv_ready_it = -1;
+      uint64_t t_idle = 0;
+      uint32_t spins = 0;
+      while (cd.valid) {
+        bool progressed = false;
+        if (cs.valid && cs.g - cd.g < 2) {
+          bool ready = true;
+          if (kv_ready_it != cs.it) {
+            ready = mbar_test(kv_full, (uint32_t)cs.it & 1u);
+            if (ready) kv_ready_it = cs.it;
           }
+          const int s = cs.g % NS;
+          if (ready && mbar_test(&qdo_full[s], (uint32_t)(cs.g / NS) & 1u)) {
+            tc_fence_after();
+            trace_ev(p.trace, p.trace_cap, 1, 2, cs.g);
+            const uint32_t b = (uint32_t)(cs.g & 1);
+            const uint32_t sQ = smem_u32(smem + C::OFF_QDO + s * 2 * C::Q_BYTES);
+            const uint32_t sDO = sQ + C::Q_BYTES;
 #pragma unroll
-          for (int ks = 0; ks < HD / 16; ++ks) {
-            const uint32_t qo = (uint32_t)((ks * 16 / 64) * BQ * 128 + (ks * 16 % 64) * 2);
-            const uint32_t ko = (uint32_t)((ks * 16 / 64) * BKV * 128 + (ks * 16 % 64) * 2);
-            mma_bf16(tbase + C::DP_COL + b * 64, sw128_desc(sDO + qo, 16, 1024), sw128_desc(sV + ko, 16, 1024), idS,
-                     ks > 0 ? 1u : 0u);
+            for (int ks = 0; ks < HD / 16; ++ks) {
+              const uint32_t qo = (uint32_t)((ks * 16 / 64) * BQ * 128 + (ks * 16 % 64) * 2);
+              const uint32_t ko = (uint32_t)((ks * 16 / 64) * BKV * 128 + (ks * 16 % 64) * 2);
+              mma_bf16(tbase + C::S_COL + b * 64, sw128_desc(sQ + qo, 16, 1024), sw128_desc(sK + ko, 16, 1024), idS,
+                       ks > 0 ? 1u : 0u);
+            }
+#pragma unroll
+            for (int ks = 0; ks < HD / 16; ++ks) {
+              const uint32_t qo = (uint32_t)((ks * 16 / 64) * BQ * 128 + (ks * 16 % 64) * 2);
+              const uint32_t ko = (uint32_t)((ks * 16 / 64) * BKV * 128 + (ks * 16 % 64) * 2);
+              mma_bf16(tbase + C::DP_COL + b * 64, sw128_desc(sDO + qo, 16, 1024), sw128_desc(sV + ko, 16, 1024),
+                       idS, ks > 0 ? 1u : 0u);
+            }
+            mma_commit(&sdp_full[b]);
+            if (cs.t == cs.n - 1) mma_commit(kv_empty);  // K_j / V_j are only read by S and dP
+            cursor_next(cs, p, p.T_n);
+            progressed = true;
           }
-          mma_commit(&sdp_full[b]);
-          if (t == m.n - 1) mma_commit(kv_empty);  // K_j / V_j are only read by S and dP
-          if (pd.valid) issue_dvdk(pd);
-          pd = Pend{g, it, s, t == 0, t == m.n - 1, true};
         }
-        ++it;
+        if (cd.g < cs.g) {
+          const int pb = cd.g & 1;
+          const bool acc_ok =
+              !(cd.t == 0 && cd.it >= 2) || mbar_test(&acc_empty[cd.it & 1], ((uint32_t)(cd.it >> 1) + 1u) & 1u);
+          if (acc_ok && mbar_test(&pds_full[pb], (uint32_t)(cd.g >> 1) & 1u)) {
+            tc_fence_after();
+            trace_ev(p.trace, p.trace_cap, 1, 4, cd.g);
+            const int s = cd.g % NS;
+            const uint32_t acc = tbase + C::ACC_COL + (uint32_t)((cd.it & 1) * 128);
+            const uint32_t sQ = smem_u32(smem + C::OFF_QDO + s * 2 * C::Q_BYTES);
+            const uint32_t sDO = sQ + C::Q_BYTES;
+            const uint32_t sP = smem_u32(smem + C::OFF_PDS + pb * 2 * C::PB), sDS = sP + C::PB;
+            const bool first = cd.t == 0;
+#pragma unroll
+            for (int ks = 0; ks < BQ / 16; ++ks) {
+              const uint32_t ro = (uint32_t)(ks * 2048);
+              mma_bf16(acc, sw128_desc(sDO + ro, BQ * 128, 1024), sw128_desc(sP + ro, BQ * 128, 1024), idT,
+                       (!first || ks > 0) ? 1u : 0u);
+            }
+#pragma unroll
+            for (int ks = 0; ks < BQ / 16; ++ks) {
+              const uint32_t ro = (uint32_t)(ks * 2048);
+              mma_bf16(acc + 64, sw128_desc(sQ + ro, BQ * 128, 1024), sw128_desc(sDS + ro, BQ * 128, 1024), idT,
+                       (!first || ks > 0) ? 1u : 0u);
+            }
+            mma_commit(&pds_free[pb]);
+            mma_commit(&qdo_empty[s]);
+            if (cd.t == cd.n - 1) mma_commit(&acc_full[cd.it & 1]);
+            cursor_next(cd, p, p.T_n);
+            progressed = true;
+          }
+        }
+        if (progressed) {
+          spins = 0;
+        } else if ((++spins & 1023u) == 0) {
+          if (t_idle == 0) t_idle = globaltimer();
+          else if (globaltimer() - t_idle > SPA2_WATCHDOG_NS) {
+            printf("spa2 watchdog: k_dkdv MMA issuer stalled (block %d, gs %d, gd %d)\n", blockIdx.x, cs.g, cd.g);
+            __trap();
+          }
+        }
+        if (progressed) t_idle = 0;
       }
-      if (pd.valid) issue_dvdk(pd);
     }
     __syncwarp();
-  } else if (warp < 6) {
-    // ---------------- P / dS warps (2..5) ----------------
+  } else if (warp < 10) {
+    // ---------------- P / dS warps (2..9): 2 warps per TMEM lane quarter, 32 columns each ----
     const int q4 = warp & 3;
+    const int half = (warp - 2) >> 2;
     const int row = q4 * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    const uint32_t col0 = (uint32_t)(32 * half);
     const float sl2 = p.sl2;
+    const bool tr = threadIdx.x == 64;
     int g = 0;
     for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
       const Item m = get_item(p, wi, p.T_n);
@@ -576,33 +639,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t b = (uint32_t)(g & 1);
         float lse2_n = 0.f, dlt_n = 0.f;
         if (t + 1 < m.n) load_stats(t + 1, lse2_n, dlt_n);  // prefetch the next tile's row statistics
-        const bool tr = threadIdx.x == 64;
         if (tr) trace_ev(p.trace, p.trace_cap, 2, 1, g);
         mbar_wait(&sdp_full[b], (uint32_t)(g >> 1) & 1u);
         if (tr) trace_ev(p.trace, p.trace_cap, 2, 2, g);
         tc_fence_after();
+        uint32_t sr[32], dr[32];
+        tmem_ld32(tbase + lane_off + C::S_COL + b * 64 + col0, sr);
+        tmem_ld32(tbase + lane_off + C::DP_COL + b * 64 + col0, dr);
+        uint32_t pp[16], pd[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          const float p0 = ex2(fmaf(__uint_as_float(sr[2 * c]), sl2, -lse2));
+          const float p1 = ex2(fmaf(__uint_as_float(sr[2 * c + 1]), sl2, -lse2));
+          pp[c] = pack_bf16(p0, p1);
+          pd[c] = pack_bf16(p0 * (__uint_as_float(dr[2 * c]) - dlt), p1 * (__uint_as_float(dr[2 * c + 1]) - dlt));
+        }
         if (g >= 2) mbar_wait(&pds_free[b], ((uint32_t)(g >> 1) + 1u) & 1u);  // buffer b free (tile g-2 done)
         if (tr) trace_ev(p.trace, p.trace_cap, 2, 3, g);
         const uint32_t sP = smem_u32(smem + C::OFF_PDS + (int)b * 2 * C::PB), sDS = sP + C::PB;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          uint32_t sr[32], dr[32];
-          tmem_ld32(tbase + lane_off + C::S_COL + b * 64 + (uint32_t)(32 * h), sr);
-          tmem_ld32(tbase + lane_off + C::DP_COL + b * 64 + (uint32_t)(32 * h), dr);
-          uint32_t pp[16], pd[16];
-#pragma unroll
-          for (int c = 0; c < 16; ++c) {
-            const float p0 = ex2(fmaf(__uint_as_float(sr[2 * c]), sl2, -lse2));
-            const float p1 = ex2(fmaf(__uint_as_float(sr[2 * c + 1]), sl2, -lse2));
-            pp[c] = pack_bf16(p0, p1);
-            pd[c] = pack_bf16(p0 * (__uint_as_float(dr[2 * c]) - dlt), p1 * (__uint_as_float(dr[2 * c + 1]) - dlt));
-          }
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const uint32_t off = sw128_offset((uint32_t)row, (uint32_t)(4 * h + u));
-            st_shared_v4(sP + off, pp[4 * u], pp[4 * u + 1], pp[4 * u + 2], pp[4 * u + 3]);
-            st_shared_v4(sDS + off, pd[4 * u], pd[4 * u + 1], pd[4 * u + 2], pd[4 * u + 3]);
-          }
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t off = sw128_offset((uint32_t)row, (uint32_t)(4 * half + u));
+          st_shared_v4(sP + off, pp[4 * u], pp[4 * u + 1], pp[4 * u + 2], pp[4 * u + 3]);
+          st_shared_v4(sDS + off, pd[4 * u], pd[4 * u + 1], pd[4 * u + 2], pd[4 * u + 3]);
         }
         fence_proxy_async_smem();
         tc_fence_before();
@@ -613,7 +672,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // ---------------- epilogue warps (6..9): TMEM -> registers -> coalesced global stores ----
+    // ---------------- epilogue warps (10..13): TMEM -> registers -> coalesced global stores ----
     const int q4 = warp & 3;
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
     const int dim = (HD == 128) ? q4 * 32 + lane : 16 * q4 + lane;  // M=64 accumulators: lanes 0-15 per quarter
@@ -635,25 +694,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         continue;
       }
       const int st = it & 1;
-      if (threadIdx.x == kEpiTid0) trace_ev(p.trace, p.trace_cap, 3, 1, it);
+      if (threadIdx.x == kDkvEpi0) trace_ev(p.trace, p.trace_cap, 3, 1, it);
       mbar_wait(&acc_full[st], (uint32_t)(it >> 1) & 1u);
-      if (threadIdx.x == kEpiTid0) trace_ev(p.trace, p.trace_cap, 3, 2, it);
+      if (threadIdx.x == kDkvEpi0) trace_ev(p.trace, p.trace_cap, 3, 2, it);
       tc_fence_after();
-      uint32_t rv[64], rk[64];
-      tmem_ld64(tbase + lane_off + C::ACC_COL + (uint32_t)(st * 128), rv);
-      tmem_ld64(tbase + lane_off + C::ACC_COL + (uint32_t)(st * 128 + 64), rk);
-      tc_fence_before();
-      mbar_arrive(&acc_empty[st]);  // accumulators are in registers: TMEM set reusable
-      if (own) {
+#pragma unroll 1
+      for (int which = 0; which < 2; ++which) {
+        uint32_t r64[64];
+        tmem_ld64(tbase + lane_off + C::ACC_COL + (uint32_t)(st * 128 + which * 64), r64);
+        if (which == 1) {
+          tc_fence_before();
+          mbar_arrive(&acc_empty[st]);  // both accumulators read: TMEM set reusable
+        }
+        __nv_bfloat16* dst = which ? dk : dv;
+        const int64_t sn = which ? p.o0_sn : p.o1_sn;
+        const float mul = which ? p.scale : 1.f;
+        if (own) {
 #pragma unroll
-        for (int r = 0; r < BKV; ++r) {
-          if (r < rows) {
-            dv[(int64_t)r * p.o1_sn] = __float2bfloat16(__uint_as_float(rv[r]));
-            dk[(int64_t)r * p.o0_sn] = __float2bfloat16(__uint_as_float(rk[r]) * p.scale);
-          }
+          for (int r = 0; r < BKV; ++r)
+            if (r < rows) dst[(int64_t)r * sn] = __float2bfloat16(__uint_as_float(r64[r]) * mul);
         }
       }
-      if (threadIdx.x == kEpiTid0) trace_ev(p.trace, p.trace_cap, 3, 3, it);
+      if (threadIdx.x == kDkvEpi0) trace_ev(p.trace, p.trace_cap, 3, 3, it);
       ++it;
     }
   }
@@ -719,7 +781,7 @@ int launch_attn_bwd(int which, const spa2_view& q, const spa2_view& k, const spa
     prm.o1_sb = out1->sb, prm.o1_sh = out1->sh, prm.o1_sn = out1->sn;
     auto kern = k_dkdv<HD>;
     SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvCfg<HD>::SMEM));
-    kern<<<grid, kThreads, DkvCfg<HD>::SMEM, st>>>(m.q, m.k, m.v, m.dout, prm);
+    kern<<<grid, kDkvThreads, DkvCfg<HD>::SMEM, st>>>(m.q, m.k, m.v, m.dout, prm);
   }
   SPA2_LAUNCH_CHECK();
   return SPA2_OK;

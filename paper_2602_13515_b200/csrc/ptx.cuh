@@ -71,6 +71,17 @@ __device__ __forceinline__ uint32_t mbar_try_wait(uint32_t addr, uint32_t parity
       : "memory");
   return ok;
 }
+// Non-blocking probe: has the phase with parity `parity` of `bar` completed?
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\tmbarrier.test_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 // Wait until the phase with parity `parity` of `bar` has completed.  Traps (instead of
 // hanging the GPU) if it does not happen within SPA2_WATCHDOG_NS.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
