@@ -198,7 +198,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int t = 0; t < m.n; ++t, ++g) {
           const int j = p.idx[m.beg + t];
           const int sk = g % NSK, sv = g % NSV;
+          trace_ev(p.trace, p.trace_cap, 0, 1, g);
           if (g >= NSK) mbar_wait(&k_empty[sk], ((uint32_t)(g / NSK) + 1u) & 1u);
+          trace_ev(p.trace, p.trace_cap, 0, 2, g);
           mbar_expect_tx(&k_full[sk], C::KV_BYTES);
 #pragma unroll
           for (int c = 0; c < HD / 64; ++c)
@@ -226,7 +228,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto issue_dq = [&](const Pend& q) {
         const uint32_t acc = tbase + C::ACC_COL + (uint32_t)((q.it & 1) * 128);
         if (q.first && q.it >= 2) mbar_wait(&acc_empty[q.it & 1], ((uint32_t)(q.it >> 1) + 1u) & 1u);
+        trace_ev(p.trace, p.trace_cap, 1, 3, q.g);
         mbar_wait(&ds_full[q.g & 1], (uint32_t)(q.g >> 1) & 1u);
+        trace_ev(p.trace, p.trace_cap, 1, 4, q.g);
         tc_fence_after();
         const uint32_t sK = smem_u32(smem + C::OFF_K + q.sk * C::KV_BYTES);
 #pragma unroll
@@ -249,8 +253,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int t = 0; t < m.n; ++t, ++g) {
           const uint32_t b = (uint32_t)(g & 1);
           const int sk = g % NSK, sv = g % NSV;
+          trace_ev(p.trace, p.trace_cap, 1, 1, g);
           if (g >= 2) mbar_wait(dq_done, (uint32_t)(g - 2) & 1u);  // dS_{g-2} lives in S[b]
+          trace_ev(p.trace, p.trace_cap, 1, 5, g);
           mbar_wait(&k_full[sk], (uint32_t)(g / NSK) & 1u);
+          trace_ev(p.trace, p.trace_cap, 1, 2, g);
           tc_fence_after();
           const uint32_t sK = smem_u32(smem + C::OFF_K + sk * C::KV_BYTES);
 #pragma unroll
@@ -298,7 +305,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int t = 0; t < m.n; ++t, ++g) {
         const uint32_t b = (uint32_t)(g & 1);
         const bool tail = p.idx[m.beg + t] == p.T_n - 1 && kv_tail < BKV;
+        const bool tr = threadIdx.x == 64;
+        if (tr) trace_ev(p.trace, p.trace_cap, 2, 1, g);
         mbar_wait(&s_full[b], (uint32_t)(g >> 1) & 1u);
+        if (tr) trace_ev(p.trace, p.trace_cap, 2, 2, g);
         tc_fence_after();
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -321,6 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&ds_full[b]);
+        if (tr) trace_ev(p.trace, p.trace_cap, 2, 4, g);
       }
     }
   } else {

@@ -47,24 +47,26 @@ def main():
         rec[(role, idx)][kind] = t - t0
     tiles = sorted(i for (r, i) in rec if r == 2)
     print(f"events {n}; tiles traced {len(tiles)}; span {max(e[0] for e in ev) - t0} cycles")
-    print(" g | sm_wait S/dP | sm_wait Pbuf | sm_compute | mma wait QdO | mma wait P/dS | prod wait")
-    agg = defaultdict(float)
-    for g in tiles[5:]:
-        s = rec[(2, g)]
-        m = rec.get((1, g), {})
-        pr = rec.get((0, g), {})
-        row = (s.get(2, 0) - s.get(1, 0), s.get(3, 0) - s.get(2, 0), s.get(4, 0) - s.get(3, 0),
-               m.get(2, 0) - m.get(1, 0), m.get(4, 0) - m.get(3, 0), pr.get(2, 0) - pr.get(1, 0))
+    print("stage lifetime of tile g (cycles): load issued -> S/dP issued -> softmax done -> dV/dK issued -> "
+          "stage reloaded (tile g+2)")
+    cols = ["load->SdP", "SdP->smx_done", "smx->dVdK", "dVdK->reload", "smx wait S/dP", "smx wait Pbuf", "smx compute"]
+    agg, cnt = defaultdict(float), 0
+    for g in tiles[5:-3]:
+        ld, sdp = rec.get((0, g), {}).get(2), rec.get((1, g), {}).get(2)
+        smx, dvdk = rec.get((2, g), {}), rec.get((1, g), {}).get(4)
+        rel = rec.get((0, g + 2), {}).get(2)
+        if None in (ld, sdp, dvdk, rel) or 4 not in smx:
+            continue
+        row = (sdp - ld, smx[4] - sdp, dvdk - smx[4], rel - dvdk, smx[2] - smx[1], smx[3] - smx[2], smx[4] - smx[3])
         for i, x in enumerate(row):
             agg[i] += x
-        if g < 40:
-            print(f"{g:3d} | " + " | ".join(f"{x:12d}" for x in row))
-    cnt = max(1, len(tiles) - 5)
-    print("mean | " + " | ".join(f"{agg[i] / cnt:12.0f}" for i in range(6)))
-    # period between consecutive softmax completions
+        cnt += 1
+        if cnt <= 12:
+            print(f"{g:4d} " + " ".join(f"{x:>14d}" for x in row))
+    print("mean " + " ".join(f"{agg[i] / max(cnt, 1):>14.0f}" for i in range(len(cols))))
+    print("     " + " ".join(f"{c:>14s}" for c in cols))
     done = [rec[(2, g)].get(4, 0) for g in tiles]
-    per = [b - a for a, b in zip(done, done[1:])]
-    per.sort()
+    per = sorted(b - a for a, b in zip(done, done[1:]))
     print("tile period cycles: median", per[len(per) // 2], "p10", per[len(per) // 10], "p90", per[9 * len(per) // 10])
 
 
