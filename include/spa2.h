@@ -150,7 +150,8 @@ int spa2_probe_mma_rate(int m, int n, int k, int a_mn, int b_mn, int a_tmem, int
                         unsigned long long* cycles, void* stream);
 
 /* Diagnostic: record per-role pipeline events of CTA 0 of the next backward launches into a
- * device buffer (u64[2 + 2*capacity], buf[0] must be zeroed by the caller); NULL disables. */
+ * zeroed device buffer u64[2 + capacity]: clock64 of event (role, index, kind) at
+ * buf[2 + role*(capacity/4) + index*8 + kind]; NULL disables. */
 int spa2_debug_trace(void* buf, int capacity);
 
 #ifdef __cplusplus

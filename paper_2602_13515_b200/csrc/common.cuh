@@ -52,15 +52,12 @@ template <>
 __device__ __forceinline__ double to_f64<__half>(__half x) { return (double)__half2float(x); }
 
 // ---- diagnostic in-kernel trace (CTA 0 only; disabled unless spa2_debug_trace set a buffer) ----
-// buf[0] = event counter; events are (clock64, role<<48 | kind<<32 | index) pairs from buf[2].
+// Fixed slot per (role, index, kind): buf[2 + role*(cap/4) + index*8 + kind] = clock64.  Plain
+// stores, no atomics, so tracing barely perturbs the pipeline it observes.
 __device__ __forceinline__ void trace_ev(unsigned long long* buf, int cap, int role, int kind, int idx) {
   if (buf == nullptr || blockIdx.x != 0) return;
-  const unsigned long long t = clock64();
-  const int i = atomicAdd(reinterpret_cast<int*>(buf), 1);
-  if (i < cap) {
-    buf[2 + 2 * i] = t;
-    buf[3 + 2 * i] = ((unsigned long long)role << 48) | ((unsigned long long)kind << 32) | (unsigned)idx;
-  }
+  const int slot = idx * 8 + kind;
+  if (slot < cap / 4) buf[2 + role * (cap / 4) + slot] = clock64();
 }
 namespace spa2 {
 extern unsigned long long* g_trace_buf;

@@ -33,20 +33,25 @@ def main():
     o, lse = at.fwd(q, k, v, lists, scale)
     at.bwd(q, k, v, o, do, lse, lists, scale)
     cap = 1 << 16
-    buf = torch.zeros(2 + 2 * cap, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(2 + cap, dtype=torch.int64, device="cuda")
     _lib.load().spa2_debug_trace(_lib.ptr(buf), cap)
     at.bwd(q, k, v, o, do, lse, lists, scale)
     torch.cuda.synchronize()
     _lib.load().spa2_debug_trace(None, 0)
-    n = min(int(buf[0].item()) & 0xFFFFFFFF, cap)
-    ev = buf[2:2 + 2 * n].view(n, 2).cpu().tolist()
-    t0 = min(e[0] for e in ev)
+    R = cap // 4
+    raw = buf[2:].view(4, R).cpu()
     rec = defaultdict(dict)
-    for t, code in ev:
-        role, kind, idx = (code >> 48) & 0xFF, (code >> 32) & 0xFFFF, code & 0xFFFFFFFF
-        rec[(role, idx)][kind] = t - t0
+    t0 = None
+    nz = raw.nonzero().tolist()
+    for role, slot in nz:
+        t = int(raw[role, slot])
+        t0 = t if t0 is None else min(t0, t)
+    for role, slot in nz:
+        rec[(role, slot // 8)][slot % 8] = int(raw[role, slot]) - t0
+    n = len(nz)
+    ev = [(0, 0)]
     tiles = sorted(i for (r, i) in rec if r == 2)
-    print(f"events {n}; tiles traced {len(tiles)}; span {max(e[0] for e in ev) - t0} cycles")
+    print(f"events {n}; tiles traced {len(tiles)}")
     print("stage lifetime of tile g (cycles): load issued -> S/dP issued -> softmax done -> dV/dK issued -> "
           "stage reloaded (tile g+2)")
     cols = ["load->SdP", "SdP->smx_done", "smx->dVdK", "dVdK->reload", "smx wait S/dP", "smx wait Pbuf", "smx compute"]

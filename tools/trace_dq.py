@@ -24,19 +24,25 @@ lib = _lib.load()
 _lib.check(lib.spa2_bwd_delta(_lib.view4(o), _lib.view4(do), _lib.ptr(delta), 0, 1, 12, 32760, 128, st), "d")
 dq = torch.empty_like(q)
 cap = 1 << 16
-buf = torch.zeros(2 + 2 * cap, dtype=torch.int64, device="cuda")
+buf = torch.zeros(2 + cap, dtype=torch.int64, device="cuda")
 lib.spa2_debug_trace(_lib.ptr(buf), cap)
 _lib.check(lib.spa2_bwd_dq(_lib.view4(q), _lib.view4(k), _lib.view4(v), _lib.view4(do), _lib.ptr(lse), _lib.ptr(delta),
                            _lib.view4(dq), 0, 1, 12, 32760, 128, 128, 64, _lib.ptr(lists.row_ptr), _lib.ptr(lists.row_idx),
                            _lib.ptr(lists.row_order), scale, st), "dq")
 torch.cuda.synchronize()
 lib.spa2_debug_trace(None, 0)
-n = min(int(buf[0].item()) & 0xFFFFFFFF, cap)
-ev = buf[2:2 + 2 * n].view(n, 2).cpu().tolist()
-t0 = min(e[0] for e in ev)
+R = cap // 4
+raw = buf[2:].view(4, R).cpu()
 rec = defaultdict(dict)
-for t, code in ev:
-    rec[((code >> 48) & 0xFF, code & 0xFFFFFFFF)][(code >> 32) & 0xFFFF] = t - t0
+t0 = None
+nz = raw.nonzero().tolist()
+for role, slot in nz:
+    t = int(raw[role, slot])
+    t0 = t if t0 is None else min(t0, t)
+for role, slot in nz:
+    rec[(role, slot // 8)][slot % 8] = int(raw[role, slot]) - t0
+n = len(nz)
+ev = [(0, 0)]
 tiles = sorted(i for (r, i) in rec if r == 2)
 cols = ["mma wait dq_done", "mma wait K", "mma wait dS", "smx wait S", "smx compute", "prod wait Kslot"]
 agg, cnt = defaultdict(float), 0
