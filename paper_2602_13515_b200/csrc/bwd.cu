@@ -112,17 +112,16 @@ __global__ void __launch_bounds__(256) k_delta(spa2_view o, spa2_view dout, floa
 // ---------------------------------------------------------------------------------------
 template <int HD>
 struct DqCfg {
-  static constexpr int NSK = 4, NSV = 2, NB = 3;  // K ring, V ring, S/dP TMEM ring depth
+  static constexpr int NSK = 3, NSV = 2;
   static constexpr int Q_BYTES = BQ * HD * 2;
   static constexpr int KV_BYTES = BKV * HD * 2;
   static constexpr int OFF_QDO = 0;  // [2 item stages][Q | dO]
   static constexpr int OFF_K = 4 * Q_BYTES;
   static constexpr int OFF_V = OFF_K + NSK * KV_BYTES;
   static constexpr int OFF_BAR = OFF_V + NSV * KV_BYTES;
-  static constexpr int NUM_BARS = 4 + 2 * NSK + 2 * NSV + 3 * NB + 2;
+  static constexpr int NUM_BARS = 4 + 2 * NSK + 2 * NSV + 2 + 2 + 1 + 4;
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;
-  // TMEM: S[b] at 64b, dP[b] at 192 + 64b (b < 3), dQ accumulator at 384
-  static constexpr uint32_t S_COL = 0, DP_COL = 192, ACC_COL = 384;
+  static constexpr uint32_t S_COL = 0, DP_COL = 128, ACC_COL = 256;
 };
 
 template <int HD>
@@ -131,7 +130,7 @@ __global__ void __launch_bounds__(kThreads, 1)
          const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
          const __grid_constant__ CUtensorMap tmDQ, const BwdParams p) {
   using C = DqCfg<HD>;
-  constexpr int NSK = C::NSK, NSV = C::NSV, NB = C::NB;
+  constexpr int NSK = C::NSK, NSV = C::NSV;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* qdo_full = bars;            // [2]
@@ -140,12 +139,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* k_empty = k_full + NSK;     // [NSK]
   uint64_t* v_full = k_empty + NSK;     // [NSV]
   uint64_t* v_empty = v_full + NSV;     // [NSV]
-  uint64_t* s_full = v_empty + NSV;     // [NB] S and dP of tile g landed in buffer g % NB
-  uint64_t* ds_full = s_full + NB;      // [NB] dS of tile g packed into TMEM
-  uint64_t* dq_done = ds_full + NB;     // [NB] dQ MMA of tile g done (buffer g % NB reusable)
-  uint64_t* acc_full = dq_done + NB;    // dQ of item `it` complete
-  uint64_t* acc_empty = acc_full + 1;   // epilogue has read it
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  uint64_t* s_full = v_empty + NSV;     // [2] S and dP of tile g landed
+  uint64_t* ds_full = s_full + 2;       // [2] dS of tile g packed into TMEM
+  uint64_t* dq_done = ds_full + 2;      // one completion per dQ MMA group
+  uint64_t* acc_full = dq_done + 1;     // [2]
+  uint64_t* acc_empty = acc_full + 2;   // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = (int)warp_id(), lane = (int)lane_id();
   if (threadIdx.x == 0) {
@@ -153,6 +152,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < 2; ++s) {
       mbar_init(&qdo_full[s], 1);
       mbar_init(&qdo_empty[s], 1);
+      mbar_init(&s_full[s], 1);
+      mbar_init(&ds_full[s], 128);
+      mbar_init(&acc_full[s], 1);
+      mbar_init(&acc_empty[s], 128);
     }
     for (int s = 0; s < NSK; ++s) {
       mbar_init(&k_full[s], 1);
@@ -162,13 +165,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], 1);
     }
-    for (int b = 0; b < NB; ++b) {
-      mbar_init(&s_full[b], 1);
-      mbar_init(&ds_full[b], 128);
-      mbar_init(&dq_done[b], 1);
-    }
-    mbar_init(acc_full, 1);
-    mbar_init(acc_empty, 128);
+    mbar_init(dq_done, 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tmem_holder, 512);
@@ -229,20 +226,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         bool first, last, valid;
       } pd{0, 0, 0, false, false, false};
       auto issue_dq = [&](const Pend& q) {
-        const int b = q.g % NB;
-        if (q.first && q.it >= 1) mbar_wait(acc_empty, (uint32_t)(q.it - 1) & 1u);
+        const uint32_t acc = tbase + C::ACC_COL + (uint32_t)((q.it & 1) * 128);
+        if (q.first && q.it >= 2) mbar_wait(&acc_empty[q.it & 1], ((uint32_t)(q.it >> 1) + 1u) & 1u);
         trace_ev(p.trace, p.trace_cap, 1, 3, q.g);
-        mbar_wait(&ds_full[b], (uint32_t)(q.g / NB) & 1u);
+        mbar_wait(&ds_full[q.g & 1], (uint32_t)(q.g >> 1) & 1u);
         trace_ev(p.trace, p.trace_cap, 1, 4, q.g);
         tc_fence_after();
         const uint32_t sK = smem_u32(smem + C::OFF_K + q.sk * C::KV_BYTES);
 #pragma unroll
         for (int ks = 0; ks < BKV / 16; ++ks)
-          mma_bf16_ts(tbase + C::ACC_COL, tbase + C::S_COL + (uint32_t)(b * 64 + ks * 8),
+          mma_bf16_ts(acc, tbase + C::S_COL + (uint32_t)((q.g & 1) * 64 + ks * 8),
                       sw128_desc(sK + (uint32_t)(ks * 2048), BKV * 128, 1024), idQ, (!q.first || ks > 0) ? 1u : 0u);
-        mma_commit(&dq_done[b]);
+        mma_commit(dq_done);
         mma_commit(&k_empty[q.sk]);
-        if (q.last) mma_commit(acc_full);
+        if (q.last) mma_commit(&acc_full[q.it & 1]);
       };
       int it = 0, g = 0;
       for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
@@ -254,10 +251,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t sQ = smem_u32(smem + C::OFF_QDO + st * 2 * C::Q_BYTES);
         const uint32_t sDO = sQ + C::Q_BYTES;
         for (int t = 0; t < m.n; ++t, ++g) {
-          const int b = g % NB;
+          const uint32_t b = (uint32_t)(g & 1);
           const int sk = g % NSK, sv = g % NSV;
           trace_ev(p.trace, p.trace_cap, 1, 1, g);
-          if (g >= NB) mbar_wait(&dq_done[b], ((uint32_t)(g / NB) + 1u) & 1u);  // dS_{g-3} lives in S[b]
+          if (g >= 2) mbar_wait(dq_done, (uint32_t)(g - 2) & 1u);  // dS_{g-2} lives in S[b]
           trace_ev(p.trace, p.trace_cap, 1, 5, g);
           mbar_wait(&k_full[sk], (uint32_t)(g / NSK) & 1u);
           trace_ev(p.trace, p.trace_cap, 1, 2, g);
@@ -267,8 +264,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int ks = 0; ks < HD / 16; ++ks) {
             const uint32_t qo = (uint32_t)((ks * 16 / 64) * BQ * 128 + (ks * 16 % 64) * 2);
             const uint32_t ko = (uint32_t)((ks * 16 / 64) * BKV * 128 + (ks * 16 % 64) * 2);
-            mma_bf16(tbase + C::S_COL + (uint32_t)(b * 64), sw128_desc(sQ + qo, 16, 1024),
-                     sw128_desc(sK + ko, 16, 1024), idS, ks > 0 ? 1u : 0u);
+            mma_bf16(tbase + C::S_COL + b * 64, sw128_desc(sQ + qo, 16, 1024), sw128_desc(sK + ko, 16, 1024), idS,
+                     ks > 0 ? 1u : 0u);
           }
           mbar_wait(&v_full[sv], (uint32_t)(g / NSV) & 1u);
           tc_fence_after();
@@ -277,8 +274,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int ks = 0; ks < HD / 16; ++ks) {
             const uint32_t qo = (uint32_t)((ks * 16 / 64) * BQ * 128 + (ks * 16 % 64) * 2);
             const uint32_t vo = (uint32_t)((ks * 16 / 64) * BKV * 128 + (ks * 16 % 64) * 2);
-            mma_bf16(tbase + C::DP_COL + (uint32_t)(b * 64), sw128_desc(sDO + qo, 16, 1024),
-                     sw128_desc(sV + vo, 16, 1024), idS, ks > 0 ? 1u : 0u);
+            mma_bf16(tbase + C::DP_COL + b * 64, sw128_desc(sDO + qo, 16, 1024), sw128_desc(sV + vo, 16, 1024), idS,
+                     ks > 0 ? 1u : 0u);
           }
           mma_commit(&s_full[b]);
           mma_commit(&v_empty[sv]);
@@ -297,7 +294,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
     const int kv_tail = p.N - (p.T_n - 1) * BKV;
     const float sl2 = p.sl2;
-    const bool tr = threadIdx.x == 64;
     int g = 0;
     for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
       const Item m = get_item(p, wi, p.T_m);
@@ -307,17 +303,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float lse2 = valid ? p.lse[(int64_t)m.bh * p.N + tok] * kLog2e : INFINITY;
       const float dlt = valid ? p.delta[(int64_t)m.bh * p.N + tok] : 0.f;
       for (int t = 0; t < m.n; ++t, ++g) {
-        const int b = g % NB;
+        const uint32_t b = (uint32_t)(g & 1);
         const bool tail = p.idx[m.beg + t] == p.T_n - 1 && kv_tail < BKV;
+        const bool tr = threadIdx.x == 64;
         if (tr) trace_ev(p.trace, p.trace_cap, 2, 1, g);
-        mbar_wait(&s_full[b], (uint32_t)(g / NB) & 1u);
+        mbar_wait(&s_full[b], (uint32_t)(g >> 1) & 1u);
         if (tr) trace_ev(p.trace, p.trace_cap, 2, 2, g);
         tc_fence_after();
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           uint32_t sr[32], dr[32];
-          tmem_ld32(tbase + lane_off + C::S_COL + (uint32_t)(b * 64 + 32 * h), sr);
-          tmem_ld32(tbase + lane_off + C::DP_COL + (uint32_t)(b * 64 + 32 * h), dr);
+          tmem_ld32(tbase + lane_off + C::S_COL + b * 64 + (uint32_t)(32 * h), sr);
+          tmem_ld32(tbase + lane_off + C::DP_COL + b * 64 + (uint32_t)(32 * h), dr);
           uint32_t pk[16];
 #pragma unroll
           for (int c = 0; c < 16; ++c) {
@@ -329,7 +326,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             pk[c] = pack_bf16(p0 * (__uint_as_float(dr[2 * c]) - dlt), p1 * (__uint_as_float(dr[2 * c + 1]) - dlt));
           }
-          tmem_st16(tbase + lane_off + C::S_COL + (uint32_t)(b * 64 + 16 * h), pk);
+          tmem_st16(tbase + lane_off + C::S_COL + b * 64 + (uint32_t)(16 * h), pk);
         }
         tmem_st_wait();
         tc_fence_before();
@@ -355,27 +352,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         continue;
       }
       const int st = it & 1;
-      mbar_wait(acc_full, (uint32_t)it & 1u);
+      mbar_wait(&acc_full[st], (uint32_t)(it >> 1) & 1u);
       tc_fence_after();
       uint8_t* sOut = smem + C::OFF_QDO + st * 2 * C::Q_BYTES;  // Q of this item is dead
       fence_proxy_async_smem();
-      uint32_t pk[HD / 2];
-#pragma unroll
+#pragma unroll 1
       for (int c0 = 0; c0 < HD; c0 += 32) {
         uint32_t o[32];
-        tmem_ld32(tbase + lane_off + C::ACC_COL + (uint32_t)c0, o);
+        tmem_ld32(tbase + lane_off + C::ACC_COL + (uint32_t)(st * 128 + c0), o);
+        uint32_t pk[16];
 #pragma unroll
         for (int c = 0; c < 16; ++c)
-          pk[c0 / 2 + c] = pack_bf16(__uint_as_float(o[2 * c]) * p.scale, __uint_as_float(o[2 * c + 1]) * p.scale);
+          pk[c] = pack_bf16(__uint_as_float(o[2 * c]) * p.scale, __uint_as_float(o[2 * c + 1]) * p.scale);
+        const uint32_t base = smem_u32(sOut + (c0 / 64) * BQ * 128);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          st_shared_v4(base + sw128_offset((uint32_t)row, (uint32_t)((c0 % 64) / 8 + u)), pk[4 * u], pk[4 * u + 1],
+                       pk[4 * u + 2], pk[4 * u + 3]);
       }
       tc_fence_before();
-      mbar_arrive(acc_empty);  // dQ is in registers: the accumulator is reusable
-#pragma unroll
-      for (int u = 0; u < HD / 8; ++u) {
-        const uint32_t base = smem_u32(sOut + (u / 8) * BQ * 128);
-        st_shared_v4(base + sw128_offset((uint32_t)row, (uint32_t)(u % 8)), pk[4 * u], pk[4 * u + 1], pk[4 * u + 2],
-                     pk[4 * u + 3]);
-      }
+      mbar_arrive(&acc_empty[st]);
       fence_proxy_async_smem();
       named_bar_sync(1, 128);
       if (threadIdx.x == kEpiTid0) {
@@ -394,6 +390,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tmem_dealloc(tbase, 512);
 }
 
+// ---------------------------------------------------------------------------------------
+// K6: dK and dV.  Work item = key block; tiles = query blocks keeping it.  Accumulators
+// transposed (TMEM lanes = head dim).
+// ---------------------------------------------------------------------------------------
 // Work-list cursor shared by the roles of the persistent kernels: walks this CTA's items
 // (blockIdx.x, +gridDim.x, ...) skipping empty ones, one tile at a time.
 struct Cursor {
