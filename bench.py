@@ -289,16 +289,14 @@ def gpu_arm(args, rank: int, world: int, dev):
 
     # ---- e2e through the public API with host buffers ----
     if not args.no_e2e:
+        from paper_2602_13515_b200.host import HostPipeline
+
         hq, hk, hv, hdo = (t.cpu().pin_memory() for t in (q, k, v, do))
         outs = [torch.empty(q.shape, dtype=q.dtype).pin_memory() for _ in range(4)]
+        pipe = HostPipeline(dev, groups=args.e2e_groups)
 
         def e2e_step():
-            qs, ks, vs = (t.to(dev, non_blocking=True).requires_grad_(True) for t in (hq, hk, hv))
-            dod = hdo.to(dev, non_blocking=True)
-            r = spa.sparse_attention(qs, ks, vs, cfg, check_finite=False)
-            r.out.backward(dod)
-            for dst, src in zip(outs, (r.out, qs.grad, ks.grad, vs.grad)):
-                dst.copy_(src, non_blocking=True)
+            pipe.fwd_bwd(hq, hk, hv, hdo, cfg, *outs)
 
         for _ in range(2):
             e2e_step()
@@ -320,7 +318,8 @@ def gpu_arm(args, rank: int, world: int, dev):
         nbytes = q.numel() * q.element_size()
         out["e2e"] = {"value": world * dense_equiv_flops() / (e_step * 1e-3) / 1e12, "unit": UNIT,
                       "h2d_bytes_per_step": 4 * nbytes, "d2h_bytes_per_step": 4 * nbytes, "ms_per_step": e_step,
-                      "steps": n_e2e}
+                      "steps": n_e2e, "api": f"paper_2602_13515_b200.host.HostPipeline.fwd_bwd "
+                                             f"({args.e2e_groups} head groups, H2D/compute/D2H overlapped)"}
 
     # ---- dense baselines on the same GPU (rank 0, N=1) ----
     if rank == 0 and world == 1 and not args.no_dense:
@@ -395,6 +394,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--e2e-groups", type=int, default=4)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
