@@ -394,7 +394,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
-    ap.add_argument("--e2e-groups", type=int, default=4)
+    ap.add_argument("--e2e-groups", type=int, default=6)
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
