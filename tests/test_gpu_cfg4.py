@@ -63,8 +63,8 @@ def test_dkdv_for_key_blocks(run):
     q, k, v, do = (x[h] for x in host)
     keep = res.mask_used.keep_numpy()[0, h]
     scale = 1.0 / math.sqrt(D)
-    lse_all = res.lse[0, h].double().cpu().numpy()
-    out_all = res.out[0, h].double().cpu().numpy()
+    lse_all = res.lse[0, h].detach().double().cpu().numpy()
+    out_all = res.out[0, h].detach().double().cpu().numpy()
     for j in (int(np.argmax(keep.sum(axis=0))), 1181):  # the most-kept key block and the 16-row tail
         kv = slice(j * 64, min((j + 1) * 64, N))
         dk_ref = np.zeros((kv.stop - kv.start, D))
