@@ -25,6 +25,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "ptx.cuh"
@@ -394,6 +395,232 @@ __global__ void __launch_bounds__(kThreads, 1)
 // K6: dK and dV.  Work item = key block; tiles = query blocks keeping it.  Accumulators
 // transposed (TMEM lanes = head dim).
 // ---------------------------------------------------------------------------------------
+// ---------------------------------------------------------------------------------------
+// K7 variant: dQ with one query block per CTA and TWO CTAs per SM (TMEM 256 columns and
+// <= 112 KB smem each).  The per-CTA pipeline is simple (S/dP single-buffered, the tensor
+// pipe idles while this CTA's warps compute dS) and the second CTA on the SM fills those
+// gaps — the same structure as the forward kernel.
+// ---------------------------------------------------------------------------------------
+constexpr int kDq2Threads = 192;
+
+template <int HD>
+struct Dq2Cfg {
+  static constexpr int NSK = 2;
+  static constexpr int Q_BYTES = BQ * HD * 2;
+  static constexpr int KV_BYTES = BKV * HD * 2;
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_DO = Q_BYTES;
+  static constexpr int OFF_K = 2 * Q_BYTES;
+  static constexpr int OFF_V = OFF_K + NSK * KV_BYTES;
+  static constexpr int OFF_BAR = OFF_V + KV_BYTES;
+  static constexpr int NUM_BARS = 1 + 2 * NSK + 2 + 4;
+  static constexpr int SMEM_USED = OFF_BAR + NUM_BARS * 8 + 16;
+  static constexpr int SMEM = SMEM_USED < 80 * 1024 ? 80 * 1024 : SMEM_USED;  // never 3 CTAs/SM (TMEM)
+  static constexpr uint32_t S_COL = 0, DP_COL = 64, ACC_COL = 128;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(kDq2Threads, 2)
+    k_dq2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+          const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO,
+          const __grid_constant__ CUtensorMap tmDQ, const BwdParams p) {
+  using C = Dq2Cfg<HD>;
+  constexpr int NSK = C::NSK;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* qdo_full = bars;
+  uint64_t* k_full = qdo_full + 1;   // [NSK]
+  uint64_t* k_empty = k_full + NSK;  // [NSK]
+  uint64_t* v_full = k_empty + NSK;
+  uint64_t* v_empty = v_full + 1;
+  uint64_t* s_full = v_empty + 1;    // S and dP of tile t landed
+  uint64_t* ds_full = s_full + 1;    // dS of tile t packed into TMEM
+  uint64_t* dq_done = ds_full + 1;   // dQ MMA of tile t done
+  uint64_t* acc_full = dq_done + 1;  // last dQ MMA done
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_full + 1);
+
+  const int warp = (int)warp_id(), lane = (int)lane_id();
+  const int w = p.order ? p.order[blockIdx.x] : (int)blockIdx.x;
+  const int bh = w / p.T_m, qi = w % p.T_m;
+  const int hh = bh % p.H, bb = bh / p.H;
+  const int beg = p.ptr[w];
+  const int n = p.ptr[w + 1] - beg;
+  const int32_t* list = p.idx + beg;
+
+  if (threadIdx.x == 0) {
+    if (smem_u32(smem) & 1023u) __trap();
+    mbar_init(qdo_full, 1);
+    for (int s = 0; s < NSK; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
+    mbar_init(v_full, 1);
+    mbar_init(v_empty, 1);
+    mbar_init(s_full, 1);
+    mbar_init(ds_full, 128);
+    mbar_init(dq_done, 1);
+    mbar_init(acc_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_holder, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_holder;
+
+  if (n == 0) {
+    if (warp >= 2) {
+      const int tok = qi * BQ + (warp & 3) * 32 + lane;
+      if (tok < p.N) {
+        __nv_bfloat16* o = p.out0 + bb * p.o0_sb + hh * p.o0_sh + (int64_t)tok * p.o0_sn;
+        for (int c = 0; c < HD; ++c) o[c] = __float2bfloat16(0.f);
+      }
+    }
+  } else if (warp == 0) {
+    if (elect_one()) {
+      tma_prefetch(&tmQ);
+      tma_prefetch(&tmDO);
+      tma_prefetch(&tmK);
+      tma_prefetch(&tmV);
+      mbar_expect_tx(qdo_full, 2 * C::Q_BYTES);
+#pragma unroll
+      for (int c = 0; c < HD / 64; ++c) {
+        tma_load_4d(smem + C::OFF_Q + c * BQ * 128, &tmQ, qdo_full, c * 64, qi * BQ, hh, bb);
+        tma_load_4d(smem + C::OFF_DO + c * BQ * 128, &tmDO, qdo_full, c * 64, qi * BQ, hh, bb);
+      }
+      for (int t = 0; t < n; ++t) {
+        const int j = list[t];
+        const int sk = t % NSK;
+        if (t >= NSK) mbar_wait(&k_empty[sk], ((uint32_t)(t / NSK) + 1u) & 1u);
+        mbar_expect_tx(&k_full[sk], C::KV_BYTES);
+#pragma unroll
+        for (int c = 0; c < HD / 64; ++c)
+          tma_load_4d(smem + C::OFF_K + sk * C::KV_BYTES + c * BKV * 128, &tmK, &k_full[sk], c * 64, j * BKV, hh, bb);
+        if (t >= 1) mbar_wait(v_empty, (uint32_t)(t - 1) & 1u);
+        mbar_expect_tx(v_full, C::KV_BYTES);
+#pragma unroll
+        for (int c = 0; c < HD / 64; ++c)
+          tma_load_4d(smem + C::OFF_V + c * BKV * 128, &tmV, v_full, c * 64, j * BKV, hh, bb);
+      }
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      constexpr uint32_t idS = idesc_bf16(BQ, BKV, false, false);
+      constexpr uint32_t idQ = idesc_bf16(BQ, HD, false, true);
+      const uint32_t sQ = smem_u32(smem + C::OFF_Q), sDO = smem_u32(smem + C::OFF_DO);
+      const uint32_t sV = smem_u32(smem + C::OFF_V);
+      mbar_wait(qdo_full, 0);
+      for (int t = 0; t < n; ++t) {
+        const int sk = t % NSK;
+        if (t >= 1) mbar_wait(dq_done, (uint32_t)(t - 1) & 1u);  // dS_{t-1} (in S) consumed
+        mbar_wait(&k_full[sk], (uint32_t)(t / NSK) & 1u);
+        tc_fence_after();
+        const uint32_t sK = smem_u32(smem + C::OFF_K + sk * C::KV_BYTES);
+#pragma unroll
+        for (int ks = 0; ks < HD / 16; ++ks) {
+          const uint32_t qo = (uint32_t)((ks * 16 / 64) * BQ * 128 + (ks * 16 % 64) * 2);
+          const uint32_t ko = (uint32_t)((ks * 16 / 64) * BKV * 128 + (ks * 16 % 64) * 2);
+          mma_bf16(tbase + C::S_COL, sw128_desc(sQ + qo, 16, 1024), sw128_desc(sK + ko, 16, 1024), idS,
+                   ks > 0 ? 1u : 0u);
+        }
+        mbar_wait(v_full, (uint32_t)t & 1u);
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < HD / 16; ++ks) {
+          const uint32_t qo = (uint32_t)((ks * 16 / 64) * BQ * 128 + (ks * 16 % 64) * 2);
+          const uint32_t vo = (uint32_t)((ks * 16 / 64) * BKV * 128 + (ks * 16 % 64) * 2);
+          mma_bf16(tbase + C::DP_COL, sw128_desc(sDO + qo, 16, 1024), sw128_desc(sV + vo, 16, 1024), idS,
+                   ks > 0 ? 1u : 0u);
+        }
+        mma_commit(s_full);
+        mma_commit(v_empty);
+        mbar_wait(ds_full, (uint32_t)t & 1u);
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < BKV / 16; ++ks)
+          mma_bf16_ts(tbase + C::ACC_COL, tbase + C::S_COL + (uint32_t)(ks * 8),
+                      sw128_desc(sK + (uint32_t)(ks * 2048), BKV * 128, 1024), idQ, (t > 0 || ks > 0) ? 1u : 0u);
+        mma_commit(dq_done);
+        mma_commit(&k_empty[sk]);
+      }
+      mma_commit(acc_full);
+    }
+    __syncwarp();
+  } else {
+    const int q4 = warp & 3;
+    const int row = q4 * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    const int tok = qi * BQ + row;
+    const bool valid = tok < p.N;
+    const float lse2 = valid ? p.lse[(int64_t)bh * p.N + tok] * kLog2e : INFINITY;
+    const float dlt = valid ? p.delta[(int64_t)bh * p.N + tok] : 0.f;
+    const int kv_tail = p.N - (p.T_n - 1) * BKV;
+    const float sl2 = p.sl2;
+    for (int t = 0; t < n; ++t) {
+      const bool tail = list[t] == p.T_n - 1 && kv_tail < BKV;
+      mbar_wait(s_full, (uint32_t)t & 1u);
+      tc_fence_after();
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t sr[32], dr[32];
+        tmem_ld32(tbase + lane_off + C::S_COL + (uint32_t)(32 * h), sr);
+        tmem_ld32(tbase + lane_off + C::DP_COL + (uint32_t)(32 * h), dr);
+        uint32_t pk[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          float p0 = ex2(fmaf(__uint_as_float(sr[2 * c]), sl2, -lse2));
+          float p1 = ex2(fmaf(__uint_as_float(sr[2 * c + 1]), sl2, -lse2));
+          if (tail) {
+            if (32 * h + 2 * c >= kv_tail) p0 = 0.f;
+            if (32 * h + 2 * c + 1 >= kv_tail) p1 = 0.f;
+          }
+          pk[c] = pack_bf16(p0 * (__uint_as_float(dr[2 * c]) - dlt), p1 * (__uint_as_float(dr[2 * c + 1]) - dlt));
+        }
+        tmem_st16(tbase + lane_off + C::S_COL + (uint32_t)(16 * h), pk);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(ds_full);
+    }
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    uint8_t* sOut = smem + C::OFF_Q;  // every MMA has completed: Q is dead
+#pragma unroll 1
+    for (int c0 = 0; c0 < HD; c0 += 32) {
+      uint32_t o[32];
+      tmem_ld32(tbase + lane_off + C::ACC_COL + (uint32_t)c0, o);
+      uint32_t pk[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c)
+        pk[c] = pack_bf16(__uint_as_float(o[2 * c]) * p.scale, __uint_as_float(o[2 * c + 1]) * p.scale);
+      const uint32_t base = smem_u32(sOut + (c0 / 64) * BQ * 128);
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        st_shared_v4(base + sw128_offset((uint32_t)row, (uint32_t)((c0 % 64) / 8 + u)), pk[4 * u], pk[4 * u + 1],
+                     pk[4 * u + 2], pk[4 * u + 3]);
+    }
+    fence_proxy_async_smem();
+    named_bar_sync(1, 128);
+    if (threadIdx.x == 64) {
+#pragma unroll
+      for (int c = 0; c < HD / 64; ++c) tma_store_4d(&tmDQ, sOut + c * BQ * 128, c * 64, qi * BQ, hh, bb);
+      tma_store_commit();
+      tma_store_wait_all();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tbase, 256);
+}
+
+bool dq_variant2() {
+  static const bool v = [] {
+    const char* e = getenv("SPA2_DQ_PERSISTENT");
+    return !(e != nullptr && e[0] == '1');
+  }();
+  return v;
+}
+
 // Work-list cursor shared by the roles of the persistent kernels: walks this CTA's items
 // (blockIdx.x, +gridDim.x, ...) skipping empty ones, one tile at a time.
 struct Cursor {
@@ -783,7 +1010,11 @@ int launch_attn_bwd(int which, const spa2_view& q, const spa2_view& k, const spa
   prm.trace = g_trace_buf;
   prm.trace_cap = g_trace_cap;
   const unsigned grid = (unsigned)std::min<int64_t>(prm.num_items, num_sms());
-  if (which == 0) {
+  if (which == 0 && dq_variant2()) {
+    auto kern = k_dq2<HD>;
+    SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Dq2Cfg<HD>::SMEM));
+    kern<<<(unsigned)prm.num_items, kDq2Threads, Dq2Cfg<HD>::SMEM, st>>>(m.q, m.k, m.v, m.dout, m.out0, prm);
+  } else if (which == 0) {
     auto kern = k_dq<HD>;
     SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DqCfg<HD>::SMEM));
     kern<<<grid, kThreads, DqCfg<HD>::SMEM, st>>>(m.q, m.k, m.v, m.dout, m.out0, prm);
