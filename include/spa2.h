@@ -149,6 +149,11 @@ int spa2_probe_gemm(const void* a, const void* b, float* d, int m, int n, int k,
 int spa2_probe_mma_rate(int m, int n, int k, int a_mn, int b_mn, int a_tmem, int reps, int ctas,
                         unsigned long long* cycles, void* stream);
 
+/* TMA streaming-rate probe (diagnostic): `ctas` CTAs each load `iters` random (box_rows x 64)
+ * bf16 tiles of a [rows, 64] buffer through a `stages`-deep ring; cycles[cta] = clock64 span. */
+int spa2_probe_tma_rate(const void* buf, long long rows, int box_rows, int stages, int iters, int ctas,
+                        unsigned long long* cycles, void* stream);
+
 /* Diagnostic: record per-role pipeline events of CTA 0 of the next backward launches into a
  * zeroed device buffer u64[2 + capacity]: clock64 of event (role, index, kind) at
  * buf[2 + role*(capacity/4) + index*8 + kind]; NULL disables. */

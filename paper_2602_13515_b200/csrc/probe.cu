@@ -210,3 +210,49 @@ extern "C" int spa2_probe_mma_rate(int m, int n, int k, int a_mn, int b_mn, int 
   SPA2_LAUNCH_CHECK();
   return SPA2_OK;
 }
+
+// ---- TMA streaming-rate probe (diagnostic): L2/HBM -> SMEM bandwidth with no compute ----
+namespace spa2 {
+namespace {
+__global__ void __launch_bounds__(32) k_tma_rate(const __grid_constant__ CUtensorMap map, int rows_total, int iters,
+                                                 int stages, int box_rows, unsigned long long* cycles) {
+  extern __shared__ uint8_t smem_dyn[];
+  __shared__ uint64_t full[8];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+  const uint32_t bytes = (uint32_t)box_rows * 128u;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  if (threadIdx.x == 0) {
+    const int tiles = rows_total / box_rows;
+    uint32_t r = (uint32_t)blockIdx.x * 2654435761u;
+    const uint64_t t0 = clock64();
+    for (int i = 0; i < iters + stages; ++i) {
+      const int s = i % stages;
+      if (i >= stages) mbar_wait(&full[s], (uint32_t)((i - stages) / stages) & 1u);
+      if (i < iters) {
+        r = r * 1664525u + 1013904223u;
+        mbar_expect_tx(&full[s], bytes);
+        tma_load_2d(base + s * bytes, &map, &full[s], 0, (int)((r >> 8) % (uint32_t)tiles) * box_rows);
+      }
+    }
+    cycles[blockIdx.x] = clock64() - t0;
+  }
+}
+}  // namespace
+}  // namespace spa2
+
+extern "C" int spa2_probe_tma_rate(const void* buf, long long rows, int box_rows, int stages, int iters, int ctas,
+                                   unsigned long long* cycles, void* stream) {
+  SPA2_REQUIRE(stages >= 1 && stages <= 8 && box_rows >= 8 && box_rows <= 256, SPA2_ERR_VALUE, "tma_rate: bad args");
+  CUtensorMap map;
+  int rc = make_tma_bf16_2d(&map, buf, 64, (uint64_t)rows, 64, 64, (uint32_t)box_rows);
+  if (rc) return rc;
+  const size_t smem = (size_t)stages * box_rows * 128 + 1024;
+  SPA2_CUDA_TRY(cudaFuncSetAttribute(k_tma_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_tma_rate<<<ctas, 32, smem, (cudaStream_t)stream>>>(map, (int)rows, iters, stages, box_rows, cycles);
+  SPA2_LAUNCH_CHECK();
+  return SPA2_OK;
+}
