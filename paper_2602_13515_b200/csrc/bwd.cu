@@ -191,10 +191,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (it >= 2) mbar_wait(&qdo_empty[st], ((uint32_t)(it >> 1) + 1u) & 1u);
         mbar_expect_tx(&qdo_full[st], 2 * C::Q_BYTES);
         uint8_t* sq = smem + C::OFF_QDO + st * 2 * C::Q_BYTES;
-#pragma unroll
-        for (int c = 0; c < HD / 64; ++c) {
-          tma_load_4d(sq + c * BQ * 128, &tmQ, &qdo_full[st], c * 64, m.blk * BQ, hh, bb);
-          tma_load_4d(sq + C::Q_BYTES + c * BQ * 128, &tmDO, &qdo_full[st], c * 64, m.blk * BQ, hh, bb);
+        {
+          tma_load_5d(sq, &tmQ, &qdo_full[st], 0, m.blk * BQ, 0, hh, bb);
+          tma_load_5d(sq + C::Q_BYTES, &tmDO, &qdo_full[st], 0, m.blk * BQ, 0, hh, bb);
         }
         for (int t = 0; t < m.n; ++t, ++g) {
           const int j = p.idx[m.beg + t];
@@ -203,16 +202,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (g >= NSK) mbar_wait(&k_empty[sk], ((uint32_t)(g / NSK) + 1u) & 1u);
           trace_ev(p.trace, p.trace_cap, 0, 2, g);
           mbar_expect_tx(&k_full[sk], C::KV_BYTES);
-#pragma unroll
-          for (int c = 0; c < HD / 64; ++c)
-            tma_load_4d(smem + C::OFF_K + sk * C::KV_BYTES + c * BKV * 128, &tmK, &k_full[sk], c * 64, j * BKV, hh,
-                        bb);
+          tma_load_5d(smem + C::OFF_K + sk * C::KV_BYTES, &tmK, &k_full[sk], 0, j * BKV, 0, hh, bb);
           if (g >= NSV) mbar_wait(&v_empty[sv], ((uint32_t)(g / NSV) + 1u) & 1u);
           mbar_expect_tx(&v_full[sv], C::KV_BYTES);
-#pragma unroll
-          for (int c = 0; c < HD / 64; ++c)
-            tma_load_4d(smem + C::OFF_V + sv * C::KV_BYTES + c * BKV * 128, &tmV, &v_full[sv], c * 64, j * BKV, hh,
-                        bb);
+          tma_load_5d(smem + C::OFF_V + sv * C::KV_BYTES, &tmV, &v_full[sv], 0, j * BKV, 0, hh, bb);
         }
         ++it;
       }
@@ -376,8 +369,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       fence_proxy_async_smem();
       named_bar_sync(1, 128);
       if (threadIdx.x == kEpiTid0) {
-#pragma unroll
-        for (int c = 0; c < HD / 64; ++c) tma_store_4d(&tmDQ, sOut + c * BQ * 128, c * 64, m.blk * BQ, hh, bb);
+        tma_store_5d(&tmDQ, sOut, 0, m.blk * BQ, 0, hh, bb);
         tma_store_commit();
         tma_store_wait_read();
         mbar_arrive(&qdo_empty[st]);
@@ -483,24 +475,19 @@ __global__ void __launch_bounds__(kDq2Threads, 2)
       tma_prefetch(&tmK);
       tma_prefetch(&tmV);
       mbar_expect_tx(qdo_full, 2 * C::Q_BYTES);
-#pragma unroll
-      for (int c = 0; c < HD / 64; ++c) {
-        tma_load_4d(smem + C::OFF_Q + c * BQ * 128, &tmQ, qdo_full, c * 64, qi * BQ, hh, bb);
-        tma_load_4d(smem + C::OFF_DO + c * BQ * 128, &tmDO, qdo_full, c * 64, qi * BQ, hh, bb);
+      {
+        tma_load_5d(smem + C::OFF_Q, &tmQ, qdo_full, 0, qi * BQ, 0, hh, bb);
+        tma_load_5d(smem + C::OFF_DO, &tmDO, qdo_full, 0, qi * BQ, 0, hh, bb);
       }
       for (int t = 0; t < n; ++t) {
         const int j = list[t];
         const int sk = t % NSK;
         if (t >= NSK) mbar_wait(&k_empty[sk], ((uint32_t)(t / NSK) + 1u) & 1u);
         mbar_expect_tx(&k_full[sk], C::KV_BYTES);
-#pragma unroll
-        for (int c = 0; c < HD / 64; ++c)
-          tma_load_4d(smem + C::OFF_K + sk * C::KV_BYTES + c * BKV * 128, &tmK, &k_full[sk], c * 64, j * BKV, hh, bb);
+        tma_load_5d(smem + C::OFF_K + sk * C::KV_BYTES, &tmK, &k_full[sk], 0, j * BKV, 0, hh, bb);
         if (t >= 1) mbar_wait(v_empty, (uint32_t)(t - 1) & 1u);
         mbar_expect_tx(v_full, C::KV_BYTES);
-#pragma unroll
-        for (int c = 0; c < HD / 64; ++c)
-          tma_load_4d(smem + C::OFF_V + c * BKV * 128, &tmV, v_full, c * 64, j * BKV, hh, bb);
+        tma_load_5d(smem + C::OFF_V, &tmV, v_full, 0, j * BKV, 0, hh, bb);
       }
     }
   } else if (warp == 1) {
@@ -602,8 +589,7 @@ __global__ void __launch_bounds__(kDq2Threads, 2)
     fence_proxy_async_smem();
     named_bar_sync(1, 128);
     if (threadIdx.x == 64) {
-#pragma unroll
-      for (int c = 0; c < HD / 64; ++c) tma_store_4d(&tmDQ, sOut + c * BQ * 128, c * 64, qi * BQ, hh, bb);
+      tma_store_5d(&tmDQ, sOut, 0, qi * BQ, 0, hh, bb);
       tma_store_commit();
       tma_store_wait_all();
     }
@@ -734,10 +720,9 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         const int hh = m.bh % p.H, bb = m.bh / p.H;
         if (it >= 1) mbar_wait(kv_empty, (uint32_t)(it - 1) & 1u);
         mbar_expect_tx(kv_full, 2 * C::KV_BYTES);
-#pragma unroll
-        for (int c = 0; c < HD / 64; ++c) {
-          tma_load_4d(smem + C::OFF_KV + c * BKV * 128, &tmK, kv_full, c * 64, m.blk * BKV, hh, bb);
-          tma_load_4d(smem + C::OFF_KV + C::KV_BYTES + c * BKV * 128, &tmV, kv_full, c * 64, m.blk * BKV, hh, bb);
+        {
+          tma_load_5d(smem + C::OFF_KV, &tmK, kv_full, 0, m.blk * BKV, 0, hh, bb);
+          tma_load_5d(smem + C::OFF_KV + C::KV_BYTES, &tmV, kv_full, 0, m.blk * BKV, 0, hh, bb);
         }
         for (int t = 0; t < m.n; ++t, ++g) {
           const int i = p.idx[m.beg + t];
@@ -747,10 +732,9 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
           trace_ev(p.trace, p.trace_cap, 0, 2, g);
           mbar_expect_tx(&qdo_full[s], 2 * C::Q_BYTES);
           uint8_t* sq = smem + C::OFF_QDO + s * 2 * C::Q_BYTES;
-#pragma unroll
-          for (int c = 0; c < HD / 64; ++c) {
-            tma_load_4d(sq + c * BQ * 128, &tmQ, &qdo_full[s], c * 64, i * BQ, hh, bb);
-            tma_load_4d(sq + C::Q_BYTES + c * BQ * 128, &tmDO, &qdo_full[s], c * 64, i * BQ, hh, bb);
+          {
+            tma_load_5d(sq, &tmQ, &qdo_full[s], 0, i * BQ, 0, hh, bb);
+            tma_load_5d(sq + C::Q_BYTES, &tmDO, &qdo_full[s], 0, i * BQ, 0, hh, bb);
           }
         }
         ++it;

@@ -59,6 +59,34 @@ int make_tma_bf16_4d(CUtensorMap* map, const void* base, const uint64_t dims[4],
   return SPA2_OK;
 }
 
+int make_tma_bf16_5d(CUtensorMap* map, const void* base, const uint64_t dims[5], const uint64_t strides_bytes[4],
+                     const uint32_t box[5]) {
+  auto fn = encode_fn();
+  SPA2_REQUIRE(fn != nullptr, SPA2_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+  SPA2_REQUIRE((reinterpret_cast<uintptr_t>(base) & 15) == 0, SPA2_ERR_UNSUPPORTED,
+               "TMA operand base pointer must be 16-byte aligned");
+  cuuint64_t gdim[5], gstride[4];
+  cuuint32_t bx[5], es[5] = {1, 1, 1, 1, 1};
+  for (int i = 0; i < 5; ++i) {
+    gdim[i] = dims[i];
+    bx[i] = box[i];
+  }
+  for (int i = 0; i < 4; ++i) {
+    gstride[i] = strides_bytes[i];
+    if (gstride[i] % 16 != 0) {
+      SPA2_REQUIRE(dims[i + 1] == 1, SPA2_ERR_UNSUPPORTED,
+                   "TMA operand strides must be multiples of 8 elements (got %llu bytes)",
+                   (unsigned long long)strides_bytes[i]);
+      gstride[i] = (gstride[i] + 15) / 16 * 16;  // size-1 axis: unused
+    }
+  }
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), gdim, gstride, bx, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  SPA2_REQUIRE(r == CUDA_SUCCESS, SPA2_ERR_CUDA, "cuTensorMapEncodeTiled (5-D) failed (%d)", (int)r);
+  return SPA2_OK;
+}
+
 int make_tma_bf16_2d(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint64_t row_stride_elems,
                      uint32_t box_cols, uint32_t box_rows) {
   auto fn = encode_fn();

@@ -131,23 +131,17 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
       tma_prefetch(&tmK);
       tma_prefetch(&tmV);
       mbar_expect_tx(q_full, C::Q_BYTES);
-#pragma unroll
-      for (int c = 0; c < HD / 64; ++c)
-        tma_load_4d(smem + C::OFF_Q + c * BQ * 128, &tmQ, q_full, c * 64, qi * BQ, hh, bb);
+      tma_load_5d(smem + C::OFF_Q, &tmQ, q_full, 0, qi * BQ, 0, hh, bb);
       for (int t = 0; t < n; ++t) {
         const int s = t % NS;
         const uint32_t ph = (uint32_t)(t / NS) & 1u;
         const int j = list[t];
         if (t >= NS) mbar_wait(&k_empty[s], ph ^ 1u);
         mbar_expect_tx(&k_full[s], C::KV_BYTES);
-#pragma unroll
-        for (int c = 0; c < HD / 64; ++c)
-          tma_load_4d(smem + C::OFF_K + s * C::KV_BYTES + c * BKV * 128, &tmK, &k_full[s], c * 64, j * BKV, hh, bb);
+        tma_load_5d(smem + C::OFF_K + s * C::KV_BYTES, &tmK, &k_full[s], 0, j * BKV, 0, hh, bb);
         if (t >= NS) mbar_wait(&v_empty[s], ph ^ 1u);
         mbar_expect_tx(&v_full[s], C::KV_BYTES);
-#pragma unroll
-        for (int c = 0; c < HD / 64; ++c)
-          tma_load_4d(smem + C::OFF_V + s * C::KV_BYTES + c * BKV * 128, &tmV, &v_full[s], c * 64, j * BKV, hh, bb);
+        tma_load_5d(smem + C::OFF_V + s * C::KV_BYTES, &tmV, &v_full[s], 0, j * BKV, 0, hh, bb);
       }
     }
   } else if (warp == 1) {
@@ -298,8 +292,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
     if (tok < p.N) p.lse[(int64_t)bh * p.N + tok] = (m + log2f(l)) * 0.69314718055994530942f;
     named_bar_sync(1, 128);
     if (threadIdx.x == 64) {
-#pragma unroll
-      for (int c = 0; c < HD / 64; ++c) tma_store_4d(&tmO, sO + c * BQ * 128, c * 64, qi * BQ, hh, bb);
+      tma_store_5d(&tmO, sO, 0, qi * BQ, 0, hh, bb);
       tma_store_commit();
       if (p.counter) atomicAdd(p.counter, (unsigned long long)n);
       tma_store_wait_all();
@@ -332,10 +325,10 @@ bool fwd_p_in_smem() {
 }  // namespace
 
 int make_qkv_map(CUtensorMap* m, const spa2_view& v, int64_t B, int64_t H, int64_t N, int64_t d, int rows) {
-  const uint64_t dims[4] = {(uint64_t)d, (uint64_t)N, (uint64_t)H, (uint64_t)B};
-  const uint64_t strides[3] = {(uint64_t)v.sn, (uint64_t)v.sh, (uint64_t)v.sb};
-  const uint32_t box[4] = {64, (uint32_t)rows, 1, 1};
-  return make_tma_bf16_4d(m, v.ptr, dims, strides, box);
+  const uint64_t dims[5] = {64, (uint64_t)N, (uint64_t)(d / 64), (uint64_t)H, (uint64_t)B};
+  const uint64_t strides[4] = {(uint64_t)v.sn * 2, 128, (uint64_t)v.sh * 2, (uint64_t)v.sb * 2};
+  const uint32_t box[5] = {64, (uint32_t)rows, (uint32_t)(d / 64), 1, 1};
+  return make_tma_bf16_5d(m, v.ptr, dims, strides, box);
 }
 
 }  // namespace spa2
