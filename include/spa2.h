@@ -153,6 +153,11 @@ int spa2_probe_mma_rate(int m, int n, int k, int a_mn, int b_mn, int a_tmem, int
  * bf16 tiles of a [rows, 64] buffer through a `stages`-deep ring; cycles[cta] = clock64 span. */
 int spa2_probe_tma_rate(const void* buf, long long rows, int box_rows, int stages, int iters, int ctas,
                         unsigned long long* cycles, void* stream);
+/* Variant (diagnostic): `issuers` warps per CTA with their own rings; requests are tensor boxes
+ * of box_rows x 64 x chunks (mode 0) or 1-D bulk copies of the same size (mode 1) over a
+ * [rows][128] bf16 matrix.  cycles[ctas*4] receives per-(CTA, issuer) cycle counts. */
+int spa2_probe_tma_rate2(const void* buf, long long rows, int box_rows, int chunks, int stages, int issuers,
+                         int mode, int iters, int ctas, unsigned long long* cycles, void* stream);
 
 /* Diagnostic: record per-role pipeline events of CTA 0 of the next backward launches into a
  * zeroed device buffer u64[2 + capacity]: clock64 of event (role, index, kind) at

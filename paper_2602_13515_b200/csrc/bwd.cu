@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 // pipe idles while this CTA's warps compute dS) and the second CTA on the SM fills those
 // gaps — the same structure as the forward kernel.
 // ---------------------------------------------------------------------------------------
-constexpr int kDq2Threads = 192;
+constexpr int kDq2Threads = 224;  // warp 6: second TMA producer (dO, V)
 
 template <int HD>
 struct Dq2Cfg {
@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(kDq2Threads, 2)
 
   if (threadIdx.x == 0) {
     if (smem_u32(smem) & 1023u) __trap();
-    mbar_init(qdo_full, 1);
+    mbar_init(qdo_full, 2);  // Q from warp 0, dO from warp 6
     for (int s = 0; s < NSK; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
@@ -461,7 +461,7 @@ __global__ void __launch_bounds__(kDq2Threads, 2)
   const uint32_t tbase = *tmem_holder;
 
   if (n == 0) {
-    if (warp >= 2) {
+    if (warp >= 2 && warp < 6) {
       const int tok = qi * BQ + (warp & 3) * 32 + lane;
       if (tok < p.N) {
         __nv_bfloat16* o = p.out0 + bb * p.o0_sb + hh * p.o0_sh + (int64_t)tok * p.o0_sn;
@@ -474,20 +474,26 @@ __global__ void __launch_bounds__(kDq2Threads, 2)
       tma_prefetch(&tmDO);
       tma_prefetch(&tmK);
       tma_prefetch(&tmV);
-      mbar_expect_tx(qdo_full, 2 * C::Q_BYTES);
-      {
-        tma_load_5d(smem + C::OFF_Q, &tmQ, qdo_full, 0, qi * BQ, 0, hh, bb);
-        tma_load_5d(smem + C::OFF_DO, &tmDO, qdo_full, 0, qi * BQ, 0, hh, bb);
-      }
+      mbar_expect_tx(qdo_full, C::Q_BYTES);
+      tma_load_5d(smem + C::OFF_Q, &tmQ, qdo_full, 0, qi * BQ, 0, hh, bb);
       for (int t = 0; t < n; ++t) {
         const int j = list[t];
         const int sk = t % NSK;
         if (t >= NSK) mbar_wait(&k_empty[sk], ((uint32_t)(t / NSK) + 1u) & 1u);
         mbar_expect_tx(&k_full[sk], C::KV_BYTES);
         tma_load_5d(smem + C::OFF_K + sk * C::KV_BYTES, &tmK, &k_full[sk], 0, j * BKV, 0, hh, bb);
+      }
+    }
+  } else if (warp == 6) {
+    // second producer: dO, then V (TMA requests issued by one warp are served one at a
+    // time; two issuing warps double the fill rate, tools/tma_rate.py)
+    if (elect_one()) {
+      mbar_expect_tx(qdo_full, C::Q_BYTES);
+      tma_load_5d(smem + C::OFF_DO, &tmDO, qdo_full, 0, qi * BQ, 0, hh, bb);
+      for (int t = 0; t < n; ++t) {
         if (t >= 1) mbar_wait(v_empty, (uint32_t)(t - 1) & 1u);
         mbar_expect_tx(v_full, C::KV_BYTES);
-        tma_load_5d(smem + C::OFF_V, &tmV, v_full, 0, j * BKV, 0, hh, bb);
+        tma_load_5d(smem + C::OFF_V, &tmV, v_full, 0, list[t] * BKV, 0, hh, bb);
       }
     }
   } else if (warp == 1) {
@@ -533,7 +539,7 @@ __global__ void __launch_bounds__(kDq2Threads, 2)
       mma_commit(acc_full);
     }
     __syncwarp();
-  } else {
+  } else if (warp < 6) {
     const int q4 = warp & 3;
     const int row = q4 * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
@@ -645,8 +651,15 @@ __device__ __forceinline__ void cursor_next(Cursor& c, const BwdParams& p, int n
   if (++c.t >= c.n) cursor_item(c, p, nblk);
 }
 
-constexpr int kDkvThreads = 448;  // 14 warps: TMA, MMA, 8 elementwise, 4 epilogue
-constexpr int kDkvEpi0 = 320;     // first epilogue thread (warp 10)
+// Warp roles: 0 TMA (K, Q), 1 MMA, 2 .. 2+EWW-1 elementwise (EWW/4 warps per TMEM lane
+// quarter, 256/EWW columns each), then 4 epilogue warps, then TMA (V, dO).
+template <int EWW>
+struct DkvRoles {
+  static constexpr int EPI0 = 2 + EWW;           // first epilogue warp
+  static constexpr int PROD2 = EPI0 + 4;         // second producer warp
+  static constexpr int THREADS = 32 * (PROD2 + 1);
+  static constexpr int CPT = 256 / EWW;          // S/dP columns per elementwise thread
+};
 
 template <int HD>
 struct DkvCfg {
@@ -658,26 +671,30 @@ struct DkvCfg {
   static constexpr int OFF_QDO = 2 * KV_BYTES;                // [NS stages][Q | dO]
   static constexpr int OFF_PDS = OFF_QDO + NS * 2 * Q_BYTES;  // [2 buffers][P | dS]
   static constexpr int OFF_BAR = OFF_PDS + 2 * 2 * PB;
-  static constexpr int NUM_BARS = 2 + 2 * NS + 2 + 2 + 2 + 4;
+  static constexpr int NUM_BARS = 2 + 2 * NS + 2 * 7;
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr uint32_t S_COL = 0, DP_COL = 128, ACC_COL = 256;  // acc a: dV at +a*128, dK at +a*128+64
 };
 
-template <int HD>
-__global__ void __launch_bounds__(kDkvThreads, 1)
+template <int HD, int EWW>
+__global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
     k_dkdv(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
            const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO, const BwdParams p) {
   using C = DkvCfg<HD>;
+  using R = DkvRoles<EWW>;
   constexpr int NS = C::NS;
+  constexpr int EWT = 32 * EWW;  // elementwise threads
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* kv_full = bars;             // K/V of item `it` landed
   uint64_t* kv_empty = kv_full + 1;     // last S/dP MMA of item `it` done: K/V slot reusable
   uint64_t* qdo_full = kv_empty + 1;    // [NS]
   uint64_t* qdo_empty = qdo_full + NS;  // [NS]
-  uint64_t* sdp_full = qdo_empty + NS;  // [2]
-  uint64_t* pds_full = sdp_full + 2;    // [2] P/dS buffer b written
-  uint64_t* pds_free = pds_full + 2;    // [2] dV/dK MMAs reading buffer b done
+  uint64_t* s_full = qdo_empty + NS;    // [2] S of tile g in TMEM buffer g&1
+  uint64_t* dp_full = s_full + 2;       // [2] dP of tile g
+  uint64_t* p_full = dp_full + 2;       // [2] P of tile g in smem buffer g&1
+  uint64_t* ds_full = p_full + 2;       // [2] dS of tile g in smem (S/dP TMEM buffer read)
+  uint64_t* pds_free = ds_full + 2;     // [2] dV/dK MMAs reading buffer b done
   uint64_t* acc_full = pds_free + 2;    // [2]
   uint64_t* acc_empty = acc_full + 2;   // [2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 2);
@@ -685,17 +702,19 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
   const int warp = (int)warp_id(), lane = (int)lane_id();
   if (threadIdx.x == 0) {
     if (smem_u32(smem) & 1023u) __trap();
-    mbar_init(kv_full, 1);
+    mbar_init(kv_full, 2);  // two producers: warp 0 (K, Q) and warp PROD2 (V, dO)
     mbar_init(kv_empty, 1);
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&sdp_full[s], 1);
-      mbar_init(&pds_full[s], 256);
+      mbar_init(&s_full[s], 1);
+      mbar_init(&dp_full[s], 1);
+      mbar_init(&p_full[s], EWT);
+      mbar_init(&ds_full[s], EWT);
       mbar_init(&pds_free[s], 1);
       mbar_init(&acc_full[s], 1);
       mbar_init(&acc_empty[s], 128);
     }
     for (int s = 0; s < NS; ++s) {
-      mbar_init(&qdo_full[s], 1);
+      mbar_init(&qdo_full[s], 2);
       mbar_init(&qdo_empty[s], 1);
     }
     fence_mbar_init();
@@ -706,45 +725,43 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
   tc_fence_after();
   const uint32_t tbase = *tmem_holder;
 
-  if (warp == 0) {
-    // ---------------- TMA producer ----------------
+  if (warp == 0 || warp == R::PROD2) {
+    // ---------------- TMA producers: warp 0 loads K and Q, warp PROD2 loads V and dO ----------------
+    // (requests issued by one warp are served one at a time; two issuing warps double the
+    // per-SM fill rate, tools/tma_rate.py)
     if (elect_one()) {
-      tma_prefetch(&tmQ);
-      tma_prefetch(&tmDO);
-      tma_prefetch(&tmK);
-      tma_prefetch(&tmV);
+      const bool second = warp == R::PROD2;
+      const CUtensorMap* tmKV = second ? &tmV : &tmK;
+      const CUtensorMap* tmR = second ? &tmDO : &tmQ;
+      tma_prefetch(tmKV);
+      tma_prefetch(tmR);
+      uint8_t* const kv_dst = smem + C::OFF_KV + (second ? C::KV_BYTES : 0);
+      const int r_off = second ? C::Q_BYTES : 0;
       int it = 0, g = 0;
       for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
         const Item m = get_item(p, wi, p.T_n);
         if (m.n == 0) continue;
         const int hh = m.bh % p.H, bb = m.bh / p.H;
         if (it >= 1) mbar_wait(kv_empty, (uint32_t)(it - 1) & 1u);
-        mbar_expect_tx(kv_full, 2 * C::KV_BYTES);
-        {
-          tma_load_5d(smem + C::OFF_KV, &tmK, kv_full, 0, m.blk * BKV, 0, hh, bb);
-          tma_load_5d(smem + C::OFF_KV + C::KV_BYTES, &tmV, kv_full, 0, m.blk * BKV, 0, hh, bb);
-        }
+        mbar_expect_tx(kv_full, C::KV_BYTES);
+        tma_load_5d(kv_dst, tmKV, kv_full, 0, m.blk * BKV, 0, hh, bb);
         for (int t = 0; t < m.n; ++t, ++g) {
           const int i = p.idx[m.beg + t];
           const int s = g % NS;
-          trace_ev(p.trace, p.trace_cap, 0, 1, g);
+          if (!second) trace_ev(p.trace, p.trace_cap, 0, 1, g);
           if (g >= NS) mbar_wait(&qdo_empty[s], ((uint32_t)(g / NS) + 1u) & 1u);
-          trace_ev(p.trace, p.trace_cap, 0, 2, g);
-          mbar_expect_tx(&qdo_full[s], 2 * C::Q_BYTES);
-          uint8_t* sq = smem + C::OFF_QDO + s * 2 * C::Q_BYTES;
-          {
-            tma_load_5d(sq, &tmQ, &qdo_full[s], 0, i * BQ, 0, hh, bb);
-            tma_load_5d(sq + C::Q_BYTES, &tmDO, &qdo_full[s], 0, i * BQ, 0, hh, bb);
-          }
+          if (!second) trace_ev(p.trace, p.trace_cap, 0, 2, g);
+          mbar_expect_tx(&qdo_full[s], C::Q_BYTES);
+          tma_load_5d(smem + C::OFF_QDO + s * 2 * C::Q_BYTES + r_off, tmR, &qdo_full[s], 0, i * BQ, 0, hh, bb);
         }
         ++it;
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer: dataflow order ----------------
-    // Two streams of work: S/dP of tile gs (needs its Q/dO, and the S/dP buffer, i.e. at
-    // most one tile ahead of the dV/dK stream) and dV/dK of tile gd (needs its P/dS).
-    // Whichever is ready is issued, so dV/dK never waits behind the next tile's load.
+    // Two streams: S/dP of tile gs (needs its Q/dO and a free S/dP TMEM buffer, i.e. at
+    // most one tile ahead of the accumulate stream) and dV (needs P) then dK (needs dS) of
+    // tile gd.  Whichever is ready is issued, so accumulation never waits behind a load.
     if (elect_one()) {
       constexpr uint32_t idS = idesc_bf16(BQ, BKV, false, false);
       constexpr uint32_t idT = idesc_bf16(HD, BKV, true, true);
@@ -753,6 +770,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
       cursor_init(cs, p, p.T_n);
       cursor_init(cd, p, p.T_n);
       int kv_ready_it = -1;
+      int dphase = 0;  // 0: dV of tile cd.g next, 1: dK of tile cd.g next
       uint64_t t_idle = 0;
       uint32_t spins = 0;
       while (cd.valid) {
@@ -777,6 +795,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
               mma_bf16(tbase + C::S_COL + b * 64, sw128_desc(sQ + qo, 16, 1024), sw128_desc(sK + ko, 16, 1024), idS,
                        ks > 0 ? 1u : 0u);
             }
+            mma_commit(&s_full[b]);
 #pragma unroll
             for (int ks = 0; ks < HD / 16; ++ks) {
               const uint32_t qo = (uint32_t)((ks * 16 / 64) * BQ * 128 + (ks * 16 % 64) * 2);
@@ -784,7 +803,7 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
               mma_bf16(tbase + C::DP_COL + b * 64, sw128_desc(sDO + qo, 16, 1024), sw128_desc(sV + ko, 16, 1024),
                        idS, ks > 0 ? 1u : 0u);
             }
-            mma_commit(&sdp_full[b]);
+            mma_commit(&dp_full[b]);
             if (cs.t == cs.n - 1) mma_commit(kv_empty);  // K_j / V_j are only read by S and dP
             cursor_next(cs, p, p.T_n);
             progressed = true;
@@ -792,23 +811,31 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         }
         if (cd.g < cs.g) {
           const int pb = cd.g & 1;
-          const bool acc_ok =
-              !(cd.t == 0 && cd.it >= 2) || mbar_test(&acc_empty[cd.it & 1], ((uint32_t)(cd.it >> 1) + 1u) & 1u);
-          if (acc_ok && mbar_test(&pds_full[pb], (uint32_t)(cd.g >> 1) & 1u)) {
-            tc_fence_after();
-            trace_ev(p.trace, p.trace_cap, 1, 4, cd.g);
-            const int s = cd.g % NS;
-            const uint32_t acc = tbase + C::ACC_COL + (uint32_t)((cd.it & 1) * 128);
-            const uint32_t sQ = smem_u32(smem + C::OFF_QDO + s * 2 * C::Q_BYTES);
-            const uint32_t sDO = sQ + C::Q_BYTES;
-            const uint32_t sP = smem_u32(smem + C::OFF_PDS + pb * 2 * C::PB), sDS = sP + C::PB;
-            const bool first = cd.t == 0;
+          const int s = cd.g % NS;
+          const uint32_t acc = tbase + C::ACC_COL + (uint32_t)((cd.it & 1) * 128);
+          const uint32_t sQ = smem_u32(smem + C::OFF_QDO + s * 2 * C::Q_BYTES);
+          const uint32_t sDO = sQ + C::Q_BYTES;
+          const uint32_t sP = smem_u32(smem + C::OFF_PDS + pb * 2 * C::PB), sDS = sP + C::PB;
+          const bool first = cd.t == 0;
+          if (dphase == 0) {
+            const bool acc_ok =
+                !(first && cd.it >= 2) || mbar_test(&acc_empty[cd.it & 1], ((uint32_t)(cd.it >> 1) + 1u) & 1u);
+            if (acc_ok && mbar_test(&p_full[pb], (uint32_t)(cd.g >> 1) & 1u)) {
+              tc_fence_after();
+              trace_ev(p.trace, p.trace_cap, 1, 4, cd.g);
 #pragma unroll
-            for (int ks = 0; ks < BQ / 16; ++ks) {
-              const uint32_t ro = (uint32_t)(ks * 2048);
-              mma_bf16(acc, sw128_desc(sDO + ro, BQ * 128, 1024), sw128_desc(sP + ro, BQ * 128, 1024), idT,
-                       (!first || ks > 0) ? 1u : 0u);
+              for (int ks = 0; ks < BQ / 16; ++ks) {
+                const uint32_t ro = (uint32_t)(ks * 2048);
+                mma_bf16(acc, sw128_desc(sDO + ro, BQ * 128, 1024), sw128_desc(sP + ro, BQ * 128, 1024), idT,
+                         (!first || ks > 0) ? 1u : 0u);
+              }
+              dphase = 1;
+              progressed = true;
             }
+          }
+          if (dphase == 1 && mbar_test(&ds_full[pb], (uint32_t)(cd.g >> 1) & 1u)) {
+            tc_fence_after();
+            trace_ev(p.trace, p.trace_cap, 1, 5, cd.g);
 #pragma unroll
             for (int ks = 0; ks < BQ / 16; ++ks) {
               const uint32_t ro = (uint32_t)(ks * 2048);
@@ -819,11 +846,13 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
             mma_commit(&qdo_empty[s]);
             if (cd.t == cd.n - 1) mma_commit(&acc_full[cd.it & 1]);
             cursor_next(cd, p, p.T_n);
+            dphase = 0;
             progressed = true;
           }
         }
         if (progressed) {
           spins = 0;
+          t_idle = 0;
         } else if ((++spins & 1023u) == 0) {
           if (t_idle == 0) t_idle = globaltimer();
           else if (globaltimer() - t_idle > SPA2_WATCHDOG_NS) {
@@ -831,17 +860,17 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
             __trap();
           }
         }
-        if (progressed) t_idle = 0;
       }
     }
     __syncwarp();
-  } else if (warp < 10) {
-    // ---------------- P / dS warps (2..9): 2 warps per TMEM lane quarter, 32 columns each ----
+  } else if (warp < R::EPI0) {
+    // ---------------- P / dS warps: EWW/4 warps per TMEM lane quarter, CPT columns each ----
+    constexpr int CPT = R::CPT;
     const int q4 = warp & 3;
-    const int half = (warp - 2) >> 2;
+    const int grp = (warp - 2) >> 2;
     const int row = q4 * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
-    const uint32_t col0 = (uint32_t)(32 * half);
+    const uint32_t col0 = (uint32_t)(CPT * grp);
     const float sl2 = p.sl2;
     const bool tr = threadIdx.x == 64;
     int g = 0;
@@ -862,43 +891,58 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         float lse2_n = 0.f, dlt_n = 0.f;
         if (t + 1 < m.n) load_stats(t + 1, lse2_n, dlt_n);  // prefetch the next tile's row statistics
         if (tr) trace_ev(p.trace, p.trace_cap, 2, 1, g);
-        mbar_wait(&sdp_full[b], (uint32_t)(g >> 1) & 1u);
+        mbar_wait(&s_full[b], (uint32_t)(g >> 1) & 1u);
         if (tr) trace_ev(p.trace, p.trace_cap, 2, 2, g);
         tc_fence_after();
-        uint32_t sr[32], dr[32];
-        tmem_ld32(tbase + lane_off + C::S_COL + b * 64 + col0, sr);
-        tmem_ld32(tbase + lane_off + C::DP_COL + b * 64 + col0, dr);
-        uint32_t pp[16], pd[16];
+        uint32_t sr[CPT];
+        if constexpr (CPT == 32) tmem_ld32(tbase + lane_off + C::S_COL + b * 64 + col0, sr);
+        else tmem_ld16(tbase + lane_off + C::S_COL + b * 64 + col0, sr);
+        float pv[CPT];
+        uint32_t pk[CPT / 2];
 #pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          const float p0 = ex2(fmaf(__uint_as_float(sr[2 * c]), sl2, -lse2));
-          const float p1 = ex2(fmaf(__uint_as_float(sr[2 * c + 1]), sl2, -lse2));
-          pp[c] = pack_bf16(p0, p1);
-          pd[c] = pack_bf16(p0 * (__uint_as_float(dr[2 * c]) - dlt), p1 * (__uint_as_float(dr[2 * c + 1]) - dlt));
-        }
+        for (int c = 0; c < CPT; ++c) pv[c] = ex2(fmaf(__uint_as_float(sr[c]), sl2, -lse2));
+#pragma unroll
+        for (int c = 0; c < CPT / 2; ++c) pk[c] = pack_bf16(pv[2 * c], pv[2 * c + 1]);
         if (g >= 2) mbar_wait(&pds_free[b], ((uint32_t)(g >> 1) + 1u) & 1u);  // buffer b free (tile g-2 done)
         if (tr) trace_ev(p.trace, p.trace_cap, 2, 3, g);
         const uint32_t sP = smem_u32(smem + C::OFF_PDS + (int)b * 2 * C::PB), sDS = sP + C::PB;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const uint32_t off = sw128_offset((uint32_t)row, (uint32_t)(4 * half + u));
-          st_shared_v4(sP + off, pp[4 * u], pp[4 * u + 1], pp[4 * u + 2], pp[4 * u + 3]);
-          st_shared_v4(sDS + off, pd[4 * u], pd[4 * u + 1], pd[4 * u + 2], pd[4 * u + 3]);
+        for (int u = 0; u < CPT / 8; ++u) {
+          const uint32_t off = sw128_offset((uint32_t)row, col0 / 8 + (uint32_t)u);
+          st_shared_v4(sP + off, pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(&p_full[b]);
+        if (tr) trace_ev(p.trace, p.trace_cap, 2, 5, g);
+        mbar_wait(&dp_full[b], (uint32_t)(g >> 1) & 1u);
+        tc_fence_after();
+        uint32_t dr[CPT];
+        if constexpr (CPT == 32) tmem_ld32(tbase + lane_off + C::DP_COL + b * 64 + col0, dr);
+        else tmem_ld16(tbase + lane_off + C::DP_COL + b * 64 + col0, dr);
+#pragma unroll
+        for (int c = 0; c < CPT / 2; ++c)
+          pk[c] = pack_bf16(pv[2 * c] * (__uint_as_float(dr[2 * c]) - dlt),
+                            pv[2 * c + 1] * (__uint_as_float(dr[2 * c + 1]) - dlt));
+#pragma unroll
+        for (int u = 0; u < CPT / 8; ++u) {
+          const uint32_t off = sw128_offset((uint32_t)row, col0 / 8 + (uint32_t)u);
+          st_shared_v4(sDS + off, pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
         }
         fence_proxy_async_smem();
         tc_fence_before();
-        mbar_arrive(&pds_full[b]);
+        mbar_arrive(&ds_full[b]);
         if (tr) trace_ev(p.trace, p.trace_cap, 2, 4, g);
         lse2 = lse2_n;
         dlt = dlt_n;
       }
     }
-  } else {
-    // ---------------- epilogue warps (10..13): TMEM -> registers -> coalesced global stores ----
+  } else if (warp < R::PROD2) {
+    // ---------------- epilogue warps: TMEM -> registers -> coalesced global stores ----
     const int q4 = warp & 3;
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
     const int dim = (HD == 128) ? q4 * 32 + lane : 16 * q4 + lane;  // M=64 accumulators: lanes 0-15 per quarter
     const bool own = (HD == 128) || lane < 16;
+    const bool tr = threadIdx.x == 32 * R::EPI0;
     int it = 0;
     for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
       const Item m = get_item(p, wi, p.T_n);
@@ -916,34 +960,44 @@ __global__ void __launch_bounds__(kDkvThreads, 1)
         continue;
       }
       const int st = it & 1;
-      if (threadIdx.x == kDkvEpi0) trace_ev(p.trace, p.trace_cap, 3, 1, it);
+      if (tr) trace_ev(p.trace, p.trace_cap, 3, 1, it);
       mbar_wait(&acc_full[st], (uint32_t)(it >> 1) & 1u);
-      if (threadIdx.x == kDkvEpi0) trace_ev(p.trace, p.trace_cap, 3, 2, it);
+      if (tr) trace_ev(p.trace, p.trace_cap, 3, 2, it);
       tc_fence_after();
 #pragma unroll 1
-      for (int which = 0; which < 2; ++which) {
-        uint32_t r64[64];
-        tmem_ld64(tbase + lane_off + C::ACC_COL + (uint32_t)(st * 128 + which * 64), r64);
-        if (which == 1) {
+      for (int part = 0; part < 4; ++part) {  // dV rows 0-31, 32-63, then dK rows 0-31, 32-63
+        uint32_t r32[32];
+        tmem_ld32(tbase + lane_off + C::ACC_COL + (uint32_t)(st * 128 + part * 32), r32);
+        if (part == 3) {
           tc_fence_before();
           mbar_arrive(&acc_empty[st]);  // both accumulators read: TMEM set reusable
         }
-        __nv_bfloat16* dst = which ? dk : dv;
-        const int64_t sn = which ? p.o0_sn : p.o1_sn;
-        const float mul = which ? p.scale : 1.f;
+        const bool is_k = part >= 2;
+        __nv_bfloat16* dst = (is_k ? dk : dv) + (int64_t)((part & 1) * 32) * (is_k ? p.o0_sn : p.o1_sn);
+        const int64_t sn = is_k ? p.o0_sn : p.o1_sn;
+        const float mul = is_k ? p.scale : 1.f;
+        const int rr = rows - (part & 1) * 32;
         if (own) {
 #pragma unroll
-          for (int r = 0; r < BKV; ++r)
-            if (r < rows) dst[(int64_t)r * sn] = __float2bfloat16(__uint_as_float(r64[r]) * mul);
+          for (int r = 0; r < 32; ++r)
+            if (r < rr) dst[(int64_t)r * sn] = __float2bfloat16(__uint_as_float(r32[r]) * mul);
         }
       }
-      if (threadIdx.x == kDkvEpi0) trace_ev(p.trace, p.trace_cap, 3, 3, it);
+      if (tr) trace_ev(p.trace, p.trace_cap, 3, 3, it);
       ++it;
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tbase, 512);
+}
+
+int dkdv_ew_warps() {
+  static const int v = [] {
+    const char* e = getenv("SPA2_DKDV_EW");
+    return (e != nullptr && e[0] == '1' && e[1] == '6') ? 16 : 8;
+  }();
+  return v;
 }
 
 int num_sms() {
@@ -1005,9 +1059,15 @@ int launch_attn_bwd(int which, const spa2_view& q, const spa2_view& k, const spa
   } else {
     prm.out1 = (__nv_bfloat16*)out1->ptr;
     prm.o1_sb = out1->sb, prm.o1_sh = out1->sh, prm.o1_sn = out1->sn;
-    auto kern = k_dkdv<HD>;
-    SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvCfg<HD>::SMEM));
-    kern<<<grid, kDkvThreads, DkvCfg<HD>::SMEM, st>>>(m.q, m.k, m.v, m.dout, prm);
+    if (dkdv_ew_warps() == 16) {
+      auto kern = k_dkdv<HD, 16>;
+      SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvCfg<HD>::SMEM));
+      kern<<<grid, DkvRoles<16>::THREADS, DkvCfg<HD>::SMEM, st>>>(m.q, m.k, m.v, m.dout, prm);
+    } else {
+      auto kern = k_dkdv<HD, 8>;
+      SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvCfg<HD>::SMEM));
+      kern<<<grid, DkvRoles<8>::THREADS, DkvCfg<HD>::SMEM, st>>>(m.q, m.k, m.v, m.dout, prm);
+    }
   }
   SPA2_LAUNCH_CHECK();
   return SPA2_OK;

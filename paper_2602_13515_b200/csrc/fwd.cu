@@ -6,7 +6,10 @@
 // O = acc / l (bf16) and LSE = m + ln l (fp32, natural log, attention.py:112-113).
 //
 // One CTA = one query block; 192 threads, warp-specialised:
-//   warp 0      TMA producer: Q once, then K_j / V_j into two NS-deep rings
+//   warp 0      TMA producer: Q once, then K_j into an NS-deep ring
+//   warp 6      TMA producer: V_j into an NS-deep ring (TMA requests issued by one warp are
+//               served one at a time: two issuing warps double the per-CTA fill rate,
+//               tools/tma_rate.py)
 //   warp 1      TMEM owner + single-thread tcgen05.mma issuer
 //   warps 2..5  softmax: one TMEM lane (= query row) per thread; rescale O in TMEM only
 //               when the running max grows by > 8 (log2 units); epilogue via TMA store
@@ -29,7 +32,7 @@ using namespace ptx;
 
 constexpr int BQ = 128;
 constexpr int BKV = 64;
-constexpr int kFwdThreads = 192;
+constexpr int kFwdThreads = 224;  // + warp 6: second TMA producer (V)
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: P entries stay <= 2^8
 
 template <int HD, bool P_TMEM>
@@ -115,7 +118,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
   if (n == 0) {
     // A query block with no kept key block (rejected by BlockMask; reachable only through
     // the raw C ABI): define O = 0 and LSE = -inf rather than reading garbage.
-    if (warp >= 2) {
+    if (warp >= 2 && warp < 6) {
       const int row = (warp & 3) * 32 + lane;
       const int tok = qi * BQ + row;
       if (tok < p.N) {
@@ -125,23 +128,30 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
       }
     }
   } else if (warp == 0) {
-    // ---------------- TMA producer ----------------
+    // ---------------- TMA producer: Q, K ----------------
     if (elect_one()) {
       tma_prefetch(&tmQ);
       tma_prefetch(&tmK);
-      tma_prefetch(&tmV);
       mbar_expect_tx(q_full, C::Q_BYTES);
       tma_load_5d(smem + C::OFF_Q, &tmQ, q_full, 0, qi * BQ, 0, hh, bb);
       for (int t = 0; t < n; ++t) {
         const int s = t % NS;
         const uint32_t ph = (uint32_t)(t / NS) & 1u;
-        const int j = list[t];
         if (t >= NS) mbar_wait(&k_empty[s], ph ^ 1u);
         mbar_expect_tx(&k_full[s], C::KV_BYTES);
-        tma_load_5d(smem + C::OFF_K + s * C::KV_BYTES, &tmK, &k_full[s], 0, j * BKV, 0, hh, bb);
+        tma_load_5d(smem + C::OFF_K + s * C::KV_BYTES, &tmK, &k_full[s], 0, list[t] * BKV, 0, hh, bb);
+      }
+    }
+  } else if (warp == 6) {
+    // ---------------- TMA producer: V ----------------
+    if (elect_one()) {
+      tma_prefetch(&tmV);
+      for (int t = 0; t < n; ++t) {
+        const int s = t % NS;
+        const uint32_t ph = (uint32_t)(t / NS) & 1u;
         if (t >= NS) mbar_wait(&v_empty[s], ph ^ 1u);
         mbar_expect_tx(&v_full[s], C::KV_BYTES);
-        tma_load_5d(smem + C::OFF_V + s * C::KV_BYTES, &tmV, &v_full[s], 0, j * BKV, 0, hh, bb);
+        tma_load_5d(smem + C::OFF_V + s * C::KV_BYTES, &tmV, &v_full[s], 0, list[t] * BKV, 0, hh, bb);
       }
     }
   } else if (warp == 1) {
@@ -194,7 +204,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
       }
     }
     __syncwarp();
-  } else {
+  } else if (warp < 6) {
     // ---------------- softmax warps (2..5) ----------------
     const int q4 = warp & 3;
     const int row = q4 * 32 + lane;

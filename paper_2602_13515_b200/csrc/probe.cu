@@ -82,8 +82,11 @@ __global__ void __launch_bounds__(128) k_probe(const __nv_bfloat16* a, const __n
   if (threadIdx.x == 0) {
     tc_fence_after();
     const uint32_t idesc = idesc_bf16(M, N, a_mn != 0, b_mn != 0);
+    if (use_tma == 3)  // A: smem (K-major SW128) -> TMEM columns [128, 128 + K/2) by tcgen05.cp
+      for (int ks = 0; ks < K / 16; ++ks)
+        tmem_cp_128x256b(tbase + 128u + (uint32_t)(ks * 8), operand_desc(smem_u32(sa), false, Ra, ks));
     for (int ks = 0; ks < K / 16; ++ks) {
-      if (use_tma == 2)
+      if (use_tma >= 2)
         mma_bf16_ts(tbase, tbase + 128u + (uint32_t)(ks * 8), operand_desc(smem_u32(sb), b_mn, Rb, ks), idesc,
                     ks > 0 ? 1u : 0u);
       else
@@ -110,6 +113,52 @@ __global__ void __launch_bounds__(128) k_probe(const __nv_bfloat16* a, const __n
   if (warp_id() == 0) tmem_dealloc(tbase, 256);
 }
 
+
+// Variant: `issuers` warps each run their own ring of `stages` requests; a request is either
+// one tensor-map box of (64 cols x box_rows x chunks) over a [rows][128] bf16 matrix (mode 0)
+// or one 1-D cp.async.bulk of the same byte count from a contiguous random offset (mode 1).
+__global__ void __launch_bounds__(512) k_tma_rate2(const __grid_constant__ CUtensorMap map, const uint8_t* gbuf,
+                                                  int rows_total, int iters, int stages, int box_rows, int chunks,
+                                                  int mode, unsigned long long* cycles) {
+  extern __shared__ uint8_t smem_dyn[];
+  __shared__ uint64_t full[4][8];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+  const uint32_t bytes = (uint32_t)box_rows * 128u * (uint32_t)chunks;
+  const int stride = max(1, mode >> 8);
+  mode &= 0xff;
+  const int w = (int)warp_id() / stride;
+  const bool issuer = lane_id() == 0 && (int)warp_id() % stride == 0;
+  if (issuer) {
+    for (int s = 0; s < stages; ++s) mbar_init(&full[w][s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (issuer) {
+    uint8_t* mine = base + (size_t)w * stages * bytes;
+    const int tiles = rows_total / box_rows;
+    uint32_t r = ((uint32_t)blockIdx.x * 4u + (uint32_t)w) * 2654435761u;
+    const uint64_t t0 = clock64();
+    for (int i = 0; i < iters + stages; ++i) {
+      const int s = i % stages;
+      if (i >= stages) mbar_wait(&full[w][s], (uint32_t)((i - stages) / stages) & 1u);
+      if (i < iters) {
+        r = r * 1664525u + 1013904223u;
+        const int tile = (int)((r >> 8) % (uint32_t)tiles);
+        mbar_expect_tx(&full[w][s], bytes);
+        if (mode == 0) {
+          tma_load_5d(mine + s * bytes, &map, &full[w][s], 0, tile * box_rows, 0, 0, 0);
+        } else {
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  smem_u32(mine + s * bytes)),
+              "l"(gbuf + (size_t)tile * box_rows * 256), "r"(bytes), "r"(smem_u32(&full[w][s]))
+              : "memory");
+        }
+      }
+    }
+    cycles[blockIdx.x * 4 + w] = clock64() - t0;
+  }
+}
 }  // namespace
 }  // namespace spa2
 
@@ -120,8 +169,8 @@ extern "C" int spa2_probe_gemm(const void* a, const void* b, float* d, int m, in
   SPA2_REQUIRE(m == 64 || m == 128, SPA2_ERR_UNSUPPORTED, "probe: m must be 64 or 128");
   SPA2_REQUIRE(n == 64 || n == 128, SPA2_ERR_UNSUPPORTED, "probe: n must be 64 or 128");
   SPA2_REQUIRE(k == 64 || k == 128, SPA2_ERR_UNSUPPORTED, "probe: k must be 64 or 128");
-  SPA2_REQUIRE(use_tma >= 0 && use_tma <= 2, SPA2_ERR_VALUE, "probe: mode must be 0, 1 or 2");
-  SPA2_REQUIRE(use_tma != 2 || (m == 128 && a_mn == 0), SPA2_ERR_UNSUPPORTED, "probe: TMEM A needs m=128, K-major");
+  SPA2_REQUIRE(use_tma >= 0 && use_tma <= 3, SPA2_ERR_VALUE, "probe: mode must be 0..3");
+  SPA2_REQUIRE(use_tma < 2 || (m == 128 && a_mn == 0), SPA2_ERR_UNSUPPORTED, "probe: TMEM A needs m=128, K-major");
   CUtensorMap ta, tb;
   memset(&ta, 0, sizeof(ta));
   memset(&tb, 0, sizeof(tb));
@@ -253,6 +302,26 @@ extern "C" int spa2_probe_tma_rate(const void* buf, long long rows, int box_rows
   const size_t smem = (size_t)stages * box_rows * 128 + 1024;
   SPA2_CUDA_TRY(cudaFuncSetAttribute(k_tma_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k_tma_rate<<<ctas, 32, smem, (cudaStream_t)stream>>>(map, (int)rows, iters, stages, box_rows, cycles);
+  SPA2_LAUNCH_CHECK();
+  return SPA2_OK;
+}
+
+extern "C" int spa2_probe_tma_rate2(const void* buf, long long rows, int box_rows, int chunks, int stages, int issuers,
+                                    int mode, int iters, int ctas, unsigned long long* cycles, void* stream) {
+  SPA2_REQUIRE(stages >= 1 && stages <= 8 && issuers >= 1 && issuers <= 4 && box_rows >= 8 && box_rows <= 256 &&
+                   (chunks == 1 || chunks == 2),
+               SPA2_ERR_VALUE, "tma_rate2: bad args");
+  CUtensorMap map;
+  const uint64_t dims[5] = {64, (uint64_t)rows, 2, 1, 1};
+  const uint64_t strides[4] = {256, 128, (uint64_t)rows * 256, (uint64_t)rows * 256};
+  const uint32_t box[5] = {64, (uint32_t)box_rows, (uint32_t)chunks, 1, 1};
+  int rc = make_tma_bf16_5d(&map, buf, dims, strides, box);
+  if (rc) return rc;
+  const size_t smem = (size_t)issuers * stages * box_rows * 128 * chunks + 1024;
+  SPA2_REQUIRE(smem <= 232448, SPA2_ERR_VALUE, "tma_rate2: %zu bytes of smem", smem);
+  SPA2_CUDA_TRY(cudaFuncSetAttribute(k_tma_rate2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_tma_rate2<<<ctas, 32 * issuers * max(1, mode >> 8), smem, (cudaStream_t)stream>>>(map, (const uint8_t*)buf, (int)rows, iters, stages,
+                                                                  box_rows, chunks, mode, cycles);
   SPA2_LAUNCH_CHECK();
   return SPA2_OK;
 }

@@ -211,6 +211,12 @@ __device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, ui
       : "memory");
 }
 // Arrive once on `bar` when every MMA previously issued by this thread has completed.
+// smem -> TMEM copy of a 128-row x 32-byte slab described by a UMMA smem descriptor: row r
+// lands in TMEM lane r, 8 consecutive 32-bit columns (the TMEM A-operand layout of one
+// K=16 bf16 step).  Asynchronous; ordered with tcgen05.mma issued by the same thread.
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+}
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))

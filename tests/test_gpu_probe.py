@@ -30,3 +30,19 @@ def test_probe_gemm(m, n, k, a_mn, b_mn, use_tma):
     want = a.float() @ b.float().t()
     err = (d - want).abs().max().item()
     assert err <= 1e-3 * max(1.0, want.abs().max().item()), (m, n, k, a_mn, b_mn, use_tma, err)
+
+
+@pytest.mark.parametrize("n,k", [(64, 128), (128, 128), (128, 64), (64, 64)])
+def test_probe_tmem_cp_a_operand(n, k):
+    """A staged K-major SWIZZLE_128B in smem, copied to TMEM with tcgen05.cp (128x256b per
+    K=16 step), then consumed by TS MMAs — the Q/dO-in-TMEM layout of the fwd/dQ kernels."""
+    g = torch.Generator(device="cuda").manual_seed(n + k)
+    a = torch.randn(128, k, device="cuda", generator=g).to(torch.bfloat16)
+    b = torch.randn(n, k, device="cuda", generator=g).to(torch.bfloat16)
+    d = torch.full((128, n), float("nan"), device="cuda", dtype=torch.float32)
+    lib = _lib.load()
+    _lib.check(lib.spa2_probe_gemm(_lib.ptr(a), _lib.ptr(b), _lib.ptr(d), 128, n, k, 0, 0, 3,
+                                   torch.cuda.current_stream().cuda_stream), "probe")
+    torch.cuda.synchronize()
+    want = a.float() @ b.float().t()
+    assert (d - want).abs().max().item() <= 1e-3 * max(1.0, want.abs().max().item())

@@ -75,5 +75,41 @@ def main():
     print("tile period cycles: median", per[len(per) // 2], "p10", per[len(per) // 10], "p90", per[9 * len(per) // 10])
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and len(sys.argv) == 1:
     main()
+
+
+def timeline():
+    """Per-tile event timeline (cycles relative to the first shown event) for a steady-state
+    window: producer P1/P2 (wait free stage / load issued), MMA M2 (S/dP issued), M4 (dV
+    issued), M5 (dK issued), elementwise E1/E2 (wait S / S landed), E3 (P buffer free), E5 (P
+    stored), E4 (dS stored)."""
+    q, k, v = wan_like_qkv(1, 12, 32760, 128, 0.9, seed=0)
+    do = torch.randn_like(q)
+    cfg = spa.SparsityConfig(0.03, 0.2, 128, 64)
+    bm = at._hybrid_mask_device(q, k, cfg, False)
+    lists = at.mask_lists(bm, 1, 12, 32760)
+    scale = 1 / math.sqrt(128)
+    o, lse = at.fwd(q, k, v, lists, scale)
+    at.bwd(q, k, v, o, do, lse, lists, scale)
+    cap = 1 << 16
+    buf = torch.zeros(2 + cap, dtype=torch.int64, device="cuda")
+    _lib.load().spa2_debug_trace(_lib.ptr(buf), cap)
+    at.bwd(q, k, v, o, do, lse, lists, scale)
+    torch.cuda.synchronize()
+    _lib.load().spa2_debug_trace(None, 0)
+    R = cap // 4
+    raw = buf[2:].view(4, R).cpu()
+    names = {0: "P", 1: "M", 2: "E", 3: "X"}
+    ev = []
+    for role, slot in raw.nonzero().tolist():
+        ev.append((int(raw[role, slot]), f"{names[role]}{slot % 8}", slot // 8))
+    ev.sort()
+    lo = [e for e in ev if e[1][0] in "PME" and 40 <= e[2] < 46]
+    t0 = lo[0][0]
+    for t, kind, g in lo:
+        print(f"{t - t0:7d} {kind} g={g}")
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "timeline":
+    timeline()
