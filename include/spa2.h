@@ -156,6 +156,8 @@ int spa2_probe_tma_rate(const void* buf, long long rows, int box_rows, int stage
 /* Variant (diagnostic): `issuers` warps per CTA with their own rings; requests are tensor boxes
  * of box_rows x 64 x chunks (mode 0) or 1-D bulk copies of the same size (mode 1) over a
  * [rows][128] bf16 matrix.  cycles[ctas*4] receives per-(CTA, issuer) cycle counts. */
+/* MMA mix probe (diagnostic): the dQ kernel's per-tile tcgen05 sequence in isolation; see probe.cu. */
+int spa2_probe_mma_mix(int reps, int flags, int ctas, const void* gsrc, unsigned long long* cycles, void* stream);
 int spa2_probe_tma_rate2(const void* buf, long long rows, int box_rows, int chunks, int stages, int issuers,
                          int mode, int iters, int ctas, unsigned long long* cycles, void* stream);
 

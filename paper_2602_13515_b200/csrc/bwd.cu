@@ -58,6 +58,7 @@ struct BwdParams {
   int64_t o1_sb, o1_sh, o1_sn;
   unsigned long long* trace;  // diagnostic (spa2_debug_trace), normally null
   int trace_cap;
+  int dbg;                    // diagnostic timing experiments (SPA2_DEBUG_FLAGS), normally 0
 };
 
 struct Item {
@@ -72,6 +73,44 @@ __device__ __forceinline__ Item get_item(const BwdParams& p, int wi, int nblk) {
   m.beg = p.ptr[w];
   m.n = p.ptr[w + 1] - m.beg;
   return m;
+}
+
+// Work-list cursor shared by the roles of the persistent kernels: walks this CTA's items
+// (blockIdx.x, +gridDim.x, ...) skipping empty ones, one tile at a time.
+struct Cursor {
+  int wi, it, t, n, beg, bh, blk, g;
+  bool valid;
+};
+__device__ __forceinline__ void cursor_item(Cursor& c, const BwdParams& p, int nblk) {
+  for (;;) {
+    c.wi += gridDim.x;
+    if (c.wi >= p.num_items) {
+      c.valid = false;
+      return;
+    }
+    const Item m = get_item(p, c.wi, nblk);
+    if (m.n > 0) {
+      c.n = m.n;
+      c.beg = m.beg;
+      c.bh = m.bh;
+      c.blk = m.blk;
+      c.t = 0;
+      ++c.it;
+      c.valid = true;
+      return;
+    }
+  }
+}
+__device__ __forceinline__ void cursor_init(Cursor& c, const BwdParams& p, int nblk) {
+  c.wi = (int)blockIdx.x - (int)gridDim.x;
+  c.it = -1;
+  c.g = 0;
+  c.valid = false;
+  cursor_item(c, p, nblk);
+}
+__device__ __forceinline__ void cursor_next(Cursor& c, const BwdParams& p, int nblk) {
+  ++c.g;
+  if (++c.t >= c.n) cursor_item(c, p, nblk);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -605,6 +644,354 @@ __global__ void __launch_bounds__(kDq2Threads, 2)
   if (warp == 1) tmem_dealloc(tbase, 256);
 }
 
+// ---------------------------------------------------------------------------------------
+// K7 (default): dQ, persistent (one CTA per SM), with Q_i and dO_i RESIDENT IN TMEM.
+// Work item = query block i; tiles = its kept key blocks j.  Q_i and dO_i are staged once
+// per item by TMA and copied into TMEM with tcgen05.cp, so S = Q K_jᵀ and dP = dO V_jᵀ are
+// TS-MMAs that read only K_j / V_j from shared memory (2 KB per K=16 step instead of 6 KB:
+// the SS form is smem-bandwidth bound at 48 cycles per step, profiles/mma_rate_r01.md).
+// TMEM (512 columns): Q [0,64) | dO [64,128) | S/dP double buffer [128,384) | dQ acc [384,512).
+// dS (bf16) overwrites the S columns its thread group read and feeds dQ += dS K_j (TS).
+// Warps: 0 TMA (Q, K ring), 1 MMA, 2-9 elementwise (2 per TMEM lane quarter, 32 columns
+// each), 10-13 epilogue (acc -> bf16 -> global), 14 TMA (dO, V ring).
+// ---------------------------------------------------------------------------------------
+// Warp roles of k_dq3 for EWW elementwise warps (EWW/4 per TMEM lane quarter).
+template <int EWW>
+struct Dq3Roles {
+  static constexpr int EPI0 = 2 + EWW, PROD2 = EPI0 + 4, ISSUE_DP = PROD2 + 1, ISSUE_DQ = PROD2 + 2;
+  static constexpr int THREADS = 32 * (ISSUE_DQ + 1);
+  static constexpr int CPT = 256 / EWW;  // S/dP columns per elementwise thread
+};
+
+template <int HD>
+struct Dq3Cfg {
+  static constexpr int NK = 4, NV = 4;
+  static constexpr int Q_BYTES = BQ * HD * 2;
+  static constexpr int KV_BYTES = BKV * HD * 2;
+  static constexpr int OFF_QS = 0;  // staging [Q | dO] of the next item
+  static constexpr int OFF_K = 2 * Q_BYTES;
+  static constexpr int OFF_V = OFF_K + NK * KV_BYTES;
+  static constexpr int OFF_BAR = OFF_V + NV * KV_BYTES;
+  static constexpr int NUM_BARS = 4 + 2 * NK + 2 * NV + 2 * 4 + 2;
+  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;
+  static constexpr uint32_t Q_COL = 0, DO_COL = 64, SDP_COL = 128, ACC_COL = 384;  // S at +b*128, dP at +64
+};
+
+// TMEM column of the packed bf16 dS for K step ks: thread group g read S columns
+// [CPT·g, CPT·(g+1)) and packs its dS into the first CPT/2 of them.
+template <int CPT>
+__device__ __forceinline__ uint32_t ds_col(int ks) {
+  return (uint32_t)((16 * ks / CPT) * CPT + (16 * ks % CPT) / 2);
+}
+
+template <int HD, int EWW>
+__global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
+    k_dq3(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+          const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO, const BwdParams p) {
+  using C = Dq3Cfg<HD>;
+  using R = Dq3Roles<EWW>;
+  constexpr int NK = C::NK, NV = C::NV;
+  constexpr int CPT = R::CPT;
+  constexpr int kPolyPairs = CPT / 8;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* qs_full = bars;         // staging holds Q_i and dO_i of item `it`
+  uint64_t* qs_free = bars + 1;     // tcgen05.cp of item `it` done: staging reusable
+  uint64_t* qd_free = bars + 2;     // last S/dP MMA of item `it` done: TMEM Q/dO reusable
+  uint64_t* qd_ready = bars + 3;    // Q/dO of item `it` copied into TMEM
+  uint64_t* k_full = bars + 4;      // [NK]
+  uint64_t* k_empty = k_full + NK;  // [NK]
+  uint64_t* v_full = k_empty + NK;  // [NV]
+  uint64_t* v_empty = v_full + NV;  // [NV]
+  uint64_t* s_full = v_empty + NV;  // [2]
+  uint64_t* dp_full = s_full + 2;   // [2]
+  uint64_t* ds_full = dp_full + 2;  // [2] dS of tile g packed into TMEM buffer g&1
+  uint64_t* dq_done = ds_full + 2;  // [2] dQ MMA of tile g done (buffer and K slot free)
+  uint64_t* acc_full = dq_done + 2;
+  uint64_t* acc_empty = acc_full + 1;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 1);
+
+  const int warp = (int)warp_id(), lane = (int)lane_id();
+  if (threadIdx.x == 0) {
+    if (smem_u32(smem) & 1023u) __trap();
+    mbar_init(qs_full, 2);  // Q from warp 0, dO from warp 14
+    mbar_init(qs_free, 1);
+    mbar_init(qd_free, 2);  // last S (warp 1) and last dP (warp 15) of the item
+    mbar_init(qd_ready, 1);
+    for (int s = 0; s < NK; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < NV; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&dp_full[b], 1);
+      mbar_init(&ds_full[b], 32 * EWW);
+      mbar_init(&dq_done[b], 1);
+    }
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, 128);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_holder, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_holder;
+
+  if (warp == 0 || warp == R::PROD2) {
+    // ---------------- TMA producers: warp 0 Q + K ring, warp 14 dO + V ring ----------------
+    if (elect_one()) {
+      const bool second = warp == R::PROD2;
+      const CUtensorMap* tmR = second ? &tmDO : &tmQ;
+      const CUtensorMap* tmKV = second ? &tmV : &tmK;
+      tma_prefetch(tmR);
+      tma_prefetch(tmKV);
+      uint64_t* full = second ? v_full : k_full;
+      uint64_t* empty = second ? v_empty : k_empty;
+      const int ns = second ? NV : NK;
+      uint8_t* const ring = smem + (second ? C::OFF_V : C::OFF_K);
+      int it = 0, g = 0;
+      for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
+        const Item m = get_item(p, wi, p.T_m);
+        if (m.n == 0) continue;
+        const int hh = m.bh % p.H, bb = m.bh / p.H;
+        if (it >= 1) mbar_wait(qs_free, (uint32_t)(it - 1) & 1u);
+        mbar_expect_tx(qs_full, C::Q_BYTES);
+        tma_load_5d(smem + C::OFF_QS + (second ? C::Q_BYTES : 0), tmR, qs_full, 0, m.blk * BQ, 0, hh, bb);
+        for (int t = 0; t < m.n; ++t, ++g) {
+          const int s = g % ns;
+          if (!second) trace_ev(p.trace, p.trace_cap, 0, 1, g);
+          if (g >= ns) mbar_wait(&empty[s], ((uint32_t)(g / ns) + 1u) & 1u);
+          if (!second) trace_ev(p.trace, p.trace_cap, 0, 2, g);
+          mbar_expect_tx(&full[s], C::KV_BYTES);
+          tma_load_5d(ring + s * C::KV_BYTES, tmKV, &full[s], 0, p.idx[m.beg + t] * BKV, 0, hh, bb);
+        }
+        ++it;
+      }
+    }
+  } else if (warp == 1 || warp == R::ISSUE_DP || warp == R::ISSUE_DQ) {
+    // ---------------- MMA issue: three warps, one per independent stream ----------------
+    // warp 1: (Q/dO copy into TMEM per item) + S = Q K_jᵀ;  warp 15: dP = dO V_jᵀ;
+    // warp 16: dQ += dS K_j.  One issuing warp cannot feed N=64 MMAs (32 cycles each) fast
+    // enough; the streams only meet through mbarriers.  Each warp issues warp-collectively.
+    constexpr uint32_t idS = idesc_bf16(BQ, BKV, false, false);
+    constexpr uint32_t idQ = idesc_bf16(BQ, HD, false, true);
+    const uint64_t dQS = sw128_desc(smem_u32(smem + C::OFF_QS), 16, 1024);
+    const uint64_t dK0 = sw128_desc(smem_u32(smem + C::OFF_K), 16, 1024);
+    const uint64_t dV0 = sw128_desc(smem_u32(smem + C::OFF_V), 16, 1024);
+    const uint64_t dKm0 = sw128_desc(smem_u32(smem + C::OFF_K), BKV * 128, 1024);
+    constexpr uint64_t KV16 = (uint64_t)(C::KV_BYTES >> 4);
+    Cursor c;
+    cursor_init(c, p, p.T_m);
+    if (warp == 1) {
+      for (; c.valid; cursor_next(c, p, p.T_m)) {
+        if (c.t == 0) {
+          mbar_wait(qs_full, (uint32_t)c.it & 1u);
+          if (c.it >= 1) mbar_wait(qd_free, (uint32_t)(c.it - 1) & 1u);
+          tc_fence_after();
+#pragma unroll
+          for (int ks = 0; ks < HD / 16; ++ks) {
+            const uint64_t qo = (uint64_t)(((ks * 16 / 64) * BQ * 128 + (ks * 16 % 64) * 2) >> 4);
+            tmem_cp_128x256b_w(tbase + C::Q_COL + (uint32_t)(ks * 8), dQS + qo);
+            tmem_cp_128x256b_w(tbase + C::DO_COL + (uint32_t)(ks * 8), dQS + (uint64_t)(C::Q_BYTES >> 4) + qo);
+          }
+          mma_commit_w(qs_free);
+          mma_commit_w(qd_ready);
+        }
+        const int b = c.g & 1, sk = c.g % NK;
+        if (c.g >= 2) mbar_wait(&dq_done[b], (uint32_t)((c.g - 2) >> 1) & 1u);  // dS of tile g-2 consumed
+        mbar_wait(&k_full[sk], (uint32_t)(c.g / NK) & 1u);
+        tc_fence_after();
+        trace_ev(p.trace, p.trace_cap, 1, 2, c.g);
+        const uint64_t dK = dK0 + (uint64_t)sk * KV16;
+        const uint32_t sb = tbase + C::SDP_COL + (uint32_t)(b * 128);
+#pragma unroll
+        for (int ks = 0; ks < HD / 16; ++ks)
+          mma_bf16_ts_w(sb, tbase + C::Q_COL + (uint32_t)(ks * 8),
+                        dK + (uint64_t)((((ks * 16 / 64) * BKV * 128 + (ks * 16 % 64) * 2)) >> 4), idS, ks > 0 ? 1u : 0u);
+        mma_commit_w(&s_full[b]);
+        if (c.t == c.n - 1) mma_commit_w(qd_free);
+        trace_ev(p.trace, p.trace_cap, 1, 3, c.g);
+      }
+    } else if (warp == R::ISSUE_DP) {
+      for (; c.valid; cursor_next(c, p, p.T_m)) {
+        if (c.t == 0) mbar_wait(qd_ready, (uint32_t)c.it & 1u);
+        const int b = c.g & 1, sv = c.g % NV;
+        if (c.g >= 2) mbar_wait(&dq_done[b], (uint32_t)((c.g - 2) >> 1) & 1u);
+        mbar_wait(&v_full[sv], (uint32_t)(c.g / NV) & 1u);
+        tc_fence_after();
+        const uint64_t dV = dV0 + (uint64_t)sv * KV16;
+        const uint32_t sb = tbase + C::SDP_COL + (uint32_t)(b * 128) + 64u;
+#pragma unroll
+        for (int ks = 0; ks < HD / 16; ++ks)
+          mma_bf16_ts_w(sb, tbase + C::DO_COL + (uint32_t)(ks * 8),
+                        dV + (uint64_t)((((ks * 16 / 64) * BKV * 128 + (ks * 16 % 64) * 2)) >> 4), idS, ks > 0 ? 1u : 0u);
+        mma_commit_w(&dp_full[b]);
+        mma_commit_w(&v_empty[sv]);
+        if (c.t == c.n - 1) mma_commit_w(qd_free);
+      }
+    } else {
+      for (; c.valid; cursor_next(c, p, p.T_m)) {
+        const int b = c.g & 1, sk = c.g % NK;
+        if (c.t == 0 && c.it >= 1) mbar_wait(acc_empty, (uint32_t)(c.it - 1) & 1u);
+        mbar_wait(&ds_full[b], (uint32_t)(c.g >> 1) & 1u);
+        tc_fence_after();
+        trace_ev(p.trace, p.trace_cap, 1, 4, c.g);
+        const uint64_t dKm = dKm0 + (uint64_t)sk * KV16;
+        const uint32_t sb = tbase + C::SDP_COL + (uint32_t)(b * 128);
+#pragma unroll
+        for (int ks = 0; ks < BKV / 16; ++ks)
+          mma_bf16_ts_w(tbase + C::ACC_COL, sb + ds_col<CPT>(ks), dKm + (uint64_t)((ks * 2048) >> 4), idQ,
+                        (c.t > 0 || ks > 0) ? 1u : 0u);
+        mma_commit_w(&dq_done[b]);
+        mma_commit_w(&k_empty[sk]);
+        if (c.t == c.n - 1) mma_commit_w(acc_full);
+        trace_ev(p.trace, p.trace_cap, 1, 5, c.g);
+      }
+    }
+  } else if (warp < R::EPI0) {
+    // ---------------- elementwise: dS = P ∘ (dP − δ), P = exp2(S·c − LSE·log2e) ----------------
+    const int q4 = warp & 3;
+    const int grp = (warp - 2) >> 2;
+    const int row = q4 * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    const int col0 = CPT * grp;
+    const int kv_tail = p.N - (p.T_n - 1) * BKV;
+    const float sl2 = p.sl2;
+    int g = 0;
+    for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
+      const Item m = get_item(p, wi, p.T_m);
+      if (m.n == 0) continue;
+      const int tok = m.blk * BQ + row;
+      const bool valid = tok < p.N;
+      const float lse2 = valid ? __ldg(p.lse + (int64_t)m.bh * p.N + tok) * kLog2e : INFINITY;
+      const float dlt = valid ? __ldg(p.delta + (int64_t)m.bh * p.N + tok) : 0.f;
+      // key-block index of the next tile is loaded one tile ahead (off the critical path)
+      int j_next = __ldg(p.idx + m.beg);
+      for (int t = 0; t < m.n; ++t, ++g) {
+        const int b = g & 1;
+        const bool tail = kv_tail < BKV && j_next == p.T_n - 1;
+        if (t + 1 < m.n) j_next = __ldg(p.idx + m.beg + t + 1);
+        const uint32_t sb = tbase + lane_off + C::SDP_COL + (uint32_t)(b * 128);
+        if (threadIdx.x == 64) trace_ev(p.trace, p.trace_cap, 2, 1, g);
+        mbar_wait(&s_full[b], (uint32_t)(g >> 1) & 1u);
+        if (threadIdx.x == 64) trace_ev(p.trace, p.trace_cap, 2, 2, g);
+        tc_fence_after();
+        if (p.dbg & 1) {  // timing experiment: no elementwise work
+          tc_fence_before();
+          mbar_arrive(&ds_full[b]);
+          continue;
+        }
+        uint32_t sr[CPT];
+        if constexpr (CPT == 32) tmem_ld32(sb + (uint32_t)col0, sr);
+        else tmem_ld16(sb + (uint32_t)col0, sr);
+        // packed fp32x2 math (FFMA2/FADD2/FMUL2): the issue slots of this SM sub-partition are
+        // shared with an MMA-issuing warp, so fewer instructions per element = faster MMAs
+        float pv[CPT];
+#pragma unroll
+        for (int c = 0; c < CPT / 2; ++c) {
+          const float2 x = __ffma2_rn(make_float2(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1])),
+                                      make_float2(sl2, sl2), make_float2(-lse2, -lse2));
+          if (c < kPolyPairs) {  // a quarter of the exponentials on the FMA pipe
+            const float2 e = exp2_poly2(x);
+            pv[2 * c] = e.x;
+            pv[2 * c + 1] = e.y;
+          } else {
+            pv[2 * c] = ex2(x.x);
+            pv[2 * c + 1] = ex2(x.y);
+          }
+        }
+        if (tail) {
+#pragma unroll
+          for (int c = 0; c < CPT; ++c)
+            if (col0 + c >= kv_tail) pv[c] = 0.f;
+        }
+        mbar_wait(&dp_full[b], (uint32_t)(g >> 1) & 1u);
+        if (threadIdx.x == 64) trace_ev(p.trace, p.trace_cap, 2, 3, g);
+        tc_fence_after();
+        uint32_t dr[CPT];
+        if constexpr (CPT == 32) tmem_ld32(sb + 64u + (uint32_t)col0, dr);
+        else tmem_ld16(sb + 64u + (uint32_t)col0, dr);
+        uint32_t pk[CPT / 2];
+#pragma unroll
+        for (int c = 0; c < CPT / 2; ++c) {
+          const float2 ds = __fmul2_rn(make_float2(pv[2 * c], pv[2 * c + 1]),
+                                       __fadd2_rn(make_float2(__uint_as_float(dr[2 * c]), __uint_as_float(dr[2 * c + 1])),
+                                                  make_float2(-dlt, -dlt)));
+          pk[c] = pack_bf16(ds.x, ds.y);
+        }
+        if constexpr (CPT == 32) tmem_st16(sb + (uint32_t)col0, pk);
+        else tmem_st8(sb + (uint32_t)col0, pk);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&ds_full[b]);
+        if (threadIdx.x == 64) trace_ev(p.trace, p.trace_cap, 2, 4, g);
+      }
+    }
+  } else if (warp < R::PROD2) {
+    // ---------------- epilogue: dQ = scale · acc -> bf16, direct 16-byte row stores ----------------
+    const int q4 = warp & 3;
+    const int row = q4 * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    int it = 0;
+    for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
+      const Item m = get_item(p, wi, p.T_m);
+      const int hh = m.bh % p.H, bb = m.bh / p.H;
+      const int tok = m.blk * BQ + row;
+      __nv_bfloat16* dst = p.out0 + bb * p.o0_sb + hh * p.o0_sh + (int64_t)tok * p.o0_sn;
+      if (m.n == 0) {
+        if (tok < p.N)
+          for (int c = 0; c < HD; c += 8) *reinterpret_cast<uint4*>(dst + c) = make_uint4(0, 0, 0, 0);
+        continue;
+      }
+      mbar_wait(acc_full, (uint32_t)it & 1u);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c0 = 0; c0 < HD; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tbase + lane_off + C::ACC_COL + (uint32_t)c0, r);
+        if (c0 + 32 == HD) {
+          tc_fence_before();
+          mbar_arrive(acc_empty);
+        }
+        uint32_t pk[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+          pk[c] = pack_bf16(__uint_as_float(r[2 * c]) * p.scale, __uint_as_float(r[2 * c + 1]) * p.scale);
+        if (tok < p.N) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            *reinterpret_cast<uint4*>(dst + c0 + 8 * u) = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        }
+      }
+      ++it;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tbase, 512);
+}
+
+int dq_ew_warps() {
+  static const int v = [] {
+    const char* e = getenv("SPA2_DQ_EW");
+    return (e != nullptr && atoi(e) == 8) ? 8 : 16;
+  }();
+  return v;
+}
+
+int dq_variant() {
+  static const int v = [] {
+    const char* e = getenv("SPA2_DQ_VARIANT");
+    return e != nullptr ? atoi(e) : 3;
+  }();
+  return v;
+}
+
 bool dq_variant2() {
   static const bool v = [] {
     const char* e = getenv("SPA2_DQ_PERSISTENT");
@@ -613,43 +1000,6 @@ bool dq_variant2() {
   return v;
 }
 
-// Work-list cursor shared by the roles of the persistent kernels: walks this CTA's items
-// (blockIdx.x, +gridDim.x, ...) skipping empty ones, one tile at a time.
-struct Cursor {
-  int wi, it, t, n, beg, bh, blk, g;
-  bool valid;
-};
-__device__ __forceinline__ void cursor_item(Cursor& c, const BwdParams& p, int nblk) {
-  for (;;) {
-    c.wi += gridDim.x;
-    if (c.wi >= p.num_items) {
-      c.valid = false;
-      return;
-    }
-    const Item m = get_item(p, c.wi, nblk);
-    if (m.n > 0) {
-      c.n = m.n;
-      c.beg = m.beg;
-      c.bh = m.bh;
-      c.blk = m.blk;
-      c.t = 0;
-      ++c.it;
-      c.valid = true;
-      return;
-    }
-  }
-}
-__device__ __forceinline__ void cursor_init(Cursor& c, const BwdParams& p, int nblk) {
-  c.wi = (int)blockIdx.x - (int)gridDim.x;
-  c.it = -1;
-  c.g = 0;
-  c.valid = false;
-  cursor_item(c, p, nblk);
-}
-__device__ __forceinline__ void cursor_next(Cursor& c, const BwdParams& p, int nblk) {
-  ++c.g;
-  if (++c.t >= c.n) cursor_item(c, p, nblk);
-}
 
 // Warp roles: 0 TMA (K, Q), 1 MMA, 2 .. 2+EWW-1 elementwise (EWW/4 warps per TMEM lane
 // quarter, 256/EWW columns each), then 4 epilogue warps, then TMA (V, dO).
@@ -657,7 +1007,8 @@ template <int EWW>
 struct DkvRoles {
   static constexpr int EPI0 = 2 + EWW;           // first epilogue warp
   static constexpr int PROD2 = EPI0 + 4;         // second producer warp
-  static constexpr int THREADS = 32 * (PROD2 + 1);
+  static constexpr int ISSUE2 = PROD2 + 1;       // dV/dK issuing warp
+  static constexpr int THREADS = 32 * (ISSUE2 + 1);
   static constexpr int CPT = 256 / EWW;          // S/dP columns per elementwise thread
 };
 
@@ -757,112 +1108,74 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
         ++it;
       }
     }
-  } else if (warp == 1) {
-    // ---------------- MMA issuer: dataflow order ----------------
-    // Two streams: S/dP of tile gs (needs its Q/dO and a free S/dP TMEM buffer, i.e. at
-    // most one tile ahead of the accumulate stream) and dV (needs P) then dK (needs dS) of
-    // tile gd.  Whichever is ready is issued, so accumulation never waits behind a load.
-    if (elect_one()) {
-      constexpr uint32_t idS = idesc_bf16(BQ, BKV, false, false);
-      constexpr uint32_t idT = idesc_bf16(HD, BKV, true, true);
-      const uint32_t sK = smem_u32(smem + C::OFF_KV), sV = sK + C::KV_BYTES;
-      Cursor cs, cd;
-      cursor_init(cs, p, p.T_n);
-      cursor_init(cd, p, p.T_n);
-      int kv_ready_it = -1;
-      int dphase = 0;  // 0: dV of tile cd.g next, 1: dK of tile cd.g next
-      uint64_t t_idle = 0;
-      uint32_t spins = 0;
-      while (cd.valid) {
-        bool progressed = false;
-        if (cs.valid && cs.g - cd.g < 2) {
-          bool ready = true;
-          if (kv_ready_it != cs.it) {
-            ready = mbar_test(kv_full, (uint32_t)cs.it & 1u);
-            if (ready) kv_ready_it = cs.it;
-          }
-          const int s = cs.g % NS;
-          if (ready && mbar_test(&qdo_full[s], (uint32_t)(cs.g / NS) & 1u)) {
-            tc_fence_after();
-            trace_ev(p.trace, p.trace_cap, 1, 2, cs.g);
-            const uint32_t b = (uint32_t)(cs.g & 1);
-            const uint32_t sQ = smem_u32(smem + C::OFF_QDO + s * 2 * C::Q_BYTES);
-            const uint32_t sDO = sQ + C::Q_BYTES;
+  } else if (warp == 1 || warp == R::ISSUE2) {
+    // ---------------- MMA issue: two warps, one per stream ----------------
+    // warp 1: S = Q_i K_jᵀ and dP = dO_i V_jᵀ of tile g into TMEM buffer g&1 (free once the
+    // elementwise warps have consumed tile g-2);  warp ISSUE2: dVᵀ += dO_iᵀ P (after P is in
+    // smem) then dKᵀ += Q_iᵀ dS (after dS).  Warp-collective issue, warp-uniform descriptors.
+    constexpr uint32_t idS = idesc_bf16(BQ, BKV, false, false);
+    constexpr uint32_t idT = idesc_bf16(HD, BKV, true, true);
+    const uint64_t dK = sw128_desc(smem_u32(smem + C::OFF_KV), 16, 1024);
+    const uint64_t dV = dK + (uint64_t)(C::KV_BYTES >> 4);
+    const uint64_t dQk0 = sw128_desc(smem_u32(smem + C::OFF_QDO), 16, 1024);        // K-major Q / dO
+    const uint64_t dQm0 = sw128_desc(smem_u32(smem + C::OFF_QDO), BQ * 128, 1024);  // MN-major Q / dO
+    const uint64_t dPm0 = sw128_desc(smem_u32(smem + C::OFF_PDS), BQ * 128, 1024);  // MN-major P / dS
+    constexpr uint64_t STAGE16 = (uint64_t)((2 * C::Q_BYTES) >> 4), Q16 = (uint64_t)(C::Q_BYTES >> 4);
+    constexpr uint64_t PBUF16 = (uint64_t)((2 * C::PB) >> 4), PB16 = (uint64_t)(C::PB >> 4);
+    Cursor c;
+    cursor_init(c, p, p.T_n);
+    if (warp == 1) {
+      for (; c.valid; cursor_next(c, p, p.T_n)) {
+        if (c.t == 0) mbar_wait(kv_full, (uint32_t)c.it & 1u);
+        const int s = c.g % NS;
+        const uint32_t b = (uint32_t)(c.g & 1);
+        if (c.g >= 2) mbar_wait(&ds_full[b], (uint32_t)((c.g - 2) >> 1) & 1u);  // S/dP buffer b read
+        mbar_wait(&qdo_full[s], (uint32_t)(c.g / NS) & 1u);
+        tc_fence_after();
+        trace_ev(p.trace, p.trace_cap, 1, 2, c.g);
+        const uint64_t dQ = dQk0 + (uint64_t)s * STAGE16, dDO = dQ + Q16;
 #pragma unroll
-            for (int ks = 0; ks < HD / 16; ++ks) {
-              const uint32_t qo = (uint32_t)((ks * 16 / 64) * BQ * 128 + (ks * 16 % 64) * 2);
-              const uint32_t ko = (uint32_t)((ks * 16 / 64) * BKV * 128 + (ks * 16 % 64) * 2);
-              mma_bf16(tbase + C::S_COL + b * 64, sw128_desc(sQ + qo, 16, 1024), sw128_desc(sK + ko, 16, 1024), idS,
-                       ks > 0 ? 1u : 0u);
-            }
-            mma_commit(&s_full[b]);
-#pragma unroll
-            for (int ks = 0; ks < HD / 16; ++ks) {
-              const uint32_t qo = (uint32_t)((ks * 16 / 64) * BQ * 128 + (ks * 16 % 64) * 2);
-              const uint32_t ko = (uint32_t)((ks * 16 / 64) * BKV * 128 + (ks * 16 % 64) * 2);
-              mma_bf16(tbase + C::DP_COL + b * 64, sw128_desc(sDO + qo, 16, 1024), sw128_desc(sV + ko, 16, 1024),
-                       idS, ks > 0 ? 1u : 0u);
-            }
-            mma_commit(&dp_full[b]);
-            if (cs.t == cs.n - 1) mma_commit(kv_empty);  // K_j / V_j are only read by S and dP
-            cursor_next(cs, p, p.T_n);
-            progressed = true;
-          }
+        for (int ks = 0; ks < HD / 16; ++ks) {
+          const uint64_t qo = (uint64_t)(((ks * 16 / 64) * BQ * 128 + (ks * 16 % 64) * 2) >> 4);
+          const uint64_t ko = (uint64_t)(((ks * 16 / 64) * BKV * 128 + (ks * 16 % 64) * 2) >> 4);
+          mma_bf16_w(tbase + C::S_COL + b * 64, dQ + qo, dK + ko, idS, ks > 0 ? 1u : 0u);
         }
-        if (cd.g < cs.g) {
-          const int pb = cd.g & 1;
-          const int s = cd.g % NS;
-          const uint32_t acc = tbase + C::ACC_COL + (uint32_t)((cd.it & 1) * 128);
-          const uint32_t sQ = smem_u32(smem + C::OFF_QDO + s * 2 * C::Q_BYTES);
-          const uint32_t sDO = sQ + C::Q_BYTES;
-          const uint32_t sP = smem_u32(smem + C::OFF_PDS + pb * 2 * C::PB), sDS = sP + C::PB;
-          const bool first = cd.t == 0;
-          if (dphase == 0) {
-            const bool acc_ok =
-                !(first && cd.it >= 2) || mbar_test(&acc_empty[cd.it & 1], ((uint32_t)(cd.it >> 1) + 1u) & 1u);
-            if (acc_ok && mbar_test(&p_full[pb], (uint32_t)(cd.g >> 1) & 1u)) {
-              tc_fence_after();
-              trace_ev(p.trace, p.trace_cap, 1, 4, cd.g);
+        mma_commit_w(&s_full[b]);
 #pragma unroll
-              for (int ks = 0; ks < BQ / 16; ++ks) {
-                const uint32_t ro = (uint32_t)(ks * 2048);
-                mma_bf16(acc, sw128_desc(sDO + ro, BQ * 128, 1024), sw128_desc(sP + ro, BQ * 128, 1024), idT,
-                         (!first || ks > 0) ? 1u : 0u);
-              }
-              dphase = 1;
-              progressed = true;
-            }
-          }
-          if (dphase == 1 && mbar_test(&ds_full[pb], (uint32_t)(cd.g >> 1) & 1u)) {
-            tc_fence_after();
-            trace_ev(p.trace, p.trace_cap, 1, 5, cd.g);
+        for (int ks = 0; ks < HD / 16; ++ks) {
+          const uint64_t qo = (uint64_t)(((ks * 16 / 64) * BQ * 128 + (ks * 16 % 64) * 2) >> 4);
+          const uint64_t ko = (uint64_t)(((ks * 16 / 64) * BKV * 128 + (ks * 16 % 64) * 2) >> 4);
+          mma_bf16_w(tbase + C::DP_COL + b * 64, dDO + qo, dV + ko, idS, ks > 0 ? 1u : 0u);
+        }
+        mma_commit_w(&dp_full[b]);
+        if (c.t == c.n - 1) mma_commit_w(kv_empty);  // K_j / V_j are only read by S and dP
+      }
+    } else {
+      for (; c.valid; cursor_next(c, p, p.T_n)) {
+        const int pb = c.g & 1;
+        const int s = c.g % NS;
+        const uint32_t acc = tbase + C::ACC_COL + (uint32_t)((c.it & 1) * 128);
+        const uint64_t dQm = dQm0 + (uint64_t)s * STAGE16, dDOm = dQm + Q16;
+        const uint64_t dP = dPm0 + (uint64_t)pb * PBUF16, dDS = dP + PB16;
+        const bool first = c.t == 0;
+        if (first && c.it >= 2) mbar_wait(&acc_empty[c.it & 1], ((uint32_t)(c.it >> 1) + 1u) & 1u);
+        mbar_wait(&p_full[pb], (uint32_t)(c.g >> 1) & 1u);
+        tc_fence_after();
+        trace_ev(p.trace, p.trace_cap, 1, 4, c.g);
 #pragma unroll
-            for (int ks = 0; ks < BQ / 16; ++ks) {
-              const uint32_t ro = (uint32_t)(ks * 2048);
-              mma_bf16(acc + 64, sw128_desc(sQ + ro, BQ * 128, 1024), sw128_desc(sDS + ro, BQ * 128, 1024), idT,
-                       (!first || ks > 0) ? 1u : 0u);
-            }
-            mma_commit(&pds_free[pb]);
-            mma_commit(&qdo_empty[s]);
-            if (cd.t == cd.n - 1) mma_commit(&acc_full[cd.it & 1]);
-            cursor_next(cd, p, p.T_n);
-            dphase = 0;
-            progressed = true;
-          }
-        }
-        if (progressed) {
-          spins = 0;
-          t_idle = 0;
-        } else if ((++spins & 1023u) == 0) {
-          if (t_idle == 0) t_idle = globaltimer();
-          else if (globaltimer() - t_idle > SPA2_WATCHDOG_NS) {
-            printf("spa2 watchdog: k_dkdv MMA issuer stalled (block %d, gs %d, gd %d)\n", blockIdx.x, cs.g, cd.g);
-            __trap();
-          }
-        }
+        for (int ks = 0; ks < BQ / 16; ++ks)
+          mma_bf16_w(acc, dDOm + (uint64_t)(ks * 128), dP + (uint64_t)(ks * 128), idT, (!first || ks > 0) ? 1u : 0u);
+        mbar_wait(&ds_full[pb], (uint32_t)(c.g >> 1) & 1u);
+        tc_fence_after();
+        trace_ev(p.trace, p.trace_cap, 1, 5, c.g);
+#pragma unroll
+        for (int ks = 0; ks < BQ / 16; ++ks)
+          mma_bf16_w(acc + 64, dQm + (uint64_t)(ks * 128), dDS + (uint64_t)(ks * 128), idT, (!first || ks > 0) ? 1u : 0u);
+        mma_commit_w(&pds_free[pb]);
+        mma_commit_w(&qdo_empty[s]);
+        if (c.t == c.n - 1) mma_commit_w(&acc_full[c.it & 1]);
       }
     }
-    __syncwarp();
   } else if (warp < R::EPI0) {
     // ---------------- P / dS warps: EWW/4 warps per TMEM lane quarter, CPT columns each ----
     constexpr int CPT = R::CPT;
@@ -900,9 +1213,19 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
         float pv[CPT];
         uint32_t pk[CPT / 2];
 #pragma unroll
-        for (int c = 0; c < CPT; ++c) pv[c] = ex2(fmaf(__uint_as_float(sr[c]), sl2, -lse2));
-#pragma unroll
-        for (int c = 0; c < CPT / 2; ++c) pk[c] = pack_bf16(pv[2 * c], pv[2 * c + 1]);
+        for (int c = 0; c < CPT / 2; ++c) {
+          const float2 x = __ffma2_rn(make_float2(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1])),
+                                      make_float2(sl2, sl2), make_float2(-lse2, -lse2));
+          if (c < CPT / 8) {  // a quarter of the exponentials on the FMA pipe (exp2_poly2)
+            const float2 e = exp2_poly2(x);
+            pv[2 * c] = e.x;
+            pv[2 * c + 1] = e.y;
+          } else {
+            pv[2 * c] = ex2(x.x);
+            pv[2 * c + 1] = ex2(x.y);
+          }
+          pk[c] = pack_bf16(pv[2 * c], pv[2 * c + 1]);
+        }
         if (g >= 2) mbar_wait(&pds_free[b], ((uint32_t)(g >> 1) + 1u) & 1u);  // buffer b free (tile g-2 done)
         if (tr) trace_ev(p.trace, p.trace_cap, 2, 3, g);
         const uint32_t sP = smem_u32(smem + C::OFF_PDS + (int)b * 2 * C::PB), sDS = sP + C::PB;
@@ -920,9 +1243,12 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
         if constexpr (CPT == 32) tmem_ld32(tbase + lane_off + C::DP_COL + b * 64 + col0, dr);
         else tmem_ld16(tbase + lane_off + C::DP_COL + b * 64 + col0, dr);
 #pragma unroll
-        for (int c = 0; c < CPT / 2; ++c)
-          pk[c] = pack_bf16(pv[2 * c] * (__uint_as_float(dr[2 * c]) - dlt),
-                            pv[2 * c + 1] * (__uint_as_float(dr[2 * c + 1]) - dlt));
+        for (int c = 0; c < CPT / 2; ++c) {
+          const float2 ds = __fmul2_rn(make_float2(pv[2 * c], pv[2 * c + 1]),
+                                       __fadd2_rn(make_float2(__uint_as_float(dr[2 * c]), __uint_as_float(dr[2 * c + 1])),
+                                                  make_float2(-dlt, -dlt)));
+          pk[c] = pack_bf16(ds.x, ds.y);
+        }
 #pragma unroll
         for (int u = 0; u < CPT / 8; ++u) {
           const uint32_t off = sw128_offset((uint32_t)row, col0 / 8 + (uint32_t)u);
@@ -1047,8 +1373,25 @@ int launch_attn_bwd(int which, const spa2_view& q, const spa2_view& k, const spa
   prm.num_items = (int)(B * H * (which == 0 ? T_m : T_n));
   prm.trace = g_trace_buf;
   prm.trace_cap = g_trace_cap;
+  {
+    static const int dbg = [] {
+      const char* e = getenv("SPA2_DEBUG_FLAGS");
+      return e != nullptr ? atoi(e) : 0;
+    }();
+    prm.dbg = dbg;
+  }
   const unsigned grid = (unsigned)std::min<int64_t>(prm.num_items, num_sms());
-  if (which == 0 && dq_variant2()) {
+  if (which == 0 && dq_variant() == 3) {
+    if (dq_ew_warps() == 16) {
+      auto kern = k_dq3<HD, 16>;
+      SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Dq3Cfg<HD>::SMEM));
+      kern<<<grid, Dq3Roles<16>::THREADS, Dq3Cfg<HD>::SMEM, st>>>(m.q, m.k, m.v, m.dout, prm);
+    } else {
+      auto kern = k_dq3<HD, 8>;
+      SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Dq3Cfg<HD>::SMEM));
+      kern<<<grid, Dq3Roles<8>::THREADS, Dq3Cfg<HD>::SMEM, st>>>(m.q, m.k, m.v, m.dout, prm);
+    }
+  } else if (which == 0 && dq_variant2()) {
     auto kern = k_dq2<HD>;
     SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Dq2Cfg<HD>::SMEM));
     kern<<<(unsigned)prm.num_items, kDq2Threads, Dq2Cfg<HD>::SMEM, st>>>(m.q, m.k, m.v, m.dout, m.out0, prm);

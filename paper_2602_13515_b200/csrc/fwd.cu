@@ -155,55 +155,54 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
-    if (elect_one()) {
-      constexpr uint32_t idS = idesc_bf16(BQ, BKV, false, false);
-      constexpr uint32_t idO = idesc_bf16(BQ, HD, false, true);
-      const uint32_t sQ = smem_u32(smem + C::OFF_Q);
-      mbar_wait(q_full, 0);
-      for (int t = 0; t <= n; ++t) {
-        if (t < n) {
-          const uint32_t s_col = tbase + (uint32_t)((t & 1) * 64);
-          if (P_TMEM && t >= 2) mbar_wait(o_done, (uint32_t)(t - 2) & 1u);  // P_{t-2} lives in this buffer
-          const int s = t % NS;
-          mbar_wait(&k_full[s], (uint32_t)(t / NS) & 1u);
-          tc_fence_after();
-          const uint32_t sK = smem_u32(smem + C::OFF_K + s * C::KV_BYTES);
+    // ---------------- MMA issuer (whole warp: warp-collective issue) ----------------
+    constexpr uint32_t idS = idesc_bf16(BQ, BKV, false, false);
+    constexpr uint32_t idO = idesc_bf16(BQ, HD, false, true);
+    const uint64_t dQ = sw128_desc(smem_u32(smem + C::OFF_Q), 16, 1024);
+    const uint64_t dK0 = sw128_desc(smem_u32(smem + C::OFF_K), 16, 1024);
+    const uint64_t dV0 = sw128_desc(smem_u32(smem + C::OFF_V), BKV * 128, 1024);
+    const uint64_t dP = sw128_desc(smem_u32(smem + C::OFF_P), 16, 1024);
+    constexpr uint64_t KV16 = (uint64_t)(C::KV_BYTES >> 4);
+    mbar_wait(q_full, 0);
+    for (int t = 0; t <= n; ++t) {
+      if (t < n) {
+        const uint32_t s_col = tbase + (uint32_t)((t & 1) * 64);
+        if (P_TMEM && t >= 2) mbar_wait(o_done, (uint32_t)(t - 2) & 1u);  // P_{t-2} lives in this buffer
+        const int s = t % NS;
+        mbar_wait(&k_full[s], (uint32_t)(t / NS) & 1u);
+        tc_fence_after();
+        const uint64_t dK = dK0 + (uint64_t)s * KV16;
 #pragma unroll
-          for (int ks = 0; ks < HD / 16; ++ks) {
-            const int k0 = ks * 16;
-            const uint64_t a = sw128_desc(sQ + (uint32_t)((k0 / 64) * BQ * 128 + (k0 % 64) * 2), 16, 1024);
-            const uint64_t b = sw128_desc(sK + (uint32_t)((k0 / 64) * BKV * 128 + (k0 % 64) * 2), 16, 1024);
-            mma_bf16(s_col, a, b, idS, ks > 0 ? 1u : 0u);
-          }
-          mma_commit(&s_full[t & 1]);
-          mma_commit(&k_empty[s]);
+        for (int ks = 0; ks < HD / 16; ++ks) {
+          const int k0 = ks * 16;
+          mma_bf16_w(s_col, dQ + (uint64_t)(((k0 / 64) * BQ * 128 + (k0 % 64) * 2) >> 4),
+                     dK + (uint64_t)(((k0 / 64) * BKV * 128 + (k0 % 64) * 2) >> 4), idS, ks > 0 ? 1u : 0u);
         }
-        if (t >= 1) {
-          const int u = t - 1;
-          const int s = u % NS;
-          mbar_wait(&p_full[u & 1], (uint32_t)(u >> 1) & 1u);
-          mbar_wait(&v_full[s], (uint32_t)(u / NS) & 1u);
-          tc_fence_after();
-          const uint32_t sV = smem_u32(smem + C::OFF_V + s * C::KV_BYTES);
+        mma_commit_w(&s_full[t & 1]);
+        mma_commit_w(&k_empty[s]);
+      }
+      if (t >= 1) {
+        const int u = t - 1;
+        const int s = u % NS;
+        mbar_wait(&p_full[u & 1], (uint32_t)(u >> 1) & 1u);
+        mbar_wait(&v_full[s], (uint32_t)(u / NS) & 1u);
+        tc_fence_after();
+        const uint64_t dV = dV0 + (uint64_t)s * KV16;
 #pragma unroll
-          for (int ks = 0; ks < BKV / 16; ++ks) {
-            const uint64_t b = sw128_desc(sV + (uint32_t)(ks * 16 * 128), BKV * 128, 1024);
-            const uint32_t acc = (u > 0 || ks > 0) ? 1u : 0u;
-            if constexpr (P_TMEM) {
-              mma_bf16_ts(tbase + C::O_COL, tbase + (uint32_t)((u & 1) * 64 + ks * 8), b, idO, acc);
-            } else {
-              const uint64_t a = sw128_desc(smem_u32(smem + C::OFF_P) + (uint32_t)(ks * 32), 16, 1024);
-              mma_bf16(tbase + C::O_COL, a, b, idO, acc);
-            }
+        for (int ks = 0; ks < BKV / 16; ++ks) {
+          const uint32_t acc = (u > 0 || ks > 0) ? 1u : 0u;
+          if constexpr (P_TMEM) {
+            mma_bf16_ts_w(tbase + C::O_COL, tbase + (uint32_t)((u & 1) * 64 + ks * 8), dV + (uint64_t)(ks * 128), idO,
+                          acc);
+          } else {
+            mma_bf16_w(tbase + C::O_COL, dP + (uint64_t)(ks * 2), dV + (uint64_t)(ks * 128), idO, acc);
           }
-          mma_commit(o_done);
-          mma_commit(&v_empty[s]);
-          if (u == n - 1) mma_commit(o_final);
         }
+        mma_commit_w(o_done);
+        mma_commit_w(&v_empty[s]);
+        if (u == n - 1) mma_commit_w(o_final);
       }
     }
-    __syncwarp();
   } else if (warp < 6) {
     // ---------------- softmax warps (2..5) ----------------
     const int q4 = warp & 3;

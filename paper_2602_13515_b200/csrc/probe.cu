@@ -260,6 +260,170 @@ extern "C" int spa2_probe_mma_rate(int m, int n, int k, int a_mn, int b_mn, int 
   return SPA2_OK;
 }
 
+// ---- MMA mix probe (diagnostic): the dQ kernel's per-tile MMA sequence in isolation ----
+// S (8 TS steps, N=64) + dP (8 TS steps) + dQ (4 TS steps, N=128) per rep, buffers
+// alternating like the kernel.  flags: 1 = random operand data, 2 = 256 noise threads doing
+// tcgen05.ld/st on other TMEM columns, 4 = SS form (A from smem) for S/dP,
+// 8 = wait for each rep's completion before the next (serialised), 16 = S only (8 steps),
+// 32 = accumulate into D from the first step too, 64 = one S/dP buffer (no alternation),
+// 128 = S B operand from the same K=16 slab every step (no k offset),
+// 256 = warp-collective issue with precomputed descriptors (TS, the kernels' new form),
+// 512 = (with 256) commit to mbarriers after each group like the kernel,
+// 1024 = (with 256) wait for the S group's commit before issuing dP (a dependent consumer),
+// 2048 = two extra warps stream 16 KB bulk copies from `gsrc` into unused smem meanwhile.
+namespace spa2 {
+namespace {
+__global__ void __launch_bounds__(448) k_mma_mix(int reps, int flags, const uint8_t* gsrc, unsigned long long* cycles) {
+  extern __shared__ uint8_t smem_dyn[];
+  __shared__ uint64_t bar_mma, bars[8];
+  __shared__ uint32_t tmem_base;
+  __shared__ volatile int stop;
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+  for (int i = threadIdx.x; i < 131072 / 16; i += blockDim.x) {
+    uint32_t x = (uint32_t)i * 2654435761u + 12345u;
+    const uint32_t v = (flags & 1) ? ((x >> 9) & 0x007f007fu) | 0x3c003c00u : 0x3f803f80u;
+    reinterpret_cast<uint4*>(base)[i] = make_uint4(v, v ^ 0x00010001u, v, v ^ 0x00020002u);
+  }
+  if (warp_id() == 0) tmem_alloc(&tmem_base, 512);
+  if (threadIdx.x == 32) {
+    mbar_init(&bar_mma, 1);
+    for (int i = 0; i < 8; ++i) mbar_init(&bars[i], 1);
+    stop = 0;
+    fence_mbar_init();
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tmem_base;
+  const uint32_t sK = smem_u32(base), sV = sK + 16384, sQ = sK + 32768, sDO = sK + 65536;
+  if ((flags & 256) && warp_id() == 0) {
+    constexpr uint32_t idS = idesc_bf16(128, 64, false, false);
+    constexpr uint32_t idQ = idesc_bf16(128, 128, false, true);
+    const uint64_t dK = sw128_desc(sK, 16, 1024), dV = sw128_desc(sV, 16, 1024);
+    const uint64_t dKm = sw128_desc(sK, 64 * 128, 1024);
+    const uint64_t t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+      const uint32_t sb = tbase + 128u + (uint32_t)((r & 1) * 128);
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks)
+        mma_bf16_ts_w(sb, tbase + (uint32_t)(ks * 8), dK + (uint64_t)((((ks / 4) * 64 * 128 + (ks % 4) * 32)) >> 4), idS,
+                      ks > 0 ? 1u : 0u);
+      if (flags & 1536) mma_commit_w(&bars[0]);
+      if (flags & 1024) mbar_wait(&bars[0], (uint32_t)r & 1u);
+      if (!(flags & 16)) {
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)
+          mma_bf16_ts_w(sb + 64, tbase + 64u + (uint32_t)(ks * 8),
+                        dV + (uint64_t)((((ks / 4) * 64 * 128 + (ks % 4) * 32)) >> 4), idS, ks > 0 ? 1u : 0u);
+        if (flags & 512) {
+          mma_commit_w(&bars[1]);
+          mma_commit_w(&bars[2]);
+        }
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)
+          mma_bf16_ts_w(tbase + 384u, sb + (uint32_t)(32 * (ks >> 1) + 8 * (ks & 1)), dKm + (uint64_t)((ks * 2048) >> 4),
+                        idQ, 1u);
+        if (flags & 512) {
+          mma_commit_w(&bars[3]);
+          mma_commit_w(&bars[4]);
+        }
+      }
+    }
+    mma_commit_w(&bar_mma);
+    mbar_wait(&bar_mma, 0);
+    if (lane_id() == 0) cycles[blockIdx.x] = clock64() - t0;
+    stop = 1;
+  } else if (threadIdx.x == 0 && !(flags & 256)) {
+    constexpr uint32_t idS = idesc_bf16(128, 64, false, false);
+    constexpr uint32_t idQ = idesc_bf16(128, 128, false, true);
+    const uint64_t t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+      const uint32_t sb = tbase + 128u + (uint32_t)((flags & 64) ? 0 : (r & 1) * 128);
+      const uint32_t acc0 = (flags & 32) ? 1u : 0u;
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        const uint32_t ko = (flags & 128) ? 0u : (uint32_t)((ks / 4) * 64 * 128 + (ks % 4) * 32);
+        const uint32_t qo = (uint32_t)((ks / 4) * 128 * 128 + (ks % 4) * 32);
+        if (flags & 4) mma_bf16(sb, sw128_desc(sQ + qo, 16, 1024), sw128_desc(sK + ko, 16, 1024), idS, ks > 0 ? 1u : acc0);
+        else mma_bf16_ts(sb, tbase + (uint32_t)(ks * 8), sw128_desc(sK + ko, 16, 1024), idS, ks > 0 ? 1u : acc0);
+      }
+      if (!(flags & 16)) {
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+          const uint32_t ko = (uint32_t)((ks / 4) * 64 * 128 + (ks % 4) * 32);
+          const uint32_t qo = (uint32_t)((ks / 4) * 128 * 128 + (ks % 4) * 32);
+          if (flags & 4) mma_bf16(sb + 64, sw128_desc(sDO + qo, 16, 1024), sw128_desc(sV + ko, 16, 1024), idS, ks > 0);
+          else mma_bf16_ts(sb + 64, tbase + 64u + (uint32_t)(ks * 8), sw128_desc(sV + ko, 16, 1024), idS, ks > 0);
+        }
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)
+          mma_bf16_ts(tbase + 384u, sb + (uint32_t)(32 * (ks >> 1) + 8 * (ks & 1)),
+                      sw128_desc(sK + (uint32_t)(ks * 2048), 64 * 128, 1024), idQ, 1u);
+      }
+      if (flags & 8) {
+        mma_commit(&bar_mma);
+        mbar_wait(&bar_mma, (uint32_t)r & 1u);
+      }
+    }
+    mma_commit(&bar_mma);
+    if (!(flags & 8)) mbar_wait(&bar_mma, 0);
+    else mbar_wait(&bar_mma, (uint32_t)reps & 1u);
+    cycles[blockIdx.x] = clock64() - t0;
+    stop = 1;
+  } else if (threadIdx.x >= 384 && (flags & 2048)) {
+    // TMA noise: two warps, each with a 2-deep ring of 16 KB bulk copies into [96 KB, 128 KB)
+    if (lane_id() == 0) {
+      const int w = (int)warp_id() - 12;
+      uint64_t* fb = &bars[5 + w];
+      uint8_t* dst = base + 98304 + w * 16384;
+      uint32_t ph = 0;
+      uint32_t x = 12345u + (uint32_t)w;
+      while (!stop) {
+        x = x * 1664525u + 1013904223u;
+        mbar_expect_tx(fb, 16384);
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(dst)),
+                     "l"(gsrc + (size_t)((x >> 8) % 1024) * 16384), "r"(16384), "r"(smem_u32(fb))
+                     : "memory");
+        mbar_wait(fb, ph);
+        ph ^= 1u;
+      }
+    }
+  } else if (threadIdx.x >= 128 && threadIdx.x < 384 && (flags & 2)) {
+    // noise: tcgen05.ld/st on columns [256, 384) of this warp's lane quarter
+    const int w = (int)warp_id();
+    const uint32_t lane_off = (uint32_t)((w & 3) * 32) << 16;
+    uint32_t acc = 0;
+    while (!stop) {
+      uint32_t r32[32];
+      tmem_ld32(tbase + lane_off + 256u + (uint32_t)(32 * ((w >> 2) & 1)), r32);
+      uint32_t pk[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) pk[c] = r32[2 * c] ^ r32[2 * c + 1];
+      tmem_st16(tbase + lane_off + 256u + (uint32_t)(32 * ((w >> 2) & 1)), pk);
+      tmem_st_wait();
+      acc += pk[0];
+    }
+    if (acc == 0xdeadbeefu) cycles[gridDim.x] = acc;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp_id() == 0) tmem_dealloc(tbase, 512);
+}
+}  // namespace
+}  // namespace spa2
+
+extern "C" int spa2_probe_mma_mix(int reps, int flags, int ctas, const void* gsrc, unsigned long long* cycles,
+                                  void* stream) {
+  const size_t smem = 131072 + 1024;
+  SPA2_CUDA_TRY(cudaFuncSetAttribute(k_mma_mix, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_mma_mix<<<ctas, (flags & 2048) ? 448 : (flags & 2) ? 384 : 128, smem, (cudaStream_t)stream>>>(
+      reps, flags, (const uint8_t*)gsrc, cycles);
+  SPA2_LAUNCH_CHECK();
+  return SPA2_OK;
+}
+
 // ---- TMA streaming-rate probe (diagnostic): L2/HBM -> SMEM bandwidth with no compute ----
 namespace spa2 {
 namespace {
