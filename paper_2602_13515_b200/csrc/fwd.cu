@@ -63,6 +63,8 @@ struct FwdParams {
   unsigned long long* counter;
   __nv_bfloat16* o_ptr;  // for rows of empty lists only
   int64_t o_sb, o_sh, o_sn;
+  unsigned long long* trace;  // diagnostic (spa2_debug_trace), normally null
+  int trace_cap;
 };
 
 template <int HD, bool P_TMEM>
@@ -137,7 +139,9 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
       for (int t = 0; t < n; ++t) {
         const int s = t % NS;
         const uint32_t ph = (uint32_t)(t / NS) & 1u;
+        trace_ev(p.trace, p.trace_cap, 0, 1, t);
         if (t >= NS) mbar_wait(&k_empty[s], ph ^ 1u);
+        trace_ev(p.trace, p.trace_cap, 0, 2, t);
         mbar_expect_tx(&k_full[s], C::KV_BYTES);
         tma_load_5d(smem + C::OFF_K + s * C::KV_BYTES, &tmK, &k_full[s], 0, list[t] * BKV, 0, hh, bb);
       }
@@ -171,6 +175,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
         const int s = t % NS;
         mbar_wait(&k_full[s], (uint32_t)(t / NS) & 1u);
         tc_fence_after();
+        trace_ev(p.trace, p.trace_cap, 1, 2, t);
         const uint64_t dK = dK0 + (uint64_t)s * KV16;
 #pragma unroll
         for (int ks = 0; ks < HD / 16; ++ks) {
@@ -187,6 +192,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
         mbar_wait(&p_full[u & 1], (uint32_t)(u >> 1) & 1u);
         mbar_wait(&v_full[s], (uint32_t)(u / NS) & 1u);
         tc_fence_after();
+        trace_ev(p.trace, p.trace_cap, 1, 4, u);
         const uint64_t dV = dV0 + (uint64_t)s * KV16;
 #pragma unroll
         for (int ks = 0; ks < BKV / 16; ++ks) {
@@ -211,23 +217,32 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
     const int kv_tail = p.N - (p.T_n - 1) * BKV;  // valid columns of the last key block
     const float sl2 = p.scale_log2;
     float m = -INFINITY, l = 0.f;
+    int j_next = list[0];  // key-block index of the next tile, loaded one tile ahead
     for (int t = 0; t < n; ++t) {
+      const bool tail = j_next == p.T_n - 1 && kv_tail < BKV;
+      if (t + 1 < n) j_next = list[t + 1];
       const uint32_t s_col = tbase + lane_off + (uint32_t)((t & 1) * 64);
+      if (threadIdx.x == 64) trace_ev(p.trace, p.trace_cap, 2, 1, t);
       mbar_wait(&s_full[t & 1], (uint32_t)(t >> 1) & 1u);
+      if (threadIdx.x == 64) trace_ev(p.trace, p.trace_cap, 2, 2, t);
       tc_fence_after();
       uint32_t r[64];
       tmem_ld64(s_col, r);
       float sv[64];
 #pragma unroll
       for (int c = 0; c < 64; ++c) sv[c] = __uint_as_float(r[c]);
-      if (list[t] == p.T_n - 1 && kv_tail < BKV) {
+      if (tail) {
 #pragma unroll
         for (int c = 0; c < 64; ++c)
           if (c >= kv_tail) sv[c] = -INFINITY;
       }
-      float smax = sv[0];
+      float mx8[8];  // tree max: short dependency chains
 #pragma unroll
-      for (int c = 1; c < 64; ++c) smax = fmaxf(smax, sv[c]);
+      for (int u = 0; u < 8; ++u)
+        mx8[u] = fmaxf(fmaxf(fmaxf(sv[8 * u], sv[8 * u + 1]), fmaxf(sv[8 * u + 2], sv[8 * u + 3])),
+                       fmaxf(fmaxf(sv[8 * u + 4], sv[8 * u + 5]), fmaxf(sv[8 * u + 6], sv[8 * u + 7])));
+      const float smax = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
       const float mx = smax * sl2;
       bool waited = false;
       if (t == 0) {
@@ -251,17 +266,24 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
         l *= alpha;
         m = m_new;
       }
-      const float neg_m = -m;
+      // P = 2^(S·c − m): packed fp32x2 math, a quarter of the exponentials on the FMA pipe
+      // (exp2_poly2) so the MUFU pipe (16/clk/SM) is not the limit of the two softmax CTAs
       uint32_t pk[32];
-      float lsum = 0.f;
+      float2 lsum = make_float2(0.f, 0.f);
 #pragma unroll
       for (int c = 0; c < 32; ++c) {
-        const float p0 = ex2(fmaf(sv[2 * c], sl2, neg_m));
-        const float p1 = ex2(fmaf(sv[2 * c + 1], sl2, neg_m));
-        lsum += p0 + p1;
-        pk[c] = pack_bf16(p0, p1);
+        const float2 x = __ffma2_rn(make_float2(sv[2 * c], sv[2 * c + 1]), make_float2(sl2, sl2), make_float2(-m, -m));
+        float2 e;
+        if (c < 8) {  // a quarter of the exponentials on the FMA pipe
+          e = exp2_poly2(x);
+        } else {
+          e.x = ex2(x.x);
+          e.y = ex2(x.y);
+        }
+        lsum = __fadd2_rn(lsum, e);
+        pk[c] = pack_bf16(e.x, e.y);
       }
-      l += lsum;
+      l += lsum.x + lsum.y;
       if constexpr (P_TMEM) {
         tmem_st32(s_col, pk);
         tmem_st_wait();
@@ -276,6 +298,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
       }
       tc_fence_before();
       mbar_arrive(&p_full[t & 1]);
+      if (threadIdx.x == 64) trace_ev(p.trace, p.trace_cap, 2, 4, t);
     }
     // ---------------- epilogue ----------------
     mbar_wait(o_final, 0);
@@ -378,6 +401,8 @@ extern "C" int spa2_fwd(spa2_view q, spa2_view k, spa2_view v, spa2_view o, floa
   prm.o_sb = o.sb;
   prm.o_sh = o.sh;
   prm.o_sn = o.sn;
+  prm.trace = g_trace_buf;
+  prm.trace_cap = g_trace_cap;
   const unsigned grid = (unsigned)(B * H * T_m);
   cudaStream_t st = (cudaStream_t)stream;
   const bool psmem = fwd_p_in_smem();

@@ -10,6 +10,7 @@
 // Everything after the bf16 load is IEEE float64, so the pooled map agrees with the
 // reference to ~1e-16 relative and the block selection is bit-exact for a given map.
 #include <math.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <type_traits>
@@ -93,38 +94,88 @@ __global__ void __launch_bounds__(256) k_pool(spa2_view q, spa2_view k, int H, i
 }
 
 // ---------------------------------------------------------------------------------------
-// K1b: scores S = Q̄ K̄ᵀ / √d in float64 (written into `probs`).  64x64 output tiles, 256
-// threads x (4x4) register blocking, k-chunks of 32 staged transposed in shared memory.
+// K1a (bf16 fast path): one CTA per (b, h, block).  The block's rows are streamed into
+// shared memory with coalesced 16-byte loads (all in flight at once), then thread c sums
+// column c over the rows strictly in order — numpy's add.reduceat order — in float64.
 // ---------------------------------------------------------------------------------------
-constexpr int kSTI = 64, kSTJ = 64, kSTK = 32, kSTP = kSTI + 2;
+constexpr int kPoolThreads = 256;
+constexpr int kPoolMaxBytes = 128 * 256 * 2;  // rows x d x sizeof(bf16) upper bound (64 KB)
+
+__global__ void __launch_bounds__(kPoolThreads) k_pool_bf16(spa2_view q, spa2_view k, int H, int N, int d, int b_q,
+                                                            int b_kv, int T_m, int T_n, int64_t BH,
+                                                            double* __restrict__ qbar, double* __restrict__ kbar,
+                                                            int32_t* __restrict__ nonfinite) {
+  extern __shared__ __align__(16) uint8_t pool_smem[];
+  const int64_t nq = BH * T_m;
+  const int64_t g = blockIdx.x;
+  const bool is_q = g < nq;
+  const int64_t blk_g = is_q ? g : g - nq;
+  const int nblk = is_q ? T_m : T_n;
+  const int64_t bh = blk_g / nblk;
+  const int blk = (int)(blk_g % nblk);
+  const int bsz = is_q ? b_q : b_kv;
+  const spa2_view vw = is_q ? q : k;
+  const int row0 = blk * bsz;
+  const int rows = min(bsz, N - row0);
+  const __nv_bfloat16* base =
+      reinterpret_cast<const __nv_bfloat16*>(vw.ptr) + (bh / H) * vw.sb + (bh % H) * vw.sh + (int64_t)row0 * vw.sn;
+  const int upr = d / 8;  // 16-byte units per row
+  uint4* sm = reinterpret_cast<uint4*>(pool_smem);
+  bool bad = false;
+  for (int e = threadIdx.x; e < rows * upr; e += kPoolThreads) {
+    const int r = e / upr, u = e % upr;
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(base + (int64_t)r * vw.sn) + u);
+    sm[e] = v;
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int x = 0; x < 4; ++x)  // exponent all ones in either half: inf or nan
+      bad |= ((w[x] & 0x7F80u) == 0x7F80u) || ((w[x] & 0x7F800000u) == 0x7F800000u);
+  }
+  __syncthreads();
+  const __nv_bfloat16* sb = reinterpret_cast<const __nv_bfloat16*>(pool_smem);
+  for (int c = threadIdx.x; c < d; c += kPoolThreads) {
+    double acc = 0.0;
+    for (int r = 0; r < rows; ++r) acc += (double)__bfloat162float(sb[r * d + c]);
+    (is_q ? qbar : kbar)[blk_g * (int64_t)d + c] = acc / (double)rows;
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0 && nonfinite != nullptr) atomicOr(nonfinite, 1);
+}
+
+// ---------------------------------------------------------------------------------------
+// K1b: scores S = Q̄ K̄ᵀ / √d in float64 (written into `probs`).  64x64 output tiles, 256
+// threads, each owning the 4x4 outputs (ty + 16x, tx + 16y): a warp reads 2 Q̄ rows
+// (broadcast) and 16 consecutive K̄ rows per k step, so with a 33-double row pitch the
+// shared-memory reads are conflict-free and the fp64 pipe, not the LSU, is the limit.
+// ---------------------------------------------------------------------------------------
+constexpr int kSTI = 64, kSTJ = 64, kSTK = 32, kSTP = kSTK + 1;
 
 __global__ void __launch_bounds__(256) k_scores(const double* __restrict__ qbar,
                                                 const double* __restrict__ kbar, int T_m, int T_n,
                                                 int d, double sqrt_d, double* __restrict__ s_out) {
-  __shared__ __align__(16) double sq[kSTK][kSTP];
-  __shared__ __align__(16) double sk[kSTK][kSTP];
+  __shared__ double sq[kSTI][kSTP];
+  __shared__ double sk[kSTJ][kSTP];
   const int64_t bh = blockIdx.z;
   const int i0 = blockIdx.y * kSTI, j0 = blockIdx.x * kSTJ;
   const double* qb = qbar + bh * (int64_t)T_m * d;
   const double* kb = kbar + bh * (int64_t)T_n * d;
-  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;  // 4 rows (ty) x 4 cols (tx) each
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
   double acc[4][4] = {};
   for (int c0 = 0; c0 < d; c0 += kSTK) {
+#pragma unroll
     for (int e = threadIdx.x; e < kSTI * kSTK; e += 256) {
-      const int ii = e / kSTK, cc = e % kSTK;
-      const int i = i0 + ii, j = j0 + ii, c = c0 + cc;
-      sq[cc][ii] = (i < T_m && c < d) ? qb[(int64_t)i * d + c] : 0.0;
-      sk[cc][ii] = (j < T_n && c < d) ? kb[(int64_t)j * d + c] : 0.0;
+      const int rr = e / kSTK, cc = e % kSTK;
+      const int i = i0 + rr, j = j0 + rr, c = c0 + cc;
+      sq[rr][cc] = (i < T_m && c < d) ? qb[(int64_t)i * d + c] : 0.0;
+      sk[rr][cc] = (j < T_n && c < d) ? kb[(int64_t)j * d + c] : 0.0;
     }
     __syncthreads();
-#pragma unroll
+#pragma unroll 8
     for (int cc = 0; cc < kSTK; ++cc) {
-      const double2 a01 = *reinterpret_cast<const double2*>(&sq[cc][4 * ty]);
-      const double2 a23 = *reinterpret_cast<const double2*>(&sq[cc][4 * ty + 2]);
-      const double2 b01 = *reinterpret_cast<const double2*>(&sk[cc][4 * tx]);
-      const double2 b23 = *reinterpret_cast<const double2*>(&sk[cc][4 * tx + 2]);
-      const double a[4] = {a01.x, a01.y, a23.x, a23.y};
-      const double b[4] = {b01.x, b01.y, b23.x, b23.y};
+      double a[4], b[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) a[x] = sq[ty + 16 * x][cc];
+#pragma unroll
+      for (int y = 0; y < 4; ++y) b[y] = sk[tx + 16 * y][cc];
 #pragma unroll
       for (int x = 0; x < 4; ++x)
 #pragma unroll
@@ -134,11 +185,11 @@ __global__ void __launch_bounds__(256) k_scores(const double* __restrict__ qbar,
   }
 #pragma unroll
   for (int x = 0; x < 4; ++x) {
-    const int i = i0 + 4 * ty + x;
+    const int i = i0 + ty + 16 * x;
     if (i >= T_m) continue;
 #pragma unroll
     for (int y = 0; y < 4; ++y) {
-      const int j = j0 + 4 * tx + y;
+      const int j = j0 + tx + 16 * y;
       if (j < T_n) s_out[(bh * T_m + i) * (int64_t)T_n + j] = acc[x][y] / sqrt_d;
     }
   }
@@ -508,6 +559,14 @@ __global__ void k_fill_rows(const uint8_t* __restrict__ keep, int64_t nrows, int
   }
 }
 
+bool pool_smem_path() {
+  static const bool v = [] {
+    const char* e = getenv("SPA2_POOL_SMEM");
+    return e != nullptr && e[0] == '1';
+  }();
+  return v;
+}
+
 template <typename T>
 int launch_pool(spa2_view q, spa2_view k, int64_t B, int64_t H, int64_t N, int64_t d, int64_t b_q, int64_t b_kv,
                 int64_t T_m, int64_t T_n, double* qbar, double* kbar, int32_t* nonfinite, cudaStream_t st) {
@@ -521,6 +580,17 @@ int launch_pool(spa2_view q, spa2_view k, int64_t B, int64_t H, int64_t N, int64
   const int64_t threads = BH * (T_m + T_n) * (d / cpt);
   SPA2_REQUIRE(threads < (1ll << 40), SPA2_ERR_UNSUPPORTED, "pooled_map: problem too large");
   const unsigned grid = (unsigned)ceil_div(threads, 256);
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    const size_t bytes = (size_t)std::max(b_q, b_kv) * d * 2;
+    if (pool_smem_path() && vec && d % 8 == 0 && bytes <= (size_t)kPoolMaxBytes) {
+      if (bytes > 48 * 1024)
+        SPA2_CUDA_TRY(cudaFuncSetAttribute(k_pool_bf16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+      k_pool_bf16<<<(unsigned)(BH * (T_m + T_n)), kPoolThreads, bytes, st>>>(
+          q, k, (int)H, (int)N, (int)d, (int)b_q, (int)b_kv, (int)T_m, (int)T_n, BH, qbar, kbar, nonfinite);
+      SPA2_LAUNCH_CHECK();
+      return SPA2_OK;
+    }
+  }
   if (vec)
     k_pool<T, CV><<<grid, 256, 0, st>>>(q, k, (int)H, (int)N, (int)d, (int)b_q, (int)b_kv, (int)T_m, (int)T_n, BH,
                                         qbar, kbar, nonfinite);

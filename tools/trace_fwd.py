@@ -1,0 +1,36 @@
+"""Event timeline of the forward kernel (CTA 0 = the longest query block of head 0).
+P1/P2 producer before/after waiting a free K slot for tile t; M2 S issue; M4 PV issue;
+E1/E2 softmax before/after S landed, E4 P written."""
+import math, os, sys
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2602_13515_b200 as spa  # noqa: E402
+from paper_2602_13515_b200 import _lib  # noqa: E402
+from paper_2602_13515_b200 import attention as at  # noqa: E402
+from paper_2602_13515_b200.synthetic import wan_like_qkv  # noqa: E402
+
+q, k, v = wan_like_qkv(1, 12, 32760, 128, 0.9, seed=0)
+bm = at._hybrid_mask_device(q, k, spa.SparsityConfig(0.03, 0.2, 128, 64), False)
+lists = at.mask_lists(bm, 1, 12, 32760)
+scale = 1 / math.sqrt(128)
+at.fwd(q, k, v, lists, scale)
+cap = 1 << 16
+buf = torch.zeros(2 + cap, dtype=torch.int64, device="cuda")
+lib = _lib.load()
+lib.spa2_debug_trace(_lib.ptr(buf), cap)
+at.fwd(q, k, v, lists, scale)
+torch.cuda.synchronize()
+lib.spa2_debug_trace(None, 0)
+R = cap // 4
+raw = buf[2:].view(4, R).cpu()
+names = {0: "P", 1: "M", 2: "E", 3: "X"}
+ev = sorted((int(raw[r, s]), f"{names[r]}{s % 8}", s // 8) for r, s in raw.nonzero().tolist())
+lo = int(sys.argv[1]) if len(sys.argv) > 1 else 10
+win = [e for e in ev if lo <= e[2] < lo + 5]
+t0 = win[0][0]
+for t, kind, g in win:
+    print(f"{t - t0:7d} {kind} t={g}")
+m2 = {g: t for t, kd, g in ev if kd == "M2"}
+gs = sorted(m2)
+d = sorted(m2[b] - m2[a] for a, b in zip(gs, gs[1:]) if b == a + 1)
+print("S issue period: median", d[len(d) // 2], "n", len(d), "tiles", len(gs))
