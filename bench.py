@@ -231,8 +231,8 @@ def gpu_arm(args, rank: int, world: int, dev):
         step()
     torch.cuda.synchronize()
 
-    timed_names = ("spa2_fwd", "spa2_bwd_dq", "spa2_bwd_dkdv", "spa2_pooled_map", "spa2_select", "spa2_build_lists",
-                   "spa2_bwd_delta")
+    timed_names = ("spa2_fwd", "spa2_bwd_dq_delta", "spa2_bwd_dkdv", "spa2_pooled_map", "spa2_select",
+                   "spa2_build_lists")
     _lib.STATS.timing = {n: [] for n in timed_names}
     launches0 = _lib.STATS.launches
     uuid = None
@@ -266,7 +266,7 @@ def gpu_arm(args, rank: int, world: int, dev):
     _lib.STATS.timing = None
 
     # ---- roofline of the dominant kernel (tensor-bound attention kernels) ----
-    kflops = {"spa2_fwd": tile_flops(keep, N, d, 4), "spa2_bwd_dq": tile_flops(keep, N, d, 6),
+    kflops = {"spa2_fwd": tile_flops(keep, N, d, 4), "spa2_bwd_dq_delta": tile_flops(keep, N, d, 6),
               "spa2_bwd_dkdv": tile_flops(keep, N, d, 8)}
     dom = max(kflops, key=lambda n: per_kernel_ms[n])
     peaks = load_peaks()

@@ -127,6 +127,13 @@ int spa2_bwd_dq(spa2_view q, spa2_view k, spa2_view v, spa2_view dout, const flo
                 const float* delta, spa2_view dq, int dtype, int64_t B, int64_t H, int64_t N,
                 int64_t d, int64_t b_q, int64_t b_kv, const int32_t* row_ptr, const int32_t* row_idx,
                 const int32_t* row_order, float scale, void* stream);
+/* K5 fused into K7: dq AND delta (written to `delta` for spa2_bwd_dkdv) in one launch; the
+ * dQ kernel's idle epilogue warps compute δ = rowsum(dout ∘ o) one query block ahead with
+ * spa2_bwd_delta's exact arithmetic (bit-identical δ).  o/dout rows must be 16-byte aligned. */
+int spa2_bwd_dq_delta(spa2_view q, spa2_view k, spa2_view v, spa2_view o, spa2_view dout, const float* lse,
+                      float* delta, spa2_view dq, int dtype, int64_t B, int64_t H, int64_t N, int64_t d,
+                      int64_t b_q, int64_t b_kv, const int32_t* row_ptr, const int32_t* row_idx,
+                      const int32_t* row_order, float scale, void* stream);
 int spa2_bwd_dkdv(spa2_view q, spa2_view k, spa2_view v, spa2_view dout, const float* lse,
                   const float* delta, spa2_view dk, spa2_view dv, int dtype, int64_t B, int64_t H,
                   int64_t N, int64_t d, int64_t b_q, int64_t b_kv, const int32_t* col_ptr,

@@ -56,6 +56,8 @@ SIGNATURES = {
                      _P], _I32),
     "spa2_bwd_dkdv": ([View, View, View, View, _P, _P, View, View, _I32, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P,
                        _P, _F32, _P], _I32),
+    "spa2_bwd_dq_delta": ([View, View, View, View, View, _P, _P, View, _I32, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P,
+                           _P, _F32, _P], _I32),
     "spa2_probe_gemm": ([_P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _P], _I32),
     "spa2_probe_mma_rate": ([_I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P, _P], _I32),
     "spa2_debug_trace": ([_P, _I32], _I32),
@@ -66,7 +68,8 @@ SIGNATURES = {
 
 # Kernels each entry point launches (for the bench's gpu_launches accounting).
 KERNELS_PER_CALL = {"spa2_pooled_map": 3, "spa2_select": 1, "spa2_build_lists": 6, "spa2_fwd": 1,
-                    "spa2_bwd_delta": 1, "spa2_bwd_dq": 1, "spa2_bwd_dkdv": 1, "spa2_bwd": 3}
+                    "spa2_bwd_delta": 1, "spa2_bwd_dq": 1, "spa2_bwd_dkdv": 1, "spa2_bwd": 2,
+                    "spa2_bwd_dq_delta": 1}
 
 
 class LaunchStats:

@@ -177,10 +177,9 @@ def bwd(q4, k4, v4, o4, do4, lse, lists: BlockLists, scale: float):
     delta = torch.empty((B, H, N), device=q4.device, dtype=torch.float32)
     st = torch.cuda.current_stream(q4.device)
     dt = _lib.DTYPE_CODES[q4.dtype]
-    _lib.call("spa2_bwd_delta", _lib.view4(o4), _lib.view4(do4), _lib.ptr(delta), dt, B, H, N, d, st.cuda_stream,
-              stream_obj=st)
-    _lib.call("spa2_bwd_dq", _lib.view4(q4), _lib.view4(k4), _lib.view4(v4), _lib.view4(do4), _lib.ptr(lse),
-              _lib.ptr(delta), _lib.view4(dq), dt, B, H, N, d, BQ, BKV, _lib.ptr(lists.row_ptr),
+    # δ = rowsum(dO ∘ O) is computed inside the dQ kernel (spa2_bwd_dq_delta)
+    _lib.call("spa2_bwd_dq_delta", _lib.view4(q4), _lib.view4(k4), _lib.view4(v4), _lib.view4(o4), _lib.view4(do4),
+              _lib.ptr(lse), _lib.ptr(delta), _lib.view4(dq), dt, B, H, N, d, BQ, BKV, _lib.ptr(lists.row_ptr),
               _lib.ptr(lists.row_idx), _lib.ptr(lists.row_order), scale, st.cuda_stream, stream_obj=st)
     _lib.call("spa2_bwd_dkdv", _lib.view4(q4), _lib.view4(k4), _lib.view4(v4), _lib.view4(do4), _lib.ptr(lse),
               _lib.ptr(delta), _lib.view4(dk), _lib.view4(dv), dt, B, H, N, d, BQ, BKV, _lib.ptr(lists.col_ptr),

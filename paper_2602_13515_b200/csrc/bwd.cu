@@ -59,6 +59,12 @@ struct BwdParams {
   unsigned long long* trace;  // diagnostic (spa2_debug_trace), normally null
   int trace_cap;
   int dbg;                    // diagnostic timing experiments (SPA2_DEBUG_FLAGS), normally 0
+  // fused δ (k_dq3 with delta_out != null): δ = rowsum(dO ∘ O) computed in the kernel
+  const __nv_bfloat16* o_in;
+  int64_t oi_sb, oi_sh, oi_sn;
+  const __nv_bfloat16* do_in;
+  int64_t di_sb, di_sh, di_sn;
+  float* delta_out;
 };
 
 struct Item {
@@ -111,6 +117,44 @@ __device__ __forceinline__ void cursor_init(Cursor& c, const BwdParams& p, int n
 __device__ __forceinline__ void cursor_next(Cursor& c, const BwdParams& p, int nblk) {
   ++c.g;
   if (++c.t >= c.n) cursor_item(c, p, nblk);
+}
+
+// δ of one row computed by a single thread with exactly k_delta's arithmetic (HD/8 parts
+// of 8 fused multiply-adds, then the xor-butterfly combination), so fused and separate δ
+// are bit-identical.
+template <int HD>
+__device__ __forceinline__ float row_delta(const __nv_bfloat16* op, const __nv_bfloat16* dp) {
+  constexpr int TPR = HD / 8;
+  float part[TPR];
+#pragma unroll
+  for (int q = 0; q < TPR; q += 4) {
+    uint4 a[4], c[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a[u] = __ldg(reinterpret_cast<const uint4*>(op + (q + u) * 8));
+      c[u] = __ldg(reinterpret_cast<const uint4*>(dp + (q + u) * 8));
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a[u]);
+      const __nv_bfloat162* c2 = reinterpret_cast<const __nv_bfloat162*>(&c[u]);
+      float acc = 0.f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 x = __bfloat1622float2(a2[e]);
+        const float2 y = __bfloat1622float2(c2[e]);
+        acc = fmaf(x.x, y.x, acc);
+        acc = fmaf(x.y, y.y, acc);
+      }
+      part[q + u] = acc;
+    }
+  }
+#pragma unroll
+  for (int off = TPR / 2; off > 0; off >>= 1)
+#pragma unroll
+    for (int i = 0; i < TPR; ++i)
+      if ((i & off) == 0) part[i] = part[i] + part[i | off];
+  return part[0];
 }
 
 // ---------------------------------------------------------------------------------------
@@ -671,8 +715,9 @@ struct Dq3Cfg {
   static constexpr int OFF_QS = 0;  // staging [Q | dO] of the next item
   static constexpr int OFF_K = 2 * Q_BYTES;
   static constexpr int OFF_V = OFF_K + NK * KV_BYTES;
-  static constexpr int OFF_BAR = OFF_V + NV * KV_BYTES;
-  static constexpr int NUM_BARS = 4 + 2 * NK + 2 * NV + 2 * 4 + 2;
+  static constexpr int OFF_DLT = OFF_V + NV * KV_BYTES;  // fused δ: float [2 items][128 rows]
+  static constexpr int OFF_BAR = OFF_DLT + 2 * BQ * 4;
+  static constexpr int NUM_BARS = 4 + 2 * NK + 2 * NV + 2 * 4 + 2 + 2;
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr uint32_t Q_COL = 0, DO_COL = 64, SDP_COL = 128, ACC_COL = 384;  // S at +b*128, dP at +64
 };
@@ -709,7 +754,10 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
   uint64_t* dq_done = ds_full + 2;  // [2] dQ MMA of tile g done (buffer and K slot free)
   uint64_t* acc_full = dq_done + 2;
   uint64_t* acc_empty = acc_full + 1;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  uint64_t* dlt_full = acc_empty + 1;  // [2] fused δ of item `it` in sdelta[it & 1]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(dlt_full + 2);
+  float* sdelta = reinterpret_cast<float*>(smem + C::OFF_DLT);
+  const bool fused_delta = p.delta_out != nullptr;
 
   const int warp = (int)warp_id(), lane = (int)lane_id();
   if (threadIdx.x == 0) {
@@ -734,6 +782,8 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
     }
     mbar_init(acc_full, 1);
     mbar_init(acc_empty, 128);
+    mbar_init(&dlt_full[0], 128);
+    mbar_init(&dlt_full[1], 128);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tmem_holder, 512);
@@ -862,14 +912,21 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
     const int col0 = CPT * grp;
     const int kv_tail = p.N - (p.T_n - 1) * BKV;
     const float sl2 = p.sl2;
-    int g = 0;
+    int g = 0, it = 0;
     for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
       const Item m = get_item(p, wi, p.T_m);
       if (m.n == 0) continue;
       const int tok = m.blk * BQ + row;
       const bool valid = tok < p.N;
       const float lse2 = valid ? __ldg(p.lse + (int64_t)m.bh * p.N + tok) * kLog2e : INFINITY;
-      const float dlt = valid ? __ldg(p.delta + (int64_t)m.bh * p.N + tok) : 0.f;
+      float dlt;
+      if (fused_delta) {  // computed one item ahead by the epilogue warps
+        mbar_wait(&dlt_full[it & 1], (uint32_t)(it >> 1) & 1u);
+        dlt = valid ? sdelta[(it & 1) * BQ + row] : 0.f;
+      } else {
+        dlt = valid ? __ldg(p.delta + (int64_t)m.bh * p.N + tok) : 0.f;
+      }
+      ++it;
       // key-block index of the next tile is loaded one tile ahead (off the critical path)
       int j_next = __ldg(p.idx + m.beg);
       for (int t = 0; t < m.n; ++t, ++g) {
@@ -934,20 +991,15 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
     }
   } else if (warp < R::PROD2) {
     // ---------------- epilogue: dQ = scale · acc -> bf16, direct 16-byte row stores ----------------
+    // With fused δ these warps also compute δ = rowsum(dO ∘ O) of each item BEFORE draining
+    // the previous item's accumulator, so the elementwise warps find it ready.
     const int q4 = warp & 3;
     const int row = q4 * 32 + lane;
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
-    int it = 0;
-    for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
-      const Item m = get_item(p, wi, p.T_m);
+    auto drain = [&](const Item& m, int it) {
       const int hh = m.bh % p.H, bb = m.bh / p.H;
       const int tok = m.blk * BQ + row;
       __nv_bfloat16* dst = p.out0 + bb * p.o0_sb + hh * p.o0_sh + (int64_t)tok * p.o0_sn;
-      if (m.n == 0) {
-        if (tok < p.N)
-          for (int c = 0; c < HD; c += 8) *reinterpret_cast<uint4*>(dst + c) = make_uint4(0, 0, 0, 0);
-        continue;
-      }
       mbar_wait(acc_full, (uint32_t)it & 1u);
       tc_fence_after();
 #pragma unroll 1
@@ -968,8 +1020,39 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
             *reinterpret_cast<uint4*>(dst + c0 + 8 * u) = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
         }
       }
+    };
+    int it = 0;
+    bool pend = false;
+    Item pm{};
+    for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
+      const Item m = get_item(p, wi, p.T_m);
+      const int hh = m.bh % p.H, bb = m.bh / p.H;
+      const int tok = m.blk * BQ + row;
+      if (fused_delta) {
+        float dl = 0.f;
+        if (tok < p.N) {
+          dl = row_delta<HD>(p.o_in + bb * p.oi_sb + hh * p.oi_sh + (int64_t)tok * p.oi_sn,
+                             p.do_in + bb * p.di_sb + hh * p.di_sh + (int64_t)tok * p.di_sn);
+          p.delta_out[(int64_t)m.bh * p.N + tok] = dl;
+        }
+        if (m.n > 0) {
+          sdelta[(it & 1) * BQ + row] = dl;  // slot last read at the start of item it-2 (drained)
+          mbar_arrive(&dlt_full[it & 1]);
+        }
+      }
+      if (m.n == 0) {
+        if (tok < p.N) {
+          __nv_bfloat16* dst = p.out0 + bb * p.o0_sb + hh * p.o0_sh + (int64_t)tok * p.o0_sn;
+          for (int c = 0; c < HD; c += 8) *reinterpret_cast<uint4*>(dst + c) = make_uint4(0, 0, 0, 0);
+        }
+        continue;
+      }
+      if (pend) drain(pm, it - 1);
+      pm = m;
+      pend = true;
       ++it;
     }
+    if (pend) drain(pm, it - 1);
   }
   tc_fence_before();
   __syncthreads();
@@ -1337,6 +1420,14 @@ int num_sms() {
   return n;
 }
 
+struct FusedDelta {
+  const __nv_bfloat16* o;
+  int64_t o_sb, o_sh, o_sn;
+  const __nv_bfloat16* dout;
+  int64_t d_sb, d_sh, d_sn;
+  float* delta;
+};
+
 struct BwdMaps {
   CUtensorMap q, k, v, dout, out0, out1;
 };
@@ -1346,7 +1437,7 @@ template <int HD>
 int launch_attn_bwd(int which, const spa2_view& q, const spa2_view& k, const spa2_view& v, const spa2_view& dout,
                     const float* lse, const float* delta, const spa2_view& out0, const spa2_view* out1, int64_t B,
                     int64_t H, int64_t N, const int32_t* ptr, const int32_t* idx, const int32_t* order, float scale,
-                    cudaStream_t st) {
+                    cudaStream_t st, const FusedDelta* fd = nullptr) {
   const int64_t T_m = ceil_div(N, BQ), T_n = ceil_div(N, BKV);
   BwdMaps m;
   int rc;
@@ -1373,6 +1464,13 @@ int launch_attn_bwd(int which, const spa2_view& q, const spa2_view& k, const spa
   prm.num_items = (int)(B * H * (which == 0 ? T_m : T_n));
   prm.trace = g_trace_buf;
   prm.trace_cap = g_trace_cap;
+  if (fd != nullptr) {
+    prm.o_in = fd->o;
+    prm.oi_sb = fd->o_sb, prm.oi_sh = fd->o_sh, prm.oi_sn = fd->o_sn;
+    prm.do_in = fd->dout;
+    prm.di_sb = fd->d_sb, prm.di_sh = fd->d_sh, prm.di_sn = fd->d_sn;
+    prm.delta_out = fd->delta;
+  }
   {
     static const int dbg = [] {
       const char* e = getenv("SPA2_DEBUG_FLAGS");
@@ -1466,6 +1564,36 @@ extern "C" int spa2_bwd_dq(spa2_view q, spa2_view k, spa2_view v, spa2_view dout
                              st);
 }
 
+extern "C" int spa2_bwd_dq_delta(spa2_view q, spa2_view k, spa2_view v, spa2_view o, spa2_view dout,
+                                 const float* lse, float* delta, spa2_view dq, int dtype, int64_t B, int64_t H, int64_t N,
+                                 int64_t d, int64_t b_q, int64_t b_kv, const int32_t* row_ptr, const int32_t* row_idx,
+                                 const int32_t* row_order, float scale, void* stream) {
+  int rc;
+  if ((rc = check_bwd_args(dtype, B, H, N, d, b_q, b_kv))) return rc;
+  SPA2_REQUIRE(q.ptr && k.ptr && v.ptr && o.ptr && dout.ptr && lse && delta && dq.ptr && row_ptr && row_idx,
+               SPA2_ERR_VALUE, "bwd_dq_delta: null pointer");
+  SPA2_REQUIRE(((uintptr_t)o.ptr % 16 == 0) && ((uintptr_t)dout.ptr % 16 == 0) && o.sn % 8 == 0 && o.sh % 8 == 0 &&
+                   o.sb % 8 == 0 && dout.sn % 8 == 0 && dout.sh % 8 == 0 && dout.sb % 8 == 0,
+               SPA2_ERR_VALUE, "bwd_dq_delta: o / dout rows must be 16-byte aligned");
+  cudaStream_t st = (cudaStream_t)stream;
+  static const bool no_fuse = [] {
+    const char* e = getenv("SPA2_NO_FUSED_DELTA");
+    return e != nullptr && e[0] == '1';
+  }();
+  if (dq_variant() != 3 || no_fuse) {  // other dQ kernels take δ from a separate pass
+    if ((rc = spa2_bwd_delta(o, dout, delta, dtype, B, H, N, d, stream))) return rc;
+    return spa2_bwd_dq(q, k, v, dout, lse, delta, dq, dtype, B, H, N, d, b_q, b_kv, row_ptr, row_idx, row_order,
+                       scale, stream);
+  }
+  FusedDelta fd{(const __nv_bfloat16*)o.ptr, o.sb, o.sh, o.sn, (const __nv_bfloat16*)dout.ptr, dout.sb, dout.sh,
+                dout.sn, delta};
+  if (d == 128)
+    return launch_attn_bwd<128>(0, q, k, v, dout, lse, delta, dq, nullptr, B, H, N, row_ptr, row_idx, row_order,
+                                scale, st, &fd);
+  return launch_attn_bwd<64>(0, q, k, v, dout, lse, delta, dq, nullptr, B, H, N, row_ptr, row_idx, row_order, scale,
+                             st, &fd);
+}
+
 extern "C" int spa2_bwd_dkdv(spa2_view q, spa2_view k, spa2_view v, spa2_view dout, const float* lse,
                              const float* delta, spa2_view dk, spa2_view dv, int dtype, int64_t B, int64_t H,
                              int64_t N, int64_t d, int64_t b_q, int64_t b_kv, const int32_t* col_ptr,
@@ -1487,9 +1615,8 @@ extern "C" int spa2_bwd(spa2_view q, spa2_view k, spa2_view v, spa2_view o, spa2
                         const int32_t* row_idx, const int32_t* row_order, const int32_t* col_ptr,
                         const int32_t* col_idx, const int32_t* col_order, float scale, void* stream) {
   int rc;
-  if ((rc = spa2_bwd_delta(o, dout, delta, dtype, B, H, N, d, stream))) return rc;
-  if ((rc = spa2_bwd_dq(q, k, v, dout, lse, delta, dq, dtype, B, H, N, d, b_q, b_kv, row_ptr, row_idx, row_order,
-                        scale, stream)))
+  if ((rc = spa2_bwd_dq_delta(q, k, v, o, dout, lse, delta, dq, dtype, B, H, N, d, b_q, b_kv, row_ptr, row_idx,
+                              row_order, scale, stream)))
     return rc;
   return spa2_bwd_dkdv(q, k, v, dout, lse, delta, dk, dv, dtype, B, H, N, d, b_q, b_kv, col_ptr, col_idx, col_order,
                        scale, stream);

@@ -35,6 +35,10 @@ constexpr int BQ = 128;
 constexpr int BKV = 64;
 constexpr int kFwdThreads = 224;  // + warp 6: second TMA producer (V)
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: P entries stay <= 2^8
+#ifndef SPA2_FWD_EXP_MODE
+#define SPA2_FWD_EXP_MODE 0
+#endif
+constexpr int kExpMode = SPA2_FWD_EXP_MODE;  // 1: f16x2 MUFU exponentials, 0: fp32 MUFU + FMA polynomial
 
 template <int HD, bool P_TMEM>
 struct FwdCfg {
@@ -277,7 +281,9 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
       for (int c = 0; c < 32; ++c) {
         const float2 x = __ffma2_rn(make_float2(sv[2 * c], sv[2 * c + 1]), make_float2(sl2, sl2), make_float2(-m, -m));
         float2 e;
-        if (c < 8) {  // a quarter of the exponentials on the FMA pipe
+        if (kExpMode == 1) {  // two exponentials per MUFU op (ex2.approx.f16x2); error below P's bf16 rounding
+          e = ex2_f16x2(x);
+        } else if (c < 8) {  // a quarter of the exponentials on the FMA pipe
           e = exp2_poly2(x);
         } else {
           e.x = ex2(x.x);

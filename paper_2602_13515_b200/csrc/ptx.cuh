@@ -348,6 +348,13 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
   return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23)),
                      __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23)));
 }
+// Two exponentials per MUFU op: ex2.approx.f16x2 on an fp16-rounded argument pair.
+__device__ __forceinline__ float2 ex2_f16x2(float2 x) {
+  const __half2 h = __float22half2_rn(x);
+  uint32_t r;
+  asm("ex2.approx.f16x2 %0, %1;" : "=r"(r) : "r"(*reinterpret_cast<const uint32_t*>(&h)));
+  return __half22float2(*reinterpret_cast<const __half2*>(&r));
+}
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
