@@ -717,7 +717,7 @@ struct Dq3Cfg {
   static constexpr int OFF_V = OFF_K + NK * KV_BYTES;
   static constexpr int OFF_DLT = OFF_V + NV * KV_BYTES;  // fused δ: float [2 items][128 rows]
   static constexpr int OFF_BAR = OFF_DLT + 2 * BQ * 4;
-  static constexpr int NUM_BARS = 4 + 2 * NK + 2 * NV + 2 * 4 + 2 + 2;
+  static constexpr int NUM_BARS = 4 + 2 * NK + 2 * NV + 2 * 5 + 2 + 2;
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr uint32_t Q_COL = 0, DO_COL = 64, SDP_COL = 128, ACC_COL = 384;  // S at +b*128, dP at +64
 };
@@ -755,7 +755,8 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
   uint64_t* acc_full = dq_done + 2;
   uint64_t* acc_empty = acc_full + 1;
   uint64_t* dlt_full = acc_empty + 1;  // [2] fused δ of item `it` in sdelta[it & 1]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(dlt_full + 2);
+  uint64_t* s_free = dlt_full + 2;     // [2] S of tile g read out of TMEM buffer g&1
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(s_free + 2);
   float* sdelta = reinterpret_cast<float*>(smem + C::OFF_DLT);
   const bool fused_delta = p.delta_out != nullptr;
 
@@ -778,6 +779,7 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
       mbar_init(&s_full[b], 1);
       mbar_init(&dp_full[b], 1);
       mbar_init(&ds_full[b], 32 * EWW);
+      mbar_init(&s_free[b], 32 * EWW);
       mbar_init(&dq_done[b], 1);
     }
     mbar_init(acc_full, 1);
@@ -853,7 +855,9 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
           mma_commit_w(qd_ready);
         }
         const int b = c.g & 1, sk = c.g % NK;
-        if (c.g >= 2) mbar_wait(&dq_done[b], (uint32_t)((c.g - 2) >> 1) & 1u);  // dS of tile g-2 consumed
+        // S columns of buffer b are free once the elementwise warps have read S of tile g-2
+        // (dS goes into the dP columns, so S never waits for the dQ MMA)
+        if (c.g >= 2) mbar_wait(&s_free[b], (uint32_t)((c.g - 2) >> 1) & 1u);
         mbar_wait(&k_full[sk], (uint32_t)(c.g / NK) & 1u);
         tc_fence_after();
         trace_ev(p.trace, p.trace_cap, 1, 2, c.g);
@@ -895,7 +899,7 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
         const uint32_t sb = tbase + C::SDP_COL + (uint32_t)(b * 128);
 #pragma unroll
         for (int ks = 0; ks < BKV / 16; ++ks)
-          mma_bf16_ts_w(tbase + C::ACC_COL, sb + ds_col<CPT>(ks), dKm + (uint64_t)((ks * 2048) >> 4), idQ,
+          mma_bf16_ts_w(tbase + C::ACC_COL, sb + 64u + ds_col<CPT>(ks), dKm + (uint64_t)((ks * 2048) >> 4), idQ,
                         (c.t > 0 || ks > 0) ? 1u : 0u);
         mma_commit_w(&dq_done[b]);
         mma_commit_w(&k_empty[sk]);
@@ -940,12 +944,15 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
         tc_fence_after();
         if (p.dbg & 1) {  // timing experiment: no elementwise work
           tc_fence_before();
+          mbar_arrive(&s_free[b]);
           mbar_arrive(&ds_full[b]);
           continue;
         }
         uint32_t sr[CPT];
         if constexpr (CPT == 32) tmem_ld32(sb + (uint32_t)col0, sr);
         else tmem_ld16(sb + (uint32_t)col0, sr);
+        tc_fence_before();
+        mbar_arrive(&s_free[b]);  // S(g) is in registers: the S issuer may overwrite it
         // packed fp32x2 math (FFMA2/FADD2/FMUL2): the issue slots of this SM sub-partition are
         // shared with an MMA-issuing warp, so fewer instructions per element = faster MMAs
         float pv[CPT];
@@ -981,8 +988,8 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
                                                   make_float2(-dlt, -dlt)));
           pk[c] = pack_bf16(ds.x, ds.y);
         }
-        if constexpr (CPT == 32) tmem_st16(sb + (uint32_t)col0, pk);
-        else tmem_st8(sb + (uint32_t)col0, pk);
+        if constexpr (CPT == 32) tmem_st16(sb + 64u + (uint32_t)col0, pk);  // dS over the dP columns read
+        else tmem_st8(sb + 64u + (uint32_t)col0, pk);
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&ds_full[b]);

@@ -149,39 +149,61 @@ __global__ void __launch_bounds__(kPoolThreads) k_pool_bf16(spa2_view q, spa2_vi
 // ---------------------------------------------------------------------------------------
 constexpr int kSTI = 64, kSTJ = 64, kSTK = 32, kSTP = kSTK + 1;
 
-__global__ void __launch_bounds__(256) k_scores(const double* __restrict__ qbar,
-                                                const double* __restrict__ kbar, int T_m, int T_n,
-                                                int d, double sqrt_d, double* __restrict__ s_out) {
-  __shared__ double sq[kSTI][kSTP];
-  __shared__ double sk[kSTJ][kSTP];
+__device__ __forceinline__ void cp_async_f64(double* dst, const double* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(valid ? 8 : 0)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(256, 3) k_scores(const double* __restrict__ qbar,
+                                                   const double* __restrict__ kbar, int T_m, int T_n,
+                                                   int d, double sqrt_d, double* __restrict__ s_out) {
+  // two k-chunk buffers: chunk c+1 streams in (cp.async) while chunk c is multiplied
+  extern __shared__ double sc_smem[];  // [2][sq 64 x 33 | sk 64 x 33]
   const int64_t bh = blockIdx.z;
   const int i0 = blockIdx.y * kSTI, j0 = blockIdx.x * kSTJ;
   const double* qb = qbar + bh * (int64_t)T_m * d;
   const double* kb = kbar + bh * (int64_t)T_n * d;
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-  double acc[4][4] = {};
-  for (int c0 = 0; c0 < d; c0 += kSTK) {
+  auto load = [&](int c0, int buf) {
+    double* sq = sc_smem + buf * 2 * kSTI * kSTP;
+    double* sk = sq + kSTI * kSTP;
 #pragma unroll
     for (int e = threadIdx.x; e < kSTI * kSTK; e += 256) {
       const int rr = e / kSTK, cc = e % kSTK;
       const int i = i0 + rr, j = j0 + rr, c = c0 + cc;
-      sq[rr][cc] = (i < T_m && c < d) ? qb[(int64_t)i * d + c] : 0.0;
-      sk[rr][cc] = (j < T_n && c < d) ? kb[(int64_t)j * d + c] : 0.0;
+      const bool vq = i < T_m && c < d, vk = j < T_n && c < d;
+      cp_async_f64(&sq[rr * kSTP + cc], vq ? qb + (int64_t)i * d + c : qb, vq);
+      cp_async_f64(&sk[rr * kSTP + cc], vk ? kb + (int64_t)j * d + c : kb, vk);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double acc[4][4] = {};
+  const int nch = (d + kSTK - 1) / kSTK;
+  load(0, 0);
+  for (int ch = 0; ch < nch; ++ch) {
+    if (ch + 1 < nch) {
+      load((ch + 1) * kSTK, (ch + 1) & 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
+    const double* sq = sc_smem + (ch & 1) * 2 * kSTI * kSTP;
+    const double* sk = sq + kSTI * kSTP;
 #pragma unroll 8
     for (int cc = 0; cc < kSTK; ++cc) {
       double a[4], b[4];
 #pragma unroll
-      for (int x = 0; x < 4; ++x) a[x] = sq[ty + 16 * x][cc];
+      for (int x = 0; x < 4; ++x) a[x] = sq[(ty + 16 * x) * kSTP + cc];
 #pragma unroll
-      for (int y = 0; y < 4; ++y) b[y] = sk[tx + 16 * y][cc];
+      for (int y = 0; y < 4; ++y) b[y] = sk[(tx + 16 * y) * kSTP + cc];
 #pragma unroll
       for (int x = 0; x < 4; ++x)
 #pragma unroll
         for (int y = 0; y < 4; ++y) acc[x][y] = fma(a[x], b[y], acc[x][y]);
     }
-    __syncthreads();
+    __syncthreads();  // buffer (ch & 1) is refilled by the load issued in iteration ch + 1
   }
 #pragma unroll
   for (int x = 0; x < 4; ++x) {
@@ -194,6 +216,7 @@ __global__ void __launch_bounds__(256) k_scores(const double* __restrict__ qbar,
     }
   }
 }
+constexpr int kScoresSmem = 2 * 2 * kSTI * kSTP * 8;
 
 // K1c: in-place row softmax with max subtraction (numerics.py:46-52). One warp per row.
 __global__ void k_softmax_rows(double* __restrict__ p, int64_t rows, int T_n) {
@@ -630,7 +653,8 @@ extern "C" int spa2_pooled_map(spa2_view q, spa2_view k, int dtype, int64_t B, i
   }
   if (rc != SPA2_OK) return rc;
   dim3 grid((unsigned)ceil_div(T_n, kSTJ), (unsigned)ceil_div(T_m, kSTI), (unsigned)BH);
-  k_scores<<<grid, 256, 0, st>>>(qbar, kbar, (int)T_m, (int)T_n, (int)d, sqrt((double)d), probs);
+  SPA2_CUDA_TRY(cudaFuncSetAttribute(k_scores, cudaFuncAttributeMaxDynamicSharedMemorySize, kScoresSmem));
+  k_scores<<<grid, 256, kScoresSmem, st>>>(qbar, kbar, (int)T_m, (int)T_n, (int)d, sqrt((double)d), probs);
   SPA2_LAUNCH_CHECK();
   const int64_t rows = BH * T_m;
   k_softmax_rows<<<(unsigned)ceil_div(rows, 8), 256, 0, st>>>(probs, rows, (int)T_n);

@@ -297,7 +297,42 @@ __global__ void __launch_bounds__(448) k_mma_mix(int reps, int flags, const uint
   tc_fence_after();
   const uint32_t tbase = tmem_base;
   const uint32_t sK = smem_u32(base), sV = sK + 16384, sQ = sK + 32768, sDO = sK + 65536;
-  if ((flags & 256) && warp_id() == 0) {
+  if ((flags & 4096) && warp_id() < 3) {
+    // three warps issue the S, dP and dQ streams concurrently (no cross-stream waits)
+    constexpr uint32_t idS = idesc_bf16(128, 64, false, false);
+    constexpr uint32_t idQ = idesc_bf16(128, 128, false, true);
+    const uint64_t dK = sw128_desc(sK, 16, 1024), dV = sw128_desc(sV, 16, 1024);
+    const uint64_t dKm = sw128_desc(sK, 64 * 128, 1024);
+    const int w = (int)warp_id();
+    const uint64_t t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+      const uint32_t sb = tbase + 128u + (uint32_t)((r & 1) * 128);
+      if (w == 0) {
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)
+          mma_bf16_ts_w(sb, tbase + (uint32_t)(ks * 8), dK + (uint64_t)((((ks / 4) * 64 * 128 + (ks % 4) * 32)) >> 4), idS,
+                        ks > 0 ? 1u : 0u);
+      } else if (w == 1) {
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks)
+          mma_bf16_ts_w(sb + 64, tbase + 64u + (uint32_t)(ks * 8),
+                        dV + (uint64_t)((((ks / 4) * 64 * 128 + (ks % 4) * 32)) >> 4), idS, ks > 0 ? 1u : 0u);
+      } else {
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)
+          mma_bf16_ts_w(tbase + 384u, sb + (uint32_t)(32 * (ks >> 1) + 8 * (ks & 1)), dKm + (uint64_t)((ks * 2048) >> 4),
+                        idQ, 1u);
+      }
+      if (flags & 512) mma_commit_w(&bars[w]);
+    }
+    mma_commit_w(&bars[4 + w]);
+    mbar_wait(&bars[4 + w], 0);
+    if (lane_id() == 0) atomicMax(reinterpret_cast<unsigned long long*>(&cycles[blockIdx.x]), clock64() - t0);
+    if (w == 0) {
+      __syncwarp();
+    }
+    stop = 1;
+  } else if ((flags & 256) && warp_id() == 0) {
     constexpr uint32_t idS = idesc_bf16(128, 64, false, false);
     constexpr uint32_t idQ = idesc_bf16(128, 128, false, true);
     const uint64_t dK = sw128_desc(sK, 16, 1024), dV = sw128_desc(sV, 16, 1024);

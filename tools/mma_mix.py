@@ -14,9 +14,11 @@ for flags, label in ((1, "TS random"), (256 | 1, "TS warp-issue"), (256 | 17, "T
                      (256 | 512 | 1, "TS warp-issue + commits"), (256 | 1024 | 1, "TS warp-issue, wait S"),
                      (256 | 1536 | 3, "TS warp-issue + commits + wait S + noise"),
                      (256 | 2048 | 1, "TS warp-issue + TMA noise"), (256 | 2048 | 3, "TS warp-issue + TMA + TMEM noise"),
-                     (256 | 2048 | 16 | 1, "TS warp-issue S only + TMA noise"), (2048 | 5, "SS + TMA noise")):
+                     (256 | 2048 | 16 | 1, "TS warp-issue S only + TMA noise"), (2048 | 5, "SS + TMA noise"),
+                     (4096 | 1, "3 issuing warps (S / dP / dQ)"), (4096 | 512 | 1, "3 issuing warps + commits")):
     for ctas in (1, sms):
         _lib.check(lib.spa2_probe_mma_mix(10, flags, ctas, _lib.ptr(src), _lib.ptr(out), st), "mix")
+        out.zero_()
         _lib.check(lib.spa2_probe_mma_mix(reps, flags, ctas, _lib.ptr(src), _lib.ptr(out), st), "mix")
         torch.cuda.synchronize()
         cyc = out[:ctas].double().mean().item() / reps

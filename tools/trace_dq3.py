@@ -26,9 +26,10 @@ buf = torch.zeros(2 + cap, dtype=torch.int64, device="cuda")
 
 
 def run():
-    _lib.check(lib.spa2_bwd_dq(_lib.view4(q), _lib.view4(k), _lib.view4(v), _lib.view4(do), _lib.ptr(lse),
-                               _lib.ptr(delta), _lib.view4(dq), 0, 1, 12, 32760, 128, 128, 64, _lib.ptr(lists.row_ptr),
-                               _lib.ptr(lists.row_idx), _lib.ptr(lists.row_order), scale, st), "dq")
+    _lib.check(lib.spa2_bwd_dq_delta(_lib.view4(q), _lib.view4(k), _lib.view4(v), _lib.view4(o), _lib.view4(do),
+                                     _lib.ptr(lse), _lib.ptr(delta), _lib.view4(dq), 0, 1, 12, 32760, 128, 128, 64,
+                                     _lib.ptr(lists.row_ptr), _lib.ptr(lists.row_idx), _lib.ptr(lists.row_order),
+                                     scale, st), "dq")
 
 
 run()
