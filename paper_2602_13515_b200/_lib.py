@@ -67,7 +67,7 @@ SIGNATURES = {
 }
 
 # Kernels each entry point launches (for the bench's gpu_launches accounting).
-KERNELS_PER_CALL = {"spa2_pooled_map": 3, "spa2_select": 1, "spa2_build_lists": 6, "spa2_fwd": 1,
+KERNELS_PER_CALL = {"spa2_pooled_map": 3, "spa2_select": 1, "spa2_build_lists": 3, "spa2_fwd": 1,
                     "spa2_bwd_delta": 1, "spa2_bwd_dq": 1, "spa2_bwd_dkdv": 1, "spa2_bwd": 2,
                     "spa2_bwd_dq_delta": 1}
 

@@ -400,18 +400,6 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const double* __restrict
 // ---------------------------------------------------------------------------------------
 // K3: block lists.
 // ---------------------------------------------------------------------------------------
-__global__ void k_row_counts(const uint8_t* __restrict__ keep, int64_t nrows, int T_n,
-                             int32_t* __restrict__ row_cnt) {
-  const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  const int lane = threadIdx.x % 32;
-  if (row >= nrows) return;
-  int c = 0;
-  for (int j = lane; j < T_n; j += 32) c += keep[row * T_n + j] != 0;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  if (lane == 0) row_cnt[row] = c;
-}
-
 // Column counts and column lists: one CTA per (head, 32-column chunk); lane = column, the
 // 8 warps split the T_m rows into contiguous ranges (coalesced 32-byte row segments).
 constexpr int kColWarps = 16;
@@ -422,58 +410,9 @@ __device__ __forceinline__ void col_range(int T_m, int w, int& r0, int& r1) {
   r1 = min(r0 + per, T_m);
 }
 
-__global__ void __launch_bounds__(kColWarps * 32) k_col_counts(const uint8_t* __restrict__ keep, int T_m, int T_n,
-                                                               int32_t* __restrict__ col_cnt) {
-  __shared__ int part[kColWarps][32];
-  const int64_t bh = blockIdx.y;
-  const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int j = blockIdx.x * 32 + lane;
-  int r0, r1;
-  col_range(T_m, w, r0, r1);
-  const uint8_t* base = keep + bh * (int64_t)T_m * T_n + j;
-  int c = 0;
-  if (j < T_n) {
-#pragma unroll 8
-    for (int i = r0; i < r1; ++i) c += base[(int64_t)i * T_n] != 0;
-  }
-  part[w][lane] = c;
-  __syncthreads();
-  if (w == 0 && j < T_n) {
-    int s = 0;
-#pragma unroll
-    for (int x = 0; x < kColWarps; ++x) s += part[x][lane];
-    col_cnt[bh * T_n + j] = s;
-  }
-}
-
-__global__ void __launch_bounds__(kColWarps * 32) k_fill_cols(const uint8_t* __restrict__ keep, int T_m, int T_n,
-                                                              const int32_t* __restrict__ col_ptr,
-                                                              int32_t* __restrict__ col_idx) {
-  __shared__ int part[kColWarps][32];
-  const int64_t bh = blockIdx.y;
-  const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int j = blockIdx.x * 32 + lane;
-  int r0, r1;
-  col_range(T_m, w, r0, r1);
-  const uint8_t* base = keep + bh * (int64_t)T_m * T_n + j;
-  int c = 0;
-  if (j < T_n) {
-#pragma unroll 8
-    for (int i = r0; i < r1; ++i) c += base[(int64_t)i * T_n] != 0;
-  }
-  part[w][lane] = c;
-  __syncthreads();
-  if (j >= T_n) return;
-  int off = col_ptr[bh * T_n + j];
-  for (int x = 0; x < w; ++x) off += part[x][lane];
-#pragma unroll 8
-  for (int i = r0; i < r1; ++i)
-    if (base[(int64_t)i * T_n] != 0) col_idx[off++] = i;
-}
-
 constexpr int kScanThreads = 1024;
 
-// Exclusive scan of in[0..n) into out[0..n], out[n] = total, by one CTA (warp-shuffle scan).
+// Inclusive scan across the 1024 threads of a CTA (warp-shuffle scan).
 __device__ int32_t cta_inclusive_scan_1024(int32_t v, int32_t* sh_warp) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
@@ -496,22 +435,6 @@ __device__ int32_t cta_inclusive_scan_1024(int32_t v, int32_t* sh_warp) {
   const int32_t r = v + (w > 0 ? sh_warp[w - 1] : 0);
   __syncthreads();
   return r;
-}
-
-__device__ void cta_exclusive_scan(const int32_t* in, int32_t* out, int64_t n, int32_t* sh) {
-  const int tid = threadIdx.x;
-  const int64_t per = (n + kScanThreads - 1) / kScanThreads;
-  const int64_t beg = min((int64_t)tid * per, n), end = min(beg + per, n);
-  int32_t local = 0;
-  for (int64_t i = beg; i < end; ++i) local += in[i];
-  const int32_t incl = cta_inclusive_scan_1024(local, sh);
-  int32_t run = incl - local;
-  for (int64_t i = beg; i < end; ++i) {
-    const int32_t c = in[i];
-    out[i] = run;
-    run += c;
-  }
-  if (tid == kScanThreads - 1) out[n] = incl;
 }
 
 // Longest-first order: counting sort of ids base..base+n-1 by descending count (counts in
@@ -544,41 +467,131 @@ __device__ void cta_order_desc(const int32_t* cnt, int64_t n, int maxc, int32_t*
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kScanThreads) k_scan(const int32_t* __restrict__ row_cnt,
-                                                       const int32_t* __restrict__ col_cnt, int64_t nrows,
-                                                       int64_t ncols, int32_t* row_ptr, int32_t* col_ptr) {
-  __shared__ int32_t sh_scan[kScanThreads];
-  cta_exclusive_scan(row_cnt, row_ptr, nrows, sh_scan);
-  cta_exclusive_scan(col_cnt, col_ptr, ncols, sh_scan);
+// Launch orders (k_scan_orders): head-major (so one or two heads' K/V or Q/dO stay resident
+// in the 126 MB L2 while their blocks are processed) and longest-first within each head.
+// ---------------------------------------------------------------------------------------
+// K3 (3 launches): counts -> per-head scan + launch orders -> fill.
+// ---------------------------------------------------------------------------------------
+// (a) blockIdx.x < col_chunks: column counts of 32 columns of head blockIdx.y (as k_col_counts);
+//     otherwise row counts, one warp per row (as k_row_counts).
+__global__ void __launch_bounds__(kColWarps * 32) k_counts(const uint8_t* __restrict__ keep, int T_m, int T_n,
+                                                           int col_chunks, int32_t* __restrict__ row_cnt,
+                                                           int32_t* __restrict__ col_cnt) {
+  const int64_t bh = blockIdx.y;
+  const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if ((int)blockIdx.x < col_chunks) {
+    __shared__ int part[kColWarps][32];
+    const int j = blockIdx.x * 32 + lane;
+    int r0, r1;
+    col_range(T_m, w, r0, r1);
+    const uint8_t* base = keep + bh * (int64_t)T_m * T_n + j;
+    int c = 0;
+    if (j < T_n) {
+#pragma unroll 8
+      for (int i = r0; i < r1; ++i) c += base[(int64_t)i * T_n] != 0;
+    }
+    part[w][lane] = c;
+    __syncthreads();
+    if (w == 0 && j < T_n) {
+      int sum = 0;
+#pragma unroll
+      for (int x = 0; x < kColWarps; ++x) sum += part[x][lane];
+      col_cnt[bh * T_n + j] = sum;
+    }
+  } else {
+    const int i = ((int)blockIdx.x - col_chunks) * kColWarps + w;
+    if (i >= T_m) return;
+    const uint8_t* rowp = keep + (bh * (int64_t)T_m + i) * T_n;
+    int c = 0;
+    for (int j = lane; j < T_n; j += 32) c += rowp[j] != 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) row_cnt[bh * T_m + i] = c;
+  }
 }
 
-// Launch orders: head-major (so one or two heads' K/V or Q/dO stay resident in the 126 MB
-// L2 while their blocks are processed) and longest-first within each head (load balance).
-// blockIdx.x = (b, h); blockIdx.y = 0 rows, 1 columns.
-__global__ void __launch_bounds__(kScanThreads) k_orders(const int32_t* __restrict__ row_cnt,
-                                                         const int32_t* __restrict__ col_cnt, int T_m, int T_n,
-                                                         int32_t* row_order, int32_t* col_order) {
+// (b) one CTA per (head, rows|columns): CSR offsets of that head's rows (or columns) — base =
+//     kept blocks of all earlier heads, summed here so no second global pass is needed — and
+//     its longest-first launch order.
+__global__ void __launch_bounds__(kScanThreads) k_scan_orders(const int32_t* __restrict__ row_cnt,
+                                                              const int32_t* __restrict__ col_cnt, int T_m, int T_n,
+                                                              int64_t bh_total, int32_t* row_ptr, int32_t* col_ptr,
+                                                              int32_t* row_order, int32_t* col_order) {
   extern __shared__ int32_t sh_ord[];  // [kScanThreads] + bins[max(T_m,T_n)+1]
   int32_t* bins = sh_ord + kScanThreads;
+  __shared__ int32_t s_base;
   const int64_t bh = blockIdx.x;
-  if (blockIdx.y == 0)
+  const bool rows = blockIdx.y == 0;
+  const int n = rows ? T_m : T_n;
+  const int32_t* cnt_all = rows ? row_cnt : col_cnt;
+  // kept blocks of the earlier heads
+  int32_t pre = 0;
+  for (int64_t e = threadIdx.x; e < bh * n; e += kScanThreads) pre += cnt_all[e];
+  pre = cta_inclusive_scan_1024(pre, sh_ord);
+  if (threadIdx.x == kScanThreads - 1) s_base = pre;
+  __syncthreads();
+  const int32_t base = s_base;
+  const int32_t* cnt = cnt_all + bh * n;
+  int32_t* ptr = (rows ? row_ptr : col_ptr) + bh * n;
+  const int per = (n + kScanThreads - 1) / kScanThreads;
+  const int beg = min((int)threadIdx.x * per, n), end = min(beg + per, n);
+  int32_t local = 0;
+  for (int i = beg; i < end; ++i) local += cnt[i];
+  const int32_t incl = cta_inclusive_scan_1024(local, sh_ord);
+  int32_t run = base + incl - local;
+  for (int i = beg; i < end; ++i) {
+    const int32_t c = cnt[i];
+    ptr[i] = run;
+    run += c;
+  }
+  if (bh == bh_total - 1 && threadIdx.x == kScanThreads - 1) ptr[n] = base + incl;  // the CSR end entry
+  __syncthreads();
+  if (rows)
     cta_order_desc(row_cnt, T_m, T_n, row_order, bins, sh_ord, bh * T_m);
   else
     cta_order_desc(col_cnt, T_n, T_m, col_order, bins, sh_ord, bh * T_n);
 }
 
-__global__ void k_fill_rows(const uint8_t* __restrict__ keep, int64_t nrows, int T_n,
-                            const int32_t* __restrict__ row_ptr, int32_t* __restrict__ row_idx) {
-  const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-  const int lane = threadIdx.x % 32;
-  if (row >= nrows) return;
-  int base = row_ptr[row];
-  for (int j0 = 0; j0 < T_n; j0 += 32) {
-    int j = j0 + lane;
-    bool f = j < T_n && keep[row * T_n + j] != 0;
-    unsigned m = __ballot_sync(0xffffffffu, f);
-    if (f) row_idx[base + __popc(m & ((1u << lane) - 1u))] = j;
-    base += __popc(m);
+// (c) blockIdx.x < col_chunks: column lists (as k_fill_cols); otherwise row lists, one warp
+//     per row (as k_fill_rows).
+__global__ void __launch_bounds__(kColWarps * 32) k_fill(const uint8_t* __restrict__ keep, int T_m, int T_n,
+                                                         int col_chunks, const int32_t* __restrict__ row_ptr,
+                                                         int32_t* __restrict__ row_idx,
+                                                         const int32_t* __restrict__ col_ptr,
+                                                         int32_t* __restrict__ col_idx) {
+  const int64_t bh = blockIdx.y;
+  const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if ((int)blockIdx.x < col_chunks) {
+    __shared__ int part[kColWarps][32];
+    const int j = blockIdx.x * 32 + lane;
+    int r0, r1;
+    col_range(T_m, w, r0, r1);
+    const uint8_t* base = keep + bh * (int64_t)T_m * T_n + j;
+    int c = 0;
+    if (j < T_n) {
+#pragma unroll 8
+      for (int i = r0; i < r1; ++i) c += base[(int64_t)i * T_n] != 0;
+    }
+    part[w][lane] = c;
+    __syncthreads();
+    if (j >= T_n) return;
+    int off = col_ptr[bh * T_n + j];
+    for (int x = 0; x < w; ++x) off += part[x][lane];
+#pragma unroll 8
+    for (int i = r0; i < r1; ++i)
+      if (base[(int64_t)i * T_n] != 0) col_idx[off++] = i;
+  } else {
+    const int i = ((int)blockIdx.x - col_chunks) * kColWarps + w;
+    if (i >= T_m) return;
+    const int64_t row = bh * T_m + i;
+    int b = row_ptr[row];
+    for (int j0 = 0; j0 < T_n; j0 += 32) {
+      const int j = j0 + lane;
+      const bool f = j < T_n && keep[row * T_n + j] != 0;
+      const unsigned m = __ballot_sync(0xffffffffu, f);
+      if (f) row_idx[b + __popc(m & ((1u << lane) - 1u))] = j;
+      b += __popc(m);
+    }
   }
 }
 
@@ -695,25 +708,20 @@ extern "C" int spa2_build_lists(const uint8_t* keep, int64_t bh, int64_t t_m, in
   SPA2_REQUIRE(std::max(t_m, t_n) <= 32768 && bh < 65536, SPA2_ERR_UNSUPPORTED,
                "build_lists: T_m/T_n > 32768 or B*H >= 65536");
   cudaStream_t st = (cudaStream_t)stream;
-  const int64_t nrows = bh * t_m, ncols = bh * t_n;
+  const int64_t ncols = bh * t_n;
   int32_t* col_cnt = scratch;          // [ncols]
   int32_t* row_cnt = scratch + ncols;  // [nrows]
-  const dim3 cgrid((unsigned)ceil_div(t_n, 32), (unsigned)bh);
-  k_row_counts<<<(unsigned)ceil_div(nrows, 8), 256, 0, st>>>(keep, nrows, (int)t_n, row_cnt);
-  SPA2_LAUNCH_CHECK();
-  k_col_counts<<<cgrid, kColWarps * 32, 0, st>>>(keep, (int)t_m, (int)t_n, col_cnt);
-  SPA2_LAUNCH_CHECK();
-  k_scan<<<1, kScanThreads, 0, st>>>(row_cnt, col_cnt, nrows, ncols, row_ptr, col_ptr);
+  const int col_chunks = (int)ceil_div(t_n, 32);
+  const dim3 grid((unsigned)(col_chunks + ceil_div(t_m, kColWarps)), (unsigned)bh);
+  k_counts<<<grid, kColWarps * 32, 0, st>>>(keep, (int)t_m, (int)t_n, col_chunks, row_cnt, col_cnt);
   SPA2_LAUNCH_CHECK();
   const size_t smem = (kScanThreads + std::max(t_m, t_n) + 1) * sizeof(int32_t);
   if (smem > 48 * 1024)
-    SPA2_CUDA_TRY(cudaFuncSetAttribute(k_orders, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_orders<<<dim3((unsigned)bh, 2), kScanThreads, smem, st>>>(row_cnt, col_cnt, (int)t_m, (int)t_n, row_order,
-                                                               col_order);
+    SPA2_CUDA_TRY(cudaFuncSetAttribute(k_scan_orders, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_scan_orders<<<dim3((unsigned)bh, 2), kScanThreads, smem, st>>>(row_cnt, col_cnt, (int)t_m, (int)t_n, bh, row_ptr, col_ptr,
+                                                          row_order, col_order);
   SPA2_LAUNCH_CHECK();
-  k_fill_rows<<<(unsigned)ceil_div(nrows, 8), 256, 0, st>>>(keep, nrows, (int)t_n, row_ptr, row_idx);
-  SPA2_LAUNCH_CHECK();
-  k_fill_cols<<<cgrid, kColWarps * 32, 0, st>>>(keep, (int)t_m, (int)t_n, col_ptr, col_idx);
+  k_fill<<<grid, kColWarps * 32, 0, st>>>(keep, (int)t_m, (int)t_n, col_chunks, row_ptr, row_idx, col_ptr, col_idx);
   SPA2_LAUNCH_CHECK();
   return SPA2_OK;
 }
