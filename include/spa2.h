@@ -79,6 +79,17 @@ int spa2_pooled_map(spa2_view q, spa2_view k, int dtype, int64_t B, int64_t H, i
 int spa2_select(const double* probs, int64_t rows, int64_t t_n, int64_t k_count,
                 double p_threshold, uint8_t* keep, int32_t* counts, void* stream);
 
+/* Fused K1+K2 for sparse_attention (the map itself is not returned): spa2_pooled_scores is
+ * spa2_pooled_map without its softmax stage (scores = Q̄K̄ᵀ/√d, float64), and
+ * spa2_select_scores applies the row softmax to those scores in shared memory with
+ * spa2_pooled_map's exact arithmetic before selecting — the keep/counts outputs are
+ * bit-identical to spa2_pooled_map + spa2_select.  t_n <= 4096. */
+int spa2_pooled_scores(spa2_view q, spa2_view k, int dtype, int64_t B, int64_t H, int64_t N,
+                       int64_t d, int64_t b_q, int64_t b_kv, double* scores, double* workspace,
+                       int32_t* nonfinite, void* stream);
+int spa2_select_scores(const double* scores, int64_t rows, int64_t t_n, int64_t k_count,
+                       double p_threshold, uint8_t* keep, int32_t* counts, void* stream);
+
 /* ---- K3: block lists ---------------------------------------------------------------
  * From keep uint8 [bh, t_m, t_n] build
  *   row CSR: row_ptr int32 [bh*t_m + 1], row_idx int32 [>= nnz]  (kept key blocks of

@@ -262,11 +262,21 @@ def sparse_attention_with_mask(q, k, v, bm: BlockMask, counter: BlockCounter | N
     return _run(q4, k4, v4, bm, qb, counter, _block_order)
 
 
-def _hybrid_mask_device(q4, k4, cfg: SparsityConfig, check_finite: bool) -> BlockMask:
-    probs, flag = _pooled_probs(q4, k4, cfg.b_q, cfg.b_kv, check_finite)
-    if flag is not None and int(flag.item()) != 0:
-        raise FloatingPointError("non-finite values in q or k")
-    keep, _ = _select(probs, top_k_count(cfg.k_frac, probs.shape[-1]), cfg.p_frac)
+def _hybrid_mask_device(q4, k4, cfg: SparsityConfig, check_finite: bool, fused: bool = True) -> BlockMask:
+    """hybrid_mask(pooled_map(q, k, cfg), cfg) without materialising the map: the row softmax
+    runs inside the select kernel (bit-identical masks; ``fused=False`` takes the two-step
+    pooled_map + select path)."""
+    t_n = num_blocks(q4.shape[2], cfg.b_kv)
+    if fused and t_n <= 4096:
+        scores, flag = _pooled_probs(q4, k4, cfg.b_q, cfg.b_kv, check_finite, softmax=False)
+        if flag is not None and int(flag.item()) != 0:
+            raise FloatingPointError("non-finite values in q or k")
+        keep, _ = _select(scores, top_k_count(cfg.k_frac, t_n), cfg.p_frac, from_scores=True)
+    else:
+        probs, flag = _pooled_probs(q4, k4, cfg.b_q, cfg.b_kv, check_finite)
+        if flag is not None and int(flag.item()) != 0:
+            raise FloatingPointError("non-finite values in q or k")
+        keep, _ = _select(probs, top_k_count(cfg.k_frac, probs.shape[-1]), cfg.p_frac)
     if q4.shape[0] == 1 and q4.shape[1] == 1:
         keep = keep[0, 0]
     return BlockMask._trusted(keep, cfg.b_q, cfg.b_kv, q4.shape[2])

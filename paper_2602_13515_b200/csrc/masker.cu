@@ -278,14 +278,43 @@ __device__ __forceinline__ double bucket_floor(int b) {
 // inside it; (3) only the candidates are sorted (bitonic, shared memory) and scanned.  Rows with negative entries
 // (non-monotone cumsum) take every entry as a candidate.  Output is identical to sorting the
 // whole row.
+// FROM_SCORES: the input rows are pre-softmax scores; the row softmax is applied first, into
+// shared memory, with exactly k_softmax_rows' arithmetic (warp 0: lane-strided max and
+// exp-sums, xor-butterfly combine; p = exp(x - m) / s), so the selection is identical to
+// spa2_pooled_map + spa2_select while the float64 map never goes through HBM.
+template <bool FROM_SCORES>
 __global__ void __launch_bounds__(kSelThreads) k_select(const double* __restrict__ probs, int T_n, int k_count,
                                                         double thr, int use_p, uint8_t* __restrict__ keep,
                                                         int32_t* __restrict__ counts) {
-  extern __shared__ unsigned char smem_raw[];  // cand_v[T_pad] (double), cand_c[T_pad] (int)
+  extern __shared__ __align__(16) unsigned char smem_raw[];  // [p row (FROM_SCORES)] cand_v[T_pad], cand_c[T_pad]
   __shared__ int h_cnt[kBuckets];
   __shared__ int s_neg, s_bstar, s_npos, s_kept;
+  __shared__ double s_m, s_s;
   const int64_t row = blockIdx.x;
   const double* x = probs + row * (int64_t)T_n;
+  if constexpr (FROM_SCORES) {
+    double* pr = reinterpret_cast<double*>(smem_raw);
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      double m = -INFINITY;
+      for (int j = lane; j < T_n; j += 32) m = fmax(m, x[j]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+      double sum = 0.0;
+      for (int j = lane; j < T_n; j += 32) sum += exp(x[j] - m);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      if (lane == 0) {
+        s_m = m;
+        s_s = sum;
+      }
+    }
+    __syncthreads();
+    const double m = s_m, sum = s_s;
+    for (int j = threadIdx.x; j < T_n; j += blockDim.x) pr[j] = exp(x[j] - m) / sum;
+    __syncthreads();
+    x = pr;
+  }
   for (int b = threadIdx.x; b < kBuckets; b += blockDim.x) h_cnt[b] = 0;
   if (threadIdx.x == 0) {
     s_neg = 0;
@@ -322,7 +351,7 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const double* __restrict
   }
   __syncthreads();
   const int bstar = s_bstar;
-  double* cv = reinterpret_cast<double*>(smem_raw);
+  double* cv = reinterpret_cast<double*>(smem_raw) + (FROM_SCORES ? T_n : 0);
   int T_pad = 1;
   while (T_pad < T_n) T_pad <<= 1;
   int* cc = reinterpret_cast<int*>(cv + T_pad);
@@ -642,9 +671,9 @@ int launch_pool(spa2_view q, spa2_view k, int64_t B, int64_t H, int64_t N, int64
 
 using namespace spa2;
 
-extern "C" int spa2_pooled_map(spa2_view q, spa2_view k, int dtype, int64_t B, int64_t H, int64_t N,
-                               int64_t d, int64_t b_q, int64_t b_kv, double* probs,
-                               double* workspace, int32_t* nonfinite, void* stream) {
+static int pooled_map_impl(spa2_view q, spa2_view k, int dtype, int64_t B, int64_t H, int64_t N, int64_t d,
+                           int64_t b_q, int64_t b_kv, double* probs, double* workspace, int32_t* nonfinite,
+                           void* stream, bool softmax) {
   SPA2_REQUIRE(B >= 1 && H >= 1 && N >= 1 && d >= 1, SPA2_ERR_VALUE,
                "pooled_map: bad shape B=%lld H=%lld N=%lld d=%lld", (long long)B, (long long)H,
                (long long)N, (long long)d);
@@ -669,10 +698,17 @@ extern "C" int spa2_pooled_map(spa2_view q, spa2_view k, int dtype, int64_t B, i
   SPA2_CUDA_TRY(cudaFuncSetAttribute(k_scores, cudaFuncAttributeMaxDynamicSharedMemorySize, kScoresSmem));
   k_scores<<<grid, 256, kScoresSmem, st>>>(qbar, kbar, (int)T_m, (int)T_n, (int)d, sqrt((double)d), probs);
   SPA2_LAUNCH_CHECK();
+  if (!softmax) return SPA2_OK;
   const int64_t rows = BH * T_m;
   k_softmax_rows<<<(unsigned)ceil_div(rows, 8), 256, 0, st>>>(probs, rows, (int)T_n);
   SPA2_LAUNCH_CHECK();
   return SPA2_OK;
+}
+
+extern "C" int spa2_pooled_map(spa2_view q, spa2_view k, int dtype, int64_t B, int64_t H, int64_t N,
+                               int64_t d, int64_t b_q, int64_t b_kv, double* probs,
+                               double* workspace, int32_t* nonfinite, void* stream) {
+  return pooled_map_impl(q, k, dtype, B, H, N, d, b_q, b_kv, probs, workspace, nonfinite, stream, true);
 }
 
 extern "C" int spa2_select(const double* probs, int64_t rows, int64_t t_n, int64_t k_count,
@@ -689,10 +725,39 @@ extern "C" int spa2_select(const double* probs, int64_t rows, int64_t t_n, int64
   SPA2_REQUIRE(smem <= 200 * 1024, SPA2_ERR_UNSUPPORTED, "select: T_n=%lld exceeds 16384", (long long)t_n);
   cudaStream_t st = (cudaStream_t)stream;
   if (smem > 48 * 1024)
-    SPA2_CUDA_TRY(cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SPA2_CUDA_TRY(cudaFuncSetAttribute(k_select<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int use_p = isinf(p_threshold) && p_threshold < 0 ? 0 : 1;
   const int kk = (int)std::min<int64_t>(k_count, t_n);
-  k_select<<<(unsigned)rows, kSelThreads, smem, st>>>(probs, (int)t_n, kk, p_threshold, use_p, keep, counts);
+  k_select<false><<<(unsigned)rows, kSelThreads, smem, st>>>(probs, (int)t_n, kk, p_threshold, use_p, keep, counts);
+  SPA2_LAUNCH_CHECK();
+  return SPA2_OK;
+}
+
+extern "C" int spa2_pooled_scores(spa2_view q, spa2_view k, int dtype, int64_t B, int64_t H, int64_t N, int64_t d,
+                                  int64_t b_q, int64_t b_kv, double* scores, double* workspace, int32_t* nonfinite,
+                                  void* stream) {
+  return pooled_map_impl(q, k, dtype, B, H, N, d, b_q, b_kv, scores, workspace, nonfinite, stream, false);
+}
+
+extern "C" int spa2_select_scores(const double* scores, int64_t rows, int64_t t_n, int64_t k_count,
+                                  double p_threshold, uint8_t* keep, int32_t* counts, void* stream) {
+  SPA2_REQUIRE(rows >= 1 && t_n >= 1, SPA2_ERR_VALUE, "select_scores: empty map (%lld x %lld)", (long long)rows,
+               (long long)t_n);
+  SPA2_REQUIRE(k_count >= 1, SPA2_ERR_VALUE, "select_scores: k_count must be >= 1");
+  SPA2_REQUIRE(scores && keep, SPA2_ERR_VALUE, "select_scores: null pointer");
+  SPA2_REQUIRE(!isnan(p_threshold), SPA2_ERR_VALUE, "select_scores: p_threshold is NaN");
+  SPA2_REQUIRE(rows < (1ll << 31), SPA2_ERR_UNSUPPORTED, "select_scores: too many rows");
+  SPA2_REQUIRE(t_n <= 4096, SPA2_ERR_UNSUPPORTED, "select_scores: T_n=%lld > 4096 (use pooled_map + select)",
+               (long long)t_n);
+  int t_pad = 1;
+  while (t_pad < t_n) t_pad <<= 1;
+  const size_t smem = (size_t)t_n * sizeof(double) + (size_t)t_pad * (sizeof(double) + sizeof(int));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (smem > 48 * 1024)
+    SPA2_CUDA_TRY(cudaFuncSetAttribute(k_select<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int use_p = isinf(p_threshold) && p_threshold < 0 ? 0 : 1;
+  const int kk = (int)std::min<int64_t>(k_count, t_n);
+  k_select<true><<<(unsigned)rows, kSelThreads, smem, st>>>(scores, (int)t_n, kk, p_threshold, use_p, keep, counts);
   SPA2_LAUNCH_CHECK();
   return SPA2_OK;
 }

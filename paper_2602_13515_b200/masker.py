@@ -159,16 +159,18 @@ def pooled_map(q, k, cfg: SparsityConfig) -> PooledMap:
     return PooledMap._trusted(probs, cfg.b_q, cfg.b_kv, qt.shape[2])
 
 
-def _pooled_probs(qt: torch.Tensor, kt: torch.Tensor, b_q: int, b_kv: int, check_finite: bool):
-    """Launch K1 on [B,H,N,d] tensors; returns (probs [B,H,T_m,T_n] float64, flag|None)."""
+def _pooled_probs(qt: torch.Tensor, kt: torch.Tensor, b_q: int, b_kv: int, check_finite: bool, softmax: bool = True):
+    """Launch K1 on [B,H,N,d] tensors; returns (probs [B,H,T_m,T_n] float64, flag|None).
+    ``softmax=False`` returns the pre-softmax scores Q̄K̄ᵀ/√d (for spa2_select_scores)."""
     B, H, N, d = qt.shape
     t_m, t_n = num_blocks(N, b_q), num_blocks(N, b_kv)
     probs = torch.empty((B, H, t_m, t_n), device=qt.device, dtype=torch.float64)
     work = torch.empty((B * H * (t_m + t_n) * d,), device=qt.device, dtype=torch.float64)
     flag = torch.zeros((1,), device=qt.device, dtype=torch.int32) if check_finite else None
     st = torch.cuda.current_stream(qt.device)
-    _lib.call("spa2_pooled_map", _lib.view4(qt), _lib.view4(kt), _lib.DTYPE_CODES[qt.dtype], B, H, N, d, b_q, b_kv,
-              _lib.ptr(probs), _lib.ptr(work), _lib.ptr(flag), st.cuda_stream, stream_obj=st)
+    _lib.call("spa2_pooled_map" if softmax else "spa2_pooled_scores", _lib.view4(qt), _lib.view4(kt),
+              _lib.DTYPE_CODES[qt.dtype], B, H, N, d, b_q, b_kv, _lib.ptr(probs), _lib.ptr(work), _lib.ptr(flag),
+              st.cuda_stream, stream_obj=st)
     return probs, flag
 
 
@@ -181,15 +183,16 @@ def top_k_count(k_frac: float, t_n: int) -> int:
     return max(1, math.ceil(k_frac * t_n))
 
 
-def _select(probs: torch.Tensor, k_count: int, p_frac: float | None) -> tuple[torch.Tensor, torch.Tensor]:
+def _select(probs: torch.Tensor, k_count: int, p_frac: float | None,
+            from_scores: bool = False) -> tuple[torch.Tensor, torch.Tensor]:
     t_n = probs.shape[-1]
     rows = probs.numel() // t_n
     keep = torch.empty(probs.shape, device=probs.device, dtype=torch.bool)
     counts = torch.empty(probs.shape[:-1], device=probs.device, dtype=torch.int32)
     thr = (p_frac - P_SLACK) if p_frac is not None else -math.inf
     st = torch.cuda.current_stream(probs.device)
-    _lib.call("spa2_select", _lib.ptr(probs), rows, t_n, k_count, thr, _lib.ptr(keep), _lib.ptr(counts),
-              st.cuda_stream, stream_obj=st)
+    _lib.call("spa2_select_scores" if from_scores else "spa2_select", _lib.ptr(probs), rows, t_n, k_count, thr,
+              _lib.ptr(keep), _lib.ptr(counts), st.cuda_stream, stream_obj=st)
     return keep, counts
 
 

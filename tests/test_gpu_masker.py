@@ -210,3 +210,18 @@ def test_public_names():
     for name in ("SparsityConfig", "PooledMap", "BlockMask", "pooled_map", "top_k_mask", "top_p_mask",
                  "hybrid_mask", "expand_mask"):
         assert hasattr(spa, name)
+
+
+@pytest.mark.parametrize("n,heads,s,k,p", [(32760, 12, 0.9, 0.03, 0.2), (4096, 2, 0.0, 0.1, 0.9), (777, 3, 0.5, 0.2, 0.5),
+                                           (75600 // 8, 1, 0.8, 0.03, 0.16), (1000, 1, 0.7, 0.0, 0.3)])
+def test_fused_softmax_select_is_bit_identical(n, heads, s, k, p):
+    """sparse_attention's mask path (pooled scores + softmax inside the select kernel) gives
+    exactly hybrid_mask(pooled_map(q, k)) — the map never leaves shared memory."""
+    from paper_2602_13515_b200 import attention as at
+    from paper_2602_13515_b200.synthetic import wan_like_qkv
+
+    q, kk, _ = wan_like_qkv(1, heads, n, 128, s, seed=n + heads)
+    cfg = spa.SparsityConfig(k, p, 128, 64)
+    fused = at._hybrid_mask_device(q, kk, cfg, True, fused=True).keep
+    twostep = at._hybrid_mask_device(q, kk, cfg, True, fused=False).keep
+    assert torch.equal(fused, twostep)
