@@ -232,7 +232,7 @@ def gpu_arm(args, rank: int, world: int, dev):
     torch.cuda.synchronize()
 
     timed_names = ("spa2_fwd", "spa2_bwd_dq_delta", "spa2_bwd_dkdv", "spa2_pooled_scores", "spa2_select_scores",
-                   "spa2_build_lists")
+                   "spa2_pooled_map", "spa2_select", "spa2_build_lists")
     _lib.STATS.timing = {n: [] for n in timed_names}
     launches0 = _lib.STATS.launches
     uuid = None

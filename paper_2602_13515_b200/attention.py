@@ -17,6 +17,7 @@ b_kv = 64 (the paper's setting); masks at coarser multiples of tha
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -262,11 +263,16 @@ def sparse_attention_with_mask(q, k, v, bm: BlockMask, counter: BlockCounter | N
     return _run(q4, k4, v4, bm, qb, counter, _block_order)
 
 
-def _hybrid_mask_device(q4, k4, cfg: SparsityConfig, check_finite: bool, fused: bool = True) -> BlockMask:
+_FUSED_SELECT = os.environ.get("SPA2_FUSED_SELECT", "1") != "0"
+
+
+def _hybrid_mask_device(q4, k4, cfg: SparsityConfig, check_finite: bool, fused: bool | None = None) -> BlockMask:
     """hybrid_mask(pooled_map(q, k, cfg), cfg) without materialising the map: the row softmax
     runs inside the select kernel (bit-identical masks; ``fused=False`` takes the two-step
     pooled_map + select path)."""
     t_n = num_blocks(q4.shape[2], cfg.b_kv)
+    if fused is None:
+        fused = _FUSED_SELECT
     if fused and t_n <= 4096:
         scores, flag = _pooled_probs(q4, k4, cfg.b_q, cfg.b_kv, check_finite, softmax=False)
         if flag is not None and int(flag.item()) != 0:

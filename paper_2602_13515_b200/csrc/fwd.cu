@@ -346,6 +346,301 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
 }
 
 // ---------------------------------------------------------------------------------------
+// K4 (default): the k_fwd pipeline made PERSISTENT — two CTAs per SM, each walking query
+// blocks head-major / longest-first (blockIdx.x, +gridDim.x, ...).  Barrier phases run on a
+// CTA-global tile counter g, so the producers prefetch the next query block's Q and first
+// K/V tiles while the current one finishes, and the softmax warps drain O (direct row
+// stores) while the next block's first S is already in flight.  TMEM (256 columns):
+// S[g&1] at 0 / 64 (P overwrites its first 32 columns), O at 128.
+// Warps: 0 TMA (Q, K ring), 1 MMA (S, PV), 2-5 softmax + epilogue, 6 TMA (V ring).
+// ---------------------------------------------------------------------------------------
+template <int HD>
+struct Fwd3Cfg {
+  static constexpr int NS = (HD == 128) ? 2 : 4;
+  static constexpr int Q_BYTES = BQ * HD * 2;
+  static constexpr int KV_BYTES = BKV * HD * 2;
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = OFF_Q + Q_BYTES;
+  static constexpr int OFF_V = OFF_K + NS * KV_BYTES;
+  static constexpr int OFF_BAR = OFF_V + NS * KV_BYTES;
+  static constexpr int NUM_BARS = 2 + 4 * NS + 2 * 3 + 2;
+  static constexpr int SMEM_USED = OFF_BAR + NUM_BARS * 8 + 16;
+  static constexpr int SMEM = SMEM_USED < 80 * 1024 ? 80 * 1024 : SMEM_USED;
+  static constexpr uint32_t O_COL = 128;
+};
+
+__device__ __forceinline__ void fwd_item(const FwdParams& p, int wi, int& bh, int& qi, int& beg, int& n) {
+  const int w = p.row_order ? p.row_order[wi] : wi;
+  bh = w / p.T_m;
+  qi = w % p.T_m;
+  beg = p.row_ptr[w];
+  n = p.row_ptr[w + 1] - beg;
+}
+
+template <int HD>
+__global__ void __launch_bounds__(kFwdThreads, 2)
+    k_fwd3(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+           const __grid_constant__ CUtensorMap tmV, const FwdParams p, int num_items) {
+  using C = Fwd3Cfg<HD>;
+  constexpr int NS = C::NS;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* q_full = bars;            // Q of item `it` landed
+  uint64_t* q_empty = bars + 1;       // last S MMA of item `it` done
+  uint64_t* k_full = bars + 2;        // [NS]
+  uint64_t* k_empty = k_full + NS;
+  uint64_t* v_full = k_empty + NS;
+  uint64_t* v_empty = v_full + NS;
+  uint64_t* s_full = v_empty + NS;    // [2] S of tile g in buffer g&1
+  uint64_t* p_full = s_full + 2;      // [2] P of tile g written
+  uint64_t* o_done = p_full + 2;      // [2] PV of tile g done
+  uint64_t* acc_full = o_done + 2;    // last PV of item `it` done
+  uint64_t* acc_empty = acc_full + 1;  // O of item `it` read out
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 1);
+
+  const int warp = (int)warp_id(), lane = (int)lane_id();
+  if (threadIdx.x == 0) {
+    if (smem_u32(smem) & 1023u) __trap();
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&p_full[b], 128);
+      mbar_init(&o_done[b], 1);
+    }
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, 128);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_holder, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_holder;
+
+  if (warp == 0 || warp == 6) {
+    // ---------------- TMA producers: warp 0 Q + K ring, warp 6 V ring ----------------
+    if (elect_one()) {
+      const bool second = warp == 6;
+      if (second) {
+        tma_prefetch(&tmV);
+      } else {
+        tma_prefetch(&tmQ);
+        tma_prefetch(&tmK);
+      }
+      int it = 0, g = 0;
+      for (int wi = blockIdx.x; wi < num_items; wi += gridDim.x) {
+        int bh, qi, beg, n;
+        fwd_item(p, wi, bh, qi, beg, n);
+        if (n == 0) continue;
+        const int hh = bh % p.H, bb = bh / p.H;
+        if (!second) {
+          if (it >= 1) mbar_wait(q_empty, (uint32_t)(it - 1) & 1u);
+          mbar_expect_tx(q_full, C::Q_BYTES);
+          tma_load_5d(smem + C::OFF_Q, &tmQ, q_full, 0, qi * BQ, 0, hh, bb);
+        }
+        for (int t = 0; t < n; ++t, ++g) {
+          const int s = g % NS;
+          const uint32_t ph = (uint32_t)(g / NS) & 1u;
+          const int j = p.row_idx[beg + t];
+          if (!second) {
+            if (g >= NS) mbar_wait(&k_empty[s], ph ^ 1u);
+            mbar_expect_tx(&k_full[s], C::KV_BYTES);
+            tma_load_5d(smem + C::OFF_K + s * C::KV_BYTES, &tmK, &k_full[s], 0, j * BKV, 0, hh, bb);
+          } else {
+            if (g >= NS) mbar_wait(&v_empty[s], ph ^ 1u);
+            mbar_expect_tx(&v_full[s], C::KV_BYTES);
+            tma_load_5d(smem + C::OFF_V + s * C::KV_BYTES, &tmV, &v_full[s], 0, j * BKV, 0, hh, bb);
+          }
+        }
+        ++it;
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (whole warp): S(g), then PV(g-1) ----------------
+    constexpr uint32_t idS = idesc_bf16(BQ, BKV, false, false);
+    constexpr uint32_t idO = idesc_bf16(BQ, HD, false, true);
+    const uint64_t dQ = sw128_desc(smem_u32(smem + C::OFF_Q), 16, 1024);
+    const uint64_t dK0 = sw128_desc(smem_u32(smem + C::OFF_K), 16, 1024);
+    const uint64_t dV0 = sw128_desc(smem_u32(smem + C::OFF_V), BKV * 128, 1024);
+    constexpr uint64_t KV16 = (uint64_t)(C::KV_BYTES >> 4);
+    // the pending PV: tile g-1 (its item index, position and whether it ends the item)
+    int pv_g = -1, pv_it = 0;
+    bool pv_first = false, pv_last = false;
+    auto issue_pv = [&]() {
+      const int b = pv_g & 1, s = pv_g % NS;
+      if (pv_first && pv_it >= 1) mbar_wait(acc_empty, (uint32_t)(pv_it - 1) & 1u);  // O drained
+      mbar_wait(&p_full[b], (uint32_t)(pv_g >> 1) & 1u);
+      mbar_wait(&v_full[s], (uint32_t)(pv_g / NS) & 1u);
+      tc_fence_after();
+      trace_ev(p.trace, p.trace_cap, 1, 4, pv_g);
+      const uint64_t dV = dV0 + (uint64_t)s * KV16;
+#pragma unroll
+      for (int ks = 0; ks < BKV / 16; ++ks)
+        mma_bf16_ts_w(tbase + C::O_COL, tbase + (uint32_t)(b * 64 + ks * 8), dV + (uint64_t)(ks * 128), idO,
+                      (!pv_first || ks > 0) ? 1u : 0u);
+      mma_commit_w(&o_done[b]);
+      mma_commit_w(&v_empty[s]);
+      if (pv_last) mma_commit_w(acc_full);
+    };
+    int it = 0, g = 0;
+    for (int wi = blockIdx.x; wi < num_items; wi += gridDim.x) {
+      int bh, qi, beg, n;
+      fwd_item(p, wi, bh, qi, beg, n);
+      if (n == 0) continue;
+      for (int t = 0; t < n; ++t, ++g) {
+        const int b = g & 1, s = g % NS;
+        if (t == 0) mbar_wait(q_full, (uint32_t)it & 1u);
+        if (g >= 2) mbar_wait(&o_done[b], (uint32_t)((g - 2) >> 1) & 1u);  // P of tile g-2 consumed
+        mbar_wait(&k_full[s], (uint32_t)(g / NS) & 1u);
+        tc_fence_after();
+        trace_ev(p.trace, p.trace_cap, 1, 2, g);
+        const uint64_t dK = dK0 + (uint64_t)s * KV16;
+#pragma unroll
+        for (int ks = 0; ks < HD / 16; ++ks) {
+          const int k0 = ks * 16;
+          mma_bf16_w(tbase + (uint32_t)(b * 64), dQ + (uint64_t)(((k0 / 64) * BQ * 128 + (k0 % 64) * 2) >> 4),
+                     dK + (uint64_t)(((k0 / 64) * BKV * 128 + (k0 % 64) * 2) >> 4), idS, ks > 0 ? 1u : 0u);
+        }
+        mma_commit_w(&s_full[b]);
+        mma_commit_w(&k_empty[s]);
+        if (t == n - 1) mma_commit_w(q_empty);
+        if (pv_g >= 0) issue_pv();
+        pv_g = g;
+        pv_it = it;
+        pv_first = t == 0;
+        pv_last = t == n - 1;
+      }
+      ++it;
+    }
+    if (pv_g >= 0) issue_pv();
+  } else {
+    // ---------------- softmax warps (2..5) + epilogue ----------------
+    const int q4 = warp & 3;
+    const int row = q4 * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    const int kv_tail = p.N - (p.T_n - 1) * BKV;
+    const float sl2 = p.scale_log2;
+    int it = 0, g = 0;
+    for (int wi = blockIdx.x; wi < num_items; wi += gridDim.x) {
+      int bh, qi, beg, n;
+      fwd_item(p, wi, bh, qi, beg, n);
+      const int hh = bh % p.H, bb = bh / p.H;
+      const int tok = qi * BQ + row;
+      __nv_bfloat16* orow = p.o_ptr + bb * p.o_sb + hh * p.o_sh + (int64_t)tok * p.o_sn;
+      if (n == 0) {  // reachable only through the raw C ABI: O = 0, LSE = -inf
+        if (tok < p.N) {
+          for (int c = 0; c < HD; c += 8) *reinterpret_cast<uint4*>(orow + c) = make_uint4(0, 0, 0, 0);
+          p.lse[(int64_t)bh * p.N + tok] = -INFINITY;
+        }
+        continue;
+      }
+      const int32_t* list = p.row_idx + beg;
+      float m = -INFINITY, l = 0.f;
+      int j_next = list[0];
+      for (int t = 0; t < n; ++t, ++g) {
+        const int b = g & 1;
+        const bool tail = j_next == p.T_n - 1 && kv_tail < BKV;
+        if (t + 1 < n) j_next = list[t + 1];
+        const uint32_t s_col = tbase + lane_off + (uint32_t)(b * 64);
+        mbar_wait(&s_full[b], (uint32_t)(g >> 1) & 1u);
+        tc_fence_after();
+        uint32_t r[64];
+        tmem_ld64(s_col, r);
+        float sv[64];
+#pragma unroll
+        for (int c = 0; c < 64; ++c) sv[c] = __uint_as_float(r[c]);
+        if (tail) {
+#pragma unroll
+          for (int c = 0; c < 64; ++c)
+            if (c >= kv_tail) sv[c] = -INFINITY;
+        }
+        float mx8[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          mx8[u] = fmaxf(fmaxf(fmaxf(sv[8 * u], sv[8 * u + 1]), fmaxf(sv[8 * u + 2], sv[8 * u + 3])),
+                         fmaxf(fmaxf(sv[8 * u + 4], sv[8 * u + 5]), fmaxf(sv[8 * u + 6], sv[8 * u + 7])));
+        const float mx = sl2 * fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                     fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+        if (t == 0) {
+          m = mx;
+        } else if (__any_sync(0xffffffffu, mx > m + kRescaleThreshold)) {
+          const float m_new = fmaxf(m, mx);
+          const float alpha = ex2(m - m_new);
+          mbar_wait(&o_done[(g - 1) & 1], (uint32_t)((g - 1) >> 1) & 1u);  // PV(g-1) has landed in O
+          tc_fence_after();
+#pragma unroll 1
+          for (int c0 = 0; c0 < HD; c0 += 32) {
+            uint32_t o[32];
+            tmem_ld32(tbase + lane_off + C::O_COL + (uint32_t)c0, o);
+#pragma unroll
+            for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * alpha);
+            tmem_st32(tbase + lane_off + C::O_COL + (uint32_t)c0, o);
+          }
+          tmem_st_wait();
+          l *= alpha;
+          m = m_new;
+        }
+        uint32_t pk[32];
+        float2 lsum = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const float2 x = __ffma2_rn(make_float2(sv[2 * c], sv[2 * c + 1]), make_float2(sl2, sl2), make_float2(-m, -m));
+          float2 e;
+          if (c < 8) {  // a quarter of the exponentials on the FMA pipe
+            e = exp2_poly2(x);
+          } else {
+            e.x = ex2(x.x);
+            e.y = ex2(x.y);
+          }
+          lsum = __fadd2_rn(lsum, e);
+          pk[c] = pack_bf16(e.x, e.y);
+        }
+        l += lsum.x + lsum.y;
+        tmem_st32(s_col, pk);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&p_full[b]);
+      }
+      // ---------------- epilogue: O / l -> bf16 rows, LSE ----------------
+      mbar_wait(acc_full, (uint32_t)it & 1u);
+      tc_fence_after();
+      const float inv_l = 1.f / l;
+#pragma unroll 1
+      for (int c0 = 0; c0 < HD; c0 += 32) {
+        uint32_t o[32];
+        tmem_ld32(tbase + lane_off + C::O_COL + (uint32_t)c0, o);
+        if (c0 + 32 == HD) {
+          tc_fence_before();
+          mbar_arrive(acc_empty);
+        }
+        uint32_t pk[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+          pk[c] = pack_bf16(__uint_as_float(o[2 * c]) * inv_l, __uint_as_float(o[2 * c + 1]) * inv_l);
+        if (tok < p.N) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            *reinterpret_cast<uint4*>(orow + c0 + 8 * u) = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        }
+      }
+      if (tok < p.N) p.lse[(int64_t)bh * p.N + tok] = (m + log2f(l)) * 0.69314718055994530942f;
+      if (row == 0 && p.counter) atomicAdd(p.counter, (unsigned long long)n);
+      ++it;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tbase, 256);
+}
+
+// ---------------------------------------------------------------------------------------
 // K4 variant 2 (SPA2_FWD_VARIANT=2, experimental; slower than variant 1 at the bench shape
 // because each softmax group has a single S buffer): persistent forward, one CTA per SM walking query blocks head-major,
 // longest first.  Q_i is staged by TMA and copied into TMEM (tcgen05.cp), so S = Q K_jᵀ is
@@ -698,7 +993,7 @@ __global__ void __launch_bounds__(kFwd2Threads, 1)
 int fwd_variant() {
   static const int v = [] {
     const char* e = getenv("SPA2_FWD_VARIANT");
-    return e != nullptr ? atoi(e) : 1;
+    return e != nullptr ? atoi(e) : 3;
   }();
   return v;
 }
@@ -773,6 +1068,21 @@ extern "C" int spa2_fwd(spa2_view q, spa2_view k, spa2_view v, spa2_view o, floa
   prm.trace_cap = g_trace_cap;
   const unsigned grid = (unsigned)(B * H * T_m);
   cudaStream_t st = (cudaStream_t)stream;
+  if (fwd_variant() == 3) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned pgrid = (unsigned)std::min<int64_t>(B * H * T_m, 2 * (int64_t)sms);
+    if (d == 128) {
+      SPA2_CUDA_TRY(cudaFuncSetAttribute(k_fwd3<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd3Cfg<128>::SMEM));
+      k_fwd3<128><<<pgrid, kFwdThreads, Fwd3Cfg<128>::SMEM, st>>>(tq, tk, tv, prm, (int)(B * H * T_m));
+    } else {
+      SPA2_CUDA_TRY(cudaFuncSetAttribute(k_fwd3<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd3Cfg<64>::SMEM));
+      k_fwd3<64><<<pgrid, kFwdThreads, Fwd3Cfg<64>::SMEM, st>>>(tq, tk, tv, prm, (int)(B * H * T_m));
+    }
+    SPA2_LAUNCH_CHECK();
+    return SPA2_OK;
+  }
   if (fwd_variant() == 2) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);

@@ -289,29 +289,35 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const double* __restrict
   extern __shared__ __align__(16) unsigned char smem_raw[];  // [p row (FROM_SCORES)] cand_v[T_pad], cand_c[T_pad]
   __shared__ int h_cnt[kBuckets];
   __shared__ int s_neg, s_bstar, s_npos, s_kept;
-  __shared__ double s_m, s_s;
+  __shared__ double s_s;
   const int64_t row = blockIdx.x;
   const double* x = probs + row * (int64_t)T_n;
   if constexpr (FROM_SCORES) {
+    // max: any reduction order is exact; exponentials by all threads; the sum in
+    // k_softmax_rows' order (lane l adds j = l, l+32, ... sequentially, xor-butterfly).
     double* pr = reinterpret_cast<double*>(smem_raw);
-    if (threadIdx.x < 32) {
-      const int lane = threadIdx.x;
-      double m = -INFINITY;
-      for (int j = lane; j < T_n; j += 32) m = fmax(m, x[j]);
+    __shared__ double s_red[kSelThreads / 32];
+    double m = -INFINITY;
+    for (int j = threadIdx.x; j < T_n; j += blockDim.x) m = fmax(m, x[j]);
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    m = s_red[0];
+#pragma unroll
+    for (int w = 1; w < kSelThreads / 32; ++w) m = fmax(m, s_red[w]);
+    for (int j = threadIdx.x; j < T_n; j += blockDim.x) pr[j] = exp(x[j] - m);
+    __syncthreads();
+    if (threadIdx.x < 32) {
       double sum = 0.0;
-      for (int j = lane; j < T_n; j += 32) sum += exp(x[j] - m);
+      for (int j = threadIdx.x; j < T_n; j += 32) sum += pr[j];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-      if (lane == 0) {
-        s_m = m;
-        s_s = sum;
-      }
+      if (threadIdx.x == 0) s_s = sum;
     }
     __syncthreads();
-    const double m = s_m, sum = s_s;
-    for (int j = threadIdx.x; j < T_n; j += blockDim.x) pr[j] = exp(x[j] - m) / sum;
+    const double sum = s_s;
+    for (int j = threadIdx.x; j < T_n; j += blockDim.x) pr[j] = pr[j] / sum;
     __syncthreads();
     x = pr;
   }
