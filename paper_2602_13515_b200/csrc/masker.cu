@@ -94,6 +94,68 @@ __global__ void __launch_bounds__(256) k_pool(spa2_view q, spa2_view k, int H, i
 }
 
 // ---------------------------------------------------------------------------------------
+// K1a (bf16, default): the k_pool mapping (one thread per (block, 8 columns), rows added in
+// order into 8 float64 chains) with the row loads software-pipelined: the next 8 rows are in
+// flight while the current 8 are added, so twice the bytes are outstanding per thread.
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_pool_bf16_pipe(spa2_view q, spa2_view k, int H, int N, int d, int b_q,
+                                                        int b_kv, int T_m, int T_n, int64_t BH,
+                                                        double* __restrict__ qbar, double* __restrict__ kbar,
+                                                        int32_t* __restrict__ nonfinite) {
+  constexpr int U = 8;
+  const int cpr = d / 8;
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nq = BH * T_m * cpr, nk = BH * T_n * cpr;
+  uint32_t badbits = 0;
+  if (gid < nq + nk) {
+    const bool is_q = gid < nq;
+    const int64_t gl = is_q ? gid : gid - nq;
+    const int cg = (int)(gl % cpr);
+    const int64_t blk_g = gl / cpr;
+    const int nblk = is_q ? T_m : T_n;
+    const int64_t bh = blk_g / nblk;
+    const int blk = (int)(blk_g % nblk);
+    const int bsz = is_q ? b_q : b_kv;
+    const spa2_view vw = is_q ? q : k;
+    const int row0 = blk * bsz;
+    const int rows = min(bsz, N - row0);
+    const uint4* base = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(vw.ptr) +
+                                                       (bh / H) * vw.sb + (bh % H) * vw.sh + (int64_t)row0 * vw.sn +
+                                                       cg * 8);
+    const int64_t rs = vw.sn / 8;  // row stride in uint4
+    double acc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = 0.0;
+    uint4 cur[U], nxt[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) cur[u] = u < rows ? __ldg(base + u * rs) : make_uint4(0, 0, 0, 0);
+    for (int r0 = 0; r0 < rows; r0 += U) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        nxt[u] = (r0 + U + u < rows) ? __ldg(base + (int64_t)(r0 + U + u) * rs) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (r0 + u < rows) {
+          const uint32_t w[4] = {cur[u].x, cur[u].y, cur[u].z, cur[u].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            badbits |= ((w[e] & 0x7F80u) == 0x7F80u) | ((w[e] & 0x7F800000u) == 0x7F800000u);
+            acc[2 * e] += (double)__uint_as_float(w[e] << 16);
+            acc[2 * e + 1] += (double)__uint_as_float(w[e] & 0xFFFF0000u);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) cur[u] = nxt[u];
+    }
+    double* out = (is_q ? qbar : kbar) + blk_g * (int64_t)d + cg * 8;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) out[e] = acc[e] / (double)rows;
+  }
+  if (__any_sync(0xffffffffu, badbits != 0) && (threadIdx.x & 31) == 0 && nonfinite != nullptr) atomicOr(nonfinite, 1);
+}
+
+// ---------------------------------------------------------------------------------------
 // K1a (bf16 fast path): one CTA per (b, h, block).  The block's rows are streamed into
 // shared memory with coalesced 16-byte loads (all in flight at once), then thread c sums
 // column c over the rows strictly in order — numpy's add.reduceat order — in float64.
@@ -652,6 +714,12 @@ int launch_pool(spa2_view q, spa2_view k, int64_t B, int64_t H, int64_t N, int64
   SPA2_REQUIRE(threads < (1ll << 40), SPA2_ERR_UNSUPPORTED, "pooled_map: problem too large");
   const unsigned grid = (unsigned)ceil_div(threads, 256);
   if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    if (vec && d % 8 == 0 && !pool_smem_path()) {
+      k_pool_bf16_pipe<<<grid, 256, 0, st>>>(q, k, (int)H, (int)N, (int)d, (int)b_q, (int)b_kv, (int)T_m, (int)T_n, BH,
+                                             qbar, kbar, nonfinite);
+      SPA2_LAUNCH_CHECK();
+      return SPA2_OK;
+    }
     const size_t bytes = (size_t)std::max(b_q, b_kv) * d * 2;
     if (pool_smem_path() && vec && d % 8 == 0 && bytes <= (size_t)kPoolMaxBytes) {
       if (bytes > 48 * 1024)
