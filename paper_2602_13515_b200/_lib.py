@@ -16,7 +16,7 @@ import threading
 
 import torch
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libspa2.so")
+LIB_PATH = os.environ.get("SPA2_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libspa2.so")
 HEADER_PATH = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "spa2.h")
 
 SPA2_OK = 0

@@ -1093,6 +1093,9 @@ bool dq_variant2() {
 
 // Warp roles: 0 TMA (K, Q), 1 MMA, 2 .. 2+EWW-1 elementwise (EWW/4 warps per TMEM lane
 // quarter, 256/EWW columns each), then 4 epilogue warps, then TMA (V, dO).
+#ifndef SPA2_DKDV_POLY_PAIRS_DIV
+#define SPA2_DKDV_POLY_PAIRS_DIV 8
+#endif
 template <int EWW>
 struct DkvRoles {
   static constexpr int EPI0 = 2 + EWW;           // first epilogue warp
@@ -1125,6 +1128,7 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
   using R = DkvRoles<EWW>;
   constexpr int NS = C::NS;
   constexpr int EWT = 32 * EWW;  // elementwise threads
+  constexpr int kDkvPolyPairs = R::CPT / SPA2_DKDV_POLY_PAIRS_DIV;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* kv_full = bars;             // K/V of item `it` landed
@@ -1306,7 +1310,7 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
         for (int c = 0; c < CPT / 2; ++c) {
           const float2 x = __ffma2_rn(make_float2(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1])),
                                       make_float2(sl2, sl2), make_float2(-lse2, -lse2));
-          if (c < CPT / 8) {  // a quarter of the exponentials on the FMA pipe (exp2_poly2)
+          if (c < kDkvPolyPairs) {  // part of the exponentials on the FMA pipe (exp2_poly2)
             const float2 e = exp2_poly2(x);
             pv[2 * c] = e.x;
             pv[2 * c + 1] = e.y;
