@@ -1412,6 +1412,334 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
   if (warp == 1) tmem_dealloc(tbase, 512);
 }
 
+template <int HD>
+struct Dkv5Cfg {
+  static constexpr int NSL = 5;  // 32 KB operand slots: Q(g) -> slot 2g mod 5, dO(g) -> slot 2g+1 mod 5
+  static constexpr int KV_BYTES = BKV * HD * 2;
+  static constexpr int Q_BYTES = BQ * HD * 2;
+  static constexpr int PB = BQ * BKV * 2;
+  static constexpr int OFF_KV = 0;                         // [K | V] of the current item
+  static constexpr int OFF_SL = 2 * KV_BYTES;              // [NSL] Q / dO operand slots
+  static constexpr int OFF_PDS = OFF_SL + NSL * Q_BYTES;   // [P | dS] (single buffer)
+  static constexpr int OFF_BAR = OFF_PDS + 2 * PB;
+  static constexpr int NUM_BARS = 2 + 2 * NSL + 6 + 4 + 4;
+  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;
+  static constexpr uint32_t S_COL = 0, DP_COL = 128, ACC_COL = 256;
+};
+
+// K6 variant 5: the Q and dO tiles of a kept tile live in a 5-slot ring of 32 KB operand slots
+// (2.5 tiles in flight instead of 2 stages of [Q|dO]) and each slot is released by the MMA that
+// last reads it (dO after dV, Q after dK); P and dS share one smem buffer.
+template <int HD, int EWW>
+__global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
+    k_dkdv5(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+           const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO, const BwdParams p) {
+  using C = Dkv5Cfg<HD>;
+  using R = DkvRoles<EWW>;
+  constexpr int NSL = C::NSL;
+  constexpr int EWT = 32 * EWW;  // elementwise threads
+  constexpr int kDkvPolyPairs = R::CPT / SPA2_DKDV_POLY_PAIRS_DIV;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* kv_full = bars;             // K/V of item `it` landed
+  uint64_t* kv_empty = kv_full + 1;     // last S/dP MMA of item `it` done: K/V slot reusable
+  uint64_t* sl_full = kv_empty + 1;     // [NSL] operand slot holds operand u (Q(g): u=2g, dO(g): u=2g+1)
+  uint64_t* sl_empty = sl_full + NSL;   // [NSL] the MMA reading operand u is done
+  uint64_t* s_full = sl_empty + NSL;    // [2] S of tile g in TMEM buffer g&1
+  uint64_t* dp_full = s_full + 2;       // [2] dP of tile g
+  uint64_t* sdp_read = dp_full + 2;     // [2] S and dP of tile g read out of TMEM
+  uint64_t* p_full = sdp_read + 2;      // P of tile g in smem (single buffer)
+  uint64_t* ds_full = p_full + 1;       // dS of tile g in smem
+  uint64_t* p_free = ds_full + 1;       // dV MMA of tile g done
+  uint64_t* ds_free = p_free + 1;       // dK MMA of tile g done
+  uint64_t* acc_full = ds_free + 1;     // [2]
+  uint64_t* acc_empty = acc_full + 2;   // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = (int)warp_id(), lane = (int)lane_id();
+  if (threadIdx.x == 0) {
+    if (smem_u32(smem) & 1023u) __trap();
+    mbar_init(kv_full, 2);  // two producers: warp 0 (K, Q) and warp PROD2 (V, dO)
+    mbar_init(kv_empty, 1);
+    for (int s = 0; s < NSL; ++s) {
+      mbar_init(&sl_full[s], 1);
+      mbar_init(&sl_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&s_full[s], 1);
+      mbar_init(&dp_full[s], 1);
+      mbar_init(&sdp_read[s], EWT);
+      mbar_init(&acc_full[s], 1);
+      mbar_init(&acc_empty[s], 128);
+    }
+    mbar_init(p_full, EWT);
+    mbar_init(ds_full, EWT);
+    mbar_init(p_free, 1);
+    mbar_init(ds_free, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_holder, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_holder;
+
+  if (warp == 0 || warp == R::PROD2) {
+    // ---------------- TMA producers: warp 0 loads K and Q, warp PROD2 loads V and dO ----------------
+    // (requests issued by one warp are served one at a time; two issuing warps double the
+    // per-SM fill rate, tools/tma_rate.py)
+    if (elect_one()) {
+      const bool second = warp == R::PROD2;
+      const CUtensorMap* tmKV = second ? &tmV : &tmK;
+      const CUtensorMap* tmR = second ? &tmDO : &tmQ;
+      tma_prefetch(tmKV);
+      tma_prefetch(tmR);
+      uint8_t* const kv_dst = smem + C::OFF_KV + (second ? C::KV_BYTES : 0);
+      int it = 0, g = 0;
+      for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
+        const Item m = get_item(p, wi, p.T_n);
+        if (m.n == 0) continue;
+        const int hh = m.bh % p.H, bb = m.bh / p.H;
+        if (it >= 1) mbar_wait(kv_empty, (uint32_t)(it - 1) & 1u);
+        mbar_expect_tx(kv_full, C::KV_BYTES);
+        tma_load_5d(kv_dst, tmKV, kv_full, 0, m.blk * BKV, 0, hh, bb);
+        for (int t = 0; t < m.n; ++t, ++g) {
+          const int i = p.idx[m.beg + t];
+          const int u = 2 * g + (second ? 1 : 0);  // operand index: Q(g) even, dO(g) odd
+          const int s = u % NSL;
+          if (!second) trace_ev(p.trace, p.trace_cap, 0, 1, g);
+          if (u >= NSL) mbar_wait(&sl_empty[s], ((uint32_t)(u / NSL) + 1u) & 1u);
+          if (!second) trace_ev(p.trace, p.trace_cap, 0, 2, g);
+          mbar_expect_tx(&sl_full[s], C::Q_BYTES);
+          tma_load_5d(smem + C::OFF_SL + s * C::Q_BYTES, tmR, &sl_full[s], 0, i * BQ, 0, hh, bb);
+        }
+        ++it;
+      }
+    }
+  } else if (warp == 1 || warp == R::ISSUE2) {
+    // ---------------- MMA issue: two warps, one per stream ----------------
+    // warp 1: S = Q_i K_jᵀ and dP = dO_i V_jᵀ of tile g into TMEM buffer g&1 (free once the
+    // elementwise warps have consumed tile g-2);  warp ISSUE2: dVᵀ += dO_iᵀ P (after P is in
+    // smem) then dKᵀ += Q_iᵀ dS (after dS).  Warp-collective issue, warp-uniform descriptors.
+    constexpr uint32_t idS = idesc_bf16(BQ, BKV, false, false);
+    constexpr uint32_t idT = idesc_bf16(HD, BKV, true, true);
+    const uint64_t dK = sw128_desc(smem_u32(smem + C::OFF_KV), 16, 1024);
+    const uint64_t dV = dK + (uint64_t)(C::KV_BYTES >> 4);
+    const uint64_t dSLk0 = sw128_desc(smem_u32(smem + C::OFF_SL), 16, 1024);        // K-major Q / dO slots
+    const uint64_t dSLm0 = sw128_desc(smem_u32(smem + C::OFF_SL), BQ * 128, 1024);  // MN-major Q / dO slots
+    const uint64_t dPm = sw128_desc(smem_u32(smem + C::OFF_PDS), BQ * 128, 1024);   // MN-major P
+    constexpr uint64_t SLOT16 = (uint64_t)(C::Q_BYTES >> 4), PB16 = (uint64_t)(C::PB >> 4);
+    const uint64_t dDSm = dPm + PB16;                                                // MN-major dS
+    Cursor c;
+    cursor_init(c, p, p.T_n);
+    if (warp == 1) {
+      // S (needs Q) and dP (needs dO) of tile g into TMEM buffer g&1, each as soon as its
+      // operand has landed (Q and dO live in separate ring slots)
+      for (; c.valid; cursor_next(c, p, p.T_n)) {
+        if (c.t == 0) mbar_wait(kv_full, (uint32_t)c.it & 1u);
+        const uint32_t b = (uint32_t)(c.g & 1);
+        if (c.g >= 2) mbar_wait(&sdp_read[b], (uint32_t)((c.g - 2) >> 1) & 1u);  // buffer b read out
+        const int uq = 2 * c.g, ud = uq + 1;
+        mbar_wait(&sl_full[uq % NSL], (uint32_t)(uq / NSL) & 1u);
+        tc_fence_after();
+        trace_ev(p.trace, p.trace_cap, 1, 2, c.g);
+        const uint64_t dQ = dSLk0 + (uint64_t)(uq % NSL) * SLOT16, dDO = dSLk0 + (uint64_t)(ud % NSL) * SLOT16;
+#pragma unroll
+        for (int ks = 0; ks < HD / 16; ++ks) {
+          const uint64_t qo = (uint64_t)(((ks * 16 / 64) * BQ * 128 + (ks * 16 % 64) * 2) >> 4);
+          const uint64_t ko = (uint64_t)(((ks * 16 / 64) * BKV * 128 + (ks * 16 % 64) * 2) >> 4);
+          mma_bf16_w(tbase + C::S_COL + b * 64, dQ + qo, dK + ko, idS, ks > 0 ? 1u : 0u);
+        }
+        mma_commit_w(&s_full[b]);
+        mbar_wait(&sl_full[ud % NSL], (uint32_t)(ud / NSL) & 1u);
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < HD / 16; ++ks) {
+          const uint64_t qo = (uint64_t)(((ks * 16 / 64) * BQ * 128 + (ks * 16 % 64) * 2) >> 4);
+          const uint64_t ko = (uint64_t)(((ks * 16 / 64) * BKV * 128 + (ks * 16 % 64) * 2) >> 4);
+          mma_bf16_w(tbase + C::DP_COL + b * 64, dDO + qo, dV + ko, idS, ks > 0 ? 1u : 0u);
+        }
+        mma_commit_w(&dp_full[b]);
+        if (c.t == c.n - 1) mma_commit_w(kv_empty);  // K_j / V_j are only read by S and dP
+      }
+    } else {
+      for (; c.valid; cursor_next(c, p, p.T_n)) {
+        const int uq = 2 * c.g, ud = uq + 1;
+        const uint32_t acc = tbase + C::ACC_COL + (uint32_t)((c.it & 1) * 128);
+        const uint64_t dQm = dSLm0 + (uint64_t)(uq % NSL) * SLOT16, dDOm = dSLm0 + (uint64_t)(ud % NSL) * SLOT16;
+        const bool first = c.t == 0;
+        if (first && c.it >= 2) mbar_wait(&acc_empty[c.it & 1], ((uint32_t)(c.it >> 1) + 1u) & 1u);
+        mbar_wait(p_full, (uint32_t)c.g & 1u);
+        tc_fence_after();
+        trace_ev(p.trace, p.trace_cap, 1, 4, c.g);
+#pragma unroll
+        for (int ks = 0; ks < BQ / 16; ++ks)
+          mma_bf16_w(acc, dDOm + (uint64_t)(ks * 128), dPm + (uint64_t)(ks * 128), idT, (!first || ks > 0) ? 1u : 0u);
+        mma_commit_w(p_free);
+        mma_commit_w(&sl_empty[ud % NSL]);  // dO(g) is no longer read
+        mbar_wait(ds_full, (uint32_t)c.g & 1u);
+        tc_fence_after();
+        trace_ev(p.trace, p.trace_cap, 1, 5, c.g);
+#pragma unroll
+        for (int ks = 0; ks < BQ / 16; ++ks)
+          mma_bf16_w(acc + 64, dQm + (uint64_t)(ks * 128), dDSm + (uint64_t)(ks * 128), idT, (!first || ks > 0) ? 1u : 0u);
+        mma_commit_w(ds_free);
+        mma_commit_w(&sl_empty[uq % NSL]);  // Q(g) is no longer read
+        if (c.t == c.n - 1) mma_commit_w(&acc_full[c.it & 1]);
+      }
+    }
+  } else if (warp < R::EPI0) {
+    // ---------------- P / dS warps: EWW/4 warps per TMEM lane quarter, CPT columns each ----
+    constexpr int CPT = R::CPT;
+    const int q4 = warp & 3;
+    const int grp = (warp - 2) >> 2;
+    const int row = q4 * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    const uint32_t col0 = (uint32_t)(CPT * grp);
+    const float sl2 = p.sl2;
+    const bool tr = threadIdx.x == 64;
+    int g = 0;
+    for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
+      const Item m = get_item(p, wi, p.T_n);
+      if (m.n == 0) continue;
+      const int64_t rowbase = (int64_t)m.bh * p.N;
+      auto load_stats = [&](int t, float& lse2, float& dlt) {
+        const int tok = p.idx[m.beg + t] * BQ + row;
+        const bool valid = tok < p.N;
+        lse2 = valid ? __ldg(p.lse + rowbase + tok) * kLog2e : INFINITY;
+        dlt = valid ? __ldg(p.delta + rowbase + tok) : 0.f;
+      };
+      float lse2, dlt;
+      load_stats(0, lse2, dlt);
+      for (int t = 0; t < m.n; ++t, ++g) {
+        const uint32_t b = (uint32_t)(g & 1);
+        float lse2_n = 0.f, dlt_n = 0.f;
+        if (t + 1 < m.n) load_stats(t + 1, lse2_n, dlt_n);  // prefetch the next tile's row statistics
+        if (tr) trace_ev(p.trace, p.trace_cap, 2, 1, g);
+        mbar_wait(&s_full[b], (uint32_t)(g >> 1) & 1u);
+        if (tr) trace_ev(p.trace, p.trace_cap, 2, 2, g);
+        tc_fence_after();
+        uint32_t sr[CPT];
+        if constexpr (CPT == 32) tmem_ld32(tbase + lane_off + C::S_COL + b * 64 + col0, sr);
+        else tmem_ld16(tbase + lane_off + C::S_COL + b * 64 + col0, sr);
+        float pv[CPT];
+        uint32_t pk[CPT / 2];
+#pragma unroll
+        for (int c = 0; c < CPT / 2; ++c) {
+          const float2 x = __ffma2_rn(make_float2(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1])),
+                                      make_float2(sl2, sl2), make_float2(-lse2, -lse2));
+          if (c < kDkvPolyPairs) {  // part of the exponentials on the FMA pipe (exp2_poly2)
+            const float2 e = exp2_poly2(x);
+            pv[2 * c] = e.x;
+            pv[2 * c + 1] = e.y;
+          } else {
+            pv[2 * c] = ex2(x.x);
+            pv[2 * c + 1] = ex2(x.y);
+          }
+          pk[c] = pack_bf16(pv[2 * c], pv[2 * c + 1]);
+        }
+        if (g >= 1) mbar_wait(p_free, (uint32_t)(g - 1) & 1u);  // dV of tile g-1 has read P
+        if (tr) trace_ev(p.trace, p.trace_cap, 2, 3, g);
+        const uint32_t sP = smem_u32(smem + C::OFF_PDS), sDS = sP + C::PB;
+#pragma unroll
+        for (int u = 0; u < CPT / 8; ++u) {
+          const uint32_t off = sw128_offset((uint32_t)row, col0 / 8 + (uint32_t)u);
+          st_shared_v4(sP + off, pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(p_full);
+        if (tr) trace_ev(p.trace, p.trace_cap, 2, 5, g);
+        mbar_wait(&dp_full[b], (uint32_t)(g >> 1) & 1u);
+        tc_fence_after();
+        uint32_t dr[CPT];
+        if constexpr (CPT == 32) tmem_ld32(tbase + lane_off + C::DP_COL + b * 64 + col0, dr);
+        else tmem_ld16(tbase + lane_off + C::DP_COL + b * 64 + col0, dr);
+        tc_fence_before();
+        mbar_arrive(&sdp_read[b]);  // S(g) and dP(g) are in registers: TMEM buffer b is free
+#pragma unroll
+        for (int c = 0; c < CPT / 2; ++c) {
+          const float2 ds = __fmul2_rn(make_float2(pv[2 * c], pv[2 * c + 1]),
+                                       __fadd2_rn(make_float2(__uint_as_float(dr[2 * c]), __uint_as_float(dr[2 * c + 1])),
+                                                  make_float2(-dlt, -dlt)));
+          pk[c] = pack_bf16(ds.x, ds.y);
+        }
+        if (g >= 1) mbar_wait(ds_free, (uint32_t)(g - 1) & 1u);  // dK of tile g-1 has read dS
+#pragma unroll
+        for (int u = 0; u < CPT / 8; ++u) {
+          const uint32_t off = sw128_offset((uint32_t)row, col0 / 8 + (uint32_t)u);
+          st_shared_v4(sDS + off, pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(ds_full);
+        if (tr) trace_ev(p.trace, p.trace_cap, 2, 4, g);
+        lse2 = lse2_n;
+        dlt = dlt_n;
+      }
+    }
+  } else if (warp < R::PROD2) {
+    // ---------------- epilogue warps: TMEM -> registers -> coalesced global stores ----
+    const int q4 = warp & 3;
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    const int dim = (HD == 128) ? q4 * 32 + lane : 16 * q4 + lane;  // M=64 accumulators: lanes 0-15 per quarter
+    const bool own = (HD == 128) || lane < 16;
+    const bool tr = threadIdx.x == 32 * R::EPI0;
+    int it = 0;
+    for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
+      const Item m = get_item(p, wi, p.T_n);
+      const int hh = m.bh % p.H, bb = m.bh / p.H;
+      __nv_bfloat16* dk = p.out0 + bb * p.o0_sb + hh * p.o0_sh + (int64_t)m.blk * BKV * p.o0_sn + dim;
+      __nv_bfloat16* dv = p.out1 + bb * p.o1_sb + hh * p.o1_sh + (int64_t)m.blk * BKV * p.o1_sn + dim;
+      const int rows = min(BKV, p.N - m.blk * BKV);
+      if (m.n == 0) {
+        // no query block keeps this key block: its dK and dV rows are exactly zero
+        if (own)
+          for (int r = 0; r < rows; ++r) {
+            dk[(int64_t)r * p.o0_sn] = __float2bfloat16(0.f);
+            dv[(int64_t)r * p.o1_sn] = __float2bfloat16(0.f);
+          }
+        continue;
+      }
+      const int st = it & 1;
+      if (tr) trace_ev(p.trace, p.trace_cap, 3, 1, it);
+      mbar_wait(&acc_full[st], (uint32_t)(it >> 1) & 1u);
+      if (tr) trace_ev(p.trace, p.trace_cap, 3, 2, it);
+      tc_fence_after();
+#pragma unroll 1
+      for (int part = 0; part < 4; ++part) {  // dV rows 0-31, 32-63, then dK rows 0-31, 32-63
+        uint32_t r32[32];
+        tmem_ld32(tbase + lane_off + C::ACC_COL + (uint32_t)(st * 128 + part * 32), r32);
+        if (part == 3) {
+          tc_fence_before();
+          mbar_arrive(&acc_empty[st]);  // both accumulators read: TMEM set reusable
+        }
+        const bool is_k = part >= 2;
+        __nv_bfloat16* dst = (is_k ? dk : dv) + (int64_t)((part & 1) * 32) * (is_k ? p.o0_sn : p.o1_sn);
+        const int64_t sn = is_k ? p.o0_sn : p.o1_sn;
+        const float mul = is_k ? p.scale : 1.f;
+        const int rr = rows - (part & 1) * 32;
+        if (own) {
+#pragma unroll
+          for (int r = 0; r < 32; ++r)
+            if (r < rr) dst[(int64_t)r * sn] = __float2bfloat16(__uint_as_float(r32[r]) * mul);
+        }
+      }
+      if (tr) trace_ev(p.trace, p.trace_cap, 3, 3, it);
+      ++it;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tbase, 512);
+}
+
+int dkdv_variant() {
+  static const int v = [] {
+    const char* e = getenv("SPA2_DKDV_VARIANT");
+    return e != nullptr ? atoi(e) : 5;
+  }();
+  return v;
+}
+
 int dkdv_ew_warps() {
   static const int v = [] {
     const char* e = getenv("SPA2_DKDV_EW");
@@ -1511,7 +1839,11 @@ int launch_attn_bwd(int which, const spa2_view& q, const spa2_view& k, const spa
   } else {
     prm.out1 = (__nv_bfloat16*)out1->ptr;
     prm.o1_sb = out1->sb, prm.o1_sh = out1->sh, prm.o1_sn = out1->sn;
-    if (dkdv_ew_warps() == 16) {
+    if (dkdv_variant() == 5) {
+      auto kern = k_dkdv5<HD, 8>;
+      SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Dkv5Cfg<HD>::SMEM));
+      kern<<<grid, DkvRoles<8>::THREADS, Dkv5Cfg<HD>::SMEM, st>>>(m.q, m.k, m.v, m.dout, prm);
+    } else if (dkdv_ew_warps() == 16) {
       auto kern = k_dkdv<HD, 16>;
       SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvCfg<HD>::SMEM));
       kern<<<grid, DkvRoles<16>::THREADS, DkvCfg<HD>::SMEM, st>>>(m.q, m.k, m.v, m.dout, prm);
