@@ -1743,7 +1743,7 @@ int dkdv_variant() {
 int dkdv_ew_warps() {
   static const int v = [] {
     const char* e = getenv("SPA2_DKDV_EW");
-    return (e != nullptr && e[0] == '1' && e[1] == '6') ? 16 : 8;
+    return (e != nullptr && atoi(e) == 8) ? 8 : 16;
   }();
   return v;
 }
@@ -1839,7 +1839,11 @@ int launch_attn_bwd(int which, const spa2_view& q, const spa2_view& k, const spa
   } else {
     prm.out1 = (__nv_bfloat16*)out1->ptr;
     prm.o1_sb = out1->sb, prm.o1_sh = out1->sh, prm.o1_sn = out1->sn;
-    if (dkdv_variant() == 5) {
+    if (dkdv_variant() == 5 && dkdv_ew_warps() == 16) {
+      auto kern = k_dkdv5<HD, 16>;
+      SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Dkv5Cfg<HD>::SMEM));
+      kern<<<grid, DkvRoles<16>::THREADS, Dkv5Cfg<HD>::SMEM, st>>>(m.q, m.k, m.v, m.dout, prm);
+    } else if (dkdv_variant() == 5) {
       auto kern = k_dkdv5<HD, 8>;
       SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Dkv5Cfg<HD>::SMEM));
       kern<<<grid, DkvRoles<8>::THREADS, Dkv5Cfg<HD>::SMEM, st>>>(m.q, m.k, m.v, m.dout, prm);

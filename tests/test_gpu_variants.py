@@ -6,7 +6,7 @@ case runs a small fwd + bwd parity check in a fresh interpreter:
   SPA2_DQ_VARIANT=3|2|1      dQ: Q/dO in TMEM (3) | one query block per CTA (2) | persistent SS (1)
   SPA2_NO_FUSED_DELTA=1      δ by its own kernel instead of inside the dQ kernel
   SPA2_DKDV_VARIANT=5|1      dK/dV: 5-slot Q/dO operand ring | two [Q|dO] stages
-  SPA2_DQ_EW=8, SPA2_DKDV_EW=16   elementwise warp counts
+  SPA2_DQ_EW=8, SPA2_DKDV_EW=8|16 elementwise warp counts (defaults 16, 16)
 Checked against the float64 oracle at two ragged shapes (d = 64 and 128)."""
 
 import os
@@ -50,7 +50,8 @@ VARIANTS = [
     {"SPA2_DQ_VARIANT": "1"},
     {"SPA2_NO_FUSED_DELTA": "1"},
     {"SPA2_DKDV_VARIANT": "1"},
-    {"SPA2_DQ_EW": "8", "SPA2_DKDV_EW": "16"},
+    {"SPA2_DQ_EW": "8", "SPA2_DKDV_EW": "8"},
+    {"SPA2_DKDV_VARIANT": "1", "SPA2_DKDV_EW": "16"},
 ]
 
 
