@@ -15,7 +15,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 KEYMAP = {"k_fwd": "spa2_fwd", "k_fwd3": "spa2_fwd", "k_dq": "spa2_bwd_dq", "k_dq3": "spa2_bwd_dq_delta",
-          "k_dq2": "spa2_bwd_dq", "k_pool_bf16_pipe": "spa2_pooled_scores:pool", "k_select": "spa2_select_scores", "k_dkdv": "spa2_bwd_dkdv", "k_delta": "spa2_bwd_delta",
+          "k_dq2": "spa2_bwd_dq", "k_pool_bf16_pipe": "spa2_pooled_scores:pool", "k_select": "spa2_select_scores", "k_dkdv": "spa2_bwd_dkdv", "k_dkdv5": "spa2_bwd_dkdv", "k_delta": "spa2_bwd_delta",
           "k_pool": "spa2_pooled_map:pool", "k_scores": "spa2_pooled_map:scores",
           "k_softmax_rows": "spa2_pooled_map:softmax", "k_select": "spa2_select"}
 METRICS = {
