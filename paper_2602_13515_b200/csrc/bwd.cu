@@ -793,6 +793,8 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_holder;
+  pdl_wait();  // everything above touched only this CTA's smem/TMEM
+  pdl_trigger();
 
   if (warp == 0 || warp == R::PROD2) {
     // ---------------- TMA producers: warp 0 Q + K ring, warp 14 dO + V ring ----------------
@@ -1483,6 +1485,8 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_holder;
+  pdl_wait();  // everything above touched only this CTA's smem/TMEM
+  pdl_trigger();
 
   if (warp == 0 || warp == R::PROD2) {
     // ---------------- TMA producers: warp 0 loads K and Q, warp PROD2 loads V and dO ----------------
@@ -1822,11 +1826,13 @@ int launch_attn_bwd(int which, const spa2_view& q, const spa2_view& k, const spa
     if (dq_ew_warps() == 16) {
       auto kern = k_dq3<HD, 16>;
       SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Dq3Cfg<HD>::SMEM));
-      kern<<<grid, Dq3Roles<16>::THREADS, Dq3Cfg<HD>::SMEM, st>>>(m.q, m.k, m.v, m.dout, prm);
+      SPA2_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(Dq3Roles<16>::THREADS), Dq3Cfg<HD>::SMEM, st, m.q, m.k, m.v, m.dout,
+                               prm));
     } else {
       auto kern = k_dq3<HD, 8>;
       SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Dq3Cfg<HD>::SMEM));
-      kern<<<grid, Dq3Roles<8>::THREADS, Dq3Cfg<HD>::SMEM, st>>>(m.q, m.k, m.v, m.dout, prm);
+      SPA2_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(Dq3Roles<8>::THREADS), Dq3Cfg<HD>::SMEM, st, m.q, m.k, m.v, m.dout,
+                               prm));
     }
   } else if (which == 0 && dq_variant2()) {
     auto kern = k_dq2<HD>;
@@ -1842,11 +1848,13 @@ int launch_attn_bwd(int which, const spa2_view& q, const spa2_view& k, const spa
     if (dkdv_variant() == 5 && dkdv_ew_warps() == 16) {
       auto kern = k_dkdv5<HD, 16>;
       SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Dkv5Cfg<HD>::SMEM));
-      kern<<<grid, DkvRoles<16>::THREADS, Dkv5Cfg<HD>::SMEM, st>>>(m.q, m.k, m.v, m.dout, prm);
+      SPA2_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(DkvRoles<16>::THREADS), Dkv5Cfg<HD>::SMEM, st, m.q, m.k, m.v, m.dout,
+                               prm));
     } else if (dkdv_variant() == 5) {
       auto kern = k_dkdv5<HD, 8>;
       SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Dkv5Cfg<HD>::SMEM));
-      kern<<<grid, DkvRoles<8>::THREADS, Dkv5Cfg<HD>::SMEM, st>>>(m.q, m.k, m.v, m.dout, prm);
+      SPA2_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(DkvRoles<8>::THREADS), Dkv5Cfg<HD>::SMEM, st, m.q, m.k, m.v, m.dout,
+                               prm));
     } else if (dkdv_ew_warps() == 16) {
       auto kern = k_dkdv<HD, 16>;
       SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, DkvCfg<HD>::SMEM));

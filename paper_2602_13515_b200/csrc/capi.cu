@@ -1,3 +1,4 @@
+#include <stdlib.h>
 // capi.cu — library-wide C-ABI entry points: version, thread-local error, device check,
 // and the host-side TMA descriptor encoder shared by the attention launchers.
 #include <cudaTypedefs.h>
@@ -13,6 +14,13 @@ namespace spa2 {
 
 static thread_local char g_last_error[1024] = "";
 unsigned long long* g_trace_buf = nullptr;
+bool pdl_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("SPA2_PDL");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  return v;
+}
 int g_trace_cap = 0;
 
 void set_error(const char* fmt, ...) {

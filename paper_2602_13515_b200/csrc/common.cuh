@@ -59,6 +59,33 @@ __device__ __forceinline__ void trace_ev(unsigned long long* buf, int cap, int r
   const int slot = idx * 8 + kind;
   if (slot < cap / 4) buf[2 + role * (cap / 4) + slot] = clock64();
 }
+// ---- programmatic dependent launch (PDL) ---------------------------------------------
+// Hot-path kernels are launched with programmatic stream serialization: the next kernel's
+// CTAs may be scheduled (and run their prologue: barrier init, TMEM alloc, descriptor
+// prefetch) while this one drains; pdl_wait() blocks until the previous grid has completed
+// and its writes are visible, so it must precede every global-memory access.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+namespace spa2 {
+bool pdl_enabled();
+// kernel<<<grid, block, smem, stream>>>(args...) with the PDL launch attribute when enabled.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+}  // namespace spa2
+
 namespace spa2 {
 extern unsigned long long* g_trace_buf;
 extern int g_trace_cap;

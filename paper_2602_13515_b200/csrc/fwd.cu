@@ -423,6 +423,8 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_holder;
+  pdl_wait();  // everything above touched only this CTA's smem/TMEM
+  pdl_trigger();
 
   if (warp == 0 || warp == 6) {
     // ---------------- TMA producers: warp 0 Q + K ring, warp 6 V ring ----------------
@@ -1075,10 +1077,12 @@ extern "C" int spa2_fwd(spa2_view q, spa2_view k, spa2_view v, spa2_view o, floa
     const unsigned pgrid = (unsigned)std::min<int64_t>(B * H * T_m, 2 * (int64_t)sms);
     if (d == 128) {
       SPA2_CUDA_TRY(cudaFuncSetAttribute(k_fwd3<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd3Cfg<128>::SMEM));
-      k_fwd3<128><<<pgrid, kFwdThreads, Fwd3Cfg<128>::SMEM, st>>>(tq, tk, tv, prm, (int)(B * H * T_m));
+      SPA2_CUDA_TRY(launch_pdl(k_fwd3<128>, dim3(pgrid), dim3(kFwdThreads), Fwd3Cfg<128>::SMEM, st, tq, tk, tv, prm,
+                               (int)(B * H * T_m)));
     } else {
       SPA2_CUDA_TRY(cudaFuncSetAttribute(k_fwd3<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd3Cfg<64>::SMEM));
-      k_fwd3<64><<<pgrid, kFwdThreads, Fwd3Cfg<64>::SMEM, st>>>(tq, tk, tv, prm, (int)(B * H * T_m));
+      SPA2_CUDA_TRY(launch_pdl(k_fwd3<64>, dim3(pgrid), dim3(kFwdThreads), Fwd3Cfg<64>::SMEM, st, tq, tk, tv, prm,
+                               (int)(B * H * T_m)));
     }
     SPA2_LAUNCH_CHECK();
     return SPA2_OK;

@@ -102,6 +102,8 @@ __global__ void __launch_bounds__(256) k_pool_bf16_pipe(spa2_view q, spa2_view k
                                                         int b_kv, int T_m, int T_n, int64_t BH,
                                                         double* __restrict__ qbar, double* __restrict__ kbar,
                                                         int32_t* __restrict__ nonfinite) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int U = 8;
   const int cpr = d / 8;
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -220,6 +222,8 @@ __device__ __forceinline__ void cp_async_f64(double* dst, const double* src, boo
 __global__ void __launch_bounds__(256, 3) k_scores(const double* __restrict__ qbar,
                                                    const double* __restrict__ kbar, int T_m, int T_n,
                                                    int d, double sqrt_d, double* __restrict__ s_out) {
+  pdl_wait();
+  pdl_trigger();
   // two k-chunk buffers: chunk c+1 streams in (cp.async) while chunk c is multiplied
   extern __shared__ double sc_smem[];  // [2][sq 64 x 33 | sk 64 x 33]
   const int64_t bh = blockIdx.z;
@@ -348,6 +352,8 @@ template <bool FROM_SCORES>
 __global__ void __launch_bounds__(kSelThreads) k_select(const double* __restrict__ probs, int T_n, int k_count,
                                                         double thr, int use_p, uint8_t* __restrict__ keep,
                                                         int32_t* __restrict__ counts) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) unsigned char smem_raw[];  // [p row (FROM_SCORES)] cand_v[T_pad], cand_c[T_pad]
   __shared__ int h_cnt[kBuckets];
   __shared__ int s_neg, s_bstar, s_npos, s_kept;
@@ -574,6 +580,8 @@ __device__ void cta_order_desc(const int32_t* cnt, int64_t n, int maxc, int32_t*
 __global__ void __launch_bounds__(kColWarps * 32) k_counts(const uint8_t* __restrict__ keep, int T_m, int T_n,
                                                            int col_chunks, int32_t* __restrict__ row_cnt,
                                                            int32_t* __restrict__ col_cnt) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t bh = blockIdx.y;
   const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
   if ((int)blockIdx.x < col_chunks) {
@@ -614,6 +622,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_orders(const int32_t* __r
                                                               const int32_t* __restrict__ col_cnt, int T_m, int T_n,
                                                               int64_t bh_total, int32_t* row_ptr, int32_t* col_ptr,
                                                               int32_t* row_order, int32_t* col_order) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ int32_t sh_ord[];  // [kScanThreads] + bins[max(T_m,T_n)+1]
   int32_t* bins = sh_ord + kScanThreads;
   __shared__ int32_t s_base;
@@ -656,6 +666,8 @@ __global__ void __launch_bounds__(kColWarps * 32) k_fill(const uint8_t* __restri
                                                          int32_t* __restrict__ row_idx,
                                                          const int32_t* __restrict__ col_ptr,
                                                          int32_t* __restrict__ col_idx) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t bh = blockIdx.y;
   const int w = threadIdx.x / 32, lane = threadIdx.x % 32;
   if ((int)blockIdx.x < col_chunks) {
@@ -715,8 +727,8 @@ int launch_pool(spa2_view q, spa2_view k, int64_t B, int64_t H, int64_t N, int64
   const unsigned grid = (unsigned)ceil_div(threads, 256);
   if constexpr (std::is_same<T, __nv_bfloat16>::value) {
     if (vec && d % 8 == 0 && !pool_smem_path()) {
-      k_pool_bf16_pipe<<<grid, 256, 0, st>>>(q, k, (int)H, (int)N, (int)d, (int)b_q, (int)b_kv, (int)T_m, (int)T_n, BH,
-                                             qbar, kbar, nonfinite);
+      SPA2_CUDA_TRY(launch_pdl(k_pool_bf16_pipe, dim3(grid), dim3(256), 0, st, q, k, (int)H, (int)N, (int)d, (int)b_q,
+                               (int)b_kv, (int)T_m, (int)T_n, BH, qbar, kbar, nonfinite));
       SPA2_LAUNCH_CHECK();
       return SPA2_OK;
     }
@@ -770,7 +782,8 @@ static int pooled_map_impl(spa2_view q, spa2_view k, int dtype, int64_t B, int64
   if (rc != SPA2_OK) return rc;
   dim3 grid((unsigned)ceil_div(T_n, kSTJ), (unsigned)ceil_div(T_m, kSTI), (unsigned)BH);
   SPA2_CUDA_TRY(cudaFuncSetAttribute(k_scores, cudaFuncAttributeMaxDynamicSharedMemorySize, kScoresSmem));
-  k_scores<<<grid, 256, kScoresSmem, st>>>(qbar, kbar, (int)T_m, (int)T_n, (int)d, sqrt((double)d), probs);
+  SPA2_CUDA_TRY(launch_pdl(k_scores, grid, dim3(256), kScoresSmem, st, qbar, kbar, (int)T_m, (int)T_n, (int)d,
+                           sqrt((double)d), probs));
   SPA2_LAUNCH_CHECK();
   if (!softmax) return SPA2_OK;
   const int64_t rows = BH * T_m;
@@ -831,7 +844,8 @@ extern "C" int spa2_select_scores(const double* scores, int64_t rows, int64_t t_
     SPA2_CUDA_TRY(cudaFuncSetAttribute(k_select<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int use_p = isinf(p_threshold) && p_threshold < 0 ? 0 : 1;
   const int kk = (int)std::min<int64_t>(k_count, t_n);
-  k_select<true><<<(unsigned)rows, kSelThreads, smem, st>>>(scores, (int)t_n, kk, p_threshold, use_p, keep, counts);
+  SPA2_CUDA_TRY(launch_pdl(k_select<true>, dim3((unsigned)rows), dim3(kSelThreads), smem, st, scores, (int)t_n, kk,
+                           p_threshold, use_p, keep, counts));
   SPA2_LAUNCH_CHECK();
   return SPA2_OK;
 }
@@ -852,15 +866,17 @@ extern "C" int spa2_build_lists(const uint8_t* keep, int64_t bh, int64_t t_m, in
   int32_t* row_cnt = scratch + ncols;  // [nrows]
   const int col_chunks = (int)ceil_div(t_n, 32);
   const dim3 grid((unsigned)(col_chunks + ceil_div(t_m, kColWarps)), (unsigned)bh);
-  k_counts<<<grid, kColWarps * 32, 0, st>>>(keep, (int)t_m, (int)t_n, col_chunks, row_cnt, col_cnt);
+  SPA2_CUDA_TRY(launch_pdl(k_counts, grid, dim3(kColWarps * 32), 0, st, keep, (int)t_m, (int)t_n, col_chunks, row_cnt,
+                           col_cnt));
   SPA2_LAUNCH_CHECK();
   const size_t smem = (kScanThreads + std::max(t_m, t_n) + 1) * sizeof(int32_t);
   if (smem > 48 * 1024)
     SPA2_CUDA_TRY(cudaFuncSetAttribute(k_scan_orders, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_scan_orders<<<dim3((unsigned)bh, 2), kScanThreads, smem, st>>>(row_cnt, col_cnt, (int)t_m, (int)t_n, bh, row_ptr, col_ptr,
-                                                          row_order, col_order);
+  SPA2_CUDA_TRY(launch_pdl(k_scan_orders, dim3((unsigned)bh, 2), dim3(kScanThreads), smem, st, row_cnt, col_cnt,
+                           (int)t_m, (int)t_n, bh, row_ptr, col_ptr, row_order, col_order));
   SPA2_LAUNCH_CHECK();
-  k_fill<<<grid, kColWarps * 32, 0, st>>>(keep, (int)t_m, (int)t_n, col_chunks, row_ptr, row_idx, col_ptr, col_idx);
+  SPA2_CUDA_TRY(launch_pdl(k_fill, grid, dim3(kColWarps * 32), 0, st, keep, (int)t_m, (int)t_n, col_chunks, row_ptr,
+                           row_idx, col_ptr, col_idx));
   SPA2_LAUNCH_CHECK();
   return SPA2_OK;
 }
