@@ -1414,17 +1414,18 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
   if (warp == 1) tmem_dealloc(tbase, 512);
 }
 
-template <int HD>
+template <int HD, int NSL_ = 5, int NPB_ = 1>
 struct Dkv5Cfg {
-  static constexpr int NSL = 5;  // 32 KB operand slots: Q(g) -> slot 2g mod 5, dO(g) -> slot 2g+1 mod 5
+  static constexpr int NSL = NSL_;  // 32 KB operand slots: Q(g) -> slot 2g mod NSL, dO(g) -> slot 2g+1 mod NSL
+  static constexpr int NPB = NPB_;  // [P | dS] buffers
   static constexpr int KV_BYTES = BKV * HD * 2;
   static constexpr int Q_BYTES = BQ * HD * 2;
   static constexpr int PB = BQ * BKV * 2;
   static constexpr int OFF_KV = 0;                         // [K | V] of the current item
   static constexpr int OFF_SL = 2 * KV_BYTES;              // [NSL] Q / dO operand slots
-  static constexpr int OFF_PDS = OFF_SL + NSL * Q_BYTES;   // [P | dS] (single buffer)
-  static constexpr int OFF_BAR = OFF_PDS + 2 * PB;
-  static constexpr int NUM_BARS = 2 + 2 * NSL + 6 + 4 + 4;
+  static constexpr int OFF_PDS = OFF_SL + NSL * Q_BYTES;   // [NPB][P | dS]
+  static constexpr int OFF_BAR = OFF_PDS + NPB * 2 * PB;
+  static constexpr int NUM_BARS = 2 + 2 * NSL + 6 + 4 * NPB + 4;
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr uint32_t S_COL = 0, DP_COL = 128, ACC_COL = 256;
 };
@@ -1432,13 +1433,14 @@ struct Dkv5Cfg {
 // K6 variant 5: the Q and dO tiles of a kept tile live in a 5-slot ring of 32 KB operand slots
 // (2.5 tiles in flight instead of 2 stages of [Q|dO]) and each slot is released by the MMA that
 // last reads it (dO after dV, Q after dK); P and dS share one smem buffer.
-template <int HD, int EWW>
+template <int HD, int EWW, int NSL_ = 5, int NPB_ = 1>
 __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
     k_dkdv5(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
            const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO, const BwdParams p) {
-  using C = Dkv5Cfg<HD>;
+  using C = Dkv5Cfg<HD, NSL_, NPB_>;
   using R = DkvRoles<EWW>;
   constexpr int NSL = C::NSL;
+  constexpr int NPB = C::NPB;
   constexpr int EWT = 32 * EWW;  // elementwise threads
   constexpr int kDkvPolyPairs = R::CPT / SPA2_DKDV_POLY_PAIRS_DIV;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -1450,11 +1452,11 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
   uint64_t* s_full = sl_empty + NSL;    // [2] S of tile g in TMEM buffer g&1
   uint64_t* dp_full = s_full + 2;       // [2] dP of tile g
   uint64_t* sdp_read = dp_full + 2;     // [2] S and dP of tile g read out of TMEM
-  uint64_t* p_full = sdp_read + 2;      // P of tile g in smem (single buffer)
-  uint64_t* ds_full = p_full + 1;       // dS of tile g in smem
-  uint64_t* p_free = ds_full + 1;       // dV MMA of tile g done
-  uint64_t* ds_free = p_free + 1;       // dK MMA of tile g done
-  uint64_t* acc_full = ds_free + 1;     // [2]
+  uint64_t* p_full = sdp_read + 2;      // [NPB] P of tile g in smem buffer g % NPB
+  uint64_t* ds_full = p_full + NPB;     // [NPB] dS of tile g in smem
+  uint64_t* p_free = ds_full + NPB;     // [NPB] dV MMA of tile g done
+  uint64_t* ds_free = p_free + NPB;     // [NPB] dK MMA of tile g done
+  uint64_t* acc_full = ds_free + NPB;   // [2]
   uint64_t* acc_empty = acc_full + 2;   // [2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
@@ -1474,10 +1476,12 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
       mbar_init(&acc_full[s], 1);
       mbar_init(&acc_empty[s], 128);
     }
-    mbar_init(p_full, EWT);
-    mbar_init(ds_full, EWT);
-    mbar_init(p_free, 1);
-    mbar_init(ds_free, 1);
+    for (int s = 0; s < NPB; ++s) {
+      mbar_init(&p_full[s], EWT);
+      mbar_init(&ds_full[s], EWT);
+      mbar_init(&p_free[s], 1);
+      mbar_init(&ds_free[s], 1);
+    }
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tmem_holder, 512);
@@ -1573,21 +1577,23 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
         const uint64_t dQm = dSLm0 + (uint64_t)(uq % NSL) * SLOT16, dDOm = dSLm0 + (uint64_t)(ud % NSL) * SLOT16;
         const bool first = c.t == 0;
         if (first && c.it >= 2) mbar_wait(&acc_empty[c.it & 1], ((uint32_t)(c.it >> 1) + 1u) & 1u);
-        mbar_wait(p_full, (uint32_t)c.g & 1u);
+        const int pb = c.g % NPB;
+        const uint64_t pbo = (uint64_t)pb * 2 * PB16;
+        mbar_wait(&p_full[pb], (uint32_t)(c.g / NPB) & 1u);
         tc_fence_after();
         trace_ev(p.trace, p.trace_cap, 1, 4, c.g);
 #pragma unroll
         for (int ks = 0; ks < BQ / 16; ++ks)
-          mma_bf16_w(acc, dDOm + (uint64_t)(ks * 128), dPm + (uint64_t)(ks * 128), idT, (!first || ks > 0) ? 1u : 0u);
-        mma_commit_w(p_free);
+          mma_bf16_w(acc, dDOm + (uint64_t)(ks * 128), dPm + pbo + (uint64_t)(ks * 128), idT, (!first || ks > 0) ? 1u : 0u);
+        mma_commit_w(&p_free[pb]);
         mma_commit_w(&sl_empty[ud % NSL]);  // dO(g) is no longer read
-        mbar_wait(ds_full, (uint32_t)c.g & 1u);
+        mbar_wait(&ds_full[pb], (uint32_t)(c.g / NPB) & 1u);
         tc_fence_after();
         trace_ev(p.trace, p.trace_cap, 1, 5, c.g);
 #pragma unroll
         for (int ks = 0; ks < BQ / 16; ++ks)
-          mma_bf16_w(acc + 64, dQm + (uint64_t)(ks * 128), dDSm + (uint64_t)(ks * 128), idT, (!first || ks > 0) ? 1u : 0u);
-        mma_commit_w(ds_free);
+          mma_bf16_w(acc + 64, dQm + (uint64_t)(ks * 128), dDSm + pbo + (uint64_t)(ks * 128), idT, (!first || ks > 0) ? 1u : 0u);
+        mma_commit_w(&ds_free[pb]);
         mma_commit_w(&sl_empty[uq % NSL]);  // Q(g) is no longer read
         if (c.t == c.n - 1) mma_commit_w(&acc_full[c.it & 1]);
       }
@@ -1642,16 +1648,17 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
           }
           pk[c] = pack_bf16(pv[2 * c], pv[2 * c + 1]);
         }
-        if (g >= 1) mbar_wait(p_free, (uint32_t)(g - 1) & 1u);  // dV of tile g-1 has read P
+        const int pb = g % NPB;
+        if (g >= NPB) mbar_wait(&p_free[pb], (uint32_t)((g - NPB) / NPB) & 1u);  // dV of tile g-NPB has read P
         if (tr) trace_ev(p.trace, p.trace_cap, 2, 3, g);
-        const uint32_t sP = smem_u32(smem + C::OFF_PDS), sDS = sP + C::PB;
+        const uint32_t sP = smem_u32(smem + C::OFF_PDS) + (uint32_t)(pb * 2 * C::PB), sDS = sP + C::PB;
 #pragma unroll
         for (int u = 0; u < CPT / 8; ++u) {
           const uint32_t off = sw128_offset((uint32_t)row, col0 / 8 + (uint32_t)u);
           st_shared_v4(sP + off, pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
         }
         fence_proxy_async_smem();
-        mbar_arrive(p_full);
+        mbar_arrive(&p_full[pb]);
         if (tr) trace_ev(p.trace, p.trace_cap, 2, 5, g);
         mbar_wait(&dp_full[b], (uint32_t)(g >> 1) & 1u);
         tc_fence_after();
@@ -1667,14 +1674,14 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
                                                   make_float2(-dlt, -dlt)));
           pk[c] = pack_bf16(ds.x, ds.y);
         }
-        if (g >= 1) mbar_wait(ds_free, (uint32_t)(g - 1) & 1u);  // dK of tile g-1 has read dS
+        if (g >= NPB) mbar_wait(&ds_free[pb], (uint32_t)((g - NPB) / NPB) & 1u);  // dK of tile g-NPB has read dS
 #pragma unroll
         for (int u = 0; u < CPT / 8; ++u) {
           const uint32_t off = sw128_offset((uint32_t)row, col0 / 8 + (uint32_t)u);
           st_shared_v4(sDS + off, pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
         }
         fence_proxy_async_smem();
-        mbar_arrive(ds_full);
+        mbar_arrive(&ds_full[pb]);
         if (tr) trace_ev(p.trace, p.trace_cap, 2, 4, g);
         lse2 = lse2_n;
         dlt = dlt_n;
@@ -1845,12 +1852,18 @@ int launch_attn_bwd(int which, const spa2_view& q, const spa2_view& k, const spa
   } else {
     prm.out1 = (__nv_bfloat16*)out1->ptr;
     prm.o1_sb = out1->sb, prm.o1_sh = out1->sh, prm.o1_sn = out1->sn;
-    if (dkdv_variant() == 5 && dkdv_ew_warps() == 16) {
+    if (dkdv_variant() == 6 && dkdv_ew_warps() == 16) {
+      using C6 = Dkv5Cfg<HD, 4, 2>;
+      auto kern = k_dkdv5<HD, 16, 4, 2>;
+      SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C6::SMEM));
+      SPA2_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(DkvRoles<16>::THREADS), C6::SMEM, st, m.q, m.k, m.v, m.dout,
+                               prm));
+    } else if (dkdv_variant() >= 5 && dkdv_ew_warps() == 16) {
       auto kern = k_dkdv5<HD, 16>;
       SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Dkv5Cfg<HD>::SMEM));
       SPA2_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(DkvRoles<16>::THREADS), Dkv5Cfg<HD>::SMEM, st, m.q, m.k, m.v, m.dout,
                                prm));
-    } else if (dkdv_variant() == 5) {
+    } else if (dkdv_variant() >= 5) {
       auto kern = k_dkdv5<HD, 8>;
       SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Dkv5Cfg<HD>::SMEM));
       SPA2_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(DkvRoles<8>::THREADS), Dkv5Cfg<HD>::SMEM, st, m.q, m.k, m.v, m.dout,
