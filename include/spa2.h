@@ -176,6 +176,9 @@ int spa2_probe_tma_rate(const void* buf, long long rows, int box_rows, int stage
  * [rows][128] bf16 matrix.  cycles[ctas*4] receives per-(CTA, issuer) cycle counts. */
 /* MMA mix probe (diagnostic): the dQ kernel's per-tile tcgen05 sequence in isolation; see probe.cu. */
 int spa2_probe_mma_mix(int reps, int flags, int ctas, const void* gsrc, unsigned long long* cycles, void* stream);
+/* Diagnostic: tcgen05.ld / tcgen05.st throughput (mode 0 32-col loads, 1 two loads per wait,
+ * 2 16-col loads, 3 16-col stores), `warps` warps per CTA (<= 16); cycles[ctas * 16] per warp. */
+int spa2_probe_tmem_rate(int reps, int mode, int warps, int ctas, unsigned long long* cycles, void* stream);
 int spa2_probe_tma_rate2(const void* buf, long long rows, int box_rows, int chunks, int stages, int issuers,
                          int mode, int iters, int ctas, unsigned long long* cycles, void* stream);
 

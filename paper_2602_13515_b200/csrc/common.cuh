@@ -69,6 +69,12 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 
 namespace spa2 {
 bool pdl_enabled();
+// Per-launch work counter for the persistent kernels' dynamic scheduling (ptx::item_sched):
+// int[2] from a device pool, rotated per launch; zero on entry, reset by the kernel on exit.
+// Returns nullptr on failure (error text set).
+int* sched_slot();
+// SPA2_DYNAMIC_SCHED=0 falls back to the static round-robin deal (A/B switch).
+bool dynamic_sched();
 // kernel<<<grid, block, smem, stream>>>(args...) with the PDL launch attribute when enabled.
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {

@@ -524,3 +524,71 @@ extern "C" int spa2_probe_tma_rate2(const void* buf, long long rows, int box_row
   SPA2_LAUNCH_CHECK();
   return SPA2_OK;
 }
+
+// ---- TMEM load/store rate probe (diagnostic): tcgen05.ld / tcgen05.st bytes per cycle per SM ----
+namespace spa2 {
+namespace {
+__global__ void __launch_bounds__(512, 1) k_tmem_rate(int reps, int mode, unsigned long long* cycles) {
+  __shared__ uint32_t holder;
+  const int warp = (int)warp_id();
+  if (warp == 0) tmem_alloc(&holder, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = holder;
+  const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+  const uint32_t col = (uint32_t)((warp >> 2) * 32) & 511u;
+  uint32_t acc = 0;
+  __syncthreads();
+  const uint64_t t0 = clock64();
+  if (mode == 0) {
+    for (int i = 0; i < reps; ++i) {
+      uint32_t r[32];
+      tmem_ld32(tbase + lane_off + ((col + (uint32_t)i * 64u) & 511u), r);
+#pragma unroll
+      for (int c = 0; c < 32; ++c) acc ^= r[c];
+    }
+  } else if (mode == 1) {
+    for (int i = 0; i < reps; i += 2) {
+      uint32_t r[64];
+      tmem_ld64(tbase + lane_off + ((col + (uint32_t)i * 64u) & 447u), r);
+#pragma unroll
+      for (int c = 0; c < 64; ++c) acc ^= r[c];
+    }
+  } else if (mode == 2) {
+    for (int i = 0; i < reps; ++i) {
+      uint32_t r[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) r[c] = acc + (uint32_t)c;
+      tmem_ld16(tbase + lane_off + ((col + (uint32_t)i * 64u) & 511u), r);
+#pragma unroll
+      for (int c = 0; c < 16; ++c) acc ^= r[c];
+    }
+  } else {
+    for (int i = 0; i < reps; ++i) {
+      uint32_t r[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) r[c] = acc + (uint32_t)c;
+      tmem_st16(tbase + lane_off + ((col + (uint32_t)i * 64u) & 511u), r);
+      tmem_st_wait();
+      acc += 1;
+    }
+  }
+  const uint64_t t1 = clock64();
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) cycles[blockIdx.x * 16 + warp] = t1 - t0;
+  if (acc == 0xdeadbeefu) cycles[0] = acc;
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tbase, 512);
+}
+}  // namespace
+}  // namespace spa2
+
+// mode 0: 32-column loads (4 KB per warp instruction), 1: two 32-column loads per wait,
+// 2: 16-column loads, 3: 16-column stores.  cycles[ctas * 16] per warp.
+extern "C" int spa2_probe_tmem_rate(int reps, int mode, int warps, int ctas, unsigned long long* cycles, void* stream) {
+  k_tmem_rate<<<ctas, 32 * warps, 0, (cudaStream_t)stream>>>(reps, mode, cycles);
+  SPA2_LAUNCH_CHECK();
+  return SPA2_OK;
+}

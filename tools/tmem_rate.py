@@ -1,0 +1,25 @@
+"""tcgen05.ld / tcgen05.st throughput per SM (diagnostic; numbers quoted in DESIGN.md §5).
+Every warp reads (or writes) its TMEM lane quarter, 32x32b shapes; one CTA per SM."""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2602_13515_b200 import _lib  # noqa: E402
+
+lib = _lib.load()
+st = torch.cuda.current_stream().cuda_stream
+ctas, reps = 148, 2048
+cyc = torch.zeros(ctas * 16, dtype=torch.int64, device="cuda")
+names = {0: "ld 32 col", 1: "ld 2x32 col", 2: "ld 16 col", 3: "st 16 col"}
+bytes_per = {0: 4096, 1: 4096, 2: 2048, 3: 2048}
+for mode in (0, 1, 2, 3):
+    for warps in (1, 4, 8, 16):
+        cyc.zero_()
+        _lib.check(lib.spa2_probe_tmem_rate(reps, mode, warps, ctas, _lib.ptr(cyc), st), "tmem")
+        torch.cuda.synchronize()
+        c = cyc.view(ctas, 16)[:, :warps].float()
+        tot = warps * reps * bytes_per[mode]
+        print(f"{names[mode]:12s} warps {warps:2d}: {c.mean().item() / reps:7.1f} cyc/instr per warp, "
+              f"{tot / c.max(dim=1).values.mean().item():6.1f} B/clk/SM")
