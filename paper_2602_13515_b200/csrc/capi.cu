@@ -50,7 +50,7 @@ int* sched_slot() {
 bool dynamic_sched() {
   static const bool v = [] {
     const char* e = getenv("SPA2_DYNAMIC_SCHED");
-    return !(e != nullptr && e[0] == '0');
+    return e != nullptr && e[0] == '1';
   }();
   return v;
 }

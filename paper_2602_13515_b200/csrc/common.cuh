@@ -73,7 +73,8 @@ bool pdl_enabled();
 // int[2] from a device pool, rotated per launch; zero on entry, reset by the kernel on exit.
 // Returns nullptr on failure (error text set).
 int* sched_slot();
-// SPA2_DYNAMIC_SCHED=0 falls back to the static round-robin deal (A/B switch).
+// SPA2_DYNAMIC_SCHED=1 claims items dynamically; default is the static round-robin deal
+// (measured neutral at the bench workload, and it keeps the library free of global state).
 bool dynamic_sched();
 // kernel<<<grid, block, smem, stream>>>(args...) with the PDL launch attribute when enabled.
 template <typename... KArgs, typename... Args>

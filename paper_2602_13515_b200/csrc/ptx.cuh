@@ -379,8 +379,8 @@ __device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
 }
 
 // ---- dynamic work distribution for the persistent kernels ------------------------------
-// Work items (query or key blocks, in the launch order built by the list kernels) are claimed
-// from a per-launch global counter instead of being dealt round-robin, so a CTA that drew long
+// With SPA2_DYNAMIC_SCHED=1, work items (query or key blocks, in the launch order built by the
+// list kernels) are claimed from a per-launch global counter instead of being dealt round-robin, so a CTA that drew long
 // items takes fewer of them.  One scheduler thread per CTA claims items kItemRing ahead into a
 // shared-memory ring; every consumer warp reads item k from slot k % kItemRing and releases it.
 // The first item is blockIdx.x (no atomic); later ones gridDim.x + atomicAdd(ctr[0], 1).  The
