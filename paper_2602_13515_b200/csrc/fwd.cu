@@ -461,7 +461,9 @@ __global__ void __launch_bounds__(kFwd3Threads, 2)
           const uint32_t ph = (uint32_t)(g / NS) & 1u;
           const int j = p.row_idx[beg + t];
           if (!second) {
+            trace_ev(p.trace, p.trace_cap, 0, 1, g);
             if (g >= NS) mbar_wait(&k_empty[s], ph ^ 1u);
+            trace_ev(p.trace, p.trace_cap, 0, 2, g);
             mbar_expect_tx(&k_full[s], C::KV_BYTES);
             tma_load_5d(smem + C::OFF_K + s * C::KV_BYTES, &tmK, &k_full[s], 0, j * BKV, 0, hh, bb);
           } else {
@@ -524,6 +526,7 @@ __global__ void __launch_bounds__(kFwd3Threads, 2)
         mma_commit_w(&s_full[b]);
         mma_commit_w(&k_empty[s]);
         if (t == n - 1) mma_commit_w(q_empty);
+        trace_ev(p.trace, p.trace_cap, 1, 3, g);
         if (pv_g >= 0) issue_pv();
         pv_g = g;
         pv_it = it;
@@ -567,7 +570,9 @@ __global__ void __launch_bounds__(kFwd3Threads, 2)
         const bool tail = j_next == p.T_n - 1 && kv_tail < BKV;
         if (t + 1 < n) j_next = list[t + 1];
         const uint32_t s_col = tbase + lane_off + (uint32_t)(b * 64);
+        if (threadIdx.x == 64) trace_ev(p.trace, p.trace_cap, 2, 1, g);
         mbar_wait(&s_full[b], (uint32_t)(g >> 1) & 1u);
+        if (threadIdx.x == 64) trace_ev(p.trace, p.trace_cap, 2, 2, g);
         tc_fence_after();
         uint32_t r[64];
         tmem_ld64(s_col, r);
@@ -605,6 +610,7 @@ __global__ void __launch_bounds__(kFwd3Threads, 2)
           l *= alpha;
           m = m_new;
         }
+        if (threadIdx.x == 64) trace_ev(p.trace, p.trace_cap, 2, 5, g);
         uint32_t pk[32];
         float2 lsum = make_float2(0.f, 0.f);
 #pragma unroll
@@ -625,6 +631,7 @@ __global__ void __launch_bounds__(kFwd3Threads, 2)
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&p_full[b]);
+        if (threadIdx.x == 64) trace_ev(p.trace, p.trace_cap, 2, 4, g);
       }
       // ---------------- epilogue: O / l -> bf16 rows, LSE ----------------
       mbar_wait(acc_full, (uint32_t)it & 1u);

@@ -11,7 +11,12 @@ software pipeline:
     compute  : masker+fwd+bwd(group g)   (stream `comp`)
     copy-out : D2H(group g-1)            (stream `d2h`)
 
-so the step approaches max(H2D, D2H, compute) instead of their sum.
+so the step approaches max(H2D, D2H, compute) instead of their sum.  Consecutive calls
+pipeline too: the copy-in of call s+1 does not wait for the copy-out of call s (the two
+directions of the link run concurrently), so a stream of calls is bound by
+max(H2D, D2H, compute) per call.  Host inputs must already hold their data when the call
+is made (written by the CPU or by completed copies); host outputs are valid once the
+current stream (which waits for the copy-out) has been synchronised.
 """
 
 from __future__ import annotations
@@ -44,7 +49,9 @@ class HostPipeline:
         G = max(1, min(self.groups, H))
         bounds = [(g * H // G, (g + 1) * H // G) for g in range(G)]
         main = torch.cuda.current_stream(self.device)
-        for s in (self.h2d, self.comp, self.d2h):
+        # compute and copy-out follow the caller's stream; copy-in reads host memory only,
+        # so it may run ahead of (and overlap) the previous call's copy-out
+        for s in (self.comp, self.d2h):
             s.wait_stream(main)
         ev_in, ev_done = [], []
         dev_in = []

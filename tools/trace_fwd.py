@@ -1,6 +1,6 @@
-"""Event timeline of the forward kernel (CTA 0 = the longest query block of head 0).
-P1/P2 producer before/after waiting a free K slot for tile t; M2 S issue; M4 PV issue;
-E1/E2 softmax before/after S landed, E4 P written."""
+"""Event timeline of the forward kernel (CTA 0; k_fwd3 numbers tiles by a CTA-global counter).
+P1/P2 producer before/after waiting a free K slot for tile t; M2 S issue begins, M3 S issued,
+M4 PV issue; E1/E2 softmax before/after S landed, E5 row max done, E4 P written."""
 import math, os, sys
 import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -34,3 +34,14 @@ m2 = {g: t for t, kd, g in ev if kd == "M2"}
 gs = sorted(m2)
 d = sorted(m2[b] - m2[a] for a, b in zip(gs, gs[1:]) if b == a + 1)
 print("S issue period: median", d[len(d) // 2], "n", len(d), "tiles", len(gs))
+
+# per-stage averages over all tiles of CTA 0
+import collections
+by = collections.defaultdict(dict)
+for t, kd, g in ev:
+    by[g][kd] = t
+def avg(a, b):
+    v = [x[b] - x[a] for x in by.values() if a in x and b in x]
+    return sum(v) / max(1, len(v))
+for a, b in (("E1", "E2"), ("E2", "E5"), ("E5", "E4"), ("M2", "M3"), ("M3", "E2"), ("E4", "M4")):
+    print(f"{a}->{b}: {avg(a, b):.0f} cycles")
