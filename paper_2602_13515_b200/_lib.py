@@ -134,6 +134,8 @@ def load() -> ctypes.CDLL:
                     "g.build()'` (there is no CPU fallback)")
             lib = ctypes.CDLL(LIB_PATH)
             for name, (args, res) in SIGNATURES.items():
+                if name.startswith("spa2_probe_") and not hasattr(lib, name):
+                    continue  # diagnostics only: an older A/B build may predate a probe
                 fn = getattr(lib, name)
                 fn.argtypes = args
                 fn.restype = res

@@ -59,7 +59,6 @@ struct BwdParams {
   unsigned long long* trace;  // diagnostic (spa2_debug_trace), normally null
   int trace_cap;
   int dbg;                    // diagnostic timing experiments (SPA2_DEBUG_FLAGS), normally 0
-  int* sched;                 // persistent kernels' work counter (sched_slot()), null = static deal
   // fused δ (k_dq3 with delta_out != null): δ = rowsum(dO ∘ O) computed in the kernel
   const __nv_bfloat16* o_in;
   int64_t oi_sb, oi_sh, oi_sn;
@@ -84,27 +83,16 @@ __device__ __forceinline__ Item get_item(const BwdParams& p, int wi, int nblk) {
 
 // Work-list cursor shared by the roles of the persistent kernels: walks this CTA's items
 // (blockIdx.x, +gridDim.x, ...) skipping empty ones, one tile at a time.
-// With a work ring (dynamic scheduling) the items come from ptx::item_take_w instead; the
-// whole warp must then call the cursor functions together.
 struct Cursor {
-  int wi, it, t, n, beg, bh, blk, g, k;
+  int wi, it, t, n, beg, bh, blk, g;
   bool valid;
-  const ItemRing* ring;
 };
 __device__ __forceinline__ void cursor_item(Cursor& c, const BwdParams& p, int nblk) {
   for (;;) {
-    if (c.ring != nullptr) {
-      c.wi = item_take_w(*c.ring, c.k++);
-      if (c.wi < 0) {
-        c.valid = false;
-        return;
-      }
-    } else {
-      c.wi += gridDim.x;
-      if (c.wi >= p.num_items) {
-        c.valid = false;
-        return;
-      }
+    c.wi += gridDim.x;
+    if (c.wi >= p.num_items) {
+      c.valid = false;
+      return;
     }
     const Item m = get_item(p, c.wi, nblk);
     if (m.n > 0) {
@@ -119,10 +107,8 @@ __device__ __forceinline__ void cursor_item(Cursor& c, const BwdParams& p, int n
     }
   }
 }
-__device__ __forceinline__ void cursor_init(Cursor& c, const BwdParams& p, int nblk, const ItemRing* ring = nullptr) {
+__device__ __forceinline__ void cursor_init(Cursor& c, const BwdParams& p, int nblk) {
   c.wi = (int)blockIdx.x - (int)gridDim.x;
-  c.ring = ring;
-  c.k = 0;
   c.it = -1;
   c.g = 0;
   c.valid = false;
@@ -717,20 +703,13 @@ __global__ void __launch_bounds__(kDq2Threads, 2)
 template <int EWW>
 struct Dq3Roles {
   static constexpr int EPI0 = 2 + EWW, PROD2 = EPI0 + 4, ISSUE_DP = PROD2 + 1, ISSUE_DQ = PROD2 + 2;
-  static constexpr int SCHED = ISSUE_DQ + 1;  // work scheduler
-  static constexpr int THREADS = 32 * (SCHED + 1);
+  static constexpr int THREADS = 32 * (ISSUE_DQ + 1);
   static constexpr int CPT = 256 / EWW;  // S/dP columns per elementwise thread
 };
 
-#ifndef SPA2_DQ_NK
-#define SPA2_DQ_NK 4
-#endif
-#ifndef SPA2_DQ_NV
-#define SPA2_DQ_NV 4
-#endif
 template <int HD>
 struct Dq3Cfg {
-  static constexpr int NK = SPA2_DQ_NK, NV = SPA2_DQ_NV;
+  static constexpr int NK = 4, NV = 4;
   static constexpr int Q_BYTES = BQ * HD * 2;
   static constexpr int KV_BYTES = BKV * HD * 2;
   static constexpr int OFF_QS = 0;  // staging [Q | dO] of the next item
@@ -738,9 +717,8 @@ struct Dq3Cfg {
   static constexpr int OFF_V = OFF_K + NK * KV_BYTES;
   static constexpr int OFF_DLT = OFF_V + NV * KV_BYTES;  // fused δ: float [2 items][128 rows]
   static constexpr int OFF_BAR = OFF_DLT + 2 * BQ * 4;
-  static constexpr int NUM_BARS = 4 + 2 * NK + 2 * NV + 2 * 5 + 2 + 2 + 2 * kItemRing;
-  static constexpr int OFF_ITEMS = OFF_BAR + NUM_BARS * 8;  // int[kItemRing]
-  static constexpr int SMEM = OFF_ITEMS + kItemRing * 4 + 16;
+  static constexpr int NUM_BARS = 4 + 2 * NK + 2 * NV + 2 * 5 + 2 + 2;
+  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr uint32_t Q_COL = 0, DO_COL = 64, SDP_COL = 128, ACC_COL = 384;  // S at +b*128, dP at +64
 };
 
@@ -778,15 +756,13 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
   uint64_t* acc_empty = acc_full + 1;
   uint64_t* dlt_full = acc_empty + 1;  // [2] fused δ of item `it` in sdelta[it & 1]
   uint64_t* s_free = dlt_full + 2;     // [2] S of tile g read out of TMEM buffer g&1
-  const ItemRing ring{reinterpret_cast<int*>(smem + C::OFF_ITEMS), s_free + 2, s_free + 2 + kItemRing};
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + C::OFF_ITEMS + kItemRing * 4);
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(s_free + 2);
   float* sdelta = reinterpret_cast<float*>(smem + C::OFF_DLT);
   const bool fused_delta = p.delta_out != nullptr;
 
   const int warp = (int)warp_id(), lane = (int)lane_id();
   if (threadIdx.x == 0) {
     if (smem_u32(smem) & 1023u) __trap();
-    item_ring_init(ring, R::SCHED);  // consumers: every warp but the scheduler
     mbar_init(qs_full, 2);  // Q from warp 0, dO from warp 14
     mbar_init(qs_free, 1);
     mbar_init(qd_free, 2);  // last S (warp 1) and last dP (warp 15) of the item
@@ -831,12 +807,9 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
       uint64_t* full = second ? v_full : k_full;
       uint64_t* empty = second ? v_empty : k_empty;
       const int ns = second ? NV : NK;
-      uint8_t* const kvring = smem + (second ? C::OFF_V : C::OFF_K);
+      uint8_t* const ring = smem + (second ? C::OFF_V : C::OFF_K);
       int it = 0, g = 0;
-      for (int k = 0;; ++k) {
-        const int wi = item_take(ring, k);
-        item_release(ring, k);
-        if (wi < 0) break;
+      for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
         const Item m = get_item(p, wi, p.T_m);
         if (m.n == 0) continue;
         const int hh = m.bh % p.H, bb = m.bh / p.H;
@@ -849,7 +822,7 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
           if (g >= ns) mbar_wait(&empty[s], ((uint32_t)(g / ns) + 1u) & 1u);
           if (!second) trace_ev(p.trace, p.trace_cap, 0, 2, g);
           mbar_expect_tx(&full[s], C::KV_BYTES);
-          tma_load_5d(kvring + s * C::KV_BYTES, tmKV, &full[s], 0, p.idx[m.beg + t] * BKV, 0, hh, bb);
+          tma_load_5d(ring + s * C::KV_BYTES, tmKV, &full[s], 0, p.idx[m.beg + t] * BKV, 0, hh, bb);
         }
         ++it;
       }
@@ -867,7 +840,7 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
     const uint64_t dKm0 = sw128_desc(smem_u32(smem + C::OFF_K), BKV * 128, 1024);
     constexpr uint64_t KV16 = (uint64_t)(C::KV_BYTES >> 4);
     Cursor c;
-    cursor_init(c, p, p.T_m, &ring);
+    cursor_init(c, p, p.T_m);
     if (warp == 1) {
       for (; c.valid; cursor_next(c, p, p.T_m)) {
         if (c.t == 0) {
@@ -946,9 +919,7 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
     const int kv_tail = p.N - (p.T_n - 1) * BKV;
     const float sl2 = p.sl2;
     int g = 0, it = 0;
-    for (int k = 0;; ++k) {
-      const int wi = item_take_w(ring, k);
-      if (wi < 0) break;
+    for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
       const Item m = get_item(p, wi, p.T_m);
       if (m.n == 0) continue;
       const int tok = m.blk * BQ + row;
@@ -1062,9 +1033,7 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
     int it = 0;
     bool pend = false;
     Item pm{};
-    for (int k = 0;; ++k) {
-      const int wi = item_take_w(ring, k);
-      if (wi < 0) break;
+    for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
       const Item m = get_item(p, wi, p.T_m);
       const int hh = m.bh % p.H, bb = m.bh / p.H;
       const int tok = m.blk * BQ + row;
@@ -1093,9 +1062,6 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
       ++it;
     }
     if (pend) drain(pm, it - 1);
-  } else if (warp == R::SCHED) {
-    // ---------------- work scheduler ----------------
-    if (lane == 0) item_sched(ring, p.sched, p.num_items);
   }
   tc_fence_before();
   __syncthreads();
@@ -1138,8 +1104,6 @@ struct DkvRoles {
   static constexpr int PROD2 = EPI0 + 4;         // second producer warp
   static constexpr int ISSUE2 = PROD2 + 1;       // dV/dK issuing warp
   static constexpr int THREADS = 32 * (ISSUE2 + 1);
-  static constexpr int SCHED = ISSUE2 + 1;       // k_dkdv5: work scheduler warp
-  static constexpr int THREADS5 = 32 * (SCHED + 1);
   static constexpr int CPT = 256 / EWW;          // S/dP columns per elementwise thread
 };
 
@@ -1461,9 +1425,8 @@ struct Dkv5Cfg {
   static constexpr int OFF_SL = 2 * KV_BYTES;              // [NSL] Q / dO operand slots
   static constexpr int OFF_PDS = OFF_SL + NSL * Q_BYTES;   // [NPB][P | dS]
   static constexpr int OFF_BAR = OFF_PDS + NPB * 2 * PB;
-  static constexpr int NUM_BARS = 2 + 2 * NSL + 6 + 4 * NPB + 4 + 2 * kItemRing;
-  static constexpr int OFF_ITEMS = OFF_BAR + NUM_BARS * 8;  // int[kItemRing]
-  static constexpr int SMEM = OFF_ITEMS + kItemRing * 4 + 16;
+  static constexpr int NUM_BARS = 2 + 2 * NSL + 6 + 4 * NPB + 4;
+  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr uint32_t S_COL = 0, DP_COL = 128, ACC_COL = 256;
 };
 
@@ -1471,7 +1434,7 @@ struct Dkv5Cfg {
 // (2.5 tiles in flight instead of 2 stages of [Q|dO]) and each slot is released by the MMA that
 // last reads it (dO after dV, Q after dK); P and dS share one smem buffer.
 template <int HD, int EWW, int NSL_ = 5, int NPB_ = 1>
-__global__ void __launch_bounds__(DkvRoles<EWW>::THREADS5, 1)
+__global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
     k_dkdv5(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
            const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO, const BwdParams p) {
   using C = Dkv5Cfg<HD, NSL_, NPB_>;
@@ -1495,13 +1458,11 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS5, 1)
   uint64_t* ds_free = p_free + NPB;     // [NPB] dK MMA of tile g done
   uint64_t* acc_full = ds_free + NPB;   // [2]
   uint64_t* acc_empty = acc_full + 2;   // [2]
-  const ItemRing ring{reinterpret_cast<int*>(smem + C::OFF_ITEMS), acc_empty + 2, acc_empty + 2 + kItemRing};
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + C::OFF_ITEMS + kItemRing * 4);
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = (int)warp_id(), lane = (int)lane_id();
   if (threadIdx.x == 0) {
     if (smem_u32(smem) & 1023u) __trap();
-    item_ring_init(ring, R::SCHED);  // consumers: every warp but the scheduler
     mbar_init(kv_full, 2);  // two producers: warp 0 (K, Q) and warp PROD2 (V, dO)
     mbar_init(kv_empty, 1);
     for (int s = 0; s < NSL; ++s) {
@@ -1543,10 +1504,7 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS5, 1)
       tma_prefetch(tmR);
       uint8_t* const kv_dst = smem + C::OFF_KV + (second ? C::KV_BYTES : 0);
       int it = 0, g = 0;
-      for (int k = 0;; ++k) {
-        const int wi = item_take(ring, k);
-        item_release(ring, k);
-        if (wi < 0) break;
+      for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
         const Item m = get_item(p, wi, p.T_n);
         if (m.n == 0) continue;
         const int hh = m.bh % p.H, bb = m.bh / p.H;
@@ -1581,7 +1539,7 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS5, 1)
     constexpr uint64_t SLOT16 = (uint64_t)(C::Q_BYTES >> 4), PB16 = (uint64_t)(C::PB >> 4);
     const uint64_t dDSm = dPm + PB16;                                                // MN-major dS
     Cursor c;
-    cursor_init(c, p, p.T_n, &ring);
+    cursor_init(c, p, p.T_n);
     if (warp == 1) {
       // S (needs Q) and dP (needs dO) of tile g into TMEM buffer g&1, each as soon as its
       // operand has landed (Q and dO live in separate ring slots)
@@ -1651,9 +1609,7 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS5, 1)
     const float sl2 = p.sl2;
     const bool tr = threadIdx.x == 64;
     int g = 0;
-    for (int k = 0;; ++k) {
-      const int wi = item_take_w(ring, k);
-      if (wi < 0) break;
+    for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
       const Item m = get_item(p, wi, p.T_n);
       if (m.n == 0) continue;
       const int64_t rowbase = (int64_t)m.bh * p.N;
@@ -1739,9 +1695,7 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS5, 1)
     const bool own = (HD == 128) || lane < 16;
     const bool tr = threadIdx.x == 32 * R::EPI0;
     int it = 0;
-    for (int k = 0;; ++k) {
-      const int wi = item_take_w(ring, k);
-      if (wi < 0) break;
+    for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
       const Item m = get_item(p, wi, p.T_n);
       const int hh = m.bh % p.H, bb = m.bh / p.H;
       __nv_bfloat16* dk = p.out0 + bb * p.o0_sb + hh * p.o0_sh + (int64_t)m.blk * BKV * p.o0_sn + dim;
@@ -1783,9 +1737,6 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS5, 1)
       if (tr) trace_ev(p.trace, p.trace_cap, 3, 3, it);
       ++it;
     }
-  } else if (warp == R::SCHED) {
-    // ---------------- work scheduler ----------------
-    if (lane == 0) item_sched(ring, p.sched, p.num_items);
   }
   tc_fence_before();
   __syncthreads();
@@ -1877,11 +1828,6 @@ int launch_attn_bwd(int which, const spa2_view& q, const spa2_view& k, const spa
     }();
     prm.dbg = dbg;
   }
-  prm.sched = nullptr;
-  if (dynamic_sched() && ((which == 0 && dq_variant() == 3) || (which == 1 && dkdv_variant() >= 5))) {
-    prm.sched = sched_slot();
-    if (prm.sched == nullptr) return SPA2_ERR_CUDA;
-  }
   const unsigned grid = (unsigned)std::min<int64_t>(prm.num_items, num_sms());
   if (which == 0 && dq_variant() == 3) {
     if (dq_ew_warps() == 16) {
@@ -1910,17 +1856,17 @@ int launch_attn_bwd(int which, const spa2_view& q, const spa2_view& k, const spa
       using C6 = Dkv5Cfg<HD, 4, 2>;
       auto kern = k_dkdv5<HD, 16, 4, 2>;
       SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C6::SMEM));
-      SPA2_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(DkvRoles<16>::THREADS5), C6::SMEM, st, m.q, m.k, m.v, m.dout,
+      SPA2_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(DkvRoles<16>::THREADS), C6::SMEM, st, m.q, m.k, m.v, m.dout,
                                prm));
     } else if (dkdv_variant() >= 5 && dkdv_ew_warps() == 16) {
       auto kern = k_dkdv5<HD, 16>;
       SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Dkv5Cfg<HD>::SMEM));
-      SPA2_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(DkvRoles<16>::THREADS5), Dkv5Cfg<HD>::SMEM, st, m.q, m.k, m.v, m.dout,
+      SPA2_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(DkvRoles<16>::THREADS), Dkv5Cfg<HD>::SMEM, st, m.q, m.k, m.v, m.dout,
                                prm));
     } else if (dkdv_variant() >= 5) {
       auto kern = k_dkdv5<HD, 8>;
       SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Dkv5Cfg<HD>::SMEM));
-      SPA2_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(DkvRoles<8>::THREADS5), Dkv5Cfg<HD>::SMEM, st, m.q, m.k, m.v, m.dout,
+      SPA2_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(DkvRoles<8>::THREADS), Dkv5Cfg<HD>::SMEM, st, m.q, m.k, m.v, m.dout,
                                prm));
     } else if (dkdv_ew_warps() == 16) {
       auto kern = k_dkdv<HD, 16>;

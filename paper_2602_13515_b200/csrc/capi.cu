@@ -10,7 +10,6 @@
 #include "common.cuh"
 #include "tma_host.h"
 
-#include <atomic>
 
 namespace spa2 {
 
@@ -25,35 +24,6 @@ bool pdl_enabled() {
 }
 int g_trace_cap = 0;
 
-namespace {
-constexpr int kSchedSlots = 1024;
-__device__ int g_sched_pool[2 * kSchedSlots];  // zero-initialised at module load
-}  // namespace
-int* sched_slot() {
-  static int* base[64] = {};
-  static std::atomic<unsigned> next{0};
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
-    set_error("sched_slot: no current CUDA device");
-    return nullptr;
-  }
-  if (base[dev] == nullptr) {
-    void* p = nullptr;
-    if (cudaGetSymbolAddress(&p, g_sched_pool) != cudaSuccess) {
-      set_error("sched_slot: cudaGetSymbolAddress failed");
-      return nullptr;
-    }
-    base[dev] = static_cast<int*>(p);
-  }
-  return base[dev] + 2 * (next.fetch_add(1) % kSchedSlots);
-}
-bool dynamic_sched() {
-  static const bool v = [] {
-    const char* e = getenv("SPA2_DYNAMIC_SCHED");
-    return e != nullptr && e[0] == '1';
-  }();
-  return v;
-}
 
 void set_error(const char* fmt, ...) {
   va_list ap;

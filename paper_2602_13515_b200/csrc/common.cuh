@@ -54,10 +54,14 @@ __device__ __forceinline__ double to_f64<__half>(__half x) { return (double)__ha
 // ---- diagnostic in-kernel trace (CTA 0 only; disabled unless spa2_debug_trace set a buffer) ----
 // Fixed slot per (role, index, kind): buf[2 + role*(cap/4) + index*8 + kind] = clock64.  Plain
 // stores, no atomics, so tracing barely perturbs the pipeline it observes.
+// Compiled in only with -DSPA2_TRACE (tools/build_alt.sh trace -DSPA2_TRACE; the trace tools
+// then run with SPA2_LIB_PATH=alt/trace/libspa2.so): the production kernels carry no trace code.
 __device__ __forceinline__ void trace_ev(unsigned long long* buf, int cap, int role, int kind, int idx) {
+#ifdef SPA2_TRACE
   if (buf == nullptr || blockIdx.x != 0) return;
   const int slot = idx * 8 + kind;
   if (slot < cap / 4) buf[2 + role * (cap / 4) + slot] = clock64();
+#endif
 }
 // ---- programmatic dependent launch (PDL) ---------------------------------------------
 // Hot-path kernels are launched with programmatic stream serialization: the next kernel's
@@ -69,13 +73,6 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 
 namespace spa2 {
 bool pdl_enabled();
-// Per-launch work counter for the persistent kernels' dynamic scheduling (ptx::item_sched):
-// int[2] from a device pool, rotated per launch; zero on entry, reset by the kernel on exit.
-// Returns nullptr on failure (error text set).
-int* sched_slot();
-// SPA2_DYNAMIC_SCHED=1 claims items dynamically; default is the static round-robin deal
-// (measured neutral at the bench workload, and it keeps the library free of global state).
-bool dynamic_sched();
 // kernel<<<grid, block, smem, stream>>>(args...) with the PDL launch attribute when enabled.
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {

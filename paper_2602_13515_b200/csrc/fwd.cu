@@ -70,7 +70,6 @@ struct FwdParams {
   int64_t o_sb, o_sh, o_sn;
   unsigned long long* trace;  // diagnostic (spa2_debug_trace), normally null
   int trace_cap;
-  int* sched;  // k_fwd3 work counter (sched_slot()), null = static round-robin deal
 };
 
 template <int HD, bool P_TMEM>
@@ -364,9 +363,8 @@ struct Fwd3Cfg {
   static constexpr int OFF_K = OFF_Q + Q_BYTES;
   static constexpr int OFF_V = OFF_K + NS * KV_BYTES;
   static constexpr int OFF_BAR = OFF_V + NS * KV_BYTES;
-  static constexpr int NUM_BARS = 2 + 4 * NS + 2 * 3 + 2 + 2 * kItemRing;
-  static constexpr int OFF_ITEMS = OFF_BAR + NUM_BARS * 8;  // int[kItemRing]
-  static constexpr int SMEM_USED = OFF_ITEMS + kItemRing * 4 + 16;
+  static constexpr int NUM_BARS = 2 + 4 * NS + 2 * 3 + 2;
+  static constexpr int SMEM_USED = OFF_BAR + NUM_BARS * 8 + 16;
   static constexpr int SMEM = SMEM_USED < 80 * 1024 ? 80 * 1024 : SMEM_USED;
   static constexpr uint32_t O_COL = 128;
 };
@@ -379,10 +377,8 @@ __device__ __forceinline__ void fwd_item(const FwdParams& p, int wi, int& bh, in
   n = p.row_ptr[w + 1] - beg;
 }
 
-constexpr int kFwd3Threads = kFwdThreads + 32;  // + warp 7: work scheduler
-
 template <int HD>
-__global__ void __launch_bounds__(kFwd3Threads, 2)
+__global__ void __launch_bounds__(kFwdThreads, 2)
     k_fwd3(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
            const __grid_constant__ CUtensorMap tmV, const FwdParams p, int num_items) {
   using C = Fwd3Cfg<HD>;
@@ -400,13 +396,11 @@ __global__ void __launch_bounds__(kFwd3Threads, 2)
   uint64_t* o_done = p_full + 2;      // [2] PV of tile g done
   uint64_t* acc_full = o_done + 2;    // last PV of item `it` done
   uint64_t* acc_empty = acc_full + 1;  // O of item `it` read out
-  const ItemRing ring{reinterpret_cast<int*>(smem + C::OFF_ITEMS), acc_empty + 1, acc_empty + 1 + kItemRing};
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + C::OFF_ITEMS + kItemRing * 4);
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 1);
 
   const int warp = (int)warp_id(), lane = (int)lane_id();
   if (threadIdx.x == 0) {
     if (smem_u32(smem) & 1023u) __trap();
-    item_ring_init(ring, 7);  // consumers: warps 0-6
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
     for (int s = 0; s < NS; ++s) {
@@ -443,10 +437,7 @@ __global__ void __launch_bounds__(kFwd3Threads, 2)
         tma_prefetch(&tmK);
       }
       int it = 0, g = 0;
-      for (int k = 0;; ++k) {
-        const int wi = item_take(ring, k);
-        item_release(ring, k);
-        if (wi < 0) break;
+      for (int wi = blockIdx.x; wi < num_items; wi += gridDim.x) {
         int bh, qi, beg, n;
         fwd_item(p, wi, bh, qi, beg, n);
         if (n == 0) continue;
@@ -503,9 +494,7 @@ __global__ void __launch_bounds__(kFwd3Threads, 2)
       if (pv_last) mma_commit_w(acc_full);
     };
     int it = 0, g = 0;
-    for (int k = 0;; ++k) {
-      const int wi = item_take_w(ring, k);
-      if (wi < 0) break;
+    for (int wi = blockIdx.x; wi < num_items; wi += gridDim.x) {
       int bh, qi, beg, n;
       fwd_item(p, wi, bh, qi, beg, n);
       if (n == 0) continue;
@@ -536,9 +525,6 @@ __global__ void __launch_bounds__(kFwd3Threads, 2)
       ++it;
     }
     if (pv_g >= 0) issue_pv();
-  } else if (warp == 7) {
-    // ---------------- work scheduler ----------------
-    if (lane == 0) item_sched(ring, p.sched, num_items);
   } else {
     // ---------------- softmax warps (2..5) + epilogue ----------------
     const int q4 = warp & 3;
@@ -547,9 +533,7 @@ __global__ void __launch_bounds__(kFwd3Threads, 2)
     const int kv_tail = p.N - (p.T_n - 1) * BKV;
     const float sl2 = p.scale_log2;
     int it = 0, g = 0;
-    for (int k = 0;; ++k) {
-      const int wi = item_take_w(ring, k);
-      if (wi < 0) break;
+    for (int wi = blockIdx.x; wi < num_items; wi += gridDim.x) {
       int bh, qi, beg, n;
       fwd_item(p, wi, bh, qi, beg, n);
       const int hh = bh % p.H, bb = bh / p.H;
@@ -1094,22 +1078,17 @@ extern "C" int spa2_fwd(spa2_view q, spa2_view k, spa2_view v, spa2_view o, floa
   const unsigned grid = (unsigned)(B * H * T_m);
   cudaStream_t st = (cudaStream_t)stream;
   if (fwd_variant() == 3) {
-    prm.sched = nullptr;
-    if (dynamic_sched()) {
-      prm.sched = sched_slot();
-      if (prm.sched == nullptr) return SPA2_ERR_CUDA;
-    }
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const unsigned pgrid = (unsigned)std::min<int64_t>(B * H * T_m, 2 * (int64_t)sms);
     if (d == 128) {
       SPA2_CUDA_TRY(cudaFuncSetAttribute(k_fwd3<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd3Cfg<128>::SMEM));
-      SPA2_CUDA_TRY(launch_pdl(k_fwd3<128>, dim3(pgrid), dim3(kFwd3Threads), Fwd3Cfg<128>::SMEM, st, tq, tk, tv, prm,
+      SPA2_CUDA_TRY(launch_pdl(k_fwd3<128>, dim3(pgrid), dim3(kFwdThreads), Fwd3Cfg<128>::SMEM, st, tq, tk, tv, prm,
                                (int)(B * H * T_m)));
     } else {
       SPA2_CUDA_TRY(cudaFuncSetAttribute(k_fwd3<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, Fwd3Cfg<64>::SMEM));
-      SPA2_CUDA_TRY(launch_pdl(k_fwd3<64>, dim3(pgrid), dim3(kFwd3Threads), Fwd3Cfg<64>::SMEM, st, tq, tk, tv, prm,
+      SPA2_CUDA_TRY(launch_pdl(k_fwd3<64>, dim3(pgrid), dim3(kFwdThreads), Fwd3Cfg<64>::SMEM, st, tq, tk, tv, prm,
                                (int)(B * H * T_m)));
     }
     SPA2_LAUNCH_CHECK();

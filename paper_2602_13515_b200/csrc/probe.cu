@@ -540,6 +540,50 @@ __global__ void __launch_bounds__(512, 1) k_tmem_rate(int reps, int mode, unsign
   const uint32_t col = (uint32_t)((warp >> 2) * 32) & 511u;
   uint32_t acc = 0;
   __syncthreads();
+  if (mode >= 4) {
+    // modes 4/5: warp 0 keeps the tensor core busy with N=128 SS MMAs into columns [384, 512)
+    // (mode 5: N=64 into [448, 512)) while the other warps time 32-column loads of [0, 256)
+    extern __shared__ __align__(1024) uint8_t ops[];
+    __shared__ volatile int stop;
+    __shared__ uint64_t bar;
+    if (threadIdx.x == 0) {
+      stop = 0;
+      mbar_init(&bar, 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const uint64_t da = sw128_desc(smem_u32(ops), 16, 1024), db = sw128_desc(smem_u32(ops) + 16384, 16, 1024);
+      const uint32_t id = mode == 4 ? idesc_bf16(128, 128, false, false) : idesc_bf16(128, 64, false, false);
+      const uint32_t dcol = mode == 4 ? 384u : 448u;
+      int n = 0;
+      while (!stop) {
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) mma_bf16_w(tbase + dcol, da + (uint64_t)(ks * 2), db + (uint64_t)(ks * 2), id, ks > 0);
+        ++n;
+      }
+      mma_commit_w(&bar);
+      mbar_wait(&bar, 0);
+      if (lane_id() == 0) cycles[blockIdx.x * 16] = (unsigned long long)n;
+    } else {
+      const uint64_t t0 = clock64();
+      for (int i = 0; i < reps; ++i) {
+        uint32_t r[32];
+        tmem_ld32(tbase + lane_off + ((col + (uint32_t)i * 64u) & 255u), r);
+#pragma unroll
+        for (int c = 0; c < 32; ++c) acc ^= r[c];
+      }
+      const uint64_t t1 = clock64();
+      if ((threadIdx.x & 31) == 0) cycles[blockIdx.x * 16 + warp] = t1 - t0;
+      asm volatile("bar.sync 1, %0;" ::"r"((int)blockDim.x - 32));
+      if (threadIdx.x == 32) stop = 1;
+    }
+    if (acc == 0xdeadbeefu) cycles[0] = acc;
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tbase, 512);
+    return;
+  }
   const uint64_t t0 = clock64();
   if (mode == 0) {
     for (int i = 0; i < reps; ++i) {
@@ -586,9 +630,12 @@ __global__ void __launch_bounds__(512, 1) k_tmem_rate(int reps, int mode, unsign
 }  // namespace spa2
 
 // mode 0: 32-column loads (4 KB per warp instruction), 1: two 32-column loads per wait,
-// 2: 16-column loads, 3: 16-column stores.  cycles[ctas * 16] per warp.
+// 2: 16-column loads, 3: 16-column stores, 4/5: 32-column loads by warps 1.. while warp 0
+// streams N=128 / N=64 MMAs (cycles[cta*16] = MMA groups issued).  cycles[ctas * 16] per warp.
 extern "C" int spa2_probe_tmem_rate(int reps, int mode, int warps, int ctas, unsigned long long* cycles, void* stream) {
-  k_tmem_rate<<<ctas, 32 * warps, 0, (cudaStream_t)stream>>>(reps, mode, cycles);
+  const int smem = mode >= 4 ? 32768 + 1024 : 0;
+  if (mode >= 4) SPA2_CUDA_TRY(cudaFuncSetAttribute(k_tmem_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  k_tmem_rate<<<ctas, 32 * warps, smem, (cudaStream_t)stream>>>(reps, mode, cycles);
   SPA2_LAUNCH_CHECK();
   return SPA2_OK;
 }

@@ -378,57 +378,5 @@ __device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
   return v;
 }
 
-// ---- dynamic work distribution for the persistent kernels ------------------------------
-// With SPA2_DYNAMIC_SCHED=1, work items (query or key blocks, in the launch order built by the
-// list kernels) are claimed from a per-launch global counter instead of being dealt round-robin, so a CTA that drew long
-// items takes fewer of them.  One scheduler thread per CTA claims items kItemRing ahead into a
-// shared-memory ring; every consumer warp reads item k from slot k % kItemRing and releases it.
-// The first item is blockIdx.x (no atomic); later ones gridDim.x + atomicAdd(ctr[0], 1).  The
-// last CTA to run out of items resets ctr[0..1] to zero for the next launch using the slot.
-constexpr int kItemRing = 4;
-struct ItemRing {
-  int* items;       // [kItemRing]
-  uint64_t* full;   // [kItemRing] count 1
-  uint64_t* empty;  // [kItemRing] count = consumer warps
-};
-__device__ __forceinline__ void item_ring_init(const ItemRing& r, int consumer_warps) {
-  for (int s = 0; s < kItemRing; ++s) {
-    mbar_init(&r.full[s], 1);
-    mbar_init(&r.empty[s], (uint32_t)consumer_warps);
-  }
-}
-static __device__ __noinline__ void item_sched(const ItemRing& r, int* ctr, int num_items) {
-  for (int k = 0;; ++k) {
-    const int s = k % kItemRing;
-    if (k >= kItemRing) mbar_wait(&r.empty[s], (uint32_t)((k / kItemRing) + 1) & 1u);
-    int wi = ctr == nullptr ? (int)blockIdx.x + k * (int)gridDim.x  // static deal (A/B switch)
-             : k == 0       ? (int)blockIdx.x
-                            : (int)gridDim.x + atomicAdd(ctr, 1);
-    if (wi >= num_items) wi = -1;
-    r.items[s] = wi;
-    mbar_arrive(&r.full[s]);
-    if (wi < 0) break;
-  }
-  if (ctr != nullptr && atomicAdd(ctr + 1, 1) == (int)gridDim.x - 1) {  // every CTA has made its last claim
-    atomicExch(ctr, 0);
-    atomicExch(ctr + 1, 0);
-  }
-}
-// Item k for this consumer (-1: no more work).  Called by one thread or by a whole warp; the
-// caller releases the slot once per warp with item_release.
-__device__ __forceinline__ int item_take(const ItemRing& r, int k) {
-  const int s = k % kItemRing;
-  mbar_wait(&r.full[s], (uint32_t)(k / kItemRing) & 1u);
-  return *reinterpret_cast<volatile int*>(&r.items[s]);
-}
-__device__ __forceinline__ void item_release(const ItemRing& r, int k) { mbar_arrive(&r.empty[k % kItemRing]); }
-// Whole-warp form: all lanes read, lane 0 releases.
-__device__ __forceinline__ int item_take_w(const ItemRing& r, int k) {
-  const int wi = item_take(r, k);
-  __syncwarp();
-  if (lane_id() == 0) item_release(r, k);
-  return wi;
-}
-
 }  // namespace ptx
 }  // namespace spa2

@@ -7,7 +7,6 @@ case runs a small fwd + bwd parity check in a fresh interpreter:
   SPA2_NO_FUSED_DELTA=1      δ by its own kernel instead of inside the dQ kernel
   SPA2_DKDV_VARIANT=5|6|1    dK/dV: 5-slot Q/dO ring | 4 slots + two P/dS buffers | two [Q|dO] stages
   SPA2_DQ_EW=8, SPA2_DKDV_EW=8|16 elementwise warp counts (defaults 16, 16)
-  SPA2_DYNAMIC_SCHED=1       persistent kernels claim items from a counter instead of a static deal
 Checked against the float64 oracle at two ragged shapes (d = 64 and 128)."""
 
 import os
@@ -52,7 +51,6 @@ VARIANTS = [
     {"SPA2_NO_FUSED_DELTA": "1"},
     {"SPA2_DKDV_VARIANT": "1"},
     {"SPA2_DKDV_VARIANT": "6"},
-    {"SPA2_DYNAMIC_SCHED": "1"},
     {"SPA2_DQ_EW": "8", "SPA2_DKDV_EW": "8"},
     {"SPA2_DKDV_VARIANT": "1", "SPA2_DKDV_EW": "16"},
 ]

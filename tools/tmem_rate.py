@@ -23,3 +23,12 @@ for mode in (0, 1, 2, 3):
         tot = warps * reps * bytes_per[mode]
         print(f"{names[mode]:12s} warps {warps:2d}: {c.mean().item() / reps:7.1f} cyc/instr per warp, "
               f"{tot / c.max(dim=1).values.mean().item():6.1f} B/clk/SM")
+
+# loads while the tensor core is busy (warp 0 streams MMAs into other columns)
+for mode, label in ((4, "ld 32 col + N=128 MMAs"), (5, "ld 32 col + N=64 MMAs")):
+    for warps in (2, 5, 9):
+        cyc.zero_()
+        _lib.check(lib.spa2_probe_tmem_rate(reps, mode, warps, ctas, _lib.ptr(cyc), st), "tmem")
+        torch.cuda.synchronize()
+        c = cyc.view(ctas, 16)[:, 1:warps].float()
+        print(f"{label:24s} ld warps {warps - 1}: {c.mean().item() / reps:7.1f} cyc/instr per warp")

@@ -8,7 +8,9 @@ Roles/kinds recorded by the kernel (spa2_debug_trace):
               3 before waiting for P/dS of tile g, 4 after (dV/dK issued next)
   softmax  2: 1 before waiting for S/dP of tile g, 2 after, 3 P/dS buffer free, 4 P/dS written
   epilog   3: 1 before waiting for the accumulators of item it, 2 after, 3 stores done
-"""
+
+Needs a trace build: `bash tools/build_alt.sh trace -DSPA2_TRACE`, then run with
+SPA2_LIB_PATH=alt/trace/libspa2.so (production kernels carry no trace code)."""
 import math
 import os
 import sys
@@ -40,6 +42,8 @@ def main():
     _lib.load().spa2_debug_trace(None, 0)
     R = cap // 4
     raw = buf[2:].view(4, R).cpu()
+if not raw.any():
+    sys.exit("no events recorded: run with SPA2_LIB_PATH=alt/trace/libspa2.so (tools/build_alt.sh trace -DSPA2_TRACE)")
     rec = defaultdict(dict)
     t0 = None
     nz = raw.nonzero().tolist()
@@ -100,6 +104,8 @@ def timeline():
     _lib.load().spa2_debug_trace(None, 0)
     R = cap // 4
     raw = buf[2:].view(4, R).cpu()
+if not raw.any():
+    sys.exit("no events recorded: run with SPA2_LIB_PATH=alt/trace/libspa2.so (tools/build_alt.sh trace -DSPA2_TRACE)")
     names = {0: "P", 1: "M", 2: "E", 3: "X"}
     ev = []
     for role, slot in raw.nonzero().tolist():

@@ -2,7 +2,9 @@
 producer 0: 1/2 before/after waiting for a free K slot of tile g
 mma 1: 1 before waiting dq_done(g-2), 5 after, 2 K landed (S/dP issued next), 3/4 before/after waiting dS(g)
 softmax 2: 1/2 before/after waiting S/dP(g), 4 dS written
-"""
+
+Needs a trace build: `bash tools/build_alt.sh trace -DSPA2_TRACE`, then run with
+SPA2_LIB_PATH=alt/trace/libspa2.so (production kernels carry no trace code)."""
 import math, os, sys
 from collections import defaultdict
 import torch
@@ -33,6 +35,8 @@ torch.cuda.synchronize()
 lib.spa2_debug_trace(None, 0)
 R = cap // 4
 raw = buf[2:].view(4, R).cpu()
+if not raw.any():
+    sys.exit("no events recorded: run with SPA2_LIB_PATH=alt/trace/libspa2.so (tools/build_alt.sh trace -DSPA2_TRACE)")
 rec = defaultdict(dict)
 t0 = None
 nz = raw.nonzero().tolist()

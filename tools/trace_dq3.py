@@ -1,7 +1,9 @@
 """Event timeline of the dQ kernel (CTA 0) at the bench shape — diagnostic.
 M2 S/dP issue begins, M6 S issued, M3 S/dP issued, M7 dQ wait begins, M4 dQ issue begins, M5 dQ issued;
 P1/P2 producer before/after waiting a free K slot of tile g; M2 S/dP issued; M4 dQ issued;
-E1/E2 elementwise before/after S landed, E3 dP landed, E4 dS written."""
+E1/E2 elementwise before/after S landed, E3 dP landed, E4 dS written.
+Needs a trace build: `bash tools/build_alt.sh trace -DSPA2_TRACE`, then run with
+SPA2_LIB_PATH=alt/trace/libspa2.so (production kernels carry no trace code)."""
 import math, os, sys
 import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -39,6 +41,8 @@ torch.cuda.synchronize()
 lib.spa2_debug_trace(None, 0)
 R = cap // 4
 raw = buf[2:].view(4, R).cpu()
+if not raw.any():
+    sys.exit("no events recorded: run with SPA2_LIB_PATH=alt/trace/libspa2.so (tools/build_alt.sh trace -DSPA2_TRACE)")
 names = {0: "P", 1: "M", 2: "E", 3: "X"}
 ev = sorted((int(raw[r, s]), f"{names[r]}{s % 8}", s // 8) for r, s in raw.nonzero().tolist())
 lo = int(sys.argv[1]) if len(sys.argv) > 1 else 40

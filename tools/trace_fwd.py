@@ -1,6 +1,8 @@
 """Event timeline of the forward kernel (CTA 0; k_fwd3 numbers tiles by a CTA-global counter).
 P1/P2 producer before/after waiting a free K slot for tile t; M2 S issue begins, M3 S issued,
-M4 PV issue; E1/E2 softmax before/after S landed, E5 row max done, E4 P written."""
+M4 PV issue; E1/E2 softmax before/after S landed, E5 row max done, E4 P written.
+Needs a trace build: `bash tools/build_alt.sh trace -DSPA2_TRACE`, then run with
+SPA2_LIB_PATH=alt/trace/libspa2.so (production kernels carry no trace code)."""
 import math, os, sys
 import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -23,6 +25,8 @@ torch.cuda.synchronize()
 lib.spa2_debug_trace(None, 0)
 R = cap // 4
 raw = buf[2:].view(4, R).cpu()
+if not raw.any():
+    sys.exit("no events recorded: run with SPA2_LIB_PATH=alt/trace/libspa2.so (tools/build_alt.sh trace -DSPA2_TRACE)")
 names = {0: "P", 1: "M", 2: "E", 3: "X"}
 ev = sorted((int(raw[r, s]), f"{names[r]}{s % 8}", s // 8) for r, s in raw.nonzero().tolist())
 lo = int(sys.argv[1]) if len(sys.argv) > 1 else 10
