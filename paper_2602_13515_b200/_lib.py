@@ -110,6 +110,14 @@ def call(name: str, *args, stream_obj=None):
     if start is not None:
         STATS.end(name, start, stream_obj)
     check(rc, name)
+    if _SYNC_CALLS:  # diagnostic: attribute an asynchronous fault to the call that caused it
+        try:
+            torch.cuda.synchronize()
+        except Exception as e:  # noqa: BLE001
+            raise RuntimeError(f"{name}: asynchronous failure: {e}") from e
+
+
+_SYNC_CALLS = os.environ.get("SPA2_SYNC_CALLS", "0") == "1"
 
 _lock = threading.Lock()
 _lib = None

@@ -204,7 +204,7 @@ struct DqCfg {
   static constexpr int OFF_V = OFF_K + NSK * KV_BYTES;
   static constexpr int OFF_BAR = OFF_V + NSV * KV_BYTES;
   static constexpr int NUM_BARS = 4 + 2 * NSK + 2 * NSV + 2 + 2 + 1 + 4;
-  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;
+  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + kSmemAlignSlack;
   static constexpr uint32_t S_COL = 0, DP_COL = 128, ACC_COL = 256;
 };
 
@@ -215,7 +215,8 @@ __global__ void __launch_bounds__(kThreads, 1)
          const __grid_constant__ CUtensorMap tmDQ, const BwdParams p) {
   using C = DqCfg<HD>;
   constexpr int NSK = C::NSK, NSV = C::NSV;
-  extern __shared__ __align__(1024) uint8_t smem[];
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* const smem = smem_align_1k(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* qdo_full = bars;            // [2]
   uint64_t* qdo_empty = qdo_full + 2;   // [2]
@@ -232,7 +233,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = (int)warp_id(), lane = (int)lane_id();
   if (threadIdx.x == 0) {
-    if (smem_u32(smem) & 1023u) __trap();
     for (int s = 0; s < 2; ++s) {
       mbar_init(&qdo_full[s], 1);
       mbar_init(&qdo_empty[s], 1);
@@ -490,7 +490,7 @@ struct Dq2Cfg {
   static constexpr int OFF_BAR = OFF_V + KV_BYTES;
   static constexpr int NUM_BARS = 1 + 2 * NSK + 2 + 4;
   static constexpr int SMEM_USED = OFF_BAR + NUM_BARS * 8 + 16;
-  static constexpr int SMEM = SMEM_USED < 80 * 1024 ? 80 * 1024 : SMEM_USED;  // never 3 CTAs/SM (TMEM)
+  static constexpr int SMEM = SMEM_USED + kSmemAlignSlack < 80 * 1024 ? 80 * 1024 : SMEM_USED + kSmemAlignSlack;  // never 3 CTAs/SM (TMEM)
   static constexpr uint32_t S_COL = 0, DP_COL = 64, ACC_COL = 128;
 };
 
@@ -501,7 +501,8 @@ __global__ void __launch_bounds__(kDq2Threads, 2)
           const __grid_constant__ CUtensorMap tmDQ, const BwdParams p) {
   using C = Dq2Cfg<HD>;
   constexpr int NSK = C::NSK;
-  extern __shared__ __align__(1024) uint8_t smem[];
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* const smem = smem_align_1k(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* qdo_full = bars;
   uint64_t* k_full = qdo_full + 1;   // [NSK]
@@ -523,7 +524,6 @@ __global__ void __launch_bounds__(kDq2Threads, 2)
   const int32_t* list = p.idx + beg;
 
   if (threadIdx.x == 0) {
-    if (smem_u32(smem) & 1023u) __trap();
     mbar_init(qdo_full, 2);  // Q from warp 0, dO from warp 6
     for (int s = 0; s < NSK; ++s) {
       mbar_init(&k_full[s], 1);
@@ -718,7 +718,7 @@ struct Dq3Cfg {
   static constexpr int OFF_DLT = OFF_V + NV * KV_BYTES;  // fused δ: float [2 items][128 rows]
   static constexpr int OFF_BAR = OFF_DLT + 2 * BQ * 4;
   static constexpr int NUM_BARS = 4 + 2 * NK + 2 * NV + 2 * 5 + 2 + 2;
-  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;
+  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + kSmemAlignSlack;
   static constexpr uint32_t Q_COL = 0, DO_COL = 64, SDP_COL = 128, ACC_COL = 384;  // S at +b*128, dP at +64
 };
 
@@ -738,7 +738,8 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
   constexpr int NK = C::NK, NV = C::NV;
   constexpr int CPT = R::CPT;
   constexpr int kPolyPairs = CPT / 8;
-  extern __shared__ __align__(1024) uint8_t smem[];
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* const smem = smem_align_1k(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* qs_full = bars;         // staging holds Q_i and dO_i of item `it`
   uint64_t* qs_free = bars + 1;     // tcgen05.cp of item `it` done: staging reusable
@@ -762,7 +763,6 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
 
   const int warp = (int)warp_id(), lane = (int)lane_id();
   if (threadIdx.x == 0) {
-    if (smem_u32(smem) & 1023u) __trap();
     mbar_init(qs_full, 2);  // Q from warp 0, dO from warp 14
     mbar_init(qs_free, 1);
     mbar_init(qd_free, 2);  // last S (warp 1) and last dP (warp 15) of the item
@@ -1118,7 +1118,7 @@ struct DkvCfg {
   static constexpr int OFF_PDS = OFF_QDO + NS * 2 * Q_BYTES;  // [2 buffers][P | dS]
   static constexpr int OFF_BAR = OFF_PDS + 2 * 2 * PB;
   static constexpr int NUM_BARS = 2 + 2 * NS + 2 * 7;
-  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;
+  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + kSmemAlignSlack;
   static constexpr uint32_t S_COL = 0, DP_COL = 128, ACC_COL = 256;  // acc a: dV at +a*128, dK at +a*128+64
 };
 
@@ -1131,7 +1131,8 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
   constexpr int NS = C::NS;
   constexpr int EWT = 32 * EWW;  // elementwise threads
   constexpr int kDkvPolyPairs = R::CPT / SPA2_DKDV_POLY_PAIRS_DIV;
-  extern __shared__ __align__(1024) uint8_t smem[];
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* const smem = smem_align_1k(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* kv_full = bars;             // K/V of item `it` landed
   uint64_t* kv_empty = kv_full + 1;     // last S/dP MMA of item `it` done: K/V slot reusable
@@ -1148,7 +1149,6 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
 
   const int warp = (int)warp_id(), lane = (int)lane_id();
   if (threadIdx.x == 0) {
-    if (smem_u32(smem) & 1023u) __trap();
     mbar_init(kv_full, 2);  // two producers: warp 0 (K, Q) and warp PROD2 (V, dO)
     mbar_init(kv_empty, 1);
     for (int s = 0; s < 2; ++s) {
@@ -1426,13 +1426,15 @@ struct Dkv5Cfg {
   static constexpr int OFF_PDS = OFF_SL + NSL * Q_BYTES;   // [NPB][P | dS]
   static constexpr int OFF_BAR = OFF_PDS + NPB * 2 * PB;
   static constexpr int NUM_BARS = 2 + 2 * NSL + 6 + 4 * NPB + 4;
-  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;
+  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + kSmemAlignSlack;
   static constexpr uint32_t S_COL = 0, DP_COL = 128, ACC_COL = 256;
 };
 
 // K6 variant 5: the Q and dO tiles of a kept tile live in a 5-slot ring of 32 KB operand slots
-// (2.5 tiles in flight instead of 2 stages of [Q|dO]) and each slot is released by the MMA that
-// last reads it (dO after dV, Q after dK); P and dS share one smem buffer.
+// (2.5 tiles in flight instead of 2 stages of [Q|dO]).  Each operand has two readers issued by
+// different warps (Q: S and dKᵀ, dO: dP and dVᵀ), so its slot is released by two commits, one
+// per issuer; the dVᵀ issuer also waits for dO(g) to land (P(g) existing only proves S(g)
+// finished).  P and dS share one smem buffer.
 template <int HD, int EWW, int NSL_ = 5, int NPB_ = 1>
 __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
     k_dkdv5(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -1443,12 +1445,13 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
   constexpr int NPB = C::NPB;
   constexpr int EWT = 32 * EWW;  // elementwise threads
   constexpr int kDkvPolyPairs = R::CPT / SPA2_DKDV_POLY_PAIRS_DIV;
-  extern __shared__ __align__(1024) uint8_t smem[];
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* const smem = smem_align_1k(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* kv_full = bars;             // K/V of item `it` landed
   uint64_t* kv_empty = kv_full + 1;     // last S/dP MMA of item `it` done: K/V slot reusable
   uint64_t* sl_full = kv_empty + 1;     // [NSL] operand slot holds operand u (Q(g): u=2g, dO(g): u=2g+1)
-  uint64_t* sl_empty = sl_full + NSL;   // [NSL] the MMA reading operand u is done
+  uint64_t* sl_empty = sl_full + NSL;   // [NSL] both MMAs reading operand u are done
   uint64_t* s_full = sl_empty + NSL;    // [2] S of tile g in TMEM buffer g&1
   uint64_t* dp_full = s_full + 2;       // [2] dP of tile g
   uint64_t* sdp_read = dp_full + 2;     // [2] S and dP of tile g read out of TMEM
@@ -1462,12 +1465,11 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
 
   const int warp = (int)warp_id(), lane = (int)lane_id();
   if (threadIdx.x == 0) {
-    if (smem_u32(smem) & 1023u) __trap();
     mbar_init(kv_full, 2);  // two producers: warp 0 (K, Q) and warp PROD2 (V, dO)
     mbar_init(kv_empty, 1);
     for (int s = 0; s < NSL; ++s) {
       mbar_init(&sl_full[s], 1);
-      mbar_init(&sl_empty[s], 1);
+      mbar_init(&sl_empty[s], 2);  // released by the S/dP issuer AND the dVᵀ/dKᵀ issuer
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&s_full[s], 1);
@@ -1559,6 +1561,7 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
           mma_bf16_w(tbase + C::S_COL + b * 64, dQ + qo, dK + ko, idS, ks > 0 ? 1u : 0u);
         }
         mma_commit_w(&s_full[b]);
+        mma_commit_w(&sl_empty[uq % NSL]);  // S(g) no longer reads Q(g) once complete
         mbar_wait(&sl_full[ud % NSL], (uint32_t)(ud / NSL) & 1u);
         tc_fence_after();
 #pragma unroll
@@ -1568,6 +1571,7 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
           mma_bf16_w(tbase + C::DP_COL + b * 64, dDO + qo, dV + ko, idS, ks > 0 ? 1u : 0u);
         }
         mma_commit_w(&dp_full[b]);
+        mma_commit_w(&sl_empty[ud % NSL]);  // dP(g) no longer reads dO(g) once complete
         if (c.t == c.n - 1) mma_commit_w(kv_empty);  // K_j / V_j are only read by S and dP
       }
     } else {
@@ -1580,13 +1584,15 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
         const int pb = c.g % NPB;
         const uint64_t pbo = (uint64_t)pb * 2 * PB16;
         mbar_wait(&p_full[pb], (uint32_t)(c.g / NPB) & 1u);
+        // dVᵀ reads dO(g): P(g) only proves S(g) finished, not that dO(g) has landed
+        mbar_wait(&sl_full[ud % NSL], (uint32_t)(ud / NSL) & 1u);
         tc_fence_after();
         trace_ev(p.trace, p.trace_cap, 1, 4, c.g);
 #pragma unroll
         for (int ks = 0; ks < BQ / 16; ++ks)
           mma_bf16_w(acc, dDOm + (uint64_t)(ks * 128), dPm + pbo + (uint64_t)(ks * 128), idT, (!first || ks > 0) ? 1u : 0u);
         mma_commit_w(&p_free[pb]);
-        mma_commit_w(&sl_empty[ud % NSL]);  // dO(g) is no longer read
+        mma_commit_w(&sl_empty[ud % NSL]);  // dVᵀ(g) was the other reader of dO(g)
         mbar_wait(&ds_full[pb], (uint32_t)(c.g / NPB) & 1u);
         tc_fence_after();
         trace_ev(p.trace, p.trace_cap, 1, 5, c.g);
@@ -1594,7 +1600,7 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
         for (int ks = 0; ks < BQ / 16; ++ks)
           mma_bf16_w(acc + 64, dQm + (uint64_t)(ks * 128), dDSm + pbo + (uint64_t)(ks * 128), idT, (!first || ks > 0) ? 1u : 0u);
         mma_commit_w(&ds_free[pb]);
-        mma_commit_w(&sl_empty[uq % NSL]);  // Q(g) is no longer read
+        mma_commit_w(&sl_empty[uq % NSL]);  // dKᵀ(g) was the other reader of Q(g)
         if (c.t == c.n - 1) mma_commit_w(&acc_full[c.it & 1]);
       }
     }

@@ -54,7 +54,7 @@ struct FwdCfg {
   static constexpr int NUM_BARS = 1 + 4 * NS + 2 + 2 + 1 + 1;
   static constexpr int SMEM_USED = OFF_BAR + NUM_BARS * 8 + 16;
   // never let a third CTA share the SM's 512 TMEM columns
-  static constexpr int SMEM = SMEM_USED < 80 * 1024 ? 80 * 1024 : SMEM_USED;
+  static constexpr int SMEM = SMEM_USED + kSmemAlignSlack < 80 * 1024 ? 80 * 1024 : SMEM_USED + kSmemAlignSlack;
   static constexpr uint32_t O_COL = 128;
 };
 
@@ -78,7 +78,8 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
           const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, const FwdParams p) {
   using C = FwdCfg<HD, P_TMEM>;
   constexpr int NS = C::NS;
-  extern __shared__ __align__(1024) uint8_t smem[];
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* const smem = smem_align_1k(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* q_full = bars;
   uint64_t* k_full = bars + 1;
@@ -100,7 +101,6 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
   const int32_t* list = p.row_idx + beg;
 
   if (threadIdx.x == 0) {
-    if (smem_u32(smem) & 1023u) __trap();  // SWIZZLE_128B tiles need 1 KB alignment
     mbar_init(q_full, 1);
     for (int s = 0; s < NS; ++s) {
       mbar_init(&k_full[s], 1);
@@ -365,7 +365,7 @@ struct Fwd3Cfg {
   static constexpr int OFF_BAR = OFF_V + NS * KV_BYTES;
   static constexpr int NUM_BARS = 2 + 4 * NS + 2 * 3 + 2;
   static constexpr int SMEM_USED = OFF_BAR + NUM_BARS * 8 + 16;
-  static constexpr int SMEM = SMEM_USED < 80 * 1024 ? 80 * 1024 : SMEM_USED;
+  static constexpr int SMEM = SMEM_USED + kSmemAlignSlack < 80 * 1024 ? 80 * 1024 : SMEM_USED + kSmemAlignSlack;
   static constexpr uint32_t O_COL = 128;
 };
 
@@ -383,7 +383,8 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
            const __grid_constant__ CUtensorMap tmV, const FwdParams p, int num_items) {
   using C = Fwd3Cfg<HD>;
   constexpr int NS = C::NS;
-  extern __shared__ __align__(1024) uint8_t smem[];
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* const smem = smem_align_1k(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* q_full = bars;            // Q of item `it` landed
   uint64_t* q_empty = bars + 1;       // last S MMA of item `it` done
@@ -400,7 +401,6 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
 
   const int warp = (int)warp_id(), lane = (int)lane_id();
   if (threadIdx.x == 0) {
-    if (smem_u32(smem) & 1023u) __trap();
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
     for (int s = 0; s < NS; ++s) {
@@ -679,7 +679,7 @@ struct Fwd2Cfg {
   static constexpr int OFF_RED = OFF_V + NV * KV_BYTES;  // float [2 groups][2 (m, l)][128 rows]
   static constexpr int OFF_BAR = OFF_RED + 4 * BQ * 4;
   static constexpr int NUM_BARS = 4 + 2 * NK + 2 * NV + 2 * 3 + 2;
-  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16;
+  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + kSmemAlignSlack;
   static constexpr uint32_t Q_COL = 0, S_COL = 64, O_COL = 256;  // group x: S at S_COL + 64x, O at O_COL + 128x
 };
 
@@ -702,7 +702,8 @@ __global__ void __launch_bounds__(kFwd2Threads, 1)
            const __grid_constant__ CUtensorMap tmV, const FwdParams p, int num_items) {
   using C = Fwd2Cfg<HD>;
   constexpr int NK = C::NK, NV = C::NV;
-  extern __shared__ __align__(1024) uint8_t smem[];
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* const smem = smem_align_1k(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint64_t* qs_full = bars;            // Q of item `it` staged
   uint64_t* qs_free = bars + 1;        // its tcgen05.cp done
@@ -722,7 +723,6 @@ __global__ void __launch_bounds__(kFwd2Threads, 1)
 
   const int warp = (int)warp_id(), lane = (int)lane_id();
   if (threadIdx.x == 0) {
-    if (smem_u32(smem) & 1023u) __trap();
     mbar_init(qs_full, 1);
     mbar_init(qs_free, 1);
     mbar_init(qd_free, 2);  // both S warps done with the item

@@ -87,15 +87,32 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   if (mbar_try_wait(addr, parity)) return;
+#ifdef SPA2_DEBUG_WAIT
+  // diagnostic build: name the stuck barrier after SPA2_WATCHDOG_NS of wall time
   const uint64_t t0 = globaltimer();
   uint32_t spins = 0;
   while (!mbar_try_wait(addr, parity)) {
     if ((++spins & 1023u) == 0 && globaltimer() - t0 > SPA2_WATCHDOG_NS) {
-      printf("spa2 watchdog: block (%d,%d,%d) thread %d stuck on mbarrier %u parity %u\n", blockIdx.x,
-             blockIdx.y, blockIdx.z, threadIdx.x, addr, parity);
+      printf("spa2 watchdog: block %d/%d (%d threads) thread %d stuck on mbarrier smem+%u parity %u\n",
+             blockIdx.x, gridDim.x, blockDim.x, threadIdx.x, addr, parity);
       __trap();
     }
   }
+#else
+  // production: a bare spin with a wall-clock backstop read only every 2^16 failed polls,
+  // on the 32-bit nanosecond timer (wrap-safe difference; one register): trap after ~2 s
+  // instead of hanging the GPU.  The every-poll timer + printf variant above costs 2-4 % in
+  // the hot loops (register pressure, stack).
+  uint32_t spins = 0, t0 = 0;
+  while (!mbar_try_wait(addr, parity)) {
+    if ((++spins & 0xFFFFu) == 0) {
+      uint32_t now;
+      asm volatile("mov.u32 %0, %%globaltimer_lo;" : "=r"(now));
+      if (spins == 0x10000u) t0 = now;
+      else if (now - t0 > 2000000000u) __trap();
+    }
+  }
+#endif
 }
 
 // ---- fences --------------------------------------------------------------------------
@@ -376,6 +393,16 @@ __device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
                : "r"(addr)
                : "memory");
   return v;
+}
+
+// Dynamic shared memory base, rounded up to 1 KB (SWIZZLE_128B tiles and UMMA descriptors
+// need it).  The runtime only guarantees a small alignment for the dynamic window: a CTA that
+// shares its SM with CTAs of another kernel (programmatic dependent launch overlap, two CTAs
+// per SM) can start at any 128-byte boundary, so every kernel reserves kSmemAlignSlack extra.
+constexpr int kSmemAlignSlack = 1024;
+__device__ __forceinline__ uint8_t* smem_align_1k(uint8_t* p) {
+  const uint32_t a = smem_u32(p);
+  return p + (((a + 1023u) & ~1023u) - a);
 }
 
 }  // namespace ptx
