@@ -63,12 +63,21 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 }
 __device__ __forceinline__ uint32_t mbar_try_wait(uint32_t addr, uint32_t parity) {
   uint32_t ok;
+#ifdef SPA2_WAIT_HINT_NS
+  asm volatile(
+      "{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity), "n"(SPA2_WAIT_HINT_NS)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred P;\n\tmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
       "selp.u32 %0, 1, 0, P;\n\t}"
       : "=r"(ok)
       : "r"(addr), "r"(parity)
       : "memory");
+#endif
   return ok;
 }
 // Non-blocking probe: has the phase with parity `parity` of `bar` completed?
@@ -105,6 +114,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   // the hot loops (register pressure, stack).
   uint32_t spins = 0, t0 = 0;
   while (!mbar_try_wait(addr, parity)) {
+#ifdef SPA2_WAIT_SLEEP_NS
+    if (spins >= 8) __nanosleep(SPA2_WAIT_SLEEP_NS);
+#endif
     if ((++spins & 0xFFFFu) == 0) {
       uint32_t now;
       asm volatile("mov.u32 %0, %%globaltimer_lo;" : "=r"(now));
