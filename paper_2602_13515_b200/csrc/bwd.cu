@@ -34,6 +34,20 @@
 namespace spa2 {
 namespace {
 
+// Share of the elementwise exponentials computed by exp2_poly2 on the FMA pipe instead of
+// MUFU: CPT*NUM/64 of each thread's CPT/2 pairs (NUM = 8: a quarter).
+#ifndef SPA2_DQ_POLY_NUM
+#define SPA2_DQ_POLY_NUM 8
+#endif
+#ifndef SPA2_DKDV_POLY_NUM
+#define SPA2_DKDV_POLY_NUM 8
+#endif
+#ifndef SPA2_DQ_NK
+#define SPA2_DQ_NK 4
+#endif
+#ifndef SPA2_DQ_NV
+#define SPA2_DQ_NV 4
+#endif
 using namespace ptx;
 
 constexpr int BQ = 128;
@@ -58,7 +72,6 @@ struct BwdParams {
   int64_t o1_sb, o1_sh, o1_sn;
   unsigned long long* trace;  // diagnostic (spa2_debug_trace), normally null
   int trace_cap;
-  int dbg;                    // diagnostic timing experiments (SPA2_DEBUG_FLAGS), normally 0
   // fused δ (k_dq3 with delta_out != null): δ = rowsum(dO ∘ O) computed in the kernel
   const __nv_bfloat16* o_in;
   int64_t oi_sb, oi_sh, oi_sn;
@@ -709,7 +722,7 @@ struct Dq3Roles {
 
 template <int HD>
 struct Dq3Cfg {
-  static constexpr int NK = 4, NV = 4;
+  static constexpr int NK = SPA2_DQ_NK, NV = SPA2_DQ_NV;  // K / V ring depths
   static constexpr int Q_BYTES = BQ * HD * 2;
   static constexpr int KV_BYTES = BKV * HD * 2;
   static constexpr int OFF_QS = 0;  // staging [Q | dO] of the next item
@@ -737,7 +750,7 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
   using R = Dq3Roles<EWW>;
   constexpr int NK = C::NK, NV = C::NV;
   constexpr int CPT = R::CPT;
-  constexpr int kPolyPairs = CPT / 8;
+  constexpr int kPolyPairs = CPT * SPA2_DQ_POLY_NUM / 64;  // of CPT/2 pairs
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* const smem = smem_align_1k(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
@@ -944,12 +957,6 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
         mbar_wait(&s_full[b], (uint32_t)(g >> 1) & 1u);
         if (threadIdx.x == 64) trace_ev(p.trace, p.trace_cap, 2, 2, g);
         tc_fence_after();
-        if (p.dbg & 1) {  // timing experiment: no elementwise work
-          tc_fence_before();
-          mbar_arrive(&s_free[b]);
-          mbar_arrive(&ds_full[b]);
-          continue;
-        }
         uint32_t sr[CPT];
         if constexpr (CPT == 32) tmem_ld32(sb + (uint32_t)col0, sr);
         else tmem_ld16(sb + (uint32_t)col0, sr);
@@ -1095,9 +1102,6 @@ bool dq_variant2() {
 
 // Warp roles: 0 TMA (K, Q), 1 MMA, 2 .. 2+EWW-1 elementwise (EWW/4 warps per TMEM lane
 // quarter, 256/EWW columns each), then 4 epilogue warps, then TMA (V, dO).
-#ifndef SPA2_DKDV_POLY_PAIRS_DIV
-#define SPA2_DKDV_POLY_PAIRS_DIV 8
-#endif
 template <int EWW>
 struct DkvRoles {
   static constexpr int EPI0 = 2 + EWW;           // first epilogue warp
@@ -1130,7 +1134,7 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
   using R = DkvRoles<EWW>;
   constexpr int NS = C::NS;
   constexpr int EWT = 32 * EWW;  // elementwise threads
-  constexpr int kDkvPolyPairs = R::CPT / SPA2_DKDV_POLY_PAIRS_DIV;
+  constexpr int kDkvPolyPairs = R::CPT * SPA2_DKDV_POLY_NUM / 64;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* const smem = smem_align_1k(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
@@ -1444,7 +1448,7 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
   constexpr int NSL = C::NSL;
   constexpr int NPB = C::NPB;
   constexpr int EWT = 32 * EWW;  // elementwise threads
-  constexpr int kDkvPolyPairs = R::CPT / SPA2_DKDV_POLY_PAIRS_DIV;
+  constexpr int kDkvPolyPairs = R::CPT * SPA2_DKDV_POLY_NUM / 64;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* const smem = smem_align_1k(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
@@ -1826,13 +1830,6 @@ int launch_attn_bwd(int which, const spa2_view& q, const spa2_view& k, const spa
     prm.do_in = fd->dout;
     prm.di_sb = fd->d_sb, prm.di_sh = fd->d_sh, prm.di_sn = fd->d_sn;
     prm.delta_out = fd->delta;
-  }
-  {
-    static const int dbg = [] {
-      const char* e = getenv("SPA2_DEBUG_FLAGS");
-      return e != nullptr ? atoi(e) : 0;
-    }();
-    prm.dbg = dbg;
   }
   const unsigned grid = (unsigned)std::min<int64_t>(prm.num_items, num_sms());
   if (which == 0 && dq_variant() == 3) {

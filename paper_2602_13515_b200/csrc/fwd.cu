@@ -354,6 +354,9 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
 // S[g&1] at 0 / 64 (P overwrites its first 32 columns), O at 128.
 // Warps: 0 TMA (Q, K ring), 1 MMA (S, PV), 2-5 softmax + epilogue, 6 TMA (V ring).
 // ---------------------------------------------------------------------------------------
+#ifndef SPA2_FWD3_POLY_PAIRS
+#define SPA2_FWD3_POLY_PAIRS 10  // of 32 exponential pairs per row and tile (exp2_poly2 on the FMA pipe)
+#endif
 template <int HD>
 struct Fwd3Cfg {
   static constexpr int NS = (HD == 128) ? 2 : 4;
@@ -601,7 +604,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
         for (int c = 0; c < 32; ++c) {
           const float2 x = __ffma2_rn(make_float2(sv[2 * c], sv[2 * c + 1]), make_float2(sl2, sl2), make_float2(-m, -m));
           float2 e;
-          if (c < 8) {  // a quarter of the exponentials on the FMA pipe
+          if (c < SPA2_FWD3_POLY_PAIRS) {  // part of the exponentials on the FMA pipe
             e = exp2_poly2(x);
           } else {
             e.x = ex2(x.x);
