@@ -178,6 +178,9 @@ int spa2_probe_tma_rate(const void* buf, long long rows, int box_rows, int stage
 int spa2_probe_mma_mix(int reps, int flags, int ctas, const void* gsrc, unsigned long long* cycles, void* stream);
 /* Diagnostic: tcgen05.ld / tcgen05.st throughput (mode 0 32-col loads, 1 two loads per wait,
  * 2 16-col loads, 3 16-col stores), `warps` warps per CTA (<= 16); cycles[ctas * 16] per warp. */
+/* Diagnostic: cycles per mbarrier try_wait (mode 0) / test_wait (1) / mbar_wait (2) on an
+ * already-completed phase, one CTA of `threads` threads; cycles[0] = total for `reps` polls. */
+int spa2_probe_mbar_latency(int reps, int mode, int threads, unsigned long long* cycles, void* stream);
 int spa2_probe_tmem_rate(int reps, int mode, int warps, int ctas, unsigned long long* cycles, void* stream);
 int spa2_probe_tma_rate2(const void* buf, long long rows, int box_rows, int chunks, int stages, int issuers,
                          int mode, int iters, int ctas, unsigned long long* cycles, void* stream);

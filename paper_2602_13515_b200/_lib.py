@@ -65,6 +65,7 @@ SIGNATURES = {
     "spa2_debug_trace": ([_P, _I32], _I32),
     "spa2_probe_tma_rate": ([_P, ctypes.c_longlong, _I32, _I32, _I32, _I32, _P, _P], _I32),
     "spa2_probe_mma_mix": ([_I32, _I32, _I32, _P, _P, _P], _I32),
+    "spa2_probe_mbar_latency": ([_I32, _I32, _I32, _P, _P], _I32),
     "spa2_probe_tmem_rate": ([_I32, _I32, _I32, _I32, _P, _P], _I32),
     "spa2_probe_tma_rate2": ([_P, ctypes.c_longlong, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P, _P], _I32),
 }

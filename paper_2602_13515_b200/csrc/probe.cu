@@ -639,3 +639,40 @@ extern "C" int spa2_probe_tmem_rate(int reps, int mode, int warps, int ctas, uns
   SPA2_LAUNCH_CHECK();
   return SPA2_OK;
 }
+
+// ---- mbarrier wait latency probe (diagnostic): cycles per try_wait / test_wait on a phase
+// that has ALREADY completed (the cost a consumer pays even when it never has to wait) ----
+namespace spa2 {
+namespace {
+__global__ void k_mbar_lat(int reps, int mode, unsigned long long* cycles) {
+  __shared__ uint64_t bar;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) mbar_arrive(&bar);  // phase 0 completes
+  __syncthreads();
+  uint32_t ok = 0;
+  const uint64_t t0 = clock64();
+  for (int i = 0; i < reps; ++i) {
+    if (mode == 0) ok += mbar_try_wait(smem_u32(&bar), 0u);
+    else if (mode == 1) ok += mbar_test(&bar, 0u) ? 1u : 0u;
+    else {
+      mbar_wait(&bar, 0u);
+      ok += 1;
+    }
+  }
+  const uint64_t t1 = clock64();
+  if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
+  if (ok == 0xdeadbeefu) cycles[1] = ok;
+}
+}  // namespace
+}  // namespace spa2
+
+// mode 0: mbarrier.try_wait, 1: mbarrier.test_wait, 2: mbar_wait() — each on a completed phase.
+extern "C" int spa2_probe_mbar_latency(int reps, int mode, int threads, unsigned long long* cycles, void* stream) {
+  k_mbar_lat<<<1, threads, 0, (cudaStream_t)stream>>>(reps, mode, cycles);
+  SPA2_LAUNCH_CHECK();
+  return SPA2_OK;
+}

@@ -32,3 +32,12 @@ for mode, label in ((4, "ld 32 col + N=128 MMAs"), (5, "ld 32 col + N=64 MMAs"))
         torch.cuda.synchronize()
         c = cyc.view(ctas, 16)[:, 1:warps].float()
         print(f"{label:24s} ld warps {warps - 1}: {c.mean().item() / reps:7.1f} cyc/instr per warp")
+
+# mbarrier polls on an already-completed phase
+mb = torch.zeros(4, dtype=torch.int64, device="cuda")
+for mode, label in ((0, "try_wait"), (1, "test_wait"), (2, "mbar_wait()")):
+    for threads in (32, 512):
+        mb.zero_()
+        _lib.check(lib.spa2_probe_mbar_latency(4096, mode, threads, _lib.ptr(mb), st), "mbar")
+        torch.cuda.synchronize()
+        print(f"mbarrier {label:12s} {threads:3d} threads: {mb[0].item() / 4096:6.1f} cycles per poll (completed phase)")

@@ -64,3 +64,17 @@ print("per-warp dS-written times relative to warp 2 (cycles), tiles", lo, "..", 
 for g in range(lo, lo + 6):
     if g in x and 0 in x[g]:
         print(g, [x[g].get(w, 0) - x[g][0] for w in range(8)])
+
+# per-stage averages over all tiles of CTA 0
+import collections
+by = collections.defaultdict(dict)
+for t, kd, g in ev:
+    by[g][kd] = t
+def avg(a, b):
+    v = [x[b] - x[a] for x in by.values() if a in x and b in x]
+    return sum(v) / max(1, len(v))
+for a, b in (("E1", "E2"), ("E2", "E3"), ("E3", "E4"), ("M2", "M3"), ("M3", "E2"), ("E4", "M4"), ("M4", "M5"), ("P2", "M2")):
+    print(f"{a}->{b}: {avg(a, b):.0f} cycles")
+
+ready = sum(1 for x in by.values() if "E6" in x)
+print(f"S already landed when the elementwise warps arrived: {ready} of {len(by)} tiles")
