@@ -76,5 +76,3 @@ def avg(a, b):
 for a, b in (("E1", "E2"), ("E2", "E3"), ("E3", "E4"), ("M2", "M3"), ("M3", "E2"), ("E4", "M4"), ("M4", "M5"), ("P2", "M2")):
     print(f"{a}->{b}: {avg(a, b):.0f} cycles")
 
-ready = sum(1 for x in by.values() if "E6" in x)
-print(f"S already landed when the elementwise warps arrived: {ready} of {len(by)} tiles")
