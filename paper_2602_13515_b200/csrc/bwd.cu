@@ -878,10 +878,17 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
         trace_ev(p.trace, p.trace_cap, 1, 2, c.g);
         const uint64_t dK = dK0 + (uint64_t)sk * KV16;
         const uint32_t sb = tbase + C::SDP_COL + (uint32_t)(b * 128);
+#ifdef SPA2_MMA_BATCH
+        if constexpr (HD == 128) {
+          mma_bf16_ts_k8_w<8u, 2ull, (uint64_t)(BKV * 128 / 16)>(sb, tbase + C::Q_COL, dK, idS, 0u);
+        } else
+#endif
+        {
 #pragma unroll
-        for (int ks = 0; ks < HD / 16; ++ks)
-          mma_bf16_ts_w(sb, tbase + C::Q_COL + (uint32_t)(ks * 8),
-                        dK + (uint64_t)((((ks * 16 / 64) * BKV * 128 + (ks * 16 % 64) * 2)) >> 4), idS, ks > 0 ? 1u : 0u);
+          for (int ks = 0; ks < HD / 16; ++ks)
+            mma_bf16_ts_w(sb, tbase + C::Q_COL + (uint32_t)(ks * 8),
+                          dK + (uint64_t)((((ks * 16 / 64) * BKV * 128 + (ks * 16 % 64) * 2)) >> 4), idS, ks > 0 ? 1u : 0u);
+        }
         mma_commit_w(&s_full[b]);
         if (c.t == c.n - 1) mma_commit_w(qd_free);
         trace_ev(p.trace, p.trace_cap, 1, 3, c.g);
@@ -895,10 +902,17 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
         tc_fence_after();
         const uint64_t dV = dV0 + (uint64_t)sv * KV16;
         const uint32_t sb = tbase + C::SDP_COL + (uint32_t)(b * 128) + 64u;
+#ifdef SPA2_MMA_BATCH
+        if constexpr (HD == 128) {
+          mma_bf16_ts_k8_w<8u, 2ull, (uint64_t)(BKV * 128 / 16)>(sb, tbase + C::DO_COL, dV, idS, 0u);
+        } else
+#endif
+        {
 #pragma unroll
-        for (int ks = 0; ks < HD / 16; ++ks)
-          mma_bf16_ts_w(sb, tbase + C::DO_COL + (uint32_t)(ks * 8),
-                        dV + (uint64_t)((((ks * 16 / 64) * BKV * 128 + (ks * 16 % 64) * 2)) >> 4), idS, ks > 0 ? 1u : 0u);
+          for (int ks = 0; ks < HD / 16; ++ks)
+            mma_bf16_ts_w(sb, tbase + C::DO_COL + (uint32_t)(ks * 8),
+                          dV + (uint64_t)((((ks * 16 / 64) * BKV * 128 + (ks * 16 % 64) * 2)) >> 4), idS, ks > 0 ? 1u : 0u);
+        }
         mma_commit_w(&dp_full[b]);
         mma_commit_w(&v_empty[sv]);
         if (c.t == c.n - 1) mma_commit_w(qd_free);
@@ -912,10 +926,17 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
         trace_ev(p.trace, p.trace_cap, 1, 4, c.g);
         const uint64_t dKm = dKm0 + (uint64_t)sk * KV16;
         const uint32_t sb = tbase + C::SDP_COL + (uint32_t)(b * 128);
+#ifdef SPA2_MMA_BATCH
+        if constexpr (CPT == 16) {
+          mma_bf16_ts_k4_w<16u, 128ull>(tbase + C::ACC_COL, sb + 64u, dKm, idQ, c.t > 0 ? 1u : 0u);
+        } else
+#endif
+        {
 #pragma unroll
-        for (int ks = 0; ks < BKV / 16; ++ks)
-          mma_bf16_ts_w(tbase + C::ACC_COL, sb + 64u + ds_col<CPT>(ks), dKm + (uint64_t)((ks * 2048) >> 4), idQ,
-                        (c.t > 0 || ks > 0) ? 1u : 0u);
+          for (int ks = 0; ks < BKV / 16; ++ks)
+            mma_bf16_ts_w(tbase + C::ACC_COL, sb + 64u + ds_col<CPT>(ks), dKm + (uint64_t)((ks * 2048) >> 4), idQ,
+                          (c.t > 0 || ks > 0) ? 1u : 0u);
+        }
         mma_commit_w(&dq_done[b]);
         mma_commit_w(&k_empty[sk]);
         if (c.t == c.n - 1) mma_commit_w(acc_full);
@@ -956,6 +977,13 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
         if (threadIdx.x == 64) trace_ev(p.trace, p.trace_cap, 2, 1, g);
         mbar_wait(&s_full[b], (uint32_t)(g >> 1) & 1u);
         if (threadIdx.x == 64) trace_ev(p.trace, p.trace_cap, 2, 2, g);
+#ifdef SPA2_DQ_NOEW
+        // timing experiment (wrong results): keep the barrier protocol, skip the elementwise work
+        mbar_arrive(&s_free[b]);
+        mbar_wait(&dp_full[b], (uint32_t)(g >> 1) & 1u);
+        mbar_arrive(&ds_full[b]);
+        continue;
+#endif
         tc_fence_after();
         uint32_t sr[CPT];
         if constexpr (CPT == 32) tmem_ld32(sb + (uint32_t)col0, sr);
@@ -1558,21 +1586,37 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
         tc_fence_after();
         trace_ev(p.trace, p.trace_cap, 1, 2, c.g);
         const uint64_t dQ = dSLk0 + (uint64_t)(uq % NSL) * SLOT16, dDO = dSLk0 + (uint64_t)(ud % NSL) * SLOT16;
+#ifdef SPA2_MMA_BATCH
+        if constexpr (HD == 128) {
+          mma_bf16_ss_k8_w<2ull, (uint64_t)(BQ * 128 / 16), 2ull, (uint64_t)(BKV * 128 / 16)>(tbase + C::S_COL + b * 64, dQ, dK,
+                                                                                            idS, 0u);
+        } else
+#endif
+        {
 #pragma unroll
-        for (int ks = 0; ks < HD / 16; ++ks) {
-          const uint64_t qo = (uint64_t)(((ks * 16 / 64) * BQ * 128 + (ks * 16 % 64) * 2) >> 4);
-          const uint64_t ko = (uint64_t)(((ks * 16 / 64) * BKV * 128 + (ks * 16 % 64) * 2) >> 4);
-          mma_bf16_w(tbase + C::S_COL + b * 64, dQ + qo, dK + ko, idS, ks > 0 ? 1u : 0u);
+          for (int ks = 0; ks < HD / 16; ++ks) {
+            const uint64_t qo = (uint64_t)(((ks * 16 / 64) * BQ * 128 + (ks * 16 % 64) * 2) >> 4);
+            const uint64_t ko = (uint64_t)(((ks * 16 / 64) * BKV * 128 + (ks * 16 % 64) * 2) >> 4);
+            mma_bf16_w(tbase + C::S_COL + b * 64, dQ + qo, dK + ko, idS, ks > 0 ? 1u : 0u);
+          }
         }
         mma_commit_w(&s_full[b]);
         mma_commit_w(&sl_empty[uq % NSL]);  // S(g) no longer reads Q(g) once complete
         mbar_wait(&sl_full[ud % NSL], (uint32_t)(ud / NSL) & 1u);
         tc_fence_after();
+#ifdef SPA2_MMA_BATCH
+        if constexpr (HD == 128) {
+          mma_bf16_ss_k8_w<2ull, (uint64_t)(BQ * 128 / 16), 2ull, (uint64_t)(BKV * 128 / 16)>(tbase + C::DP_COL + b * 64, dDO,
+                                                                                            dV, idS, 0u);
+        } else
+#endif
+        {
 #pragma unroll
-        for (int ks = 0; ks < HD / 16; ++ks) {
-          const uint64_t qo = (uint64_t)(((ks * 16 / 64) * BQ * 128 + (ks * 16 % 64) * 2) >> 4);
-          const uint64_t ko = (uint64_t)(((ks * 16 / 64) * BKV * 128 + (ks * 16 % 64) * 2) >> 4);
-          mma_bf16_w(tbase + C::DP_COL + b * 64, dDO + qo, dV + ko, idS, ks > 0 ? 1u : 0u);
+          for (int ks = 0; ks < HD / 16; ++ks) {
+            const uint64_t qo = (uint64_t)(((ks * 16 / 64) * BQ * 128 + (ks * 16 % 64) * 2) >> 4);
+            const uint64_t ko = (uint64_t)(((ks * 16 / 64) * BKV * 128 + (ks * 16 % 64) * 2) >> 4);
+            mma_bf16_w(tbase + C::DP_COL + b * 64, dDO + qo, dV + ko, idS, ks > 0 ? 1u : 0u);
+          }
         }
         mma_commit_w(&dp_full[b]);
         mma_commit_w(&sl_empty[ud % NSL]);  // dP(g) no longer reads dO(g) once complete
@@ -1592,17 +1636,25 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
         mbar_wait(&sl_full[ud % NSL], (uint32_t)(ud / NSL) & 1u);
         tc_fence_after();
         trace_ev(p.trace, p.trace_cap, 1, 4, c.g);
+#ifdef SPA2_MMA_BATCH
+        mma_bf16_ss_k8_w<128ull, 512ull, 128ull, 512ull>(acc, dDOm, dPm + pbo, idT, first ? 0u : 1u);
+#else
 #pragma unroll
         for (int ks = 0; ks < BQ / 16; ++ks)
           mma_bf16_w(acc, dDOm + (uint64_t)(ks * 128), dPm + pbo + (uint64_t)(ks * 128), idT, (!first || ks > 0) ? 1u : 0u);
+#endif
         mma_commit_w(&p_free[pb]);
         mma_commit_w(&sl_empty[ud % NSL]);  // dVᵀ(g) was the other reader of dO(g)
         mbar_wait(&ds_full[pb], (uint32_t)(c.g / NPB) & 1u);
         tc_fence_after();
         trace_ev(p.trace, p.trace_cap, 1, 5, c.g);
+#ifdef SPA2_MMA_BATCH
+        mma_bf16_ss_k8_w<128ull, 512ull, 128ull, 512ull>(acc + 64, dQm, dDSm + pbo, idT, first ? 0u : 1u);
+#else
 #pragma unroll
         for (int ks = 0; ks < BQ / 16; ++ks)
           mma_bf16_w(acc + 64, dQm + (uint64_t)(ks * 128), dDSm + pbo + (uint64_t)(ks * 128), idT, (!first || ks > 0) ? 1u : 0u);
+#endif
         mma_commit_w(&ds_free[pb]);
         mma_commit_w(&sl_empty[uq % NSL]);  // dKᵀ(g) was the other reader of Q(g)
         if (c.t == c.n - 1) mma_commit_w(&acc_full[c.it & 1]);

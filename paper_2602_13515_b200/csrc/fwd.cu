@@ -488,10 +488,14 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
       tc_fence_after();
       trace_ev(p.trace, p.trace_cap, 1, 4, pv_g);
       const uint64_t dV = dV0 + (uint64_t)s * KV16;
+#ifdef SPA2_MMA_BATCH
+      mma_bf16_ts_k4_w<8u, 128ull>(tbase + C::O_COL, tbase + (uint32_t)(b * 64), dV, idO, pv_first ? 0u : 1u);
+#else
 #pragma unroll
       for (int ks = 0; ks < BKV / 16; ++ks)
         mma_bf16_ts_w(tbase + C::O_COL, tbase + (uint32_t)(b * 64 + ks * 8), dV + (uint64_t)(ks * 128), idO,
                       (!pv_first || ks > 0) ? 1u : 0u);
+#endif
       mma_commit_w(&o_done[b]);
       mma_commit_w(&v_empty[s]);
       if (pv_last) mma_commit_w(acc_full);
@@ -509,11 +513,19 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
         tc_fence_after();
         trace_ev(p.trace, p.trace_cap, 1, 2, g);
         const uint64_t dK = dK0 + (uint64_t)s * KV16;
+#ifdef SPA2_MMA_BATCH
+        if constexpr (HD == 128) {
+          mma_bf16_ss_k8_w<2ull, (uint64_t)(BQ * 128 / 16), 2ull, (uint64_t)(BKV * 128 / 16)>(tbase + (uint32_t)(b * 64), dQ,
+                                                                                            dK, idS, 0u);
+        } else
+#endif
+        {
 #pragma unroll
-        for (int ks = 0; ks < HD / 16; ++ks) {
-          const int k0 = ks * 16;
-          mma_bf16_w(tbase + (uint32_t)(b * 64), dQ + (uint64_t)(((k0 / 64) * BQ * 128 + (k0 % 64) * 2) >> 4),
-                     dK + (uint64_t)(((k0 / 64) * BKV * 128 + (k0 % 64) * 2) >> 4), idS, ks > 0 ? 1u : 0u);
+          for (int ks = 0; ks < HD / 16; ++ks) {
+            const int k0 = ks * 16;
+            mma_bf16_w(tbase + (uint32_t)(b * 64), dQ + (uint64_t)(((k0 / 64) * BQ * 128 + (k0 % 64) * 2) >> 4),
+                       dK + (uint64_t)(((k0 / 64) * BKV * 128 + (k0 % 64) * 2) >> 4), idS, ks > 0 ? 1u : 0u);
+          }
         }
         mma_commit_w(&s_full[b]);
         mma_commit_w(&k_empty[s]);
