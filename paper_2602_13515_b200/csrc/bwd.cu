@@ -893,12 +893,18 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
         if (c.t == c.n - 1) mma_commit_w(qd_free);
         trace_ev(p.trace, p.trace_cap, 1, 3, c.g);
       }
-    } else if (warp == R::ISSUE_DP) {
-      for (; c.valid; cursor_next(c, p, p.T_m)) {
-        if (c.t == 0) mbar_wait(qd_ready, (uint32_t)c.it & 1u);
-        const int b = c.g & 1, sv = c.g % NV;
-        if (c.g >= 2) mbar_wait(&dq_done[b], (uint32_t)((c.g - 2) >> 1) & 1u);
-        mbar_wait(&v_full[sv], (uint32_t)(c.g / NV) & 1u);
+    } else {
+      // dP = dO V_jᵀ (TS) and dQ += dS K_j (TS), by two warps (dP(g) waits for dQ(g-2) to
+      // COMPLETE: it overwrites the TMEM columns dQ(g-2) reads dS from).  With
+      // -DSPA2_DQ_MERGED one warp issues both as dQ(g-2), dP(g), ...: tcgen05 MMAs issued by
+      // one thread execute in issue order, so the completion wait disappears.
+      auto issue_dp = [&](const Cursor& cc) {
+        if (cc.t == 0) mbar_wait(qd_ready, (uint32_t)cc.it & 1u);
+        const int b = cc.g & 1, sv = cc.g % NV;
+#ifndef SPA2_DQ_MERGED
+        if (cc.g >= 2) mbar_wait(&dq_done[b], (uint32_t)((cc.g - 2) >> 1) & 1u);
+#endif
+        mbar_wait(&v_full[sv], (uint32_t)(cc.g / NV) & 1u);
         tc_fence_after();
         const uint64_t dV = dV0 + (uint64_t)sv * KV16;
         const uint32_t sb = tbase + C::SDP_COL + (uint32_t)(b * 128) + 64u;
@@ -915,33 +921,61 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
         }
         mma_commit_w(&dp_full[b]);
         mma_commit_w(&v_empty[sv]);
-        if (c.t == c.n - 1) mma_commit_w(qd_free);
-      }
-    } else {
-      for (; c.valid; cursor_next(c, p, p.T_m)) {
-        const int b = c.g & 1, sk = c.g % NK;
-        if (c.t == 0 && c.it >= 1) mbar_wait(acc_empty, (uint32_t)(c.it - 1) & 1u);
-        mbar_wait(&ds_full[b], (uint32_t)(c.g >> 1) & 1u);
+        if (cc.t == cc.n - 1) mma_commit_w(qd_free);
+      };
+      auto issue_dq = [&](const Cursor& cc) {
+        const int b = cc.g & 1, sk = cc.g % NK;
+        if (cc.t == 0 && cc.it >= 1) mbar_wait(acc_empty, (uint32_t)(cc.it - 1) & 1u);
+        mbar_wait(&ds_full[b], (uint32_t)(cc.g >> 1) & 1u);
         tc_fence_after();
-        trace_ev(p.trace, p.trace_cap, 1, 4, c.g);
+        trace_ev(p.trace, p.trace_cap, 1, 4, cc.g);
         const uint64_t dKm = dKm0 + (uint64_t)sk * KV16;
         const uint32_t sb = tbase + C::SDP_COL + (uint32_t)(b * 128);
 #ifdef SPA2_MMA_BATCH
         if constexpr (CPT == 16) {
-          mma_bf16_ts_k4_w<16u, 128ull>(tbase + C::ACC_COL, sb + 64u, dKm, idQ, c.t > 0 ? 1u : 0u);
+          mma_bf16_ts_k4_w<16u, 128ull>(tbase + C::ACC_COL, sb + 64u, dKm, idQ, cc.t > 0 ? 1u : 0u);
         } else
 #endif
         {
 #pragma unroll
           for (int ks = 0; ks < BKV / 16; ++ks)
             mma_bf16_ts_w(tbase + C::ACC_COL, sb + 64u + ds_col<CPT>(ks), dKm + (uint64_t)((ks * 2048) >> 4), idQ,
-                          (c.t > 0 || ks > 0) ? 1u : 0u);
+                          (cc.t > 0 || ks > 0) ? 1u : 0u);
         }
+#ifndef SPA2_DQ_MERGED
         mma_commit_w(&dq_done[b]);
+#endif
         mma_commit_w(&k_empty[sk]);
-        if (c.t == c.n - 1) mma_commit_w(acc_full);
-        trace_ev(p.trace, p.trace_cap, 1, 5, c.g);
+        if (cc.t == cc.n - 1) mma_commit_w(acc_full);
+        trace_ev(p.trace, p.trace_cap, 1, 5, cc.g);
+      };
+#ifdef SPA2_DQ_MERGED
+      if (warp == R::ISSUE_DP) {
+        // order dQ(g-2), dP(g): dP(g) reuses the TMEM buffer of tile g-2, and dQ(g-2) (its dS
+        // reader) is issued just before it by this thread
+        Cursor q0 = c, q1 = c;  // pending dQ tiles g-2, g-1
+        int pending = 0;
+        for (; c.valid; cursor_next(c, p, p.T_m)) {
+          if (pending == 2) {
+            issue_dq(q0);
+            q0 = q1;
+            pending = 1;
+          }
+          issue_dp(c);
+          if (pending == 0) q0 = c;
+          else q1 = c;
+          ++pending;
+        }
+        if (pending >= 1) issue_dq(q0);
+        if (pending == 2) issue_dq(q1);
       }
+#else
+      if (warp == R::ISSUE_DP) {
+        for (; c.valid; cursor_next(c, p, p.T_m)) issue_dp(c);
+      } else {
+        for (; c.valid; cursor_next(c, p, p.T_m)) issue_dq(c);
+      }
+#endif
     }
   } else if (warp < R::EPI0) {
     // ---------------- elementwise: dS = P ∘ (dP − δ), P = exp2(S·c − LSE·log2e) ----------------
