@@ -1011,13 +1011,6 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
         if (threadIdx.x == 64) trace_ev(p.trace, p.trace_cap, 2, 1, g);
         mbar_wait(&s_full[b], (uint32_t)(g >> 1) & 1u);
         if (threadIdx.x == 64) trace_ev(p.trace, p.trace_cap, 2, 2, g);
-#ifdef SPA2_DQ_NOEW
-        // timing experiment (wrong results): keep the barrier protocol, skip the elementwise work
-        mbar_arrive(&s_free[b]);
-        mbar_wait(&dp_full[b], (uint32_t)(g >> 1) & 1u);
-        mbar_arrive(&ds_full[b]);
-        continue;
-#endif
         tc_fence_after();
         uint32_t sr[CPT];
         if constexpr (CPT == 32) tmem_ld32(sb + (uint32_t)col0, sr);
@@ -1064,6 +1057,406 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&ds_full[b]);
+        if (threadIdx.x == 64) trace_ev(p.trace, p.trace_cap, 2, 4, g);
+      }
+    }
+  } else if (warp < R::PROD2) {
+    // ---------------- epilogue: dQ = scale · acc -> bf16, direct 16-byte row stores ----------------
+    // With fused δ these warps also compute δ = rowsum(dO ∘ O) of each item BEFORE draining
+    // the previous item's accumulator, so the elementwise warps find it ready.
+    const int q4 = warp & 3;
+    const int row = q4 * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    auto drain = [&](const Item& m, int it) {
+      const int hh = m.bh % p.H, bb = m.bh / p.H;
+      const int tok = m.blk * BQ + row;
+      __nv_bfloat16* dst = p.out0 + bb * p.o0_sb + hh * p.o0_sh + (int64_t)tok * p.o0_sn;
+      mbar_wait(acc_full, (uint32_t)it & 1u);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c0 = 0; c0 < HD; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tbase + lane_off + C::ACC_COL + (uint32_t)c0, r);
+        if (c0 + 32 == HD) {
+          tc_fence_before();
+          mbar_arrive(acc_empty);
+        }
+        uint32_t pk[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+          pk[c] = pack_bf16(__uint_as_float(r[2 * c]) * p.scale, __uint_as_float(r[2 * c + 1]) * p.scale);
+        if (tok < p.N) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            *reinterpret_cast<uint4*>(dst + c0 + 8 * u) = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        }
+      }
+    };
+    int it = 0;
+    bool pend = false;
+    Item pm{};
+    for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
+      const Item m = get_item(p, wi, p.T_m);
+      const int hh = m.bh % p.H, bb = m.bh / p.H;
+      const int tok = m.blk * BQ + row;
+      if (fused_delta) {
+        float dl = 0.f;
+        if (tok < p.N) {
+          dl = row_delta<HD>(p.o_in + bb * p.oi_sb + hh * p.oi_sh + (int64_t)tok * p.oi_sn,
+                             p.do_in + bb * p.di_sb + hh * p.di_sh + (int64_t)tok * p.di_sn);
+          p.delta_out[(int64_t)m.bh * p.N + tok] = dl;
+        }
+        if (m.n > 0) {
+          sdelta[(it & 1) * BQ + row] = dl;  // slot last read at the start of item it-2 (drained)
+          mbar_arrive(&dlt_full[it & 1]);
+        }
+      }
+      if (m.n == 0) {
+        if (tok < p.N) {
+          __nv_bfloat16* dst = p.out0 + bb * p.o0_sb + hh * p.o0_sh + (int64_t)tok * p.o0_sn;
+          for (int c = 0; c < HD; c += 8) *reinterpret_cast<uint4*>(dst + c) = make_uint4(0, 0, 0, 0);
+        }
+        continue;
+      }
+      if (pend) drain(pm, it - 1);
+      pm = m;
+      pend = true;
+      ++it;
+    }
+    if (pend) drain(pm, it - 1);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tbase, 512);
+}
+
+// ---------------------------------------------------------------------------------------
+// K7 variant 4 (SPA2_DQ_VARIANT=4): k_dq3 with a 3-deep dP/dS ring.  The dQ pipeline is paced
+// by barrier hops around its 2-deep S/dP TMEM ring (a build without elementwise work still
+// takes 0.39 ms), so S moves to an SS-MMA reading Q from shared memory (Q double-buffered per
+// item) and the freed TMEM holds a third dP/dS buffer: TMEM dO 64 | S 2x64 | dP/dS 3x64 |
+// dQ 128.  The dO copy into TMEM is issued by the dP warp between the items' dP MMAs (in-order
+// tcgen05 pipeline), so S of the next item never waits for it.
+// ---------------------------------------------------------------------------------------
+#ifndef SPA2_DQ4_NK
+#define SPA2_DQ4_NK 3
+#endif
+#ifndef SPA2_DQ4_NV
+#define SPA2_DQ4_NV 3
+#endif
+template <int HD>
+struct Dq4Cfg {
+  static constexpr int NK = SPA2_DQ4_NK, NV = SPA2_DQ4_NV;
+  static constexpr int Q_BYTES = BQ * HD * 2;
+  static constexpr int KV_BYTES = BKV * HD * 2;
+  static constexpr int OFF_Q = 0;                        // [2 items] Q
+  static constexpr int OFF_DOS = 2 * Q_BYTES;            // dO staging of the next item
+  static constexpr int OFF_K = 3 * Q_BYTES;
+  static constexpr int OFF_V = OFF_K + NK * KV_BYTES;
+  static constexpr int OFF_DLT = OFF_V + NV * KV_BYTES;  // fused δ: float [2 items][128 rows]
+  static constexpr int OFF_BAR = OFF_DLT + 2 * BQ * 4;
+  static constexpr int NUM_BARS = 2 + 2 + 2 + 2 * NK + 2 * NV + 2 + 2 + 9 + 2 + 2;
+  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + kSmemAlignSlack;
+  static constexpr uint32_t DO_COL = 0, S_COL = 64, DP_COL = 192, ACC_COL = 384;
+};
+
+template <int HD, int EWW>
+__global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
+    k_dq4(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+          const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO, const BwdParams p) {
+  using C = Dq4Cfg<HD>;
+  using R = Dq3Roles<EWW>;
+  constexpr int NK = C::NK, NV = C::NV;
+  constexpr int CPT = R::CPT;
+  constexpr int kPolyPairs = CPT * SPA2_DQ_POLY_NUM / 64;  // of CPT/2 pairs
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* const smem = smem_align_1k(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* q_full = bars;             // [2] Q of item `it` in smem buffer it&1
+  uint64_t* q_free = q_full + 2;       // [2] last S MMA of the item using buffer it&1 done
+  uint64_t* do_full = q_free + 2;      // dO staging holds dO of item `it`
+  uint64_t* do_free = do_full + 1;     // tcgen05.cp of dO(it) done: staging reusable
+  uint64_t* k_full = do_free + 1;      // [NK]
+  uint64_t* k_empty = k_full + NK;     // [NK]
+  uint64_t* v_full = k_empty + NK;     // [NV]
+  uint64_t* v_empty = v_full + NV;     // [NV]
+  uint64_t* s_full = v_empty + NV;     // [2] S of tile g in S buffer g&1
+  uint64_t* s_free = s_full + 2;       // [2] S of tile g read out
+  uint64_t* dp_full = s_free + 2;      // [3] dP of tile g in dP buffer g%3
+  uint64_t* ds_full = dp_full + 3;     // [3] dS of tile g packed over its dP columns
+  uint64_t* dq_done = ds_full + 3;     // [3] dQ MMA of tile g done (dP buffer reusable)
+  uint64_t* acc_full = dq_done + 3;
+  uint64_t* acc_empty = acc_full + 1;
+  uint64_t* dlt_full = acc_empty + 1;  // [2] fused δ of item `it` in sdelta[it & 1]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(dlt_full + 2);
+  float* sdelta = reinterpret_cast<float*>(smem + C::OFF_DLT);
+  const bool fused_delta = p.delta_out != nullptr;
+
+  const int warp = (int)warp_id(), lane = (int)lane_id();
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&q_full[s], 1);
+      mbar_init(&q_free[s], 1);
+      mbar_init(&s_full[s], 1);
+      mbar_init(&s_free[s], 32 * EWW);
+    }
+    mbar_init(do_full, 1);
+    mbar_init(do_free, 1);
+    for (int s = 0; s < NK; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < NV; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int r = 0; r < 3; ++r) {
+      mbar_init(&dp_full[r], 1);
+      mbar_init(&ds_full[r], 32 * EWW);
+      mbar_init(&dq_done[r], 1);
+    }
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, 128);
+    mbar_init(&dlt_full[0], 128);
+    mbar_init(&dlt_full[1], 128);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_holder, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_holder;
+  pdl_wait();  // everything above touched only this CTA's smem/TMEM
+  pdl_trigger();
+
+  if (warp == 0 || warp == R::PROD2) {
+    // ---------------- TMA producers: warp 0 Q + K ring, warp 14 dO + V ring ----------------
+    if (elect_one()) {
+      const bool second = warp == R::PROD2;
+      const CUtensorMap* tmR = second ? &tmDO : &tmQ;
+      const CUtensorMap* tmKV = second ? &tmV : &tmK;
+      tma_prefetch(tmR);
+      tma_prefetch(tmKV);
+      uint64_t* full = second ? v_full : k_full;
+      uint64_t* empty = second ? v_empty : k_empty;
+      const int ns = second ? NV : NK;
+      uint8_t* const ring = smem + (second ? C::OFF_V : C::OFF_K);
+      int it = 0, g = 0;
+      for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
+        const Item m = get_item(p, wi, p.T_m);
+        if (m.n == 0) continue;
+        const int hh = m.bh % p.H, bb = m.bh / p.H;
+        if (!second) {  // Q(it) into its own buffer: read by the S MMAs for the whole item
+          if (it >= 2) mbar_wait(&q_free[it & 1], ((uint32_t)(it >> 1) + 1u) & 1u);
+          mbar_expect_tx(&q_full[it & 1], C::Q_BYTES);
+          tma_load_5d(smem + C::OFF_Q + (it & 1) * C::Q_BYTES, tmR, &q_full[it & 1], 0, m.blk * BQ, 0, hh, bb);
+        } else {  // dO(it) into the staging buffer, copied into TMEM by the dP issuer
+          if (it >= 1) mbar_wait(do_free, (uint32_t)(it - 1) & 1u);
+          mbar_expect_tx(do_full, C::Q_BYTES);
+          tma_load_5d(smem + C::OFF_DOS, tmR, do_full, 0, m.blk * BQ, 0, hh, bb);
+        }
+        for (int t = 0; t < m.n; ++t, ++g) {
+          const int s = g % ns;
+          if (!second) trace_ev(p.trace, p.trace_cap, 0, 1, g);
+          if (g >= ns) mbar_wait(&empty[s], ((uint32_t)(g / ns) + 1u) & 1u);
+          if (!second) trace_ev(p.trace, p.trace_cap, 0, 2, g);
+          mbar_expect_tx(&full[s], C::KV_BYTES);
+          tma_load_5d(ring + s * C::KV_BYTES, tmKV, &full[s], 0, p.idx[m.beg + t] * BKV, 0, hh, bb);
+        }
+        ++it;
+      }
+    }
+  } else if (warp == 1 || warp == R::ISSUE_DP || warp == R::ISSUE_DQ) {
+    // ---------------- MMA issue: three warps, one per independent stream ----------------
+    // warp 1: S = Q K_jᵀ (SS, Q from smem);  ISSUE_DP: dO copy into TMEM per item (issued after
+    // the previous item's last dP and before this item's first: tcgen05.cp and tcgen05.mma of
+    // one thread execute in order) + dP = dO V_jᵀ (TS);  ISSUE_DQ: dQ += dS K_j (TS).
+    constexpr uint32_t idS = idesc_bf16(BQ, BKV, false, false);
+    constexpr uint32_t idQ = idesc_bf16(BQ, HD, false, true);
+    const uint64_t dQ0 = sw128_desc(smem_u32(smem + C::OFF_Q), 16, 1024);
+    const uint64_t dDOS = sw128_desc(smem_u32(smem + C::OFF_DOS), 16, 1024);
+    const uint64_t dK0 = sw128_desc(smem_u32(smem + C::OFF_K), 16, 1024);
+    const uint64_t dV0 = sw128_desc(smem_u32(smem + C::OFF_V), 16, 1024);
+    const uint64_t dKm0 = sw128_desc(smem_u32(smem + C::OFF_K), BKV * 128, 1024);
+    constexpr uint64_t KV16 = (uint64_t)(C::KV_BYTES >> 4);
+    Cursor c;
+    cursor_init(c, p, p.T_m);
+    if (warp == 1) {
+      for (; c.valid; cursor_next(c, p, p.T_m)) {
+        if (c.t == 0) mbar_wait(&q_full[c.it & 1], (uint32_t)(c.it >> 1) & 1u);
+        const int b = c.g & 1, sk = c.g % NK;
+        if (c.g >= 2) mbar_wait(&s_free[b], (uint32_t)((c.g - 2) >> 1) & 1u);  // S(g-2) read out
+        mbar_wait(&k_full[sk], (uint32_t)(c.g / NK) & 1u);
+        tc_fence_after();
+        trace_ev(p.trace, p.trace_cap, 1, 2, c.g);
+        const uint64_t dK = dK0 + (uint64_t)sk * KV16;
+        const uint64_t dQ = dQ0 + (uint64_t)((c.it & 1) * (C::Q_BYTES >> 4));
+        const uint32_t sb = tbase + C::S_COL + (uint32_t)(b * 64);
+#ifdef SPA2_MMA_BATCH
+        if constexpr (HD == 128) {
+          mma_bf16_ss_k8_w<2ull, (uint64_t)(BQ * 128 / 16), 2ull, (uint64_t)(BKV * 128 / 16)>(sb, dQ, dK, idS, 0u);
+        } else
+#endif
+        {
+#pragma unroll
+          for (int ks = 0; ks < HD / 16; ++ks) {
+            const uint64_t qo = (uint64_t)(((ks * 16 / 64) * BQ * 128 + (ks * 16 % 64) * 2) >> 4);
+            const uint64_t ko = (uint64_t)(((ks * 16 / 64) * BKV * 128 + (ks * 16 % 64) * 2) >> 4);
+            mma_bf16_w(sb, dQ + qo, dK + ko, idS, ks > 0 ? 1u : 0u);
+          }
+        }
+        mma_commit_w(&s_full[b]);
+        if (c.t == c.n - 1) mma_commit_w(&q_free[c.it & 1]);
+        trace_ev(p.trace, p.trace_cap, 1, 3, c.g);
+      }
+    } else {
+      // dP = dO V_jᵀ (TS) and dQ += dS K_j (TS), by two warps (dP(g) waits for dQ(g-2) to
+      // COMPLETE: it overwrites the TMEM columns dQ(g-2) reads dS from).  With
+      // -DSPA2_DQ_MERGED one warp issues both as dQ(g-2), dP(g), ...: tcgen05 MMAs issued by
+      // one thread execute in issue order, so the completion wait disappears.
+      auto issue_dp = [&](const Cursor& cc) {
+        if (cc.t == 0) {  // dO(it) into TMEM, in issue order after dP of the previous item
+          mbar_wait(do_full, (uint32_t)cc.it & 1u);
+          tc_fence_after();
+#pragma unroll
+          for (int ks = 0; ks < HD / 16; ++ks) {
+            const uint64_t qo = (uint64_t)(((ks * 16 / 64) * BQ * 128 + (ks * 16 % 64) * 2) >> 4);
+            tmem_cp_128x256b_w(tbase + C::DO_COL + (uint32_t)(ks * 8), dDOS + qo);
+          }
+          mma_commit_w(do_free);
+        }
+        const int r = cc.g % 3, sv = cc.g % NV;
+        if (cc.g >= 3) mbar_wait(&dq_done[r], (uint32_t)((cc.g - 3) / 3) & 1u);  // dS(g-3) consumed
+        mbar_wait(&v_full[sv], (uint32_t)(cc.g / NV) & 1u);
+        tc_fence_after();
+        const uint64_t dV = dV0 + (uint64_t)sv * KV16;
+        const uint32_t pb = tbase + C::DP_COL + (uint32_t)(r * 64);
+#ifdef SPA2_MMA_BATCH
+        if constexpr (HD == 128) {
+          mma_bf16_ts_k8_w<8u, 2ull, (uint64_t)(BKV * 128 / 16)>(pb, tbase + C::DO_COL, dV, idS, 0u);
+        } else
+#endif
+        {
+#pragma unroll
+          for (int ks = 0; ks < HD / 16; ++ks)
+            mma_bf16_ts_w(pb, tbase + C::DO_COL + (uint32_t)(ks * 8),
+                          dV + (uint64_t)((((ks * 16 / 64) * BKV * 128 + (ks * 16 % 64) * 2)) >> 4), idS, ks > 0 ? 1u : 0u);
+        }
+        mma_commit_w(&dp_full[r]);
+        mma_commit_w(&v_empty[sv]);
+      };
+      auto issue_dq = [&](const Cursor& cc) {
+        const int r = cc.g % 3, sk = cc.g % NK;
+        if (cc.t == 0 && cc.it >= 1) mbar_wait(acc_empty, (uint32_t)(cc.it - 1) & 1u);
+        mbar_wait(&ds_full[r], (uint32_t)(cc.g / 3) & 1u);
+        tc_fence_after();
+        trace_ev(p.trace, p.trace_cap, 1, 4, cc.g);
+        const uint64_t dKm = dKm0 + (uint64_t)sk * KV16;
+        const uint32_t pb = tbase + C::DP_COL + (uint32_t)(r * 64);
+#ifdef SPA2_MMA_BATCH
+        if constexpr (CPT == 16) {
+          mma_bf16_ts_k4_w<16u, 128ull>(tbase + C::ACC_COL, pb, dKm, idQ, cc.t > 0 ? 1u : 0u);
+        } else
+#endif
+        {
+#pragma unroll
+          for (int ks = 0; ks < BKV / 16; ++ks)
+            mma_bf16_ts_w(tbase + C::ACC_COL, pb + ds_col<CPT>(ks), dKm + (uint64_t)((ks * 2048) >> 4), idQ,
+                          (cc.t > 0 || ks > 0) ? 1u : 0u);
+        }
+        mma_commit_w(&dq_done[r]);
+        mma_commit_w(&k_empty[sk]);
+        if (cc.t == cc.n - 1) mma_commit_w(acc_full);
+        trace_ev(p.trace, p.trace_cap, 1, 5, cc.g);
+      };
+      if (warp == R::ISSUE_DP) {
+        for (; c.valid; cursor_next(c, p, p.T_m)) issue_dp(c);
+      } else {
+        for (; c.valid; cursor_next(c, p, p.T_m)) issue_dq(c);
+      }
+    }
+  } else if (warp < R::EPI0) {
+    // ---------------- elementwise: dS = P ∘ (dP − δ), P = exp2(S·c − LSE·log2e) ----------------
+    const int q4 = warp & 3;
+    const int grp = (warp - 2) >> 2;
+    const int row = q4 * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    const int col0 = CPT * grp;
+    const int kv_tail = p.N - (p.T_n - 1) * BKV;
+    const float sl2 = p.sl2;
+    int g = 0, it = 0;
+    for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
+      const Item m = get_item(p, wi, p.T_m);
+      if (m.n == 0) continue;
+      const int tok = m.blk * BQ + row;
+      const bool valid = tok < p.N;
+      const float lse2 = valid ? __ldg(p.lse + (int64_t)m.bh * p.N + tok) * kLog2e : INFINITY;
+      float dlt;
+      if (fused_delta) {  // computed one item ahead by the epilogue warps
+        mbar_wait(&dlt_full[it & 1], (uint32_t)(it >> 1) & 1u);
+        dlt = valid ? sdelta[(it & 1) * BQ + row] : 0.f;
+      } else {
+        dlt = valid ? __ldg(p.delta + (int64_t)m.bh * p.N + tok) : 0.f;
+      }
+      ++it;
+      // key-block index of the next tile is loaded one tile ahead (off the critical path)
+      int j_next = __ldg(p.idx + m.beg);
+      for (int t = 0; t < m.n; ++t, ++g) {
+        const int b = g & 1;
+        const bool tail = kv_tail < BKV && j_next == p.T_n - 1;
+        if (t + 1 < m.n) j_next = __ldg(p.idx + m.beg + t + 1);
+        const int r = g % 3;
+        const uint32_t sb = tbase + lane_off + C::S_COL + (uint32_t)(b * 64);
+        const uint32_t pb = tbase + lane_off + C::DP_COL + (uint32_t)(r * 64);
+        if (threadIdx.x == 64) trace_ev(p.trace, p.trace_cap, 2, 1, g);
+        mbar_wait(&s_full[b], (uint32_t)(g >> 1) & 1u);
+        if (threadIdx.x == 64) trace_ev(p.trace, p.trace_cap, 2, 2, g);
+        tc_fence_after();
+        uint32_t sr[CPT];
+        if constexpr (CPT == 32) tmem_ld32(sb + (uint32_t)col0, sr);
+        else tmem_ld16(sb + (uint32_t)col0, sr);
+        tc_fence_before();
+        mbar_arrive(&s_free[b]);  // S(g) is in registers: the S issuer may overwrite it
+        // packed fp32x2 math (FFMA2/FADD2/FMUL2): the issue slots of this SM sub-partition are
+        // shared with an MMA-issuing warp, so fewer instructions per element = faster MMAs
+        float pv[CPT];
+#pragma unroll
+        for (int c = 0; c < CPT / 2; ++c) {
+          const float2 x = __ffma2_rn(make_float2(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1])),
+                                      make_float2(sl2, sl2), make_float2(-lse2, -lse2));
+          if (c < kPolyPairs) {  // a quarter of the exponentials on the FMA pipe
+            const float2 e = exp2_poly2(x);
+            pv[2 * c] = e.x;
+            pv[2 * c + 1] = e.y;
+          } else {
+            pv[2 * c] = ex2(x.x);
+            pv[2 * c + 1] = ex2(x.y);
+          }
+        }
+        if (tail) {
+#pragma unroll
+          for (int c = 0; c < CPT; ++c)
+            if (col0 + c >= kv_tail) pv[c] = 0.f;
+        }
+        mbar_wait(&dp_full[r], (uint32_t)(g / 3) & 1u);
+        if (threadIdx.x == 64) trace_ev(p.trace, p.trace_cap, 2, 3, g);
+        tc_fence_after();
+        uint32_t dr[CPT];
+        if constexpr (CPT == 32) tmem_ld32(pb + (uint32_t)col0, dr);
+        else tmem_ld16(pb + (uint32_t)col0, dr);
+        uint32_t pk[CPT / 2];
+#pragma unroll
+        for (int c = 0; c < CPT / 2; ++c) {
+          const float2 ds = __fmul2_rn(make_float2(pv[2 * c], pv[2 * c + 1]),
+                                       __fadd2_rn(make_float2(__uint_as_float(dr[2 * c]), __uint_as_float(dr[2 * c + 1])),
+                                                  make_float2(-dlt, -dlt)));
+          pk[c] = pack_bf16(ds.x, ds.y);
+        }
+        if constexpr (CPT == 32) tmem_st16(pb + (uint32_t)col0, pk);  // dS over the dP columns read
+        else tmem_st8(pb + (uint32_t)col0, pk);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&ds_full[r]);
         if (threadIdx.x == 64) trace_ev(p.trace, p.trace_cap, 2, 4, g);
       }
     }
@@ -1918,7 +2311,19 @@ int launch_attn_bwd(int which, const spa2_view& q, const spa2_view& k, const spa
     prm.delta_out = fd->delta;
   }
   const unsigned grid = (unsigned)std::min<int64_t>(prm.num_items, num_sms());
-  if (which == 0 && dq_variant() == 3) {
+  if (which == 0 && dq_variant() == 4) {
+    if (dq_ew_warps() == 16) {
+      auto kern = k_dq4<HD, 16>;
+      SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Dq4Cfg<HD>::SMEM));
+      SPA2_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(Dq3Roles<16>::THREADS), Dq4Cfg<HD>::SMEM, st, m.q, m.k, m.v, m.dout,
+                               prm));
+    } else {
+      auto kern = k_dq4<HD, 8>;
+      SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Dq4Cfg<HD>::SMEM));
+      SPA2_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(Dq3Roles<8>::THREADS), Dq4Cfg<HD>::SMEM, st, m.q, m.k, m.v, m.dout,
+                               prm));
+    }
+  } else if (which == 0 && dq_variant() == 3) {
     if (dq_ew_warps() == 16) {
       auto kern = k_dq3<HD, 16>;
       SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Dq3Cfg<HD>::SMEM));
@@ -2037,7 +2442,7 @@ extern "C" int spa2_bwd_dq_delta(spa2_view q, spa2_view k, spa2_view v, spa2_vie
     const char* e = getenv("SPA2_NO_FUSED_DELTA");
     return e != nullptr && e[0] == '1';
   }();
-  if (dq_variant() != 3 || no_fuse) {  // other dQ kernels take δ from a separate pass
+  if ((dq_variant() != 3 && dq_variant() != 4) || no_fuse) {  // other dQ kernels take δ from a separate pass
     if ((rc = spa2_bwd_delta(o, dout, delta, dtype, B, H, N, d, stream))) return rc;
     return spa2_bwd_dq(q, k, v, dout, lse, delta, dq, dtype, B, H, N, d, b_q, b_kv, row_ptr, row_idx, row_order,
                        scale, stream);

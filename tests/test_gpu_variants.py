@@ -3,7 +3,8 @@
 The variant is chosen once per process from the environment (static in libspa2.so), so each
 case runs a small fwd + bwd parity check in a fresh interpreter:
   SPA2_FWD_VARIANT=3|1|2     forward: persistent 2 CTAs/SM | one CTA per query block | Q in TMEM
-  SPA2_DQ_VARIANT=3|2|1      dQ: Q/dO in TMEM (3) | one query block per CTA (2) | persistent SS (1)
+  SPA2_DQ_VARIANT=3|4|2|1    dQ: Q/dO in TMEM (3) | 3-deep dP/dS ring, S from smem (4) | one query block
+                             per CTA (2) | persistent SS (1)
   SPA2_NO_FUSED_DELTA=1      δ by its own kernel instead of inside the dQ kernel
   SPA2_DKDV_VARIANT=5|6|1    dK/dV: 5-slot Q/dO ring | 4 slots + two P/dS buffers | two [Q|dO] stages
   SPA2_DQ_EW=8, SPA2_DKDV_EW=8|16 elementwise warp counts (defaults 16, 16)
@@ -46,6 +47,8 @@ print("ok")
 VARIANTS = [
     {"SPA2_FWD_VARIANT": "1"},
     {"SPA2_FWD_VARIANT": "2"},
+    {"SPA2_DQ_VARIANT": "4"},
+    {"SPA2_DQ_VARIANT": "4", "SPA2_DQ_EW": "8"},
     {"SPA2_DQ_VARIANT": "2"},
     {"SPA2_DQ_VARIANT": "1"},
     {"SPA2_NO_FUSED_DELTA": "1"},
