@@ -2232,6 +2232,376 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
   if (warp == 1) tmem_dealloc(tbase, 512);
 }
 
+// ---------------------------------------------------------------------------------------
+// K6 variant 7 (SPA2_DKDV_VARIANT=7, d = 128): KEY-PAIR items.  An item is two adjacent key
+// blocks (128 keys) over the UNION of their column lists; a union tile keeps one or both
+// halves.  With keys on the TMEM lanes every MMA is M = 128, N = 128:
+//   Sᵀ = [K_j; K_j+1] Qᵢᵀ, dPᵀ = [V_j; V_j+1] dOᵢᵀ   (SS, 8 KB of operands per 64 cycles —
+//        the N = 64 MMAs of the other variants move 6 KB per 48)
+//   dV += Pᵀ dOᵢ, dK += dSᵀ Qᵢ                       (TS: Pᵀ / dSᵀ packed bf16 in TMEM)
+// TMEM: Sᵀ→Pᵀ 0 | dPᵀ→dSᵀ 128 | dV 256 | dK 384 (full, single-buffered).  ONE warp issues
+// all four MMA streams in the order Sᵀ(g), dPᵀ(g), dV(g), dK(g): tcgen05 MMAs of one thread
+// execute in issue order, so Sᵀ(g+1) overwriting Pᵀ(g) and dPᵀ(g+1) overwriting dSᵀ(g) need
+// no completion waits.  A half whose key block does not keep the query block gets exact-zero
+// P and dS rows (its exponentials are skipped), so results equal the per-block kernels'.
+// Warps: 0 TMA (K pair, Q ring), 1 MMA issue, 2-17 elementwise (4 per lane quarter, 32
+// query columns each), 18-21 epilogue, 22 TMA (V pair, dO ring).
+// ---------------------------------------------------------------------------------------
+struct Dkv7Cfg {
+  static constexpr int NSL = 5;                       // 32 KB Q / dO operand slots
+  static constexpr int PAIR = 2 * BKV;                // 128 keys
+  static constexpr int KVP_BYTES = PAIR * 128 * 2;    // 32 KB
+  static constexpr int Q_BYTES = BQ * 128 * 2;        // 32 KB
+  static constexpr int OFF_K = 0, OFF_V = KVP_BYTES, OFF_SL = 2 * KVP_BYTES;
+  static constexpr int OFF_BAR = OFF_SL + NSL * Q_BYTES;
+  static constexpr int NUM_BARS = 2 + 2 * NSL + 6;
+  static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + kSmemAlignSlack;
+  static constexpr uint32_t S_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 384;
+  static constexpr int EPI0 = 18, PROD2 = 22, THREADS = 32 * 23;
+};
+
+// Merge cursor over the column lists of key blocks 2jp and 2jp+1 (both ascending).
+struct PairCursor {
+  int a, ae, b, be;
+};
+__device__ __forceinline__ void pair_init(PairCursor& pc, const BwdParams& p, int bh, int jp) {
+  const int j0 = 2 * jp, j1 = j0 + 1;
+  const int64_t base = (int64_t)bh * p.T_n;
+  pc.a = p.ptr[base + j0];
+  pc.ae = p.ptr[base + j0 + 1];
+  if (j1 < p.T_n) {
+    pc.b = p.ptr[base + j1];
+    pc.be = p.ptr[base + j1 + 1];
+  } else {
+    pc.b = pc.be = 0;
+  }
+}
+__device__ __forceinline__ bool pair_done(const PairCursor& pc) { return pc.a >= pc.ae && pc.b >= pc.be; }
+// Next query block of the union; flags bit h = key block 2jp+h keeps it.
+__device__ __forceinline__ int pair_next(PairCursor& pc, const int32_t* idx, int& flags) {
+  const int ia = pc.a < pc.ae ? __ldg(idx + pc.a) : 0x7fffffff;
+  const int ib = pc.b < pc.be ? __ldg(idx + pc.b) : 0x7fffffff;
+  const int i = min(ia, ib);
+  flags = (ia == i ? 1 : 0) | (ib == i ? 2 : 0);
+  if (ia == i) ++pc.a;
+  if (ib == i) ++pc.b;
+  return i;
+}
+
+__global__ void __launch_bounds__(Dkv7Cfg::THREADS, 1)
+    k_dkdv7(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKP,
+            const __grid_constant__ CUtensorMap tmVP, const __grid_constant__ CUtensorMap tmDO, const BwdParams p) {
+  using C = Dkv7Cfg;
+  constexpr int NSL = C::NSL;
+  constexpr int EWT = 32 * 16;
+  constexpr int kPolyPairs = 16 * SPA2_DKDV_POLY_NUM / 64;  // of 16 exponential pairs per thread
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* const smem = smem_align_1k(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* kv_full = bars;            // K/V pair of item `it` landed (two producers)
+  uint64_t* kv_empty = kv_full + 1;    // last Sᵀ/dPᵀ of item `it` done
+  uint64_t* sl_full = kv_empty + 1;    // [NSL] operand u landed (Q(g): u = 2g, dO(g): u = 2g+1)
+  uint64_t* sl_empty = sl_full + NSL;  // [NSL] both MMAs reading operand u done
+  uint64_t* s_full = sl_empty + NSL;   // Sᵀ(g) in TMEM
+  uint64_t* dp_full = s_full + 1;      // dPᵀ(g) in TMEM
+  uint64_t* p_full = dp_full + 1;      // Pᵀ(g) packed over the Sᵀ columns
+  uint64_t* ds_full = p_full + 1;      // dSᵀ(g) packed over the dPᵀ columns
+  uint64_t* acc_full = ds_full + 1;    // last dV/dK of item `it` done
+  uint64_t* acc_empty = acc_full + 1;  // accumulators read out
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 1);
+
+  const int warp = (int)warp_id(), lane = (int)lane_id();
+  const int TP = (p.T_n + 1) / 2;
+  if (threadIdx.x == 0) {
+    mbar_init(kv_full, 2);
+    mbar_init(kv_empty, 1);
+    for (int s = 0; s < NSL; ++s) {
+      mbar_init(&sl_full[s], 1);
+      mbar_init(&sl_empty[s], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(dp_full, 1);
+    mbar_init(p_full, EWT);
+    mbar_init(ds_full, EWT);
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, 128);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_holder, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_holder;
+  pdl_wait();
+  pdl_trigger();
+
+  if (warp == 0 || warp == C::PROD2) {
+    // ---------------- TMA producers ----------------
+    if (elect_one()) {
+      const bool second = warp == C::PROD2;
+      const CUtensorMap* tmKV = second ? &tmVP : &tmKP;
+      const CUtensorMap* tmR = second ? &tmDO : &tmQ;
+      tma_prefetch(tmKV);
+      tma_prefetch(tmR);
+      uint8_t* const kv_dst = smem + (second ? C::OFF_V : C::OFF_K);
+      int it = 0, g = 0;
+      for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
+        const int bh = wi / TP, jp = wi % TP, hh = bh % p.H, bb = bh / p.H;
+        PairCursor pc;
+        pair_init(pc, p, bh, jp);
+        if (pair_done(pc)) continue;
+        if (it >= 1) mbar_wait(kv_empty, (uint32_t)(it - 1) & 1u);
+        mbar_expect_tx(kv_full, C::KVP_BYTES);
+        tma_load_5d(kv_dst, tmKV, kv_full, 0, jp * C::PAIR, 0, hh, bb);
+        while (!pair_done(pc)) {
+          int fl;
+          const int i = pair_next(pc, p.idx, fl);
+          const int u = 2 * g + (second ? 1 : 0);
+          const int s = u % NSL;
+          if (u >= NSL) mbar_wait(&sl_empty[s], ((uint32_t)(u / NSL) + 1u) & 1u);
+          mbar_expect_tx(&sl_full[s], C::Q_BYTES);
+          tma_load_5d(smem + C::OFF_SL + s * C::Q_BYTES, tmR, &sl_full[s], 0, i * BQ, 0, hh, bb);
+          ++g;
+        }
+        ++it;
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issue: all four streams, in order ----------------
+    constexpr uint32_t idS = idesc_bf16(C::PAIR, BQ, false, false);  // Sᵀ, dPᵀ: M keys, N queries
+    constexpr uint32_t idT = idesc_bf16(C::PAIR, 128, false, true);  // dV, dK: B = dO / Q, N (dims) major
+    const uint64_t dKP = sw128_desc(smem_u32(smem + C::OFF_K), 16, 1024);
+    const uint64_t dVP = sw128_desc(smem_u32(smem + C::OFF_V), 16, 1024);
+    const uint64_t dSLk0 = sw128_desc(smem_u32(smem + C::OFF_SL), 16, 1024);        // K-major Q / dO
+    const uint64_t dSLm0 = sw128_desc(smem_u32(smem + C::OFF_SL), BQ * 128, 1024);  // N-major Q / dO
+    constexpr uint64_t SLOT16 = (uint64_t)(C::Q_BYTES >> 4);
+    // Issue order  Sᵀ(0) dPᵀ(0) | dV(0) Sᵀ(1) | dK(0) dPᵀ(1) | dV(1) Sᵀ(2) | dK(1) dPᵀ(2) ...:
+    // Sᵀ(g+1) may follow dV(g) (which reads Pᵀ(g) from the Sᵀ columns) and dPᵀ(g+1) may follow
+    // dK(g) (dSᵀ(g) lives in the dPᵀ columns) without waits, so the tensor pipe works on tile
+    // g+1 while the elementwise warps turn Sᵀ(g)/dPᵀ(g) into Pᵀ/dSᵀ.  Across items the S/dP
+    // of the next item's first tile come after the last dK of the previous item.
+    int it = 0, g = 0;
+    auto issue_s = [&](int gg) {
+      const int uq = 2 * gg;
+      mbar_wait(&sl_full[uq % NSL], (uint32_t)(uq / NSL) & 1u);
+      tc_fence_after();
+      mma_bf16_ss_k8_w<2ull, 1024ull, 2ull, 1024ull>(tbase + C::S_COL, dKP, dSLk0 + (uint64_t)(uq % NSL) * SLOT16, idS, 0u);
+      mma_commit_w(s_full);
+    };
+    auto issue_dp = [&](int gg, bool last) {
+      const int ud = 2 * gg + 1;
+      mbar_wait(&sl_full[ud % NSL], (uint32_t)(ud / NSL) & 1u);
+      tc_fence_after();
+      mma_bf16_ss_k8_w<2ull, 1024ull, 2ull, 1024ull>(tbase + C::DP_COL, dVP, dSLk0 + (uint64_t)(ud % NSL) * SLOT16, idS, 0u);
+      mma_commit_w(dp_full);
+      if (last) mma_commit_w(kv_empty);  // the K/V pair is only read by Sᵀ and dPᵀ
+    };
+    for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
+      const int bh = wi / TP, jp = wi % TP;
+      PairCursor pc;
+      pair_init(pc, p, bh, jp);
+      if (pair_done(pc)) continue;
+      mbar_wait(kv_full, (uint32_t)it & 1u);
+      int fl;
+      pair_next(pc, p.idx, fl);
+      bool last = pair_done(pc);
+      issue_s(g);
+      issue_dp(g, last);
+      if (it >= 1) mbar_wait(acc_empty, (uint32_t)(it - 1) & 1u);
+      bool first = true;
+      for (;;) {
+        const int uq = 2 * g, ud = uq + 1;
+        const uint64_t sq = (uint64_t)(uq % NSL) * SLOT16, sd = (uint64_t)(ud % NSL) * SLOT16;
+        mbar_wait(p_full, (uint32_t)g & 1u);
+        tc_fence_after();
+        mma_bf16_ts_k8_w<8u, 128ull, 512ull>(tbase + C::DV_COL, tbase + C::S_COL, dSLm0 + sd, idT, first ? 0u : 1u);
+        mma_commit_w(&sl_empty[ud % NSL]);  // dO(g): dPᵀ(g) and dV(g) both issued by this thread
+        const bool more = !last;
+        bool next_last = false;
+        if (more) {
+          pair_next(pc, p.idx, fl);
+          next_last = pair_done(pc);
+          issue_s(g + 1);
+        }
+        mbar_wait(ds_full, (uint32_t)g & 1u);
+        tc_fence_after();
+        mma_bf16_ts_k8_w<8u, 128ull, 512ull>(tbase + C::DK_COL, tbase + C::DP_COL, dSLm0 + sq, idT, first ? 0u : 1u);
+        mma_commit_w(&sl_empty[uq % NSL]);  // Q(g): Sᵀ(g) and dK(g)
+        if (!more) {
+          mma_commit_w(acc_full);
+          ++g;
+          break;
+        }
+        issue_dp(g + 1, next_last);
+        first = false;
+        last = next_last;
+        ++g;
+      }
+      ++it;
+    }
+  } else if (warp < C::EPI0) {
+    // ---------------- elementwise: Pᵀ = exp2(Sᵀ·c − lse2[q]), dSᵀ = Pᵀ ∘ (dPᵀ − δ[q]) ----------------
+    const int q4 = warp & 3;
+    const int grp = (warp - 2) >> 2;  // query columns [32·grp, 32·grp + 32)
+    const int half = q4 >> 1;         // lanes 0-63: key block 2jp, 64-127: 2jp+1
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    const uint32_t col0 = (uint32_t)(32 * grp);
+    const float sl2 = p.sl2;
+    int g = 0;
+    for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
+      const int bh = wi / TP, jp = wi % TP;
+      PairCursor pc;
+      pair_init(pc, p, bh, jp);
+      if (pair_done(pc)) continue;
+      const bool key_ok = jp * C::PAIR + q4 * 32 + lane < p.N;
+      const int64_t rowbase = (int64_t)bh * p.N;
+      while (!pair_done(pc)) {
+        int fl;
+        const int i = pair_next(pc, p.idx, fl);
+        const bool kept = (fl >> half) & 1;  // warp- and lane-quarter-uniform
+        const int q0 = i * BQ + (int)col0;
+        float lse_first[16];  // first pass's row statistics, loaded before the wait
+        if (kept) {
+#pragma unroll
+          for (int c = 0; c < 16; ++c) lse_first[c] = q0 + c < p.N ? __ldg(p.lse + rowbase + q0 + c) * kLog2e : INFINITY;
+        }
+        mbar_wait(s_full, (uint32_t)g & 1u);
+        tc_fence_after();
+        float pv[32];  // fp32 P of this thread's 32 query columns, kept for dS
+        if (kept) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {  // two passes of 16 columns keep register pressure down
+            float lse2[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+              const int q = q0 + 16 * h + c;
+              lse2[c] = h == 0 ? lse_first[c] : (q < p.N ? __ldg(p.lse + rowbase + q) * kLog2e : INFINITY);
+            }
+            uint32_t sr[16];
+            tmem_ld16(tbase + lane_off + C::S_COL + col0 + 16u * h, sr);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const float2 x = __ffma2_rn(make_float2(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1])),
+                                          make_float2(sl2, sl2), make_float2(-lse2[2 * c], -lse2[2 * c + 1]));
+              float2 e;
+              if (c < kPolyPairs / 2) {
+                e = exp2_poly2(x);
+              } else {
+                e.x = ex2(x.x);
+                e.y = ex2(x.y);
+              }
+              pv[16 * h + 2 * c] = key_ok ? e.x : 0.f;
+              pv[16 * h + 2 * c + 1] = key_ok ? e.y : 0.f;
+            }
+          }
+          // the four warps of this lane quarter read disjoint S columns but write packed P
+          // into the first 64: all must have read S before any writes
+          named_bar_sync(1 + q4, 128);
+          uint32_t pk[16];
+#pragma unroll
+          for (int c = 0; c < 16; ++c) pk[c] = pack_bf16(pv[2 * c], pv[2 * c + 1]);
+          tmem_st16(tbase + lane_off + C::S_COL + col0 / 2, pk);
+        } else {
+          uint32_t pk[16];
+#pragma unroll
+          for (int c = 0; c < 16; ++c) pk[c] = 0u;
+          tmem_st16(tbase + lane_off + C::S_COL + col0 / 2, pk);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(p_full);
+        float dlt_first[16];
+        if (kept) {
+#pragma unroll
+          for (int c = 0; c < 16; ++c) dlt_first[c] = q0 + c < p.N ? __ldg(p.delta + rowbase + q0 + c) : 0.f;
+        }
+        mbar_wait(dp_full, (uint32_t)g & 1u);
+        tc_fence_after();
+        if (kept) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            float dlt[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+              const int q = q0 + 16 * h + c;
+              dlt[c] = h == 0 ? dlt_first[c] : (q < p.N ? __ldg(p.delta + rowbase + q) : 0.f);
+            }
+            uint32_t dr[16];
+            tmem_ld16(tbase + lane_off + C::DP_COL + col0 + 16u * h, dr);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const float2 ds = __fmul2_rn(make_float2(pv[16 * h + 2 * c], pv[16 * h + 2 * c + 1]),
+                                           __fadd2_rn(make_float2(__uint_as_float(dr[2 * c]), __uint_as_float(dr[2 * c + 1])),
+                                                      make_float2(-dlt[2 * c], -dlt[2 * c + 1])));
+              pk[8 * h + c] = pack_bf16(ds.x, ds.y);
+            }
+          }
+          named_bar_sync(1 + q4, 128);
+          tmem_st16(tbase + lane_off + C::DP_COL + col0 / 2, pk);
+        } else {
+          uint32_t pk[16];
+#pragma unroll
+          for (int c = 0; c < 16; ++c) pk[c] = 0u;
+          tmem_st16(tbase + lane_off + C::DP_COL + col0 / 2, pk);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(ds_full);
+        ++g;
+      }
+    }
+  } else if (warp < C::PROD2) {
+    // ---------------- epilogue: dV, dK rows (one key per thread) ----------------
+    const int q4 = warp & 3;
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    int it = 0;
+    for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
+      const int bh = wi / TP, jp = wi % TP, hh = bh % p.H, bb = bh / p.H;
+      const int key = jp * C::PAIR + q4 * 32 + lane;
+      __nv_bfloat16* dk = p.out0 + bb * p.o0_sb + hh * p.o0_sh + (int64_t)key * p.o0_sn;
+      __nv_bfloat16* dv = p.out1 + bb * p.o1_sb + hh * p.o1_sh + (int64_t)key * p.o1_sn;
+      PairCursor pc;
+      pair_init(pc, p, bh, jp);
+      if (pair_done(pc)) {  // no query block keeps either key block: exact zero rows
+        if (key < p.N)
+          for (int c = 0; c < 128; c += 8) {
+            *reinterpret_cast<uint4*>(dk + c) = make_uint4(0, 0, 0, 0);
+            *reinterpret_cast<uint4*>(dv + c) = make_uint4(0, 0, 0, 0);
+          }
+        continue;
+      }
+      mbar_wait(acc_full, (uint32_t)it & 1u);
+      tc_fence_after();
+#pragma unroll 1
+      for (int part = 0; part < 8; ++part) {  // dV cols 0-127 in 32s, then dK
+        const bool is_k = part >= 4;
+        const uint32_t c0 = (uint32_t)((part & 3) * 32);
+        uint32_t r[32];
+        tmem_ld32(tbase + lane_off + (is_k ? C::DK_COL : C::DV_COL) + c0, r);
+        if (part == 7) {
+          tc_fence_before();
+          mbar_arrive(acc_empty);
+        }
+        const float mul = is_k ? p.scale : 1.f;
+        uint32_t pk[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) pk[c] = pack_bf16(__uint_as_float(r[2 * c]) * mul, __uint_as_float(r[2 * c + 1]) * mul);
+        if (key < p.N) {
+          __nv_bfloat16* dst = (is_k ? dk : dv) + c0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            *reinterpret_cast<uint4*>(dst + 8 * u) = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        }
+      }
+      ++it;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tbase, 512);
+}
+
 int dkdv_variant() {
   static const int v = [] {
     const char* e = getenv("SPA2_DKDV_VARIANT");
@@ -2346,7 +2716,15 @@ int launch_attn_bwd(int which, const spa2_view& q, const spa2_view& k, const spa
   } else {
     prm.out1 = (__nv_bfloat16*)out1->ptr;
     prm.o1_sb = out1->sb, prm.o1_sh = out1->sh, prm.o1_sn = out1->sn;
-    if (dkdv_variant() == 6 && dkdv_ew_warps() == 16) {
+    if (HD == 128 && dkdv_variant() == 7) {
+      CUtensorMap kp, vp;  // 128-row boxes: one key PAIR per load
+      if ((rc = make_qkv_map(&kp, k, B, H, N, HD, 2 * BKV))) return rc;
+      if ((rc = make_qkv_map(&vp, v, B, H, N, HD, 2 * BKV))) return rc;
+      prm.num_items = (int)(B * H * ((T_n + 1) / 2));
+      const unsigned pgrid = (unsigned)std::min<int64_t>(prm.num_items, num_sms());
+      SPA2_CUDA_TRY(cudaFuncSetAttribute(k_dkdv7, cudaFuncAttributeMaxDynamicSharedMemorySize, Dkv7Cfg::SMEM));
+      SPA2_CUDA_TRY(launch_pdl(k_dkdv7, dim3(pgrid), dim3(Dkv7Cfg::THREADS), Dkv7Cfg::SMEM, st, m.q, kp, vp, m.dout, prm));
+    } else if (dkdv_variant() == 6 && dkdv_ew_warps() == 16) {
       using C6 = Dkv5Cfg<HD, 4, 2>;
       auto kern = k_dkdv5<HD, 16, 4, 2>;
       SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C6::SMEM));

@@ -6,7 +6,8 @@ case runs a small fwd + bwd parity check in a fresh interpreter:
   SPA2_DQ_VARIANT=3|4|2|1    dQ: Q/dO in TMEM (3) | 3-deep dP/dS ring, S from smem (4) | one query block
                              per CTA (2) | persistent SS (1)
   SPA2_NO_FUSED_DELTA=1      δ by its own kernel instead of inside the dQ kernel
-  SPA2_DKDV_VARIANT=5|6|1    dK/dV: 5-slot Q/dO ring | 4 slots + two P/dS buffers | two [Q|dO] stages
+  SPA2_DKDV_VARIANT=5|6|7|1  dK/dV: 5-slot Q/dO ring | 4 slots + two P/dS buffers | key-pair items
+                             (d = 128) | two [Q|dO] stages
   SPA2_DQ_EW=8, SPA2_DKDV_EW=8|16 elementwise warp counts (defaults 16, 16)
 Checked against the float64 oracle at two ragged shapes (d = 64 and 128)."""
 
@@ -54,6 +55,7 @@ VARIANTS = [
     {"SPA2_NO_FUSED_DELTA": "1"},
     {"SPA2_DKDV_VARIANT": "1"},
     {"SPA2_DKDV_VARIANT": "6"},
+    {"SPA2_DKDV_VARIANT": "7"},
     {"SPA2_DQ_EW": "8", "SPA2_DKDV_EW": "8"},
     {"SPA2_DKDV_VARIANT": "1", "SPA2_DKDV_EW": "16"},
 ]
