@@ -2248,21 +2248,24 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
 // query columns each), 18-21 epilogue, 22 TMA (V pair, dO ring).
 // ---------------------------------------------------------------------------------------
 struct Dkv7Cfg {
-  static constexpr int NSL = 5;                       // 32 KB Q / dO operand slots
+  static constexpr int NSL = 4;                       // 32 KB Q / dO operand slots
   static constexpr int PAIR = 2 * BKV;                // 128 keys
   static constexpr int KVP_BYTES = PAIR * 128 * 2;    // 32 KB
   static constexpr int Q_BYTES = BQ * 128 * 2;        // 32 KB
   static constexpr int OFF_K = 0, OFF_V = KVP_BYTES, OFF_SL = 2 * KVP_BYTES;
-  static constexpr int OFF_BAR = OFF_SL + NSL * Q_BYTES;
-  static constexpr int NUM_BARS = 2 + 2 * NSL + 6;
+  static constexpr int OFF_ST = OFF_SL + NSL * Q_BYTES;  // [2 tiles][LSE 128 | δ 128] fp32
+  static constexpr int OFF_BAR = OFF_ST + 2 * 2 * BQ * 4;
+  static constexpr int NUM_BARS = 2 + 2 * NSL + 6 + 4;
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + kSmemAlignSlack;
   static constexpr uint32_t S_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 384;
   static constexpr int EPI0 = 18, PROD2 = 22, THREADS = 32 * 23;
 };
 
-// Merge cursor over the column lists of key blocks 2jp and 2jp+1 (both ascending).
+// Merge cursor over the column lists of key blocks 2jp and 2jp+1 (both ascending).  The head
+// of each list is held in a register and the next entry is loaded as soon as a head is
+// consumed, so the global-load latency is paid one union tile ahead, not on the issue path.
 struct PairCursor {
-  int a, ae, b, be;
+  int a, ae, b, be, va, vb;
 };
 __device__ __forceinline__ void pair_init(PairCursor& pc, const BwdParams& p, int bh, int jp) {
   const int j0 = 2 * jp, j1 = j0 + 1;
@@ -2275,22 +2278,29 @@ __device__ __forceinline__ void pair_init(PairCursor& pc, const BwdParams& p, in
   } else {
     pc.b = pc.be = 0;
   }
+  pc.va = pc.a < pc.ae ? __ldg(p.idx + pc.a) : 0x7fffffff;
+  pc.vb = pc.b < pc.be ? __ldg(p.idx + pc.b) : 0x7fffffff;
 }
 __device__ __forceinline__ bool pair_done(const PairCursor& pc) { return pc.a >= pc.ae && pc.b >= pc.be; }
 // Next query block of the union; flags bit h = key block 2jp+h keeps it.
 __device__ __forceinline__ int pair_next(PairCursor& pc, const int32_t* idx, int& flags) {
-  const int ia = pc.a < pc.ae ? __ldg(idx + pc.a) : 0x7fffffff;
-  const int ib = pc.b < pc.be ? __ldg(idx + pc.b) : 0x7fffffff;
-  const int i = min(ia, ib);
-  flags = (ia == i ? 1 : 0) | (ib == i ? 2 : 0);
-  if (ia == i) ++pc.a;
-  if (ib == i) ++pc.b;
+  const int i = min(pc.va, pc.vb);
+  flags = (pc.va == i ? 1 : 0) | (pc.vb == i ? 2 : 0);
+  if (pc.va == i) {
+    ++pc.a;
+    pc.va = pc.a < pc.ae ? __ldg(idx + pc.a) : 0x7fffffff;
+  }
+  if (pc.vb == i) {
+    ++pc.b;
+    pc.vb = pc.b < pc.be ? __ldg(idx + pc.b) : 0x7fffffff;
+  }
   return i;
 }
 
 __global__ void __launch_bounds__(Dkv7Cfg::THREADS, 1)
     k_dkdv7(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKP,
-            const __grid_constant__ CUtensorMap tmVP, const __grid_constant__ CUtensorMap tmDO, const BwdParams p) {
+            const __grid_constant__ CUtensorMap tmVP, const __grid_constant__ CUtensorMap tmDO,
+            const __grid_constant__ CUtensorMap tmL, const __grid_constant__ CUtensorMap tmD, const BwdParams p) {
   using C = Dkv7Cfg;
   constexpr int NSL = C::NSL;
   constexpr int EWT = 32 * 16;
@@ -2308,7 +2318,10 @@ __global__ void __launch_bounds__(Dkv7Cfg::THREADS, 1)
   uint64_t* ds_full = p_full + 1;      // dSᵀ(g) packed over the dPᵀ columns
   uint64_t* acc_full = ds_full + 1;    // last dV/dK of item `it` done
   uint64_t* acc_empty = acc_full + 1;  // accumulators read out
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(acc_empty + 1);
+  uint64_t* st_full = acc_empty + 1;   // [2] LSE/δ of the query block of tile g in slot g&1
+  uint64_t* st_empty = st_full + 2;    // [2] elementwise warps done with them
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(st_empty + 2);
+  const float* stats = reinterpret_cast<const float*>(smem + C::OFF_ST);
 
   const int warp = (int)warp_id(), lane = (int)lane_id();
   const int TP = (p.T_n + 1) / 2;
@@ -2325,6 +2338,10 @@ __global__ void __launch_bounds__(Dkv7Cfg::THREADS, 1)
     mbar_init(ds_full, EWT);
     mbar_init(acc_full, 1);
     mbar_init(acc_empty, 128);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&st_full[s], 1);
+      mbar_init(&st_empty[s], EWT);
+    }
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tmem_holder, 512);
@@ -2343,6 +2360,10 @@ __global__ void __launch_bounds__(Dkv7Cfg::THREADS, 1)
       const CUtensorMap* tmR = second ? &tmDO : &tmQ;
       tma_prefetch(tmKV);
       tma_prefetch(tmR);
+      if (!second) {
+        tma_prefetch(&tmL);
+        tma_prefetch(&tmD);
+      }
       uint8_t* const kv_dst = smem + (second ? C::OFF_V : C::OFF_K);
       int it = 0, g = 0;
       for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
@@ -2356,6 +2377,14 @@ __global__ void __launch_bounds__(Dkv7Cfg::THREADS, 1)
         while (!pair_done(pc)) {
           int fl;
           const int i = pair_next(pc, p.idx, fl);
+          if (!second) {  // the query block's LSE and δ (128 each; TMA zero-fills past N)
+            const int ss = g & 1;
+            if (g >= 2) mbar_wait(&st_empty[ss], ((uint32_t)(g >> 1) + 1u) & 1u);
+            mbar_expect_tx(&st_full[ss], 2 * BQ * 4);
+            uint8_t* sdst = smem + C::OFF_ST + ss * 2 * BQ * 4;
+            tma_load_2d(sdst, &tmL, &st_full[ss], i * BQ, bh);
+            tma_load_2d(sdst + BQ * 4, &tmD, &st_full[ss], i * BQ, bh);
+          }
           const int u = 2 * g + (second ? 1 : 0);
           const int s = u % NSL;
           if (u >= NSL) mbar_wait(&sl_empty[s], ((uint32_t)(u / NSL) + 1u) & 1u);
@@ -2414,7 +2443,7 @@ __global__ void __launch_bounds__(Dkv7Cfg::THREADS, 1)
         const uint64_t sq = (uint64_t)(uq % NSL) * SLOT16, sd = (uint64_t)(ud % NSL) * SLOT16;
         mbar_wait(p_full, (uint32_t)g & 1u);
         tc_fence_after();
-        mma_bf16_ts_k8_w<8u, 128ull, 512ull>(tbase + C::DV_COL, tbase + C::S_COL, dSLm0 + sd, idT, first ? 0u : 1u);
+        mma_bf16_ts_k8p_w<8u, 32u, 128ull, 512ull>(tbase + C::DV_COL, tbase + C::S_COL, dSLm0 + sd, idT, first ? 0u : 1u);
         mma_commit_w(&sl_empty[ud % NSL]);  // dO(g): dPᵀ(g) and dV(g) both issued by this thread
         const bool more = !last;
         bool next_last = false;
@@ -2425,7 +2454,7 @@ __global__ void __launch_bounds__(Dkv7Cfg::THREADS, 1)
         }
         mbar_wait(ds_full, (uint32_t)g & 1u);
         tc_fence_after();
-        mma_bf16_ts_k8_w<8u, 128ull, 512ull>(tbase + C::DK_COL, tbase + C::DP_COL, dSLm0 + sq, idT, first ? 0u : 1u);
+        mma_bf16_ts_k8p_w<8u, 32u, 128ull, 512ull>(tbase + C::DK_COL, tbase + C::DP_COL, dSLm0 + sq, idT, first ? 0u : 1u);
         mma_commit_w(&sl_empty[uq % NSL]);  // Q(g): Sᵀ(g) and dK(g)
         if (!more) {
           mma_commit_w(acc_full);
@@ -2454,28 +2483,28 @@ __global__ void __launch_bounds__(Dkv7Cfg::THREADS, 1)
       pair_init(pc, p, bh, jp);
       if (pair_done(pc)) continue;
       const bool key_ok = jp * C::PAIR + q4 * 32 + lane < p.N;
-      const int64_t rowbase = (int64_t)bh * p.N;
       while (!pair_done(pc)) {
         int fl;
         const int i = pair_next(pc, p.idx, fl);
         const bool kept = (fl >> half) & 1;  // warp- and lane-quarter-uniform
         const int q0 = i * BQ + (int)col0;
-        float lse_first[16];  // first pass's row statistics, loaded before the wait
-        if (kept) {
-#pragma unroll
-          for (int c = 0; c < 16; ++c) lse_first[c] = q0 + c < p.N ? __ldg(p.lse + rowbase + q0 + c) * kLog2e : INFINITY;
-        }
+        const float* st = stats + (g & 1) * 2 * BQ + col0;  // this thread's 32 columns: LSE, then δ at +BQ
+        mbar_wait(&st_full[g & 1], (uint32_t)(g >> 1) & 1u);
         mbar_wait(s_full, (uint32_t)g & 1u);
         tc_fence_after();
         float pv[32];  // fp32 P of this thread's 32 query columns, kept for dS
+        uint32_t pk[16];
         if (kept) {
 #pragma unroll
           for (int h = 0; h < 2; ++h) {  // two passes of 16 columns keep register pressure down
             float lse2[16];
 #pragma unroll
-            for (int c = 0; c < 16; ++c) {
-              const int q = q0 + 16 * h + c;
-              lse2[c] = h == 0 ? lse_first[c] : (q < p.N ? __ldg(p.lse + rowbase + q) * kLog2e : INFINITY);
+            for (int c4 = 0; c4 < 4; ++c4) {
+              const float4 l4 = *reinterpret_cast<const float4*>(st + 16 * h + 4 * c4);
+              const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                lse2[4 * c4 + e] = q0 + 16 * h + 4 * c4 + e < p.N ? lv[e] * kLog2e : INFINITY;
             }
             uint32_t sr[16];
             tmem_ld16(tbase + lane_off + C::S_COL + col0 + 16u * h, sr);
@@ -2492,59 +2521,38 @@ __global__ void __launch_bounds__(Dkv7Cfg::THREADS, 1)
               }
               pv[16 * h + 2 * c] = key_ok ? e.x : 0.f;
               pv[16 * h + 2 * c + 1] = key_ok ? e.y : 0.f;
+              pk[8 * h + c] = pack_bf16(pv[16 * h + 2 * c], pv[16 * h + 2 * c + 1]);
             }
           }
-          // the four warps of this lane quarter read disjoint S columns but write packed P
-          // into the first 64: all must have read S before any writes
-          named_bar_sync(1 + q4, 128);
-          uint32_t pk[16];
-#pragma unroll
-          for (int c = 0; c < 16; ++c) pk[c] = pack_bf16(pv[2 * c], pv[2 * c + 1]);
-          tmem_st16(tbase + lane_off + C::S_COL + col0 / 2, pk);
         } else {
-          uint32_t pk[16];
 #pragma unroll
           for (int c = 0; c < 16; ++c) pk[c] = 0u;
-          tmem_st16(tbase + lane_off + C::S_COL + col0 / 2, pk);
         }
+        // packed Pᵀ goes into the first 16 of this thread's own 32 columns (the MMA reads the
+        // K steps at column offsets 0, 8, 32, 40, ...): no other thread's S is overwritten
+        tmem_st16(tbase + lane_off + C::S_COL + col0, pk);
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(p_full);
-        float dlt_first[16];
-        if (kept) {
-#pragma unroll
-          for (int c = 0; c < 16; ++c) dlt_first[c] = q0 + c < p.N ? __ldg(p.delta + rowbase + q0 + c) : 0.f;
-        }
         mbar_wait(dp_full, (uint32_t)g & 1u);
         tc_fence_after();
         if (kept) {
-          uint32_t pk[16];
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            float dlt[16];
-#pragma unroll
-            for (int c = 0; c < 16; ++c) {
-              const int q = q0 + 16 * h + c;
-              dlt[c] = h == 0 ? dlt_first[c] : (q < p.N ? __ldg(p.delta + rowbase + q) : 0.f);
-            }
             uint32_t dr[16];
             tmem_ld16(tbase + lane_off + C::DP_COL + col0 + 16u * h, dr);
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
+              const float2 dl = *reinterpret_cast<const float2*>(st + BQ + 16 * h + 2 * c);
               const float2 ds = __fmul2_rn(make_float2(pv[16 * h + 2 * c], pv[16 * h + 2 * c + 1]),
                                            __fadd2_rn(make_float2(__uint_as_float(dr[2 * c]), __uint_as_float(dr[2 * c + 1])),
-                                                      make_float2(-dlt[2 * c], -dlt[2 * c + 1])));
+                                                      make_float2(-dl.x, -dl.y)));
               pk[8 * h + c] = pack_bf16(ds.x, ds.y);
             }
           }
-          named_bar_sync(1 + q4, 128);
-          tmem_st16(tbase + lane_off + C::DP_COL + col0 / 2, pk);
-        } else {
-          uint32_t pk[16];
-#pragma unroll
-          for (int c = 0; c < 16; ++c) pk[c] = 0u;
-          tmem_st16(tbase + lane_off + C::DP_COL + col0 / 2, pk);
         }
+        mbar_arrive(&st_empty[g & 1]);
+        tmem_st16(tbase + lane_off + C::DP_COL + col0, pk);
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(ds_full);
@@ -2716,14 +2724,17 @@ int launch_attn_bwd(int which, const spa2_view& q, const spa2_view& k, const spa
   } else {
     prm.out1 = (__nv_bfloat16*)out1->ptr;
     prm.o1_sb = out1->sb, prm.o1_sh = out1->sh, prm.o1_sn = out1->sn;
-    if (HD == 128 && dkdv_variant() == 7) {
-      CUtensorMap kp, vp;  // 128-row boxes: one key PAIR per load
+    if (HD == 128 && dkdv_variant() == 7 && N % 4 == 0) {  // LSE/δ rows must be 16-byte aligned for TMA
+      CUtensorMap kp, vp, tl, td;  // 128-row boxes: one key PAIR per load; LSE/δ tiles
       if ((rc = make_qkv_map(&kp, k, B, H, N, HD, 2 * BKV))) return rc;
       if ((rc = make_qkv_map(&vp, v, B, H, N, HD, 2 * BKV))) return rc;
+      if ((rc = make_tma_f32_2d(&tl, lse, (uint64_t)N, (uint64_t)(B * H), (uint64_t)N, BQ, 1))) return rc;
+      if ((rc = make_tma_f32_2d(&td, delta, (uint64_t)N, (uint64_t)(B * H), (uint64_t)N, BQ, 1))) return rc;
       prm.num_items = (int)(B * H * ((T_n + 1) / 2));
       const unsigned pgrid = (unsigned)std::min<int64_t>(prm.num_items, num_sms());
       SPA2_CUDA_TRY(cudaFuncSetAttribute(k_dkdv7, cudaFuncAttributeMaxDynamicSharedMemorySize, Dkv7Cfg::SMEM));
-      SPA2_CUDA_TRY(launch_pdl(k_dkdv7, dim3(pgrid), dim3(Dkv7Cfg::THREADS), Dkv7Cfg::SMEM, st, m.q, kp, vp, m.dout, prm));
+      SPA2_CUDA_TRY(launch_pdl(k_dkdv7, dim3(pgrid), dim3(Dkv7Cfg::THREADS), Dkv7Cfg::SMEM, st, m.q, kp, vp, m.dout, tl, td,
+                               prm));
     } else if (dkdv_variant() == 6 && dkdv_ew_warps() == 16) {
       using C6 = Dkv5Cfg<HD, 4, 2>;
       auto kern = k_dkdv5<HD, 16, 4, 2>;

@@ -112,6 +112,22 @@ int make_tma_bf16_2d(CUtensorMap* map, const void* base, uint64_t cols, uint64_t
   return SPA2_OK;
 }
 
+// 2-D map over a row-major [rows][cols] fp32 matrix, no swizzle (row statistics tiles).
+int make_tma_f32_2d(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint64_t row_stride_elems,
+                    uint32_t box_cols, uint32_t box_rows) {
+  auto fn = encode_fn();
+  SPA2_REQUIRE(fn != nullptr, SPA2_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+  cuuint64_t gdim[2] = {cols, rows};
+  cuuint64_t gstride[1] = {row_stride_elems * 4};
+  cuuint32_t bx[2] = {box_cols, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), gdim, gstride, bx, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  SPA2_REQUIRE(r == CUDA_SUCCESS, SPA2_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return SPA2_OK;
+}
+
 }  // namespace spa2
 
 extern "C" const char* spa2_version(void) { return "spa2 0.1.0 sm_100a"; }

@@ -302,6 +302,27 @@ __device__ __forceinline__ void mma_bf16_ts_k8_w(uint32_t d_tmem, uint32_t a0, u
       "n"(6 * A_STEP), "n"(OFF4 + 2 * OFF1), "n"(7 * A_STEP), "n"(OFF4 + 3 * OFF1)
       : "memory");
 }
+// TS form, A columns a0 + (ks/2)*A2 + (ks%2)*A1 (operands packed per 32-column group).
+template <uint32_t A1, uint32_t A2, uint64_t OFF1, uint64_t OFF4>
+__device__ __forceinline__ void mma_bf16_ts_k8p_w(uint32_t d_tmem, uint32_t a0, uint64_t b0, uint32_t idesc,
+                                                  uint32_t acc0) {
+  asm volatile(
+      "{\n\t.reg .pred p, q, e;\n\t.reg .b32 a;\n\t.reg .b64 b;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 q, %4, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t"
+      "add.u32 a, %1, %5;\n\tadd.s64 b, %2, %6;\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, q;\n\t"
+      "add.u32 a, %1, %7;\n\tadd.s64 b, %2, %8;\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, q;\n\t"
+      "add.u32 a, %1, %9;\n\tadd.s64 b, %2, %10;\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, q;\n\t"
+      "add.u32 a, %1, %11;\n\tadd.s64 b, %2, %12;\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, q;\n\t"
+      "add.u32 a, %1, %13;\n\tadd.s64 b, %2, %14;\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, q;\n\t"
+      "add.u32 a, %1, %15;\n\tadd.s64 b, %2, %16;\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, q;\n\t"
+      "add.u32 a, %1, %17;\n\tadd.s64 b, %2, %18;\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, q;\n\t"
+      "}" ::"r"(d_tmem),
+      "r"(a0), "l"(b0), "r"(idesc), "r"(acc0), "n"(A1), "n"(OFF1), "n"(A2), "n"(2 * OFF1), "n"(A2 + A1),
+      "n"(3 * OFF1), "n"(2 * A2), "n"(OFF4), "n"(2 * A2 + A1), "n"(OFF4 + OFF1), "n"(3 * A2), "n"(OFF4 + 2 * OFF1),
+      "n"(3 * A2 + A1), "n"(OFF4 + 3 * OFF1)
+      : "memory");
+}
 // SS form: D (+)= A[a0 + offA(ks)] · B[b0 + offB(ks)], ks = 0..7, off(ks) = (ks/4)*O4 + (ks%4)*O1.
 template <uint64_t A1, uint64_t A4, uint64_t B1, uint64_t B4>
 __device__ __forceinline__ void mma_bf16_ss_k8_w(uint32_t d_tmem, uint64_t a0, uint64_t b0, uint32_t idesc,

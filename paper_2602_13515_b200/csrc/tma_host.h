@@ -14,6 +14,9 @@ int make_tma_bf16_5d(CUtensorMap* map, const void* base, const uint64_t dims[5],
 // 2-D map over a row-major [rows][cols] bf16 matrix.
 int make_tma_bf16_2d(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint64_t row_stride_elems,
                      uint32_t box_cols, uint32_t box_rows);
+// 2-D map over a row-major [rows][cols] fp32 matrix, no swizzle.
+int make_tma_f32_2d(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint64_t row_stride_elems,
+                    uint32_t box_cols, uint32_t box_rows);
 }  // namespace spa2
 
 #include "../../include/spa2.h"
