@@ -35,9 +35,11 @@ namespace spa2 {
 namespace {
 
 // Share of the elementwise exponentials computed by exp2_poly2 on the FMA pipe instead of
-// MUFU: CPT*NUM/64 of each thread's CPT/2 pairs (NUM = 8: a quarter).
+// MUFU: CPT*NUM/64 of each thread's CPT/2 pairs (NUM = 8: a quarter).  Measured in the
+// power-capped 400-step regime (tools/ab400.sh): dQ is fastest with none (MUFU exponentials
+// cost less energy), dK/dV with a quarter.
 #ifndef SPA2_DQ_POLY_NUM
-#define SPA2_DQ_POLY_NUM 8
+#define SPA2_DQ_POLY_NUM 0
 #endif
 #ifndef SPA2_DKDV_POLY_NUM
 #define SPA2_DKDV_POLY_NUM 8

@@ -355,7 +355,11 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
 // Warps: 0 TMA (Q, K ring), 1 MMA (S, PV), 2-5 softmax + epilogue, 6 TMA (V ring).
 // ---------------------------------------------------------------------------------------
 #ifndef SPA2_FWD3_POLY_PAIRS
-#define SPA2_FWD3_POLY_PAIRS 10  // of 32 exponential pairs per row and tile (exp2_poly2 on the FMA pipe)
+// Exponential pairs (of 32 per row and tile) evaluated by exp2_poly2 on the FMA pipe instead of
+// MUFU.  0 since the board runs at its power cap in sustained use: 10 was 2 % faster at full
+// clocks, 0 is 3 % faster at the cap (MUFU exponentials cost less energy than 6-instruction
+// polynomials; tools/ab400.sh).
+#define SPA2_FWD3_POLY_PAIRS 0
 #endif
 template <int HD>
 struct Fwd3Cfg {
