@@ -35,6 +35,9 @@ constexpr int BQ = 128;
 constexpr int BKV = 64;
 constexpr int kFwdThreads = 224;  // + warp 6: second TMA producer (V)
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: P entries stay <= 2^8
+#ifndef SPA2_FWD1_POLY_PAIRS
+#define SPA2_FWD1_POLY_PAIRS 8  // variant 1: exponential pairs (of 32) by polynomial
+#endif
 #ifndef SPA2_FWD_EXP_MODE
 #define SPA2_FWD_EXP_MODE 0
 #endif
@@ -283,7 +286,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
         float2 e;
         if (kExpMode == 1) {  // two exponentials per MUFU op (ex2.approx.f16x2); error below P's bf16 rounding
           e = ex2_f16x2(x);
-        } else if (c < 8) {  // a quarter of the exponentials on the FMA pipe
+        } else if (c < SPA2_FWD1_POLY_PAIRS) {  // part of the exponentials on the FMA pipe
           e = exp2_poly2(x);
         } else {
           e.x = ex2(x.x);
@@ -1020,8 +1023,11 @@ __global__ void __launch_bounds__(kFwd2Threads, 1)
 
 int fwd_variant() {
   static const int v = [] {
+    // default 1 (one CTA per query block, 2 per SM, the hardware block scheduler balancing
+    // the uneven list lengths): 5 % faster than the persistent variant 3 at full clocks and 2 %
+    // at the power cap once both run without trace code (tools/ab.sh, tools/ab400.sh)
     const char* e = getenv("SPA2_FWD_VARIANT");
-    return e != nullptr ? atoi(e) : 3;
+    return e != nullptr ? atoi(e) : 1;
   }();
   return v;
 }

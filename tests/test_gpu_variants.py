@@ -2,7 +2,7 @@
 
 The variant is chosen once per process from the environment (static in libspa2.so), so each
 case runs a small fwd + bwd parity check in a fresh interpreter:
-  SPA2_FWD_VARIANT=3|1|2     forward: persistent 2 CTAs/SM | one CTA per query block | Q in TMEM
+  SPA2_FWD_VARIANT=1|3|2     forward: one CTA per query block | persistent 2 CTAs/SM | Q in TMEM
   SPA2_DQ_VARIANT=3|4|2|1    dQ: Q/dO in TMEM (3) | 3-deep dP/dS ring, S from smem (4) | one query block
                              per CTA (2) | persistent SS (1)
   SPA2_NO_FUSED_DELTA=1      δ by its own kernel instead of inside the dQ kernel
@@ -46,7 +46,7 @@ print("ok")
 """
 
 VARIANTS = [
-    {"SPA2_FWD_VARIANT": "1"},
+    {"SPA2_FWD_VARIANT": "3"},
     {"SPA2_FWD_VARIANT": "2"},
     {"SPA2_DQ_VARIANT": "4"},
     {"SPA2_DQ_VARIANT": "4", "SPA2_DQ_EW": "8"},

@@ -8,7 +8,7 @@ TAG=${1:-r01}
 OUT=gpurun_out
 mkdir -p "$OUT"
 BENCH="python bench.py --steps 1 --warmup 3 --no-e2e --no-dense --no-cpu-baseline"
-KERNELS='k_dkdv|k_dq3|k_fwd3|k_pool_bf16_pipe|k_scores|k_select|k_counts|k_scan_orders|k_fill'
+KERNELS='k_dkdv|k_dq3|k_fwd|k_pool_bf16_pipe|k_scores|k_select|k_counts|k_scan_orders|k_fill'
 PER_STEP=9   # kernels of one step matching $KERNELS; the bench runs 1 + (warmup-1) + steps = 4 steps
 
 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
