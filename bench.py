@@ -300,7 +300,7 @@ def gpu_arm(args, rank: int, world: int, dev):
 
         for _ in range(2):
             e2e_step()
-        n_e2e = max(3, min(args.steps, 30))
+        n_e2e = max(3, min(args.steps, 60))
         barrier()
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
