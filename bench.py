@@ -279,9 +279,14 @@ def gpu_arm(args, rank: int, world: int, dev):
                 traffic = json.load(f).get("kernels", {}).get(dom, {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    roofline = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peaks["bf16_tflops"],
-                "unit": "TFLOP/s", "frac": achieved / peaks["bf16_tflops"], "traffic": traffic,
-                "peak_source": peaks["source"] + ", burst bf16 GEMM",
+    # the kernel runs inside a long back-to-back step loop (the board reaches its power cap),
+    # so it is held against the SUSTAINED bf16 GEMM figure; a short run uses the burst one
+    sustained = args.steps * ms_step >= 100.0
+    peak = peaks["bf16_tflops_sustained"] if sustained else peaks["bf16_tflops"]
+    roofline = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak,
+                "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                "peak_source": peaks["source"] + (", sustained bf16 GEMM (long timed loop)" if sustained
+                                                  else ", burst bf16 GEMM"),
                 "flops_per_launch": kflops[dom], "ms_per_launch": per_kernel_ms[dom]}
 
     out = {"ms_step": ms_step, "sparsity": sparsity, "clocks": clocks, "launches": launches,
