@@ -2249,14 +2249,21 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
 // Warps: 0 TMA (K pair, Q ring), 1 MMA issue, 2-17 elementwise (4 per lane quarter, 32
 // query columns each), 18-21 epilogue, 22 TMA (V pair, dO ring).
 // ---------------------------------------------------------------------------------------
+#ifndef SPA2_DKDV7_NSL
+#define SPA2_DKDV7_NSL 4
+#endif
+#ifndef SPA2_DKDV7_NST
+#define SPA2_DKDV7_NST 2
+#endif
 struct Dkv7Cfg {
-  static constexpr int NSL = 4;                       // 32 KB Q / dO operand slots
+  static constexpr int NSL = SPA2_DKDV7_NSL;          // 32 KB Q / dO operand slots
   static constexpr int PAIR = 2 * BKV;                // 128 keys
   static constexpr int KVP_BYTES = PAIR * 128 * 2;    // 32 KB
   static constexpr int Q_BYTES = BQ * 128 * 2;        // 32 KB
   static constexpr int OFF_K = 0, OFF_V = KVP_BYTES, OFF_SL = 2 * KVP_BYTES;
-  static constexpr int OFF_ST = OFF_SL + NSL * Q_BYTES;  // [2 tiles][LSE 128 | δ 128] fp32
-  static constexpr int OFF_BAR = OFF_ST + 2 * 2 * BQ * 4;
+  static constexpr int NST = SPA2_DKDV7_NST;               // LSE/δ slots (tiles in flight)
+  static constexpr int OFF_ST = OFF_SL + NSL * Q_BYTES;  // [NST tiles][LSE 128 | δ 128] fp32
+  static constexpr int OFF_BAR = OFF_ST + NST * 2 * BQ * 4;
   static constexpr int NUM_BARS = 2 + 2 * NSL + 6 + 4;
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + kSmemAlignSlack;
   static constexpr uint32_t S_COL = 0, DP_COL = 128, DV_COL = 256, DK_COL = 384;
@@ -2320,8 +2327,9 @@ __global__ void __launch_bounds__(Dkv7Cfg::THREADS, 1)
   uint64_t* ds_full = p_full + 1;      // dSᵀ(g) packed over the dPᵀ columns
   uint64_t* acc_full = ds_full + 1;    // last dV/dK of item `it` done
   uint64_t* acc_empty = acc_full + 1;  // accumulators read out
-  uint64_t* st_full = acc_empty + 1;   // [2] LSE/δ of the query block of tile g in slot g&1
-  uint64_t* st_empty = st_full + 2;    // [2] elementwise warps done with them
+  constexpr int NST = C::NST;
+  uint64_t* st_full = acc_empty + 1;   // [NST] LSE/δ of the query block of tile g in slot g % NST
+  uint64_t* st_empty = st_full + 2;    // [NST] elementwise warps done with them
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(st_empty + 2);
   const float* stats = reinterpret_cast<const float*>(smem + C::OFF_ST);
 
@@ -2380,8 +2388,8 @@ __global__ void __launch_bounds__(Dkv7Cfg::THREADS, 1)
           int fl;
           const int i = pair_next(pc, p.idx, fl);
           if (!second) {  // the query block's LSE and δ (128 each; TMA zero-fills past N)
-            const int ss = g & 1;
-            if (g >= 2) mbar_wait(&st_empty[ss], ((uint32_t)(g >> 1) + 1u) & 1u);
+            const int ss = g % NST;
+            if (g >= NST) mbar_wait(&st_empty[ss], ((uint32_t)(g / NST) + 1u) & 1u);
             mbar_expect_tx(&st_full[ss], 2 * BQ * 4);
             uint8_t* sdst = smem + C::OFF_ST + ss * 2 * BQ * 4;
             tma_load_2d(sdst, &tmL, &st_full[ss], i * BQ, bh);
@@ -2389,7 +2397,9 @@ __global__ void __launch_bounds__(Dkv7Cfg::THREADS, 1)
           }
           const int u = 2 * g + (second ? 1 : 0);
           const int s = u % NSL;
+          if (!second) trace_ev(p.trace, p.trace_cap, 0, 1, g);
           if (u >= NSL) mbar_wait(&sl_empty[s], ((uint32_t)(u / NSL) + 1u) & 1u);
+          if (!second) trace_ev(p.trace, p.trace_cap, 0, 2, g);
           mbar_expect_tx(&sl_full[s], C::Q_BYTES);
           tma_load_5d(smem + C::OFF_SL + s * C::Q_BYTES, tmR, &sl_full[s], 0, i * BQ, 0, hh, bb);
           ++g;
@@ -2416,6 +2426,7 @@ __global__ void __launch_bounds__(Dkv7Cfg::THREADS, 1)
       const int uq = 2 * gg;
       mbar_wait(&sl_full[uq % NSL], (uint32_t)(uq / NSL) & 1u);
       tc_fence_after();
+      trace_ev(p.trace, p.trace_cap, 1, 1, gg);
       mma_bf16_ss_k8_w<2ull, 1024ull, 2ull, 1024ull>(tbase + C::S_COL, dKP, dSLk0 + (uint64_t)(uq % NSL) * SLOT16, idS, 0u);
       mma_commit_w(s_full);
     };
@@ -2425,6 +2436,7 @@ __global__ void __launch_bounds__(Dkv7Cfg::THREADS, 1)
       tc_fence_after();
       mma_bf16_ss_k8_w<2ull, 1024ull, 2ull, 1024ull>(tbase + C::DP_COL, dVP, dSLk0 + (uint64_t)(ud % NSL) * SLOT16, idS, 0u);
       mma_commit_w(dp_full);
+      trace_ev(p.trace, p.trace_cap, 1, 2, gg);
       if (last) mma_commit_w(kv_empty);  // the K/V pair is only read by Sᵀ and dPᵀ
     };
     for (int wi = blockIdx.x; wi < p.num_items; wi += gridDim.x) {
@@ -2445,6 +2457,7 @@ __global__ void __launch_bounds__(Dkv7Cfg::THREADS, 1)
         const uint64_t sq = (uint64_t)(uq % NSL) * SLOT16, sd = (uint64_t)(ud % NSL) * SLOT16;
         mbar_wait(p_full, (uint32_t)g & 1u);
         tc_fence_after();
+        trace_ev(p.trace, p.trace_cap, 1, 3, g);
         mma_bf16_ts_k8p_w<8u, 32u, 128ull, 512ull>(tbase + C::DV_COL, tbase + C::S_COL, dSLm0 + sd, idT, first ? 0u : 1u);
         mma_commit_w(&sl_empty[ud % NSL]);  // dO(g): dPᵀ(g) and dV(g) both issued by this thread
         const bool more = !last;
@@ -2456,6 +2469,7 @@ __global__ void __launch_bounds__(Dkv7Cfg::THREADS, 1)
         }
         mbar_wait(ds_full, (uint32_t)g & 1u);
         tc_fence_after();
+        trace_ev(p.trace, p.trace_cap, 1, 4, g);
         mma_bf16_ts_k8p_w<8u, 32u, 128ull, 512ull>(tbase + C::DK_COL, tbase + C::DP_COL, dSLm0 + sq, idT, first ? 0u : 1u);
         mma_commit_w(&sl_empty[uq % NSL]);  // Q(g): Sᵀ(g) and dK(g)
         if (!more) {
@@ -2490,9 +2504,11 @@ __global__ void __launch_bounds__(Dkv7Cfg::THREADS, 1)
         const int i = pair_next(pc, p.idx, fl);
         const bool kept = (fl >> half) & 1;  // warp- and lane-quarter-uniform
         const int q0 = i * BQ + (int)col0;
-        const float* st = stats + (g & 1) * 2 * BQ + col0;  // this thread's 32 columns: LSE, then δ at +BQ
-        mbar_wait(&st_full[g & 1], (uint32_t)(g >> 1) & 1u);
+        const float* st = stats + (g % NST) * 2 * BQ + col0;  // this thread's 32 columns: LSE, then δ at +BQ
+        if (threadIdx.x == 64) trace_ev(p.trace, p.trace_cap, 2, 1, g);
+        mbar_wait(&st_full[g % NST], (uint32_t)(g / NST) & 1u);
         mbar_wait(s_full, (uint32_t)g & 1u);
+        if (threadIdx.x == 64) trace_ev(p.trace, p.trace_cap, 2, 2, g);
         tc_fence_after();
         float pv[32];  // fp32 P of this thread's 32 query columns, kept for dS
         uint32_t pk[16];
@@ -2536,7 +2552,9 @@ __global__ void __launch_bounds__(Dkv7Cfg::THREADS, 1)
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(p_full);
+        if (threadIdx.x == 64) trace_ev(p.trace, p.trace_cap, 2, 3, g);
         mbar_wait(dp_full, (uint32_t)g & 1u);
+        if (threadIdx.x == 64) trace_ev(p.trace, p.trace_cap, 2, 4, g);
         tc_fence_after();
         if (kept) {
 #pragma unroll
@@ -2553,11 +2571,12 @@ __global__ void __launch_bounds__(Dkv7Cfg::THREADS, 1)
             }
           }
         }
-        mbar_arrive(&st_empty[g & 1]);
+        mbar_arrive(&st_empty[g % NST]);
         tmem_st16(tbase + lane_off + C::DP_COL + col0, pk);
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(ds_full);
+        if (threadIdx.x == 64) trace_ev(p.trace, p.trace_cap, 2, 5, g);
         ++g;
       }
     }
