@@ -1,0 +1,57 @@
+/*
+ * spa2_diag.h — C ABI of libspa2_diag.so: micro-benchmarks and building-block probes for
+ * the sm_100a kernels in libspa2.so (tcgen05 operand layouts, MMA issue rates, TMA and
+ * TMEM throughput, mbarrier latency).  NOT part of the drop-in boundary (include/spa2.h):
+ * only tests/ and tools/ load this library.  Same conventions as spa2.h (device
+ * pointers, stream as void*, SPA2_OK or a negative status + spa2_last_error()).
+ */
+#ifndef SPA2_DIAG_H
+#define SPA2_DIAG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+const char* spa2_last_error(void);
+
+/* tcgen05 probe (test-only): D = A·Bᵀ with logical A [m,k], B [n,k] (bf16), D fp32
+ * row-major [m,n], computed by ONE tcgen05 MMA chain through exactly the shared-memory
+ * layouts and descriptors the attention kernels use.  A is stored row-major as [m,k]
+ * (a_mn = 0, staged K-major) or as [k,m] (a_mn = 1, staged MN-major); likewise B as
+ * [n,k] or [k,n].  use_tma (staging mode): 0 = generic swizzled stores, 1 = TMA
+ * (SWIZZLE_128B), 2 = A packed into TMEM by tcgen05.st and consumed by the TS form of
+ * tcgen05.mma (m = 128, K-major A only).  m in {64,128}; n, k in {64,128}. */
+int spa2_probe_gemm(const void* a, const void* b, float* d, int m, int n, int k, int a_mn, int b_mn,
+                    int use_tma, void* stream);
+
+/* tcgen05 issue-rate probe (diagnostic): `ctas` CTAs each issue reps*(k/16) dependent-free
+ * MMAs of shape m x n x 16 with the given operand layout (a_tmem = A from TMEM) and record
+ * the clock64 cycles of the whole chain in cycles[cta]. */
+int spa2_probe_mma_rate(int m, int n, int k, int a_mn, int b_mn, int a_tmem, int reps, int ctas,
+                        unsigned long long* cycles, void* stream);
+
+/* TMA streaming-rate probe (diagnostic): `ctas` CTAs each load `iters` random (box_rows x 64)
+ * bf16 tiles of a [rows, 64] buffer through a `stages`-deep ring; cycles[cta] = clock64 span. */
+int spa2_probe_tma_rate(const void* buf, long long rows, int box_rows, int stages, int iters, int ctas,
+                        unsigned long long* cycles, void* stream);
+/* Variant (diagnostic): `issuers` warps per CTA with their own rings; requests are tensor boxes
+ * of box_rows x 64 x chunks (mode 0) or 1-D bulk copies of the same size (mode 1) over a
+ * [rows][128] bf16 matrix.  cycles[ctas*4] receives per-(CTA, issuer) cycle counts. */
+/* MMA mix probe (diagnostic): the dQ kernel's per-tile tcgen05 sequence in isolation; see probe.cu. */
+int spa2_probe_mma_mix(int reps, int flags, int ctas, const void* gsrc, unsigned long long* cycles, void* stream);
+/* Diagnostic: tcgen05.ld / tcgen05.st throughput (mode 0 32-col loads, 1 two loads per wait,
+ * 2 16-col loads, 3 16-col stores), `warps` warps per CTA (<= 16); cycles[ctas * 16] per warp. */
+/* Diagnostic: cycles per mbarrier try_wait (mode 0) / test_wait (1) / mbar_wait (2) on an
+ * already-completed phase, one CTA of `threads` threads; cycles[0] = total for `reps` polls. */
+int spa2_probe_mbar_latency(int reps, int mode, int threads, unsigned long long* cycles, void* stream);
+int spa2_probe_tmem_rate(int reps, int mode, int warps, int ctas, unsigned long long* cycles, void* stream);
+int spa2_probe_tma_rate2(const void* buf, long long rows, int box_rows, int chunks, int stages, int issuers,
+                         int mode, int iters, int ctas, unsigned long long* cycles, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPA2_DIAG_H */

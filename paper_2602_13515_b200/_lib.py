@@ -1,8 +1,10 @@
 """ctypes binding of ``libspa2.so`` (the C ABI declared in ``include/spa2.h``).
 
 The library is built in-tree by ``__graft_entry__.build()`` (``make -C csrc``) and loaded
-from this directory.  There is no fallback: if the library or a CUDA device is missing,
-every operator raises.  Status codes map to the exceptions the reference raises
+from this directory (always this file: no environment variable can swap the product
+library).  There is no fallback: if the library or a CUDA device is missing, every
+operator raises.  ``load_diag()`` loads ``libspa2_diag.so`` (``include/spa2_diag.h``:
+micro-benchmarks and probes for tests/ and tools/ only).  Status codes map to the exceptions the reference raises
 (``ValueError`` / ``FloatingPointError``, numerics.py:17-32) or ``RuntimeError`` for CUDA
 failures.
 """
@@ -16,8 +18,11 @@ import threading
 
 import torch
 
-LIB_PATH = os.environ.get("SPA2_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libspa2.so")
-HEADER_PATH = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "spa2.h")
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libspa2.so")
+DIAG_LIB_PATH = os.path.join(_HERE, "libspa2_diag.so")
+HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "spa2.h")
+DIAG_HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "spa2_diag.h")
 
 SPA2_OK = 0
 SPA2_ERR_VALUE = -1
@@ -60,9 +65,12 @@ SIGNATURES = {
                        _P, _F32, _P], _I32),
     "spa2_bwd_dq_delta": ([View, View, View, View, View, _P, _P, View, _I32, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P,
                            _P, _F32, _P], _I32),
+}
+
+DIAG_SIGNATURES = {
+    "spa2_last_error": ([], ctypes.c_char_p),
     "spa2_probe_gemm": ([_P, _P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _P], _I32),
     "spa2_probe_mma_rate": ([_I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P, _P], _I32),
-    "spa2_debug_trace": ([_P, _I32], _I32),
     "spa2_probe_tma_rate": ([_P, ctypes.c_longlong, _I32, _I32, _I32, _I32, _P, _P], _I32),
     "spa2_probe_mma_mix": ([_I32, _I32, _I32, _P, _P, _P], _I32),
     "spa2_probe_mbar_latency": ([_I32, _I32, _I32, _P, _P], _I32),
@@ -107,7 +115,14 @@ def call(name: str, *args, stream_obj=None):
     start = STATS.begin(name, stream_obj) if stream_obj is not None else None
     if stream_obj is None:
         STATS.launches += KERNELS_PER_CALL.get(name, 0)
-    rc = getattr(load(), name)(*args)
+    fn = getattr(load(), name)
+    if stream_obj is not None:
+        # the C entry points launch on the calling thread's current device: make it the
+        # device of the stream (and of the tensors) even if the caller's current device differs
+        with torch.cuda.device(stream_obj.device):
+            rc = fn(*args)
+    else:
+        rc = fn(*args)
     if start is not None:
         STATS.end(name, start, stream_obj)
     check(rc, name)
@@ -125,46 +140,76 @@ _lib = None
 _checked_devices: set[int] = set()
 
 
-def header_symbols() -> list[str]:
-    """Every function the public header declares."""
-    with open(HEADER_PATH) as f:
+def header_symbols(path: str = HEADER_PATH) -> list[str]:
+    """Every function a public header declares."""
+    with open(path) as f:
         text = f.read()
     return sorted(set(re.findall(r"^\s*(?:const\s+)?\w[\w\s\*]*?\b(spa2_\w+)\s*\(", text, flags=re.M)))
 
 
+def _open(path: str, signatures: dict) -> ctypes.CDLL:
+    if not os.path.exists(path):
+        raise RuntimeError(
+            f"{os.path.basename(path)} not found at {path}; build it with `python -c 'import __graft_entry__ as g; "
+            "g.build()'` (there is no CPU fallback)")
+    lib = ctypes.CDLL(path)
+    for name, (args, res) in signatures.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    return lib
+
+
 def load() -> ctypes.CDLL:
-    """Load (once) and type the shared library.  Raises if it has not been built."""
+    """Load (once) and type the product library.  Raises if it has not been built."""
     global _lib
     with _lock:
         if _lib is None:
-            if not os.path.exists(LIB_PATH):
-                raise RuntimeError(
-                    f"libspa2.so not found at {LIB_PATH}; build it with `python -c 'import __graft_entry__ as g; "
-                    "g.build()'` (there is no CPU fallback)")
-            lib = ctypes.CDLL(LIB_PATH)
-            for name, (args, res) in SIGNATURES.items():
-                if name.startswith("spa2_probe_") and not hasattr(lib, name):
-                    continue  # diagnostics only: an older A/B build may predate a probe
-                fn = getattr(lib, name)
-                fn.argtypes = args
-                fn.restype = res
-            _lib = lib
+            _lib = _open(LIB_PATH, SIGNATURES)
     return _lib
+
+
+_diag = None
+
+
+def load_diag() -> ctypes.CDLL:
+    """Load (once) the diagnostics library (tests/ and tools/ only)."""
+    global _diag
+    with _lock:
+        if _diag is None:
+            _diag = _open(DIAG_LIB_PATH, DIAG_SIGNATURES)
+    return _diag
+
+
+def use_library(path: str) -> None:
+    """Load the product library from ``path`` instead of the in-tree build (A/B timing of an
+    alternative build by tools; an explicit call, never an environment variable).  Must run
+    before the first operator call."""
+    global LIB_PATH
+    with _lock:
+        if _lib is not None and os.path.abspath(path) != os.path.abspath(LIB_PATH):
+            raise RuntimeError("libspa2.so is already loaded; use_library() must come first")
+        LIB_PATH = os.path.abspath(path)
 
 
 def last_error() -> str:
     return load().spa2_last_error().decode(errors="replace")
 
 
-def check(rc: int, what: str) -> None:
+def check(rc: int, what: str, _err=None) -> None:
     if rc == SPA2_OK:
         return
-    msg = f"{what}: {last_error()}"
+    msg = f"{what}: {(_err or last_error)()}"
     if rc in (SPA2_ERR_VALUE, SPA2_ERR_UNSUPPORTED):
         raise ValueError(msg)
     if rc == SPA2_ERR_NONFINITE:
         raise FloatingPointError(msg)
     raise RuntimeError(msg)
+
+
+def check_diag(rc: int, what: str) -> None:
+    """``check`` for libspa2_diag.so calls (its error message lives in that library)."""
+    check(rc, what, lambda: load_diag().spa2_last_error().decode(errors="replace"))
 
 
 def require_device(device: torch.device) -> None:

@@ -14,7 +14,6 @@
 namespace spa2 {
 
 static thread_local char g_last_error[1024] = "";
-unsigned long long* g_trace_buf = nullptr;
 bool pdl_enabled() {
   static const bool v = [] {
     const char* e = getenv("SPA2_PDL");
@@ -22,7 +21,6 @@ bool pdl_enabled() {
   }();
   return v;
 }
-int g_trace_cap = 0;
 
 
 void set_error(const char* fmt, ...) {
@@ -139,11 +137,5 @@ extern "C" int spa2_device_supported(int device) {
   SPA2_CUDA_TRY(cudaGetDeviceProperties(&prop, device));
   SPA2_REQUIRE(prop.major == 10 && prop.minor == 0, SPA2_ERR_UNSUPPORTED,
                "device %d is sm_%d%d; libspa2 is built for sm_100a only", device, prop.major, prop.minor);
-  return SPA2_OK;
-}
-
-extern "C" int spa2_debug_trace(void* buf, int capacity) {
-  spa2::g_trace_buf = reinterpret_cast<unsigned long long*>(buf);
-  spa2::g_trace_cap = capacity;
   return SPA2_OK;
 }

@@ -51,18 +51,6 @@ __device__ __forceinline__ double to_f64<__nv_bfloat16>(__nv_bfloat16 x) {
 template <>
 __device__ __forceinline__ double to_f64<__half>(__half x) { return (double)__half2float(x); }
 
-// ---- diagnostic in-kernel trace (CTA 0 only; disabled unless spa2_debug_trace set a buffer) ----
-// Fixed slot per (role, index, kind): buf[2 + role*(cap/4) + index*8 + kind] = clock64.  Plain
-// stores, no atomics, so tracing barely perturbs the pipeline it observes.
-// Compiled in only with -DSPA2_TRACE (tools/build_alt.sh trace -DSPA2_TRACE; the trace tools
-// then run with SPA2_LIB_PATH=alt/trace/libspa2.so): the production kernels carry no trace code.
-__device__ __forceinline__ void trace_ev(unsigned long long* buf, int cap, int role, int kind, int idx) {
-#ifdef SPA2_TRACE
-  if (buf == nullptr || blockIdx.x != 0) return;
-  const int slot = idx * 8 + kind;
-  if (slot < cap / 4) buf[2 + role * (cap / 4) + slot] = clock64();
-#endif
-}
 // ---- programmatic dependent launch (PDL) ---------------------------------------------
 // Hot-path kernels are launched with programmatic stream serialization: the next kernel's
 // CTAs may be scheduled (and run their prologue: barrier init, TMEM alloc, descriptor
@@ -90,7 +78,3 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 }
 }  // namespace spa2
 
-namespace spa2 {
-extern unsigned long long* g_trace_buf;
-extern int g_trace_cap;
-}  // namespace spa2

@@ -200,9 +200,9 @@ def test_probe_tmem_a_operand():
         a = torch.randn(128, k_, device="cuda").to(torch.bfloat16)
         b = torch.randn(k_, n_, device="cuda").to(torch.bfloat16)  # stored [k, n] -> MN-major B
         d = torch.empty(128, n_, device="cuda")
-        rc = _lib.load().spa2_probe_gemm(_lib.ptr(a), _lib.ptr(b), _lib.ptr(d), 128, n_, k_, 0, 1, 2,
+        rc = _lib.load_diag().spa2_probe_gemm(_lib.ptr(a), _lib.ptr(b), _lib.ptr(d), 128, n_, k_, 0, 1, 2,
                                          torch.cuda.current_stream().cuda_stream)
-        _lib.check(rc, "probe")
+        _lib.check_diag(rc, "probe")
         torch.cuda.synchronize()
         want = a.float() @ b.float()
         assert (d - want).abs().max().item() <= 1e-3 * want.abs().max().item()

@@ -22,10 +22,10 @@ def test_probe_gemm(m, n, k, a_mn, b_mn, use_tma):
     a_store = a.t().contiguous() if a_mn else a.contiguous()
     b_store = b.t().contiguous() if b_mn else b.contiguous()
     d = torch.full((m, n), float("nan"), device="cuda", dtype=torch.float32)
-    lib = _lib.load()
+    lib = _lib.load_diag()
     rc = lib.spa2_probe_gemm(_lib.ptr(a_store), _lib.ptr(b_store), _lib.ptr(d), m, n, k, a_mn, b_mn, use_tma,
                              torch.cuda.current_stream().cuda_stream)
-    _lib.check(rc, "probe")
+    _lib.check_diag(rc, "probe")
     torch.cuda.synchronize()
     want = a.float() @ b.float().t()
     err = (d - want).abs().max().item()
@@ -40,8 +40,8 @@ def test_probe_tmem_cp_a_operand(n, k):
     a = torch.randn(128, k, device="cuda", generator=g).to(torch.bfloat16)
     b = torch.randn(n, k, device="cuda", generator=g).to(torch.bfloat16)
     d = torch.full((128, n), float("nan"), device="cuda", dtype=torch.float32)
-    lib = _lib.load()
-    _lib.check(lib.spa2_probe_gemm(_lib.ptr(a), _lib.ptr(b), _lib.ptr(d), 128, n, k, 0, 0, 3,
+    lib = _lib.load_diag()
+    _lib.check_diag(lib.spa2_probe_gemm(_lib.ptr(a), _lib.ptr(b), _lib.ptr(d), 128, n, k, 0, 0, 3,
                                    torch.cuda.current_stream().cuda_stream), "probe")
     torch.cuda.synchronize()
     want = a.float() @ b.float().t()

@@ -1,14 +1,10 @@
-"""Every kernel variant behind the C ABI stays correct, not just the default ones.
+"""The A/B switches that remain in libspa2.so keep the results correct, not just the defaults.
 
-The variant is chosen once per process from the environment (static in libspa2.so), so each
-case runs a small fwd + bwd parity check in a fresh interpreter:
-  SPA2_FWD_VARIANT=1|3|2     forward: one CTA per query block | persistent 2 CTAs/SM | Q in TMEM
-  SPA2_DQ_VARIANT=3|4|2|1    dQ: Q/dO in TMEM (3) | 3-deep dP/dS ring, S from smem (4) | one query block
-                             per CTA (2) | persistent SS (1)
-  SPA2_NO_FUSED_DELTA=1      δ by its own kernel instead of inside the dQ kernel
-  SPA2_DKDV_VARIANT=5|6|7|1  dK/dV: 5-slot Q/dO ring | 4 slots + two P/dS buffers | key-pair items
-                             (d = 128) | two [Q|dO] stages
-  SPA2_DQ_EW=8, SPA2_DKDV_EW=8|16 elementwise warp counts (defaults 16, 16)
+Each switch is read once per process (static in libspa2.so / the package), so each case runs a
+small fwd + bwd parity check in a fresh interpreter:
+  SPA2_NO_FUSED_DELTA=1   δ by its own kernel (k_delta) instead of inside the dQ kernel
+  SPA2_PDL=0              no programmatic dependent launch between the hot-path kernels
+  SPA2_FUSED_SELECT=0     two-step masker (pooled map, then select) instead of the fused softmax+select
 Checked against the float64 oracle at two ragged shapes (d = 64 and 128)."""
 
 import os
@@ -32,7 +28,7 @@ for n, d, density, heads in ((1000, 128, 0.3, 2), (777, 64, 0.5, 1)):
     q, k, v, do = wan_like(5 * n + d, n, d, 128, 64, 0.7, heads=heads)
     t_m, t_n = -(-n // 128), -(-n // 64)
     keep = np.stack([random_keep(n + 7 * h, t_m, t_n, density) for h in range(heads)])
-    bm = mk.BlockMask(keep.reshape(1, heads, t_m, t_n), 128, 64, n)
+    bm = mk.BlockMask(torch.tensor(keep.reshape(1, heads, t_m, t_n), device="cuda"), 128, 64, n)
     bf = lambda x: torch.tensor(x, device="cuda").to(torch.bfloat16).view(1, heads, n, d)
     res = spa.sparse_attention_with_mask(bf(q), bf(k), bf(v), bm)
     g = spa.attention_backward(bf(q), bf(k), bf(v), bm, bf(do))
@@ -42,22 +38,21 @@ for n, d, density, heads in ((1000, 128, 0.3, 2), (777, 64, 0.5, 1)):
         assert_close(f"h{{h}}.dq", g.dq[0, h], dq, "dq")
         assert_close(f"h{{h}}.dk", g.dk[0, h], dk, "dk")
         assert_close(f"h{{h}}.dv", g.dv[0, h], dv, "dv")
+    qt = torch.tensor(q, device="cuda").to(torch.bfloat16).view(1, heads, n, d)
+    kt = torch.tensor(k, device="cuda").to(torch.bfloat16).view(1, heads, n, d)
+    cfg = mk.SparsityConfig(0.1, 0.5, 128, 64)
+    got = spa.sparse_attention(qt, kt, qt, cfg).mask_used.keep.cpu().numpy()
+    for h in range(heads):
+        want = oracle.hybrid_keep(oracle.pooled_probs(qt[0, h].double().cpu().numpy(), kt[0, h].double().cpu().numpy(),
+                                                      128, 64), 0.1, 0.5)
+        assert np.array_equal(got[0, h], want)
 print("ok")
 """
 
 VARIANTS = [
-    {"SPA2_FWD_VARIANT": "3"},
-    {"SPA2_FWD_VARIANT": "2"},
-    {"SPA2_DQ_VARIANT": "4"},
-    {"SPA2_DQ_VARIANT": "4", "SPA2_DQ_EW": "8"},
-    {"SPA2_DQ_VARIANT": "2"},
-    {"SPA2_DQ_VARIANT": "1"},
     {"SPA2_NO_FUSED_DELTA": "1"},
-    {"SPA2_DKDV_VARIANT": "1"},
-    {"SPA2_DKDV_VARIANT": "6"},
-    {"SPA2_DKDV_VARIANT": "7"},
-    {"SPA2_DQ_EW": "8", "SPA2_DKDV_EW": "8"},
-    {"SPA2_DKDV_VARIANT": "1", "SPA2_DKDV_EW": "16"},
+    {"SPA2_PDL": "0"},
+    {"SPA2_FUSED_SELECT": "0"},
 ]
 
 

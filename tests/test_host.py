@@ -19,6 +19,16 @@ def test_library_exports_every_header_symbol():
         assert hasattr(lib, name), name
     assert set(_lib.SIGNATURES) == set(names)
     assert _lib.load().spa2_version().startswith(b"spa2")
+    assert not any(n.startswith("spa2_probe") for n in names)  # diagnostics live in libspa2_diag.so
+
+
+def test_diag_library_exports_every_diag_header_symbol():
+    names = _lib.header_symbols(_lib.DIAG_HEADER_PATH)
+    lib = ctypes.CDLL(_lib.DIAG_LIB_PATH)
+    for name in names:
+        assert hasattr(lib, name), name
+    assert set(_lib.DIAG_SIGNATURES) == set(names)
+    assert not hasattr(ctypes.CDLL(_lib.LIB_PATH), "spa2_probe_gemm")
 
 
 def test_error_mapping():
@@ -39,7 +49,8 @@ def test_argument_errors_need_no_gpu():
     assert "empty" in _lib.last_error()
     assert lib.spa2_select(None, 3, 4, 0, 0.5, None, None, None) == _lib.SPA2_ERR_VALUE
     assert lib.spa2_build_lists(None, 0, 1, 1, *([None] * 7), None) == _lib.SPA2_ERR_VALUE
-    assert lib.spa2_probe_gemm(None, None, None, 32, 64, 64, 0, 0, 0, None) == _lib.SPA2_ERR_UNSUPPORTED
+    diag = _lib.load_diag()
+    assert diag.spa2_probe_gemm(None, None, None, 32, 64, 64, 0, 0, 0, None) == _lib.SPA2_ERR_UNSUPPORTED
 
 
 def test_sparsity_config_validation():

@@ -23,14 +23,14 @@ CASES = [  # (name, m, n, k, a_mn, b_mn, a_tmem)
 ]
 
 def main():
-    lib = _lib.load()
+    lib = _lib.load_diag()
     ctas = torch.cuda.get_device_properties(0).multi_processor_count
     out = torch.zeros(ctas, dtype=torch.int64, device="cuda")
     reps = 2000
     for name, m, n, k, amn, bmn, at in CASES:
         for c in (1, ctas):
             rc = lib.spa2_probe_mma_rate(m, n, k, amn, bmn, at, reps, c, _lib.ptr(out), torch.cuda.current_stream().cuda_stream)
-            _lib.check(rc, name)
+            _lib.check_diag(rc, name)
             torch.cuda.synchronize()
             cyc = out[:c].double().mean().item()
             per = cyc / (reps * 8)

@@ -9,7 +9,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2602_13515_b200 import _lib  # noqa: E402
 
-lib = _lib.load()
+lib = _lib.load_diag()
 sms = torch.cuda.get_device_properties(0).multi_processor_count
 out = torch.zeros(4 * 2 * sms, dtype=torch.int64, device="cuda")
 st = torch.cuda.current_stream().cuda_stream
@@ -31,10 +31,10 @@ for box, chunks, stages, issuers, mode, cps in cases:
     ctas = sms * cps
     iters = 300
     args = (_lib.ptr(buf), rows, box, chunks, stages, issuers, mode)
-    _lib.check(lib.spa2_probe_tma_rate2(*args, 10, ctas, _lib.ptr(out), st), "tma2")
+    _lib.check_diag(lib.spa2_probe_tma_rate2(*args, 10, ctas, _lib.ptr(out), st), "tma2")
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
-    _lib.check(lib.spa2_probe_tma_rate2(*args, iters, ctas, _lib.ptr(out), st), "tma2")
+    _lib.check_diag(lib.spa2_probe_tma_rate2(*args, iters, ctas, _lib.ptr(out), st), "tma2")
     b.record()
     torch.cuda.synchronize()
     ms = a.elapsed_time(b)

@@ -8,7 +8,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2602_13515_b200 import _lib  # noqa: E402
 
-lib = _lib.load()
+lib = _lib.load_diag()
 st = torch.cuda.current_stream().cuda_stream
 ctas, reps = 148, 2048
 cyc = torch.zeros(ctas * 16, dtype=torch.int64, device="cuda")
@@ -17,7 +17,7 @@ bytes_per = {0: 4096, 1: 4096, 2: 2048, 3: 2048}
 for mode in (0, 1, 2, 3):
     for warps in (1, 4, 8, 16):
         cyc.zero_()
-        _lib.check(lib.spa2_probe_tmem_rate(reps, mode, warps, ctas, _lib.ptr(cyc), st), "tmem")
+        _lib.check_diag(lib.spa2_probe_tmem_rate(reps, mode, warps, ctas, _lib.ptr(cyc), st), "tmem")
         torch.cuda.synchronize()
         c = cyc.view(ctas, 16)[:, :warps].float()
         tot = warps * reps * bytes_per[mode]
@@ -28,7 +28,7 @@ for mode in (0, 1, 2, 3):
 for mode, label in ((4, "ld 32 col + N=128 MMAs"), (5, "ld 32 col + N=64 MMAs")):
     for warps in (2, 5, 9):
         cyc.zero_()
-        _lib.check(lib.spa2_probe_tmem_rate(reps, mode, warps, ctas, _lib.ptr(cyc), st), "tmem")
+        _lib.check_diag(lib.spa2_probe_tmem_rate(reps, mode, warps, ctas, _lib.ptr(cyc), st), "tmem")
         torch.cuda.synchronize()
         c = cyc.view(ctas, 16)[:, 1:warps].float()
         print(f"{label:24s} ld warps {warps - 1}: {c.mean().item() / reps:7.1f} cyc/instr per warp")
@@ -38,6 +38,6 @@ mb = torch.zeros(4, dtype=torch.int64, device="cuda")
 for mode, label in ((0, "try_wait"), (1, "test_wait"), (2, "mbar_wait()")):
     for threads in (32, 512):
         mb.zero_()
-        _lib.check(lib.spa2_probe_mbar_latency(4096, mode, threads, _lib.ptr(mb), st), "mbar")
+        _lib.check_diag(lib.spa2_probe_mbar_latency(4096, mode, threads, _lib.ptr(mb), st), "mbar")
         torch.cuda.synchronize()
         print(f"mbarrier {label:12s} {threads:3d} threads: {mb[0].item() / 4096:6.1f} cycles per poll (completed phase)")
