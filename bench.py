@@ -216,7 +216,7 @@ def gpu_arm(args, rank: int, world: int, dev):
 
     def step():
         qs, ks, vs = (t.detach().requires_grad_(True) for t in (q, k, v))
-        res = spa.sparse_attention(qs, ks, vs, cfg, check_finite=False)
+        res = spa.sparse_attention(qs, ks, vs, cfg)
         res.out.backward(do)
         return res
 

@@ -150,6 +150,12 @@ int spa2_bwd_dkdv(spa2_view q, spa2_view k, spa2_view v, spa2_view dout, const f
                   int64_t N, int64_t d, int64_t b_q, int64_t b_kv, const int32_t* col_ptr,
                   const int32_t* col_idx, const int32_t* col_order, float scale, void* stream);
 
+/* Finiteness scan (numerics.ensure_finite, numerics.py:29-32) of one bf16 [B, H, N, d]
+ * operand: sets *nonfinite = 1 if any element is NaN or +-Inf (never clears it, so several
+ * scans can share one flag with spa2_pooled_map's).  16-byte aligned base, strides % 8. */
+int spa2_check_finite(spa2_view x, int dtype, int64_t B, int64_t H, int64_t N, int64_t d, int32_t* nonfinite,
+                      void* stream);
+
 #ifdef __cplusplus
 }
 #endif

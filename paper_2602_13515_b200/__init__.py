@@ -16,11 +16,14 @@ from .masker import (  # noqa: F401,E402
     expand_mask,
     hybrid_mask,
     pooled_map,
+    read_mask_csv,
     top_k_count,
     top_k_mask,
     top_p_mask,
+    write_mask_csv,
+    write_pooled_map_csv,
 )
-from .numerics import ShapeError, num_blocks  # noqa: F401,E402
+from .numerics import ShapeError, check_pending, num_blocks  # noqa: F401,E402
 from .attention import (  # noqa: F401,E402
     AttentionGrads,
     AttentionOutput,

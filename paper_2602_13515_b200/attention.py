@@ -25,7 +25,7 @@ import torch
 
 from . import _lib
 from .masker import BlockMask, SparsityConfig, _pooled_probs, _select, top_k_count
-from .numerics import from_device, num_blocks, to_device4
+from .numerics import finite_guard, from_device, num_blocks, to_device4
 
 BQ, BKV = 128, 64
 SUPPORTED_HEAD_DIMS = (64, 128)
@@ -50,8 +50,10 @@ class AttentionGrads:
 
 
 class BlockCounter:
-    """Counts computed (query block, key block) tiles (attention.py:36-43).  The GPU forward
-    adds the number of tiles it actually computed, counted on the device."""
+    """Counts computed (query block, key block) pairs of the mask's grid (attention.py:36-43).
+    On the kernels' native grid (b_q, b_kv) = (128, 64) the forward counts the tiles it
+    computed on the device; a coarser mask is refined into several kernel tiles per mask
+    block, so the count is then the mask's kept blocks (what the reference's loop visits)."""
 
     def __init__(self):
         self.count = 0
@@ -61,7 +63,8 @@ class BlockCounter:
 
 
 def full_mask(n: int) -> BlockMask:
-    """One all-kept block covering everything (attention.py:46-47)."""
+    """One all-kept block covering everything (attention.py:46-47); a host mask, as in the
+    reference."""
     return BlockMask(np.ones((1, 1), dtype=bool), b_q=n, b_kv=n, n_tokens=n)
 
 
@@ -85,7 +88,7 @@ class BlockLists:
 def _native_keep(bm: BlockMask, B: int, H: int, N: int) -> torch.Tensor:
     """keep at the kernel grid (128, 64) as uint8 [B, H, T_m, T_n] (exact refinement)."""
     t_m, t_n = num_blocks(N, BQ), num_blocks(N, BKV)
-    keep = bm.keep
+    keep = bm.dev
     if keep.dim() == 2:
         keep = keep.view(1, 1, *keep.shape)
     if (bm.b_q, bm.b_kv) != (BQ, BKV):
@@ -123,16 +126,36 @@ def build_lists(keep_u8: torch.Tensor) -> BlockLists:
     return lists
 
 
-def _lists_with_order(keep_u8: torch.Tensor, visit) -> BlockLists:
-    """Host-built row lists honouring the reference's ``_block_order`` test hook
-    (attention.py:74-81, 97-99).  Test-only: copies the mask to the host."""
+def _lists_with_order(bm: BlockMask, B: int, H: int, N: int, visit) -> BlockLists:
+    """Row lists honouring the reference's ``_block_order`` test hook (attention.py:74-81,
+    97-99), which is called with the MASK grid's row index and kept columns, as in the
+    reference; its order is then refined to the kernel grid (mask column j covers kernel
+    columns j·(b_kv/64) ...).  Test-only: copies the mask to the host."""
+    keep_u8 = _native_keep(bm, B, H, N)
     base = build_lists(keep_u8)
-    B, H, t_m, t_n = keep_u8.shape
-    keep = keep_u8.cpu().numpy().astype(bool).reshape(B * H * t_m, t_n)
+    t_m, t_n = keep_u8.shape[-2:]
+    mk = bm.keep_numpy().astype(bool)
+    mk = np.broadcast_to(mk.reshape((1, 1) + mk.shape[-2:]) if mk.ndim == 2 else mk, (B, H) + mk.shape[-2:])
+    rq = bm.b_q // BQ if bm.b_q % BQ == 0 else None
+    rk = bm.b_kv // BKV if bm.b_kv % BKV == 0 else None
     idx = []
-    for r in range(keep.shape[0]):
-        kept = np.flatnonzero(keep[r])
-        idx.append(np.asarray(visit(r % t_m, kept), dtype=np.int32))
+    for b in range(B):
+        for h in range(H):
+            for r in range(t_m):
+                if rq is None or rk is None:  # all-ones mask of an arbitrary geometry
+                    i_m = min(r * BQ // bm.b_q, mk.shape[-2] - 1)
+                    order = [int(j) for j in visit(i_m, np.flatnonzero(mk[b, h, i_m]))]
+                    seen, out = set(), []
+                    for j in order:
+                        for c in range(t_n):
+                            if c * BKV < (j + 1) * bm.b_kv and (c + 1) * BKV > j * bm.b_kv and c not in seen:
+                                seen.add(c)
+                                out.append(c)
+                else:
+                    i_m = r // rq
+                    order = [int(j) for j in visit(i_m, np.flatnonzero(mk[b, h, i_m]))]
+                    out = [c for j in order for c in range(j * rk, min((j + 1) * rk, t_n))]
+                idx.append(np.asarray(out, dtype=np.int32))
     flat = torch.tensor(np.concatenate(idx) if idx else np.zeros(0, np.int32), device=keep_u8.device)
     return BlockLists(base.row_ptr, flat, base.row_order, base.col_ptr, base.col_idx, base.col_order, base.shape)
 
@@ -193,30 +216,55 @@ class SparseAttentionFunction(torch.autograd.Function):
     (SPEC.md:260), so only q, k, v receive gradients."""
 
     @staticmethod
-    def forward(ctx, q4, k4, v4, lists, scale, counter):
+    def forward(ctx, q4, k4, v4, lists, scale, counter, finite=None):
         o, lse = fwd(q4, k4, v4, lists, scale, counter)
         ctx.save_for_backward(q4, k4, v4, o, lse)
         ctx.lists = lists
         ctx.scale = scale
+        ctx.finite = finite
         ctx.mark_non_differentiable(lse)
         return o, lse
 
     @staticmethod
     def backward(ctx, do, _dlse):
+        if ctx.finite is not None:  # no gradients from non-finite inputs (numerics.py:29-32)
+            finite_guard.resolve(ctx.finite)
         q4, k4, v4, o, lse = ctx.saved_tensors
         do = do.to(q4.dtype)
         if do.stride(-1) != 1 or any(s % 8 for s in do.stride()[:3]):
             do = do.contiguous()
         dq, dk, dv = bwd(q4, k4, v4, o, do, lse, ctx.lists, ctx.scale)
-        return dq, dk, dv, None, None, None
+        return dq, dk, dv, None, None, None, None
 
 
 # --------------------------------------------------------------------------------------
 # reference-facing API
 # --------------------------------------------------------------------------------------
 
-def _prepare(q, k, v, check_finite: bool):
-    """attention.py:50-59: same shapes (ValueError), rank (ShapeError), finite (FloatingPointError)."""
+def _host_finite(named) -> None:
+    """numerics.ensure_finite (numerics.py:29-32) on the caller's own float64 arrays."""
+    for name, x in named:
+        if not isinstance(x, torch.Tensor) and not np.all(np.isfinite(np.asarray(x, dtype=np.float64))):
+            raise FloatingPointError(f"non-finite values in {name}")
+
+
+def _scan_finite(flag: torch.Tensor, *tensors: torch.Tensor) -> None:
+    """K0: OR "has a NaN/Inf" of each bf16 [B,H,N,d] tensor into ``flag`` (no host sync)."""
+    st = torch.cuda.current_stream(flag.device)
+    for t in tensors:
+        B, H, N, d = t.shape
+        _lib.call("spa2_check_finite", _lib.view4(t), _lib.DTYPE_CODES[t.dtype], B, H, N, d, _lib.ptr(flag),
+                  st.cuda_stream, stream_obj=st)
+
+
+def _prepare(q, k, v, check_finite):
+    """attention.py:50-59: same shapes (ValueError), rank (ShapeError), finite
+    (FloatingPointError; numpy inputs are checked on the host exactly as the reference does,
+    torch inputs by the K0 scan with a deferred verdict, see ``numerics.FiniteGuard``).
+    Returns (q4, k4, v4, boundary, finite-flag or None)."""
+    if check_finite:
+        finite_guard.check_pending(block=False)  # verdicts of earlier calls that have landed
+        _host_finite((("q", q), ("k", k), ("v", v)))
     q4, qb = to_device4(q, torch.bfloat16, "q")
     k4, _ = to_device4(k, torch.bfloat16, "k", device=qb.device)
     v4, _ = to_device4(v, torch.bfloat16, "v", device=qb.device)
@@ -224,11 +272,8 @@ def _prepare(q, k, v, check_finite: bool):
         raise ValueError(f"q/k/v shapes differ: {tuple(q4.shape)}, {tuple(k4.shape)}, {tuple(v4.shape)}")
     _check_kernel_shape(q4)
     q4, k4, v4 = (_tma_ready(t) for t in (q4, k4, v4))
-    if check_finite:
-        for name, t in (("q", q4), ("k", k4), ("v", v4)):
-            if not bool(torch.isfinite(t).all()):
-                raise FloatingPointError(f"non-finite values in {name}")
-    return q4, k4, v4, qb
+    flag = finite_guard.new_flag(q4.device) if check_finite and not qb.numpy else None
+    return q4, k4, v4, qb, flag
 
 
 def _tma_ready(t: torch.Tensor) -> torch.Tensor:
@@ -238,89 +283,99 @@ def _tma_ready(t: torch.Tensor) -> torch.Tensor:
     return t
 
 
-def _run(q4, k4, v4, bm: BlockMask, qb, counter, visit=None) -> AttentionOutput:
+def _run(q4, k4, v4, bm: BlockMask, qb, counter, flag, check_finite, visit=None) -> AttentionOutput:
     B, H, N, d = q4.shape
     if bm.n_tokens != N:
         raise ValueError(f"mask built for {bm.n_tokens} tokens, inputs have {N}")
-    lists = mask_lists(bm, B, H, N) if visit is None else _lists_with_order(_native_keep(bm, B, H, N), visit)
-    ctr = torch.zeros((1,), device=q4.device, dtype=torch.int64) if counter is not None else None
-    o, lse = SparseAttentionFunction.apply(q4, k4, v4, lists, 1.0 / math.sqrt(d), ctr)
+    lists = mask_lists(bm, B, H, N) if visit is None else _lists_with_order(bm, B, H, N, visit)
+    native = (bm.b_q, bm.b_kv) == (BQ, BKV)
+    ctr = torch.zeros((1,), device=q4.device, dtype=torch.int64) if counter is not None and native else None
+    verdict = None
+    if flag is not None:
+        verdict = finite_guard.submit(flag, "q, k or v", block=check_finite == "sync")
+    o, lse = SparseAttentionFunction.apply(q4, k4, v4, lists, 1.0 / math.sqrt(d), ctr, verdict)
     if counter is not None:
-        counter.count += int(ctr.item())
+        counter.count += int(ctr.item()) if native else bm.kept_blocks()
     return AttentionOutput(out=from_device(o, qb), lse=from_device(lse, qb, 1), mask_used=bm)
 
 
 def sparse_attention_with_mask(q, k, v, bm: BlockMask, counter: BlockCounter | None = None, _block_order=None,
-                               *, check_finite: bool = True) -> AttentionOutput:
+                               *, check_finite: bool | str = True) -> AttentionOutput:
     """Tiled attention restricted to ``bm``'s kept blocks (attention.py:73-114).
 
     ``out`` is differentiable w.r.t. torch inputs.  ``_block_order(i, kept)`` may permute
-    the visit order of each row (the reference's test hook); the result does not depend
-    on it beyond float rounding.  ``check_finite=False`` skips the NaN/Inf scan (and its
-    host sync) that mirrors the reference's ``ensure_finite``.
+    the visit order of each row (the reference's test hook, called on the mask's own grid);
+    the result does not depend on it beyond float rounding.  ``check_finite``: True (the
+    reference's ``ensure_finite``; deferred for torch inputs, see ``numerics.FiniteGuard``),
+    ``"sync"`` (raise before returning) or False.
     """
-    q4, k4, v4, qb = _prepare(q, k, v, check_finite)
-    return _run(q4, k4, v4, bm, qb, counter, _block_order)
+    q4, k4, v4, qb, flag = _prepare(q, k, v, check_finite)
+    if flag is not None:
+        _scan_finite(flag, q4, k4, v4)
+    return _run(q4, k4, v4, bm, qb, counter, flag, check_finite, _block_order)
 
 
 _FUSED_SELECT = os.environ.get("SPA2_FUSED_SELECT", "1") != "0"
 
 
-def _hybrid_mask_device(q4, k4, cfg: SparsityConfig, check_finite: bool, fused: bool | None = None) -> BlockMask:
-    """hybrid_mask(pooled_map(q, k, cfg), cfg) without materialising the map: the row softmax
-    runs inside the select kernel (bit-identical masks; ``fused=False`` takes the two-step
-    pooled_map + select path)."""
+def _hybrid_mask_device(q4, k4, cfg: SparsityConfig, flag: torch.Tensor | None, fused: bool | None = None):
+    """hybrid_mask(pooled_map(q, k, cfg), cfg) as a device keep tensor, without materialising
+    the map: the row softmax runs inside the select kernel (bit-identical masks;
+    ``fused=False`` takes the two-step pooled_map + select path).  K1 ORs "q or k has a
+    NaN/Inf" into ``flag``."""
     t_n = num_blocks(q4.shape[2], cfg.b_kv)
     if fused is None:
         fused = _FUSED_SELECT
     if fused and t_n <= 4096:
-        scores, flag = _pooled_probs(q4, k4, cfg.b_q, cfg.b_kv, check_finite, softmax=False)
-        if flag is not None and int(flag.item()) != 0:
-            raise FloatingPointError("non-finite values in q or k")
+        scores = _pooled_probs(q4, k4, cfg.b_q, cfg.b_kv, flag, softmax=False)
         keep, _ = _select(scores, top_k_count(cfg.k_frac, t_n), cfg.p_frac, from_scores=True)
     else:
-        probs, flag = _pooled_probs(q4, k4, cfg.b_q, cfg.b_kv, check_finite)
-        if flag is not None and int(flag.item()) != 0:
-            raise FloatingPointError("non-finite values in q or k")
+        probs = _pooled_probs(q4, k4, cfg.b_q, cfg.b_kv, flag)
         keep, _ = _select(probs, top_k_count(cfg.k_frac, probs.shape[-1]), cfg.p_frac)
     if q4.shape[0] == 1 and q4.shape[1] == 1:
         keep = keep[0, 0]
-    return BlockMask._trusted(keep, cfg.b_q, cfg.b_kv, q4.shape[2])
+    return keep
 
 
 def sparse_attention(q, k, v, cfg: SparsityConfig, counter: BlockCounter | None = None, *,
-                     check_finite: bool = True) -> AttentionOutput:
+                     check_finite: bool | str = True) -> AttentionOutput:
     """Derive the hybrid mask from the current q/k, then run the kernel (attention.py:117-125).
-    The mask is rebuilt on every call; nothing is cached across steps."""
-    q4, k4, v4, qb = _prepare(q, k, v, check_finite=False)
-    if check_finite and not bool(torch.isfinite(v4).all()):
-        raise FloatingPointError("non-finite values in v")
-    bm = _hybrid_mask_device(q4, k4, cfg, check_finite)
-    return _run(q4, k4, v4, bm, qb, counter)
+    The mask is rebuilt on every call; nothing is cached across steps.
+    Finiteness: K1 checks q and k while pooling them, K0 scans v; no host sync for torch
+    callers (``check_finite`` as in ``sparse_attention_with_mask``)."""
+    q4, k4, v4, qb, flag = _prepare(q, k, v, check_finite)
+    if flag is not None:
+        _scan_finite(flag, v4)
+    keep = _hybrid_mask_device(q4, k4, cfg, flag)
+    bm = BlockMask._from_device(keep, cfg.b_q, cfg.b_kv, q4.shape[2], host=qb.numpy)
+    return _run(q4, k4, v4, bm, qb, counter, flag, check_finite)
 
 
-def dense_attention(q, k, v, *, check_finite: bool = True) -> AttentionOutput:
+def dense_attention(q, k, v, *, check_finite: bool | str = True) -> AttentionOutput:
     """Full softmax attention (attention.py:62-70), computed by the same kernels with every
     block kept; ``mask_used`` is ``full_mask(N)`` as in the reference."""
-    q4, k4, v4, qb = _prepare(q, k, v, check_finite)
-    N = q4.shape[2]
-    res = _run(q4, k4, v4, full_mask(N), qb, None)
-    return res
+    q4, k4, v4, qb, flag = _prepare(q, k, v, check_finite)
+    if flag is not None:
+        _scan_finite(flag, q4, k4, v4)
+    return _run(q4, k4, v4, full_mask(q4.shape[2]), qb, None, flag, check_finite)
 
 
-def attention_backward(q, k, v, bm: BlockMask, d_out, *, check_finite: bool = True) -> AttentionGrads:
+def attention_backward(q, k, v, bm: BlockMask, d_out, *, check_finite: bool | str = True) -> AttentionGrads:
     """Gradients of the masked attention output with the mask held constant
     (attention.py:128-166).  Like the reference it recomputes the forward for O and LSE."""
-    q4, k4, v4, qb = _prepare(q, k, v, check_finite)
+    if check_finite:
+        _host_finite((("d_out", d_out),))
+    q4, k4, v4, qb, flag = _prepare(q, k, v, check_finite)
     do4, _ = to_device4(d_out, torch.bfloat16, "d_out", device=qb.device)
     if do4.shape != q4.shape:
         raise ValueError(f"d_out shape {tuple(do4.shape)} != q shape {tuple(q4.shape)}")
     do4 = _tma_ready(do4)
-    if check_finite and not bool(torch.isfinite(do4).all()):
-        raise FloatingPointError("non-finite values in d_out")
     B, H, N, d = q4.shape
     if bm.n_tokens != N:
         raise ValueError(f"mask built for {bm.n_tokens} tokens, inputs have {N}")
+    if flag is not None:
+        _scan_finite(flag, q4, k4, v4, do4)
+        finite_guard.submit(flag, "q, k, v or d_out", block=check_finite == "sync")
     lists = mask_lists(bm, B, H, N)
     scale = 1.0 / math.sqrt(d)
     with torch.no_grad():

@@ -158,51 +158,27 @@ __global__ void __launch_bounds__(256) k_pool_bf16_pipe(spa2_view q, spa2_view k
 }
 
 // ---------------------------------------------------------------------------------------
-// K1a (bf16 fast path): one CTA per (b, h, block).  The block's rows are streamed into
-// shared memory with coalesced 16-byte loads (all in flight at once), then thread c sums
-// column c over the rows strictly in order — numpy's add.reduceat order — in float64.
+// K0: finiteness scan of one [B, H, N, d] bf16 operand (the reference's ensure_finite,
+// numerics.py:29-32, for the tensors K1 does not read: v, dO).  Grid-stride over 16-byte
+// chunks; a chunk holding a NaN/Inf sets *nonfinite = 1 (exponent bits all ones).
 // ---------------------------------------------------------------------------------------
-constexpr int kPoolThreads = 256;
-constexpr int kPoolMaxBytes = 128 * 256 * 2;  // rows x d x sizeof(bf16) upper bound (64 KB)
-
-__global__ void __launch_bounds__(kPoolThreads) k_pool_bf16(spa2_view q, spa2_view k, int H, int N, int d, int b_q,
-                                                            int b_kv, int T_m, int T_n, int64_t BH,
-                                                            double* __restrict__ qbar, double* __restrict__ kbar,
-                                                            int32_t* __restrict__ nonfinite) {
-  extern __shared__ __align__(16) uint8_t pool_smem[];
-  const int64_t nq = BH * T_m;
-  const int64_t g = blockIdx.x;
-  const bool is_q = g < nq;
-  const int64_t blk_g = is_q ? g : g - nq;
-  const int nblk = is_q ? T_m : T_n;
-  const int64_t bh = blk_g / nblk;
-  const int blk = (int)(blk_g % nblk);
-  const int bsz = is_q ? b_q : b_kv;
-  const spa2_view vw = is_q ? q : k;
-  const int row0 = blk * bsz;
-  const int rows = min(bsz, N - row0);
-  const __nv_bfloat16* base =
-      reinterpret_cast<const __nv_bfloat16*>(vw.ptr) + (bh / H) * vw.sb + (bh % H) * vw.sh + (int64_t)row0 * vw.sn;
-  const int upr = d / 8;  // 16-byte units per row
-  uint4* sm = reinterpret_cast<uint4*>(pool_smem);
+__global__ void __launch_bounds__(256) k_nonfinite_bf16(spa2_view x, int H, int N, int cpr, int64_t chunks,
+                                                        int32_t* __restrict__ nonfinite) {
+  pdl_wait();
+  pdl_trigger();
   bool bad = false;
-  for (int e = threadIdx.x; e < rows * upr; e += kPoolThreads) {
-    const int r = e / upr, u = e % upr;
-    const uint4 v = __ldg(reinterpret_cast<const uint4*>(base + (int64_t)r * vw.sn) + u);
-    sm[e] = v;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < chunks; c += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = c / cpr;
+    const int col = (int)(c % cpr) * 8;
+    const int64_t bh = row / N, n = row % N;
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(x.ptr) +
+                                                         (bh / H) * x.sb + (bh % H) * x.sh + n * x.sn + col));
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int x = 0; x < 4; ++x)  // exponent all ones in either half: inf or nan
-      bad |= ((w[x] & 0x7F80u) == 0x7F80u) || ((w[x] & 0x7F800000u) == 0x7F800000u);
+    for (int i = 0; i < 4; ++i)
+      bad |= ((w[i] & 0x7F80u) == 0x7F80u) | ((w[i] & 0x7F800000u) == 0x7F800000u);
   }
-  __syncthreads();
-  const __nv_bfloat16* sb = reinterpret_cast<const __nv_bfloat16*>(pool_smem);
-  for (int c = threadIdx.x; c < d; c += kPoolThreads) {
-    double acc = 0.0;
-    for (int r = 0; r < rows; ++r) acc += (double)__bfloat162float(sb[r * d + c]);
-    (is_q ? qbar : kbar)[blk_g * (int64_t)d + c] = acc / (double)rows;
-  }
-  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0 && nonfinite != nullptr) atomicOr(nonfinite, 1);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *nonfinite = 1;
 }
 
 // ---------------------------------------------------------------------------------------
@@ -704,14 +680,6 @@ __global__ void __launch_bounds__(kColWarps * 32) k_fill(const uint8_t* __restri
   }
 }
 
-bool pool_smem_path() {
-  static const bool v = [] {
-    const char* e = getenv("SPA2_POOL_SMEM");
-    return e != nullptr && e[0] == '1';
-  }();
-  return v;
-}
-
 template <typename T>
 int launch_pool(spa2_view q, spa2_view k, int64_t B, int64_t H, int64_t N, int64_t d, int64_t b_q, int64_t b_kv,
                 int64_t T_m, int64_t T_n, double* qbar, double* kbar, int32_t* nonfinite, cudaStream_t st) {
@@ -726,18 +694,9 @@ int launch_pool(spa2_view q, spa2_view k, int64_t B, int64_t H, int64_t N, int64
   SPA2_REQUIRE(threads < (1ll << 40), SPA2_ERR_UNSUPPORTED, "pooled_map: problem too large");
   const unsigned grid = (unsigned)ceil_div(threads, 256);
   if constexpr (std::is_same<T, __nv_bfloat16>::value) {
-    if (vec && d % 8 == 0 && !pool_smem_path()) {
+    if (vec && d % 8 == 0) {
       SPA2_CUDA_TRY(launch_pdl(k_pool_bf16_pipe, dim3(grid), dim3(256), 0, st, q, k, (int)H, (int)N, (int)d, (int)b_q,
                                (int)b_kv, (int)T_m, (int)T_n, BH, qbar, kbar, nonfinite));
-      SPA2_LAUNCH_CHECK();
-      return SPA2_OK;
-    }
-    const size_t bytes = (size_t)std::max(b_q, b_kv) * d * 2;
-    if (pool_smem_path() && vec && d % 8 == 0 && bytes <= (size_t)kPoolMaxBytes) {
-      if (bytes > 48 * 1024)
-        SPA2_CUDA_TRY(cudaFuncSetAttribute(k_pool_bf16, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
-      k_pool_bf16<<<(unsigned)(BH * (T_m + T_n)), kPoolThreads, bytes, st>>>(
-          q, k, (int)H, (int)N, (int)d, (int)b_q, (int)b_kv, (int)T_m, (int)T_n, BH, qbar, kbar, nonfinite);
       SPA2_LAUNCH_CHECK();
       return SPA2_OK;
     }
@@ -877,6 +836,24 @@ extern "C" int spa2_build_lists(const uint8_t* keep, int64_t bh, int64_t t_m, in
   SPA2_LAUNCH_CHECK();
   SPA2_CUDA_TRY(launch_pdl(k_fill, grid, dim3(kColWarps * 32), 0, st, keep, (int)t_m, (int)t_n, col_chunks, row_ptr,
                            row_idx, col_ptr, col_idx));
+  SPA2_LAUNCH_CHECK();
+  return SPA2_OK;
+}
+
+extern "C" int spa2_check_finite(spa2_view x, int dtype, int64_t B, int64_t H, int64_t N, int64_t d,
+                                 int32_t* nonfinite, void* stream) {
+  SPA2_REQUIRE(dtype == SPA2_BF16, SPA2_ERR_UNSUPPORTED, "check_finite: only bf16 operands are supported");
+  SPA2_REQUIRE(B >= 1 && H >= 1 && N >= 1 && d >= 8 && d % 8 == 0, SPA2_ERR_VALUE,
+               "check_finite: bad shape B=%lld H=%lld N=%lld d=%lld", (long long)B, (long long)H, (long long)N,
+               (long long)d);
+  SPA2_REQUIRE(x.ptr && nonfinite, SPA2_ERR_VALUE, "check_finite: null pointer");
+  SPA2_REQUIRE((uintptr_t)x.ptr % 16 == 0 && x.sb % 8 == 0 && x.sh % 8 == 0 && x.sn % 8 == 0, SPA2_ERR_UNSUPPORTED,
+               "check_finite: operand must be 16-byte aligned with strides %% 8 == 0");
+  SPA2_REQUIRE(N < (1ll << 31), SPA2_ERR_UNSUPPORTED, "check_finite: N too large");
+  const int64_t chunks = B * H * N * (d / 8);
+  const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(chunks, 256), 148 * 16);
+  SPA2_CUDA_TRY(launch_pdl(k_nonfinite_bf16, dim3(grid), dim3(256), 0, (cudaStream_t)stream, x, (int)H, (int)N,
+                           (int)(d / 8), chunks, nonfinite));
   SPA2_LAUNCH_CHECK();
   return SPA2_OK;
 }

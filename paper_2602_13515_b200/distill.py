@@ -106,8 +106,7 @@ class SelfAttention(nn.Module):
             out = F.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2), v.transpose(1, 2))
         else:
             # [B, N, H, d] passed as a [B, H, N, d] view: no copy, the kernels take strides
-            out = sparse_attention(q.transpose(1, 2), k.transpose(1, 2), v.transpose(1, 2), self.sparse,
-                                   check_finite=False).out
+            out = sparse_attention(q.transpose(1, 2), k.transpose(1, 2), v.transpose(1, 2), self.sparse).out
         return self.o(out.transpose(1, 2).reshape(B, N, H * d))
 
 

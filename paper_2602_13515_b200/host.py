@@ -38,7 +38,7 @@ class HostPipeline:
         self.d2h = torch.cuda.Stream(self.device)
 
     def fwd_bwd(self, q, k, v, d_out, cfg: SparsityConfig, out=None, dq=None, dk=None, dv=None,
-                check_finite: bool = False):
+                check_finite: bool | str = True):
         """q, k, v, d_out: host tensors [B, H, N, d] (pinned for overlap).  Returns host
         (out, dq, dk, dv); pass preallocated pinned outputs to avoid allocations."""
         B, H, N, d = q.shape

@@ -71,3 +71,89 @@ def from_device(t: torch.Tensor, b: Boundary, rows_dims: int = 2):
     if b.numpy:
         return t.detach().to(torch.float64).cpu().numpy()
     return t
+
+
+class FiniteGuard:
+    """Deferred finiteness verdicts (the reference's ``ensure_finite``, numerics.py:29-32).
+
+    The scans run on the GPU (K0 ``spa2_check_finite`` for v / dO, K1's pooling for q / k)
+    and set a device flag; the flag is copied to pinned host memory behind an event.  The
+    verdict is enforced
+
+    * immediately (``block=True``) for numpy callers, whose results are synchronised
+      anyway, and for ``check_finite="sync"``;
+    * otherwise without a host sync: the backward pass of the same call and every later
+      operator call enforce the verdicts that have landed by then, ``check_pending()``
+      forces all outstanding ones.
+
+    A non-finite input thus raises ``FloatingPointError`` as in the reference, for torch
+    callers possibly one call later (the output of the offending call is then non-finite).
+    """
+
+    def __init__(self):
+        self._pending: list[tuple[torch.cuda.Event, torch.Tensor, str]] = []
+
+    @staticmethod
+    def new_flag(device: torch.device) -> torch.Tensor:
+        return torch.zeros((1,), device=device, dtype=torch.int32)
+
+    def submit(self, flag: torch.Tensor, what: str, block: bool) -> tuple:
+        """Register ``flag`` (set on the current stream) as the verdict on ``what``."""
+        host = torch.empty((1,), dtype=torch.int32, pin_memory=True)
+        host.copy_(flag, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(flag.device))
+        entry = (ev, host, what)
+        if block:
+            self._verify(entry)
+        else:
+            self._pending.append(entry)
+        return entry
+
+    @staticmethod
+    def _verify(entry) -> None:
+        ev, host, what = entry
+        ev.synchronize()
+        if int(host[0]) != 0:
+            raise FloatingPointError(f"non-finite values in {what}")
+
+    def resolve(self, entry, block: bool = False) -> None:
+        """Enforce one verdict if it has landed (or wait for it with ``block``); used by the
+        backward pass of the call that made it."""
+        if entry in self._pending and (block or entry[0].query()):
+            self._pending.remove(entry)
+            self._verify(entry)
+
+    def check_pending(self, block: bool = True) -> None:
+        """Enforce outstanding verdicts: all of them (block=True) or the completed ones."""
+        keep = []
+        err = None
+        for entry in self._pending:
+            if block or entry[0].query():
+                try:
+                    self._verify(entry)
+                except FloatingPointError as e:
+                    err = err or e
+            else:
+                keep.append(entry)
+        self._pending = keep
+        if err is not None:
+            raise err
+
+
+finite_guard = FiniteGuard()
+
+
+def check_pending() -> None:
+    """Raise ``FloatingPointError`` now if any earlier call's inputs were non-finite."""
+    finite_guard.check_pending(block=True)
+
+
+def make_rng(seed: int) -> np.random.Generator:
+    """PCG64 generator, bit-identical streams on every platform (numerics.py:78-79)."""
+    return np.random.Generator(np.random.PCG64(seed))
+
+
+def format_float(v: float) -> str:
+    """Shortest round-trip decimal form (numerics.py:122-124)."""
+    return repr(float(v))

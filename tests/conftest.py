@@ -7,13 +7,34 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 GOLDEN = os.path.join(ROOT, "tests", "golden")
-for p in (ROOT, GOLDEN):
+for p in (ROOT, GOLDEN, os.path.join(ROOT, "tests")):
     if p not in sys.path:
         sys.path.insert(0, p)
 
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a) and the built libspa2.so")
+
+
+@pytest.fixture(autouse=True)
+def _parity_test_id(request):
+    import parity
+
+    parity.CURRENT_TEST["id"] = request.node.nodeid
+    yield
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """Write every parity comparison's measured error (GPU runs) for the tolerance record."""
+    import parity
+
+    if not parity.RECORD:
+        return
+    out = os.path.join(ROOT, "gpurun_out")
+    os.makedirs(out, exist_ok=True)
+    with open(os.path.join(out, "parity_measured.json"), "w") as f:
+        json.dump({"tolerances": {"cos_min/max_rel": parity.TOL, "lse_abs": parity.LSE_ABS},
+                   "cases": parity.RECORD}, f, indent=0)
 
 
 def pytest_collection_modifyitems(config, items):

@@ -35,13 +35,23 @@ def metrics(got, want):
     return cos, rel
 
 
+# every comparison's measured error, written by conftest.py at session end
+# (tests/golden/parity_measured.json is the committed copy from a B200 run)
+RECORD: list[dict] = []
+CURRENT_TEST = {"id": None}
+
+
 def assert_close(name, got, want, key=None):
     key = key or name
+    g, w = as_np(got), as_np(want)
+    max_abs = float(np.abs(g - w).max()) if g.size else 0.0
     if key == "lse":
-        err = float(np.abs(as_np(got) - as_np(want)).max())
-        assert err <= LSE_ABS, f"{name}: max|Δlse| {err:.3e} > {LSE_ABS}"
-        return err
+        RECORD.append({"test": CURRENT_TEST["id"], "name": name, "key": key, "max_abs": max_abs})
+        assert max_abs <= LSE_ABS, f"{name}: max|Δlse| {max_abs:.3e} > {LSE_ABS}"
+        return max_abs
     cos_min, rel_max = TOL[key]
-    cos, rel = metrics(got, want)
+    cos, rel = metrics(g, w)
+    RECORD.append({"test": CURRENT_TEST["id"], "name": name, "key": key, "cosine": cos, "max_rel": rel,
+                   "max_abs": max_abs, "ref_max": float(np.abs(w).max()) if w.size else 0.0})
     assert cos >= cos_min and rel <= rel_max, f"{name}: cosine {cos:.6f} (min {cos_min}), rel {rel:.3e} (max {rel_max})"
     return cos, rel

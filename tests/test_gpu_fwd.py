@@ -176,14 +176,45 @@ def test_errors():
     bad = q.clone()
     bad[3, 3] = float("inf")
     with pytest.raises(FloatingPointError):
-        spa.sparse_attention_with_mask(bad, q, q, spa.full_mask(8))
-    with pytest.raises(FloatingPointError):
-        spa.sparse_attention(q, bad, q, spa.SparsityConfig(0.5, 0.5, BQ, BKV))
+        spa.sparse_attention_with_mask(bad, q, q, spa.full_mask(8), check_finite="sync")
+    for args in ((q, bad, q), (q, q, bad), (bad, q, q)):
+        with pytest.raises(FloatingPointError):
+            spa.sparse_attention(*args, spa.SparsityConfig(0.5, 0.5, BQ, BKV), check_finite="sync")
     with pytest.raises(spa.ShapeError):
         spa.sparse_attention_with_mask(q[None], q[None], q[None], spa.full_mask(8))
     with pytest.raises(ValueError, match="head dim"):
         z = torch.zeros(8, 48, device="cuda", dtype=torch.bfloat16)
         spa.sparse_attention_with_mask(z, z, z, spa.full_mask(8))
+
+
+def test_non_finite_verdict_is_deferred_for_torch_callers():
+    """No host sync on the hot path: a torch caller's non-finite input raises at the latest at
+    the next operator call, in its own backward once the scan has landed, or at
+    check_pending() (numerics.FiniteGuard)."""
+    q = torch.randn(300, 64, device="cuda").to(torch.bfloat16)
+    bad = q.clone()
+    bad[7, 1] = float("nan")
+    cfg = spa.SparsityConfig(0.5, 0.5, BQ, BKV)
+    spa.sparse_attention(q, q, bad, cfg)  # returns without a sync
+    with pytest.raises(FloatingPointError):
+        spa.check_pending()
+    spa.check_pending()  # consumed
+    spa.sparse_attention_with_mask(bad, q, q, spa.full_mask(300))
+    torch.cuda.synchronize()
+    with pytest.raises(FloatingPointError):  # the next call enforces the landed verdict
+        spa.sparse_attention(q, q, q, cfg)
+    qs = bad.clone().requires_grad_(True)
+    res = spa.sparse_attention(qs, q, q, cfg)
+    torch.cuda.synchronize()
+    with pytest.raises(FloatingPointError):  # ... and so does the call's own backward
+        res.out.sum().backward()
+    spa.check_pending()
+    g = spa.attention_backward(q, q, q, spa.full_mask(300), bad)  # d_out is scanned too
+    with pytest.raises(FloatingPointError):
+        spa.check_pending()
+    assert g.dq.shape == q.shape
+    res = spa.sparse_attention(q, q, bad, cfg, check_finite=False)  # opt-out: no verdict at all
+    spa.check_pending()
 
 
 def test_numpy_in_numpy_out():

@@ -52,8 +52,8 @@ def main():
         q, k, v = (torch.randn(n, d, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
         t_m, t_n = -(-n // b_q), -(-n // b_kv)
         dense_bm = spa.BlockMask(torch.ones(t_m, t_n, dtype=torch.bool), b_q, b_kv, n)
-        dense_out = spa.sparse_attention_with_mask(q, k, v, dense_bm, check_finite=False).out
-        dense_s = timed(lambda: spa.sparse_attention_with_mask(q, k, v, dense_bm, check_finite=False), args.reps)
+        dense_out = spa.sparse_attention_with_mask(q, k, v, dense_bm).out
+        dense_s = timed(lambda: spa.sparse_attention_with_mask(q, k, v, dense_bm), args.reps)
         for target in (float(x) for x in args.sparsities.split(",")):
             per_row = max(1, round((1.0 - target) * t_n))
             keep = np.zeros((t_m, t_n), dtype=bool)
@@ -61,8 +61,8 @@ def main():
                 keep[i, rng.choice(t_n, size=per_row, replace=False)] = True
             bm = spa.BlockMask(torch.as_tensor(keep), b_q, b_kv, n)
             counter = spa.BlockCounter()
-            out = spa.sparse_attention_with_mask(q, k, v, bm, counter=counter, check_finite=False).out
-            sparse_s = timed(lambda: spa.sparse_attention_with_mask(q, k, v, bm, check_finite=False), args.reps)
+            out = spa.sparse_attention_with_mask(q, k, v, bm, counter=counter).out
+            sparse_s = timed(lambda: spa.sparse_attention_with_mask(q, k, v, bm), args.reps)
             total = keep.size
             assert counter.count == int(keep.sum()), "computed blocks must equal kept blocks"
             ratio = counter.count / total

@@ -35,7 +35,7 @@ def main():
 
         def step():
             a, b, c = (t.detach().requires_grad_(True) for t in (qs, ks, vs))
-            res = spa.sparse_attention(a, b, c, cfg, check_finite=False)
+            res = spa.sparse_attention(a, b, c, cfg)
             res.out.backward(dos)
             return res
 
