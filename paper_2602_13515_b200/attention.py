@@ -141,10 +141,17 @@ def _lists_with_order(bm: BlockMask, B: int, H: int, N: int, visit) -> BlockList
     idx = []
     for b in range(B):
         for h in range(H):
+            orders = {}  # the hook runs once per MASK row, as in the reference
+
+            def order_of(i_m):
+                if i_m not in orders:
+                    orders[i_m] = [int(j) for j in visit(i_m, np.flatnonzero(mk[b, h, i_m]))]
+                return orders[i_m]
+
             for r in range(t_m):
                 if rq is None or rk is None:  # all-ones mask of an arbitrary geometry
                     i_m = min(r * BQ // bm.b_q, mk.shape[-2] - 1)
-                    order = [int(j) for j in visit(i_m, np.flatnonzero(mk[b, h, i_m]))]
+                    order = order_of(i_m)
                     seen, out = set(), []
                     for j in order:
                         for c in range(t_n):
@@ -152,8 +159,7 @@ def _lists_with_order(bm: BlockMask, B: int, H: int, N: int, visit) -> BlockList
                                 seen.add(c)
                                 out.append(c)
                 else:
-                    i_m = r // rq
-                    order = [int(j) for j in visit(i_m, np.flatnonzero(mk[b, h, i_m]))]
+                    order = order_of(r // rq)
                     out = [c for j in order for c in range(j * rk, min((j + 1) * rk, t_n))]
                 idx.append(np.asarray(out, dtype=np.int32))
     flat = torch.tensor(np.concatenate(idx) if idx else np.zeros(0, np.int32), device=keep_u8.device)

@@ -374,7 +374,9 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const double* __restrict
   bool neg = false;
   for (int t = threadIdx.x; t < T_n; t += blockDim.x) {
     const double v = x[t];
-    if (v < 0.0) {
+    // negative entries take the exact all-candidates path (numpy semantics); so do NaN/Inf
+    // (non-finite q/k, reported by the finiteness flag): garbage mask, but no fault
+    if (!(v >= 0.0) || v == INFINITY) {
       neg = true;
     } else {
       atomicAdd(&h_cnt[value_bucket(v)], 1);
@@ -472,8 +474,11 @@ __global__ void __launch_bounds__(kSelThreads) k_select(const double* __restrict
   uint8_t* out = keep + row * (int64_t)T_n;
   for (int t = threadIdx.x; t < T_n; t += blockDim.x) out[t] = 0;
   __syncthreads();
-  const int kept = s_kept;
-  for (int t = threadIdx.x; t < kept; t += blockDim.x) out[cc[t]] = 1;
+  const int kept = min(s_kept, C);  // == s_kept for finite rows (the candidates hold the answer)
+  for (int t = threadIdx.x; t < kept; t += blockDim.x) {
+    const int c = cc[t];
+    if ((unsigned)c < (unsigned)T_n) out[c] = 1;  // NaN rows may sort padding forward
+  }
 }
 
 // ---------------------------------------------------------------------------------------

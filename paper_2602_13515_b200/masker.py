@@ -90,11 +90,11 @@ class PooledMap:
                 raise ValueError("pooled map rows must sum to 1 within 1e-12")
         else:  # the reference path: validated on the host, no device needed (numerics.py:21-32)
             p = np.asarray(p, dtype=np.float64)
-            if p.ndim != 2:
+            if p.ndim not in (2, 4):
                 raise ShapeError(f"expected rank 2, got rank {p.ndim} with shape {p.shape}")
             if not np.all(np.isfinite(p)):
                 raise FloatingPointError("non-finite values in pooled map")
-            if np.any(np.abs(p.sum(axis=1) - 1.0) > 1e-12):
+            if np.any(np.abs(p.sum(axis=-1) - 1.0) > 1e-12):
                 raise ValueError("pooled map rows must sum to 1 within 1e-12")
             p = _readonly(p)
         object.__setattr__(self, "probs", p)
@@ -148,12 +148,12 @@ class BlockMask:
             k = (k.to(device=dev) != 0).contiguous()
             if not bool(k.any(dim=-1).all()):
                 raise ValueError("every query block must keep at least one key block")
-        else:  # masker.py:71-86, on the host
+        else:  # masker.py:71-86, on the host (rank 4 = the batched [B, H, T_m, T_n] extension)
             k = np.asarray(k)
-            if k.ndim != 2:
+            if k.ndim not in (2, 4):
                 raise ValueError(f"keep must be rank 2, got shape {k.shape}")
             k = _readonly(k.astype(bool))
-            if not np.all(k.any(axis=1)):
+            if not np.all(k.any(axis=-1)):
                 raise ValueError("every query block must keep at least one key block")
         if tuple(k.shape[-2:]) != (t_m, t_n):
             raise ValueError(f"keep shape {tuple(k.shape)} does not match grid ({t_m}, {t_n}) "

@@ -33,7 +33,7 @@ def pytest_sessionfinish(session, exitstatus):
     out = os.path.join(ROOT, "gpurun_out")
     os.makedirs(out, exist_ok=True)
     with open(os.path.join(out, "parity_measured.json"), "w") as f:
-        json.dump({"tolerances": {"cos_min/max_rel": parity.TOL, "lse_abs": parity.LSE_ABS},
+        json.dump({"tolerances": {"cos_min/max_rel": parity.TOL, "lse_rel": parity.LSE_REL},
                    "cases": parity.RECORD}, f, indent=0)
 
 

@@ -2,22 +2,25 @@
 
 The GPU path computes on bf16 operands with fp32 accumulation (tensor cores) and emits
 bf16 O / dQ / dK / dV and fp32 LSE; the reference computes in float64 on the *same*
-bf16-representable inputs.  Stated tolerances (north_star: "max-abs/rel and cosine"):
+bf16-representable inputs.  Stated tolerances (north_star: "max-abs/rel and cosine"),
+set to about twice the worst error measured over the whole GPU suite on a B200
+(tests/golden/parity_measured.json: out rel 5.6e-3, dq 6.8e-3, dk 5.9e-3, dv 4.9e-3,
+cosine >= 0.999993, LSE 1.9e-6 absolute):
 
-  out       cosine >= 0.9999   and  max|Δ| <= 2e-2 · max|ref|
-  lse       max|Δ| <= 2e-3     (natural log units)
-  dq/dk/dv  cosine >= 0.999    and  max|Δ| <= 6e-2 · max|ref|
+  out       cosine >= 0.99998  and  max|Δ| <= 1.2e-2 · max|ref|
+  dq/dk/dv  cosine >= 0.99998  and  max|Δ| <= 1.4e-2 · max|ref|
+  lse       max|Δ| <= 4e-6 · max(1, max|ref|)   (natural log units, fp32)
 """
 
 import numpy as np
 
 TOL = {
-    "out": (0.9999, 2e-2),
-    "dq": (0.999, 6e-2),
-    "dk": (0.999, 6e-2),
-    "dv": (0.999, 6e-2),
+    "out": (0.99998, 1.2e-2),
+    "dq": (0.99998, 1.4e-2),
+    "dk": (0.99998, 1.4e-2),
+    "dv": (0.99998, 1.4e-2),
 }
-LSE_ABS = 2e-3
+LSE_REL = 4e-6
 
 
 def as_np(x):
@@ -46,8 +49,10 @@ def assert_close(name, got, want, key=None):
     g, w = as_np(got), as_np(want)
     max_abs = float(np.abs(g - w).max()) if g.size else 0.0
     if key == "lse":
-        RECORD.append({"test": CURRENT_TEST["id"], "name": name, "key": key, "max_abs": max_abs})
-        assert max_abs <= LSE_ABS, f"{name}: max|Δlse| {max_abs:.3e} > {LSE_ABS}"
+        ref_max = float(np.abs(w).max()) if w.size else 0.0
+        RECORD.append({"test": CURRENT_TEST["id"], "name": name, "key": key, "max_abs": max_abs, "ref_max": ref_max})
+        lim = LSE_REL * max(1.0, ref_max)
+        assert max_abs <= lim, f"{name}: max|Δlse| {max_abs:.3e} > {lim:.3e}"
         return max_abs
     cos_min, rel_max = TOL[key]
     cos, rel = metrics(g, w)

@@ -31,8 +31,14 @@ def _run(n, d, keep, seed):
     tag = f"n{n}.d{d}"
     assert_close(f"{tag}.out", res.out, out, "out")
     assert_close(f"{tag}.lse", res.lse, lse, "lse")
-    assert_close(f"{tag}.dq", qd.grad, dq, "dq")
-    assert_close(f"{tag}.dk", kd.grad, dk, "dk")
+    if n == 1:
+        # one key: P = 1 and dS = dP - δ = 0 exactly; the GPU's dP (tensor core) and δ (fp32 dot
+        # product) round differently, so dq/dk are zero up to fp32 rounding of |dO|·|v|
+        scale = float(np.abs(do).max() * np.abs(v).max() * d)
+        assert float(qd.grad.abs().max()) <= 1e-5 * scale and float(kd.grad.abs().max()) <= 1e-5 * scale
+    else:
+        assert_close(f"{tag}.dq", qd.grad, dq, "dq")
+        assert_close(f"{tag}.dk", kd.grad, dk, "dk")
     assert_close(f"{tag}.dv", vd.grad, dv, "dv")
     return res, (qd.grad, kd.grad, vd.grad)
 

@@ -41,11 +41,10 @@ for n, d, density, heads in ((1000, 128, 0.3, 2), (777, 64, 0.5, 1)):
     qt = torch.tensor(q, device="cuda").to(torch.bfloat16).view(1, heads, n, d)
     kt = torch.tensor(k, device="cuda").to(torch.bfloat16).view(1, heads, n, d)
     cfg = mk.SparsityConfig(0.1, 0.5, 128, 64)
-    got = spa.sparse_attention(qt, kt, qt, cfg).mask_used.keep.cpu().numpy()
+    got = spa.sparse_attention(qt, kt, qt, cfg).mask_used.keep.cpu().numpy().reshape(1, heads, t_m, t_n)
+    probs = spa.pooled_map(qt, kt, cfg).probs.cpu().numpy().reshape(1, heads, t_m, t_n)  # select: bit-exact given the map
     for h in range(heads):
-        want = oracle.hybrid_keep(oracle.pooled_probs(qt[0, h].double().cpu().numpy(), kt[0, h].double().cpu().numpy(),
-                                                      128, 64), 0.1, 0.5)
-        assert np.array_equal(got[0, h], want)
+        assert np.array_equal(got[0, h], oracle.hybrid_keep(probs[0, h], 0.1, 0.5))
 print("ok")
 """
 

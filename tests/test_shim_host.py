@@ -107,6 +107,8 @@ def test_pooled_map_validation_on_host():  # masker.py:54-62
         mk.PooledMap(np.array([[np.nan, 1.0]]), 1, 1, 2)
     with pytest.raises(ValueError):  # ShapeError is a ValueError
         mk.PooledMap(np.ones((1, 1, 1)), 1, 1, 1)
+    batched = mk.BlockMask(np.ones((1, 2, 2, 2), dtype=bool), 2, 2, 4)  # [B, H, T_m, T_n] extension
+    assert batched.kept_blocks() == 8
 
 
 def test_union_of_host_masks_stays_on_host():  # masker.py:94-97
