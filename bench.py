@@ -4,13 +4,18 @@
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
 
-One step = the trainable operator of the reference's hot path on one batch:
-``sparse_attention(q, k, v, SparsityConfig(0.03, 0.2, 128, 64))`` (pooled map -> hybrid
-Top-k∪Top-p select -> block lists -> block-sparse forward) followed by its backward
-(δ, dQ, dK/dV).  Workload = BASELINE.json configs[1]: Wan2.1-1.3B 480p attention,
-B=1, H=12, N=32760, d=128, bf16, synthetic inputs calibrated to ≈95 % block sparsity.
-Multi-GPU: every rank runs its own 12-head problem (head sharding, no data-path
-collective) -> weak scaling; timing = max over ranks.
+One step = the trainable operator of the reference's hot path on one batch, through the
+public API with its default arguments: ``sparse_attention(q, k, v, SparsityConfig(0.03,
+0.2, 128, 64))`` (finiteness scan -> pooled map -> hybrid Top-k∪Top-p select -> block
+lists -> block-sparse forward) followed by its backward (δ, dQ, dK/dV).
+Workload = BASELINE.json configs[1]: Wan2.1-1.3B 480p attention, B=1, H=12, N=32760,
+d=128, bf16, synthetic inputs calibrated to ≈95 % block sparsity.
+
+Multi-GPU (N > 1): every rank runs its own 12-head configs[1] problem (batch-sharded weak
+scaling, no data-path collective) -> `value`; plus a `cfg4` leg on BASELINE configs[3]
+(Wan2.1-14B 720p, H=40, N=75600): the ONE problem head-sharded 40/N per rank with the
+NCCL all-gather of O and dQ/dK/dV, and the Ulysses sequence-parallel form (all-to-all
+over NCCL, overlapped with the per-head-group compute), comm time reported separately.
 
 value = dense-equivalent TFLOP/s = 14·B·H·N²·d / step time, summed over ranks.
 """
@@ -29,10 +34,12 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")  # the unmodified reference (pip --target, git-ignored)
 
 METRIC = "sparse-attn fwd+bwd ms & effective TFLOPS @95% sparsity, Wan2.1 shape, 1-8 GPU"
 UNIT = "TFLOP/s (dense-equivalent, 14*B*H*N^2*d per step)"
 WORKLOAD = dict(B=1, H=12, N=32760, d=128, b_q=128, b_kv=64, k_frac=0.03, p_frac=0.2, offset_scale=0.9)
+CFG4 = dict(B=1, H=40, N=75600, d=128, k_frac=0.03, p_frac=0.16, offset_scale=0.8)
 FLOP_MULT = 14  # fwd 4 + bwd 10, per (query, key, feature) triple
 
 
@@ -53,80 +60,141 @@ def load_peaks():
 
 
 # ---------------------------------------------------------------------------------------
-# CPU arm: the reference algorithm (oracle port, float64 numpy) on the host's cores
+# CPU arm: the reference itself (baseline/_ref/sparseattn_lab) on the host's cores;
+# the oracle port only if the reference is not installed
 # ---------------------------------------------------------------------------------------
 _CPU = {}
 
 
-def _cpu_worker_init(seed: int, n: int, d: int, s: float):
+def reference_installed() -> bool:
+    return os.path.isfile(os.path.join(REF_DIR, "sparseattn_lab", "attention.py"))
+
+
+def _host_inputs(seed: int, n: int, d: int, s: float):
+    """One head of configs[1]-distributed inputs (N(0,1) + per-block N(0, s²) offsets) in float64."""
     import numpy as np
+
+    rng = np.random.Generator(np.random.PCG64(seed))
+    t_m, t_n = -(-n // 128), -(-n // 64)
+    q = rng.normal(size=(n, d)) + np.repeat(rng.normal(size=(t_m, d)) * s, 128, axis=0)[:n]
+    k = rng.normal(size=(n, d)) + np.repeat(rng.normal(size=(t_n, d)) * s, 64, axis=0)[:n]
+    return q, k, rng.normal(size=(n, d)), rng.normal(size=(n, d))
+
+
+def _import_reference():
+    """Import the UNMODIFIED reference from baseline/_ref — ahead of the repo root, whose
+    ``sparseattn_lab`` is this package's drop-in shim."""
+    if sys.path[0] != REF_DIR:
+        sys.path.insert(0, REF_DIR)
+    for m in [m for m in sys.modules if m == "sparseattn_lab" or m.startswith("sparseattn_lab.")]:
+        del sys.modules[m]
+    import sparseattn_lab.attention as at
+    import sparseattn_lab.masker as mk
+
+    if not os.path.abspath(at.__file__).startswith(REF_DIR):
+        raise RuntimeError(f"imported {at.__file__}, not the reference under {REF_DIR}")
+    return at, mk
+
+
+def _cpu_worker_init(seed: int, n: int, d: int, s: float, kind: str, blas_threads):
+    import numpy  # noqa: F401  (threadpool_limits acts on the BLAS / OpenMP libraries already loaded)
     from threadpoolctl import threadpool_limits
 
-    threadpool_limits(1)
-    rng = np.random.Generator(np.random.PCG64(seed))
-    b_q, b_kv = 128, 64
-    t_m, t_n = -(-n // b_q), -(-n // b_kv)
-    q = rng.normal(size=(n, d)) + np.repeat(rng.normal(size=(t_m, d)) * s, b_q, axis=0)[:n]
-    k = rng.normal(size=(n, d)) + np.repeat(rng.normal(size=(t_n, d)) * s, b_kv, axis=0)[:n]
-    v = rng.normal(size=(n, d))
-    do = rng.normal(size=(n, d))
-    _CPU.update(q=q, k=k, v=v, do=do, t_m=t_m)
+    if blas_threads is not None:
+        threadpool_limits(blas_threads)
+    _CPU.update(zip(("q", "k", "v", "do"), _host_inputs(seed, n, d, s)))
+    _CPU["kind"] = kind
+    if kind == "reference":
+        _CPU["at"], _CPU["mk"] = _import_reference()
 
 
-def _cpu_sample(args):
-    """Masker (pooled map + hybrid select for the sampled query blocks) + tiled forward +
-    LSE-recompute backward over `rows` query blocks of one head, as the reference runs them
-    (masker.py:100-146, attention.py:73-166).  Returns (seconds, kept blocks)."""
-    import numpy as np
-
-    import oracle
-
-    start_blk, rows, k_frac, p_frac = args
-    q, k, v, do, t_m = _CPU["q"], _CPU["k"], _CPU["v"], _CPU["do"], _CPU["t_m"]
-    start_blk = start_blk % max(1, t_m - rows)
-    sl = slice(start_blk * 128, (start_blk + rows) * 128)
+def _cpu_head(args):
+    """One head's fwd+bwd.  kind "reference": the reference's public API, exactly as its own
+    callers pair them (flowmatch.py:263-264, 317): sparse_attention (masker + tiled forward)
+    then attention_backward (LSE-recompute backward).  kind "port": the oracle restatement
+    of the same algorithm on `rows` query blocks (only when the reference is absent).
+    Returns (seconds, kept blocks, query-block rows processed)."""
+    k_frac, p_frac, rows = args
+    q, k, v, do = _CPU["q"], _CPU["k"], _CPU["v"], _CPU["do"]
     t0 = time.perf_counter()
-    q_bar = oracle.block_mean_pool(q[sl], 128)
-    k_bar = oracle.block_mean_pool(k, 64)
-    probs = oracle.softmax_rows((q_bar @ k_bar.T) / math.sqrt(q.shape[1]))
-    keep = oracle.hybrid_keep(probs, k_frac, p_frac)
-    oracle.attention_backward(q[sl], k, v, keep, 128, 64, do[sl])  # includes the forward recompute
-    return time.perf_counter() - t0, int(keep.sum())
+    if _CPU["kind"] == "reference":
+        at, mk = _CPU["at"], _CPU["mk"]
+        res = at.sparse_attention(q, k, v, mk.SparsityConfig(k_frac, p_frac, 128, 64))
+        at.attention_backward(q, k, v, res.mask_used, do)
+        kept, done_rows = res.mask_used.kept_blocks(), res.mask_used.keep.shape[0]
+    else:
+        import oracle
+
+        sl = slice(0, rows * 128)
+        probs = oracle.softmax_rows((oracle.block_mean_pool(q[sl], 128) @ oracle.block_mean_pool(k, 64).T)
+                                    / math.sqrt(q.shape[1]))
+        keep = oracle.hybrid_keep(probs, k_frac, p_frac)
+        oracle.attention_backward(q[sl], k, v, keep, 128, 64, do[sl])
+        kept, done_rows = int(keep.sum()), rows
+    return time.perf_counter() - t0, kept, done_rows
 
 
-def cpu_reference(steps: int, warmup: int, w=WORKLOAD, target_step_s: float = 0.12):
-    """Time the CPU reference path on a bounded sample; returns a dict with value (same
-    metric/unit as the GPU arm) and the sample description."""
+def _threadpool_summary():
+    try:
+        from threadpoolctl import threadpool_info
+
+        return [{k: p.get(k) for k in ("internal_api", "num_threads", "version")} for p in threadpool_info()]
+    except Exception as e:  # pragma: no cover
+        return str(e)[:200]
+
+
+def cpu_reference(steps: int, warmup: int, w=WORKLOAD, as_shipped: bool = True):
+    """Time the CPU reference on the host's cores.
+
+    mode (ii), the reported value: a process pool of min(cores, B·H) workers with one BLAS
+    thread each; one step = every worker runs one full head's fwd+bwd, so a step processes
+    `workers` of the job's B·H heads and value = their dense-equivalent FLOPs / step time
+    (nothing extrapolated: ms_per_step is the measured step).
+    mode (i), "as shipped": one process with the default BLAS threads runs one head."""
     import multiprocessing as mp
 
     cores = os.cpu_count() or 1
+    kind = "reference" if reference_installed() else "port"
     workers = max(1, min(cores, w["B"] * w["H"]))
+    t_m = -(-w["N"] // w["b_q"])
+    rows = t_m if kind == "reference" else 8
     ctx = mp.get_context("spawn")
-    with ctx.Pool(workers, initializer=_cpu_worker_init, initargs=(7, w["N"], w["d"], w["offset_scale"])) as pool:
-        t1, _ = pool.apply(_cpu_sample, ((0, 1, w["k_frac"], w["p_frac"]),))
-        rows = max(1, min(16, int(round(target_step_s / max(t1, 1e-3)))))
-        times, kept = [], []
+    init = (7, w["N"], w["d"], w["offset_scale"], kind, 1)
+    saved_env = {v: os.environ.get(v) for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")}
+    os.environ.update({v: "1" for v in saved_env})  # the workers' BLAS starts single-threaded
+    times, kept = [], []
+    with ctx.Pool(workers, initializer=_cpu_worker_init, initargs=init) as pool:
         for it in range(warmup + steps):
             t0 = time.perf_counter()
-            res = pool.map(_cpu_sample, [((it * 7 + r * 37), rows, w["k_frac"], w["p_frac"]) for r in range(workers)])
+            res = pool.map(_cpu_head, [(w["k_frac"], w["p_frac"], rows)] * workers)
             dt = time.perf_counter() - t0
             if it >= warmup:
                 times.append(dt)
-                kept.append(sum(x[1] for x in res))
+                kept.append(sum(x[1] for x in res) / workers)
+    for var, val in saved_env.items():
+        if val is None:
+            os.environ.pop(var, None)
+        else:
+            os.environ[var] = val
     t_step = statistics.median(times)
-    t_m = -(-w["N"] // w["b_q"])
-    frac_of_job = workers * rows / (w["B"] * w["H"] * t_m)  # share of the job's query blocks per step
-    value = dense_equiv_flops(w) * frac_of_job / t_step / 1e12
-    full_job_ms = t_step / frac_of_job * 1e3
-    return {
-        "value": value, "unit": UNIT, "cores": workers, "kind": "port",
-        "sample": (f"oracle/ float64 numpy port of the reference (masker + tiled fwd + LSE-recompute bwd), "
-                   f"{workers} process(es) x {rows} query-block row(s) of one Wan2.1-1.3B head each per step "
-                   f"(1 BLAS thread per process), {steps} steps; {statistics.mean(kept) / workers / rows:.1f} kept "
-                   f"blocks per row; full 12-head job extrapolated to {full_job_ms / 1e3:.1f} s"),
-        "full_job_ms": full_job_ms,
-        "host_cores": cores,
+    head_flops = dense_equiv_flops(dict(w, B=1, H=1)) * rows / t_m
+    value = workers * head_flops / t_step / 1e12
+    out = {
+        "value": value, "unit": UNIT, "cores": workers, "kind": kind, "ms_per_step": t_step * 1e3,
+        "host_cores": cores, "threadpool_info": _threadpool_summary(),
+        "sample": (f"{'sparseattn_lab (unmodified reference, baseline/_ref)' if kind == 'reference' else 'oracle/ port'}"
+                   f" sparse_attention + attention_backward, float64 numpy; {workers} worker process(es) x 1 BLAS "
+                   f"thread, each step = {workers} head(s) x {rows}/{t_m} query-block rows of the Wan2.1-1.3B shape "
+                   f"({statistics.mean(kept) / rows:.1f} kept key blocks per row), median of {steps} step(s); the "
+                   f"full {w['B'] * w['H']}-head job is {w['B'] * w['H'] * t_m / (workers * rows):.2f} such steps"),
     }
+    if as_shipped:  # mode (i): the reference as a user runs it, one process, default BLAS threads
+        _cpu_worker_init(7, w["N"], w["d"], w["offset_scale"], kind, None)
+        dt, _, _ = _cpu_head((w["k_frac"], w["p_frac"], rows))
+        out["as_shipped"] = {"ms_per_head": dt * 1e3, "value": head_flops / dt / 1e12,
+                             "blas_threads": _threadpool_summary(),
+                             "mode": "one process, default BLAS threads, one head"}
+    return out
 
 
 # ---------------------------------------------------------------------------------------
@@ -199,6 +267,32 @@ def tile_flops(keep, N: int, d: int, mult: int) -> float:
     return float(mult * d * (keep.double() * r[:, None] * c[None, :]).sum())
 
 
+def _time(fn, reps, warm):
+    import torch
+
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def _max_over_ranks(ms: float, world: int, dev) -> float:
+    if world == 1:
+        return ms
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def gpu_arm(args, rank: int, world: int, dev):
     import torch
     import torch.distributed as dist
@@ -206,7 +300,7 @@ def gpu_arm(args, rank: int, world: int, dev):
     import paper_2602_13515_b200 as spa
     from paper_2602_13515_b200 import _lib
     from paper_2602_13515_b200 import attention as at
-    from paper_2602_13515_b200.synthetic import wan_like_qkv
+    from paper_2602_13515_b200.synthetic import video_like_qkv, wan_like_qkv
 
     w = WORKLOAD
     B, H, N, d = w["B"], w["H"], w["N"], w["d"]
@@ -214,11 +308,15 @@ def gpu_arm(args, rank: int, world: int, dev):
     q, k, v = wan_like_qkv(B, H, N, d, w["offset_scale"], seed=1000 + rank)
     do = torch.randn(q.shape, device=dev, generator=torch.Generator(device=dev).manual_seed(77 + rank)).to(q.dtype)
 
-    def step():
-        qs, ks, vs = (t.detach().requires_grad_(True) for t in (q, k, v))
-        res = spa.sparse_attention(qs, ks, vs, cfg)
-        res.out.backward(do)
-        return res
+    def make_step(q, k, v):
+        def step():
+            qs, ks, vs = (t.detach().requires_grad_(True) for t in (q, k, v))
+            res = spa.sparse_attention(qs, ks, vs, cfg)  # the default API: finiteness verdicts included
+            res.out.backward(do)
+            return res
+        return step
+
+    step = make_step(q, k, v)
 
     def barrier():
         if world > 1:
@@ -231,9 +329,7 @@ def gpu_arm(args, rank: int, world: int, dev):
         step()
     torch.cuda.synchronize()
 
-    timed_names = ("spa2_fwd", "spa2_bwd_dq_delta", "spa2_bwd_dkdv", "spa2_pooled_scores", "spa2_select_scores",
-                   "spa2_pooled_map", "spa2_select", "spa2_build_lists")
-    _lib.STATS.timing = {n: [] for n in timed_names}
+    # ---- the timed region: K steps back to back, no instrumentation between launches ----
     launches0 = _lib.STATS.launches
     uuid = None
     try:
@@ -255,12 +351,18 @@ def gpu_arm(args, rank: int, world: int, dev):
     t_wall1 = time.time()
     clocks = sampler.stop(t_wall0, t_wall1)
     launches = _lib.STATS.launches - launches0
-    ms_total = ev0.elapsed_time(ev1)
-    if world > 1:
-        t = torch.tensor([ms_total], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total = float(t.item())
-    ms_step = ms_total / args.steps
+    spa.check_pending()  # every finiteness verdict of the timed steps (must all be clean)
+    ms_step = _max_over_ranks(ev0.elapsed_time(ev1), world, dev) / args.steps
+
+    # ---- per-kernel pass (separate, so the timed loop keeps its PDL overlap): CUDA events on
+    # the launching stream around each C call ----
+    timed_names = ("spa2_check_finite", "spa2_pooled_scores", "spa2_select_scores", "spa2_build_lists", "spa2_fwd",
+                   "spa2_bwd_dq_delta", "spa2_bwd_dkdv")
+    _lib.STATS.timing = {n: [] for n in timed_names}
+    n_k = max(5, min(args.steps, 30))
+    for _ in range(n_k):
+        step()
+    torch.cuda.synchronize()
     per_kernel_ms = {n: (sum(a.elapsed_time(b) for a, b in lst) / len(lst) if lst else 0.0)
                      for n, lst in _lib.STATS.timing.items()}
     _lib.STATS.timing = None
@@ -287,10 +389,24 @@ def gpu_arm(args, rank: int, world: int, dev):
                 "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                 "peak_source": peaks["source"] + (", sustained bf16 GEMM (long timed loop)" if sustained
                                                   else ", burst bf16 GEMM"),
-                "flops_per_launch": kflops[dom], "ms_per_launch": per_kernel_ms[dom]}
+                "flops_per_launch": kflops[dom], "ms_per_launch": per_kernel_ms[dom],
+                "algorithmic": "Σ_kept c·r_i·c_j·d with c = 4 (fwd), 6 (dQ: S, dP, dQ), 8 (dK/dV: S, dP, dV, dK)"}
+    # masker: HBM-bound.  K1 = pooling (reads Q and K once) + the fp64 pooled-score GEMM;
+    # K0 = the finiteness scan of V (reads V once).
+    qk_bytes = 2 * q.numel() * q.element_size()
+    hbm = peaks["hbm_gbs"]
+    masker = {"bound": "hbm", "unit": "GB/s", "peak": hbm,
+              "K1_pool_scores": {"bytes": qk_bytes, "ms": per_kernel_ms["spa2_pooled_scores"],
+                                 "achieved": qk_bytes / (per_kernel_ms["spa2_pooled_scores"] * 1e-3) / 1e9},
+              "K0_finite_scan_v": {"bytes": qk_bytes // 2, "ms": per_kernel_ms["spa2_check_finite"],
+                                   "achieved": (qk_bytes // 2) / (per_kernel_ms["spa2_check_finite"] * 1e-3) / 1e9}}
+    for kk in ("K1_pool_scores", "K0_finite_scan_v"):
+        masker[kk]["frac"] = masker[kk]["achieved"] / hbm
+    masker["note"] = ("K1's time includes the fp64 pooled-score GEMM (k_scores) after the pooling pass; "
+                      "per-kernel shares in profiles/ncu_*.md")
 
     out = {"ms_step": ms_step, "sparsity": sparsity, "clocks": clocks, "launches": launches,
-           "per_kernel_ms": per_kernel_ms, "roofline": roofline, "kflops": kflops}
+           "per_kernel_ms": per_kernel_ms, "roofline": roofline, "masker_roofline": masker, "kflops": kflops}
 
     # ---- e2e through the public API with host buffers ----
     if not args.no_e2e:
@@ -314,12 +430,8 @@ def gpu_arm(args, rank: int, world: int, dev):
             e2e_step()
         b.record()
         torch.cuda.synchronize()
-        e_ms = a.elapsed_time(b)
-        if world > 1:
-            t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_ms = float(t.item())
-        e_step = e_ms / n_e2e
+        spa.check_pending()
+        e_step = _max_over_ranks(a.elapsed_time(b), world, dev) / n_e2e
         nbytes = q.numel() * q.element_size()
         out["e2e"] = {"value": world * dense_equiv_flops() / (e_step * 1e-3) / 1e12, "unit": UNIT,
                       "h2d_bytes_per_step": 4 * nbytes, "d2h_bytes_per_step": 4 * nbytes, "ms_per_step": e_step,
@@ -360,22 +472,91 @@ def gpu_arm(args, rank: int, world: int, dev):
         dense["speedup_vs_best_dense"] = best / ms_step
         dense["speedup_vs_own_dense"] = dense["own_kernels_all_blocks_ms"] / ms_step
         out["dense_baselines"] = dense
+
+    # ---- secondary workload: spatio-temporally correlated (video-like) masks, same shape ----
+    if rank == 0 and world == 1 and not args.no_secondary:
+        q2, k2, v2 = video_like_qkv(B, H, N, d, 2.5, seed=2000)
+        step2 = make_step(q2, k2, v2)
+        r2 = step2()
+        keep2 = r2.mask_used.keep
+        ms2 = _time(step2, max(5, min(args.steps, 30)), 2)
+        spa.check_pending()
+        adj = float((keep2[..., :-1] & keep2[..., 1:]).sum() / keep2[..., :-1].sum())
+        out["secondary"] = {"workload": "video-like correlated masks (synthetic.video_like_qkv, s=2.5), same shape",
+                            "block_sparsity": r2.mask_used.sparsity(), "ms_per_step": ms2,
+                            "value": dense_equiv_flops() / (ms2 * 1e-3) / 1e12,
+                            "p_next_key_block_kept": adj,
+                            "p_next_key_block_kept_primary": float((keep[..., :-1] & keep[..., 1:]).sum()
+                                                                   / keep[..., :-1].sum())}
+        del q2, k2, v2
     return out
 
 
-def _time(fn, reps, warm):
+def cfg4_leg(args, rank: int, world: int, dev):
+    """configs[3] on `world` GPUs: ONE Wan2.1-14B 720p attention problem (H = 40, N = 75600)
+    (a) head-sharded: rank r runs heads head_range(40, r, world) of replicated q/k/v, then the
+        NCCL all-gather of O (forward) and of dQ, dK, dV (backward) assembles the full result;
+    (b) Ulysses: q/k/v/dO sequence-sharded [B, N/P, H, d] per rank, exchanged to head-sharded
+        by all-to-all (NCCL), per-head-group compute overlapped with the exchange of the next
+        group (dist.UlyssesAttention), outputs and gradients exchanged back.
+    Device time, max over ranks; comm time from CUDA events around the collectives."""
     import torch
 
-    for _ in range(warm):
-        fn()
-    torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    for _ in range(reps):
-        fn()
-    b.record()
-    torch.cuda.synchronize()
-    return a.elapsed_time(b) / reps
+    import paper_2602_13515_b200 as spa
+    from paper_2602_13515_b200 import dist as sdist
+    from paper_2602_13515_b200.synthetic import wan_like_qkv
+
+    c = CFG4
+    B, H, N, d = c["B"], c["H"], c["N"], c["d"]
+    cfg = spa.SparsityConfig(c["k_frac"], c["p_frac"], 128, 64)
+    h0, h1 = sdist.head_range(H, rank, world)
+    # every rank generates the full replicated problem from the same seed, keeps its heads
+    q, k, v = wan_like_qkv(B, H, N, d, c["offset_scale"], seed=4000)
+    do = torch.randn(q.shape, device=dev, generator=torch.Generator(device=dev).manual_seed(4001)).to(q.dtype)
+    out = {"workload": "Wan2.1-14B 720p attention (BASELINE configs[3]): B=1 H=40 N=75600 d=128, one problem over "
+                       f"{world} GPU(s)", "heads_per_rank": h1 - h0}
+    comm_ev = []
+
+    def head_sharded_step():
+        ql, kl, vl = (t[:, h0:h1].detach().requires_grad_(True) for t in (q, k, v))
+        res = spa.sparse_attention(ql, kl, vl, cfg)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        sdist.gather_heads(res.out.detach(), H)
+        e1.record()
+        res.out.backward(do[:, h0:h1])
+        e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e2.record()
+        for g in (ql.grad, kl.grad, vl.grad):
+            sdist.gather_heads(g, H)
+        e3.record()
+        comm_ev.append((e0, e1, e2, e3))
+
+    reps = max(3, min(args.steps, 10))
+    ms = _max_over_ranks(_time(head_sharded_step, reps, 2), world, dev)
+    comm = sum(a.elapsed_time(b) + c_.elapsed_time(d_) for a, b, c_, d_ in comm_ev[-reps:]) / reps
+    out["head_sharded"] = {"ms_per_step": ms, "value": dense_equiv_flops(c) / (ms * 1e-3) / 1e12,
+                           "allgather_ms_per_step": _max_over_ranks(comm, world, dev)}
+    spa.check_pending()
+    if H % world == 0 and N % world == 0:
+        n_loc = N // world
+        n0 = rank * n_loc
+        # sequence-sharded activations [B, N/P, H, d], as a DiT holds them
+        ql, kl, vl, dol = (t.permute(0, 2, 1, 3)[:, n0:n0 + n_loc].contiguous() for t in (q, k, v, do))
+        uly = sdist.UlyssesAttention(cfg, groups=args.ulysses_groups)
+
+        def ulysses_step():
+            qs, ks, vs = (t.detach().requires_grad_(True) for t in (ql, kl, vl))
+            o = uly(qs, ks, vs)
+            o.backward(dol)
+
+        ms_u = _max_over_ranks(_time(ulysses_step, reps, 2), world, dev)
+        out["ulysses"] = {"ms_per_step": ms_u, "value": dense_equiv_flops(c) / (ms_u * 1e-3) / 1e12,
+                          "groups": args.ulysses_groups,
+                          "alltoall_ms_per_step": _max_over_ranks(uly.comm_ms(reps), world, dev),
+                          "note": "all-to-all on its own stream, overlapped with the other head groups' compute"}
+        spa.check_pending()
+    return out
 
 
 def config_dict(world: int, sparsity=None):
@@ -383,7 +564,9 @@ def config_dict(world: int, sparsity=None):
     c = {"workload": "Wan2.1-1.3B 480p attention (BASELINE configs[1]): B=1 H=12 N=32760 d=128 per GPU",
          "B": w["B"], "H": w["H"], "N": w["N"], "d": w["d"], "b_q": w["b_q"], "b_kv": w["b_kv"],
          "k_frac": w["k_frac"], "p_frac": w["p_frac"], "mask": "hybrid top-k ∪ top-p, rebuilt every step",
-         "parallelism": f"head-sharded x{world} (each rank its own 12-head problem, no collective)",
+         "parallelism": (f"batch-sharded x{world}: each rank its own 12-head problem, no collective"
+                         if world > 1 else "single GPU"),
+         "api": "sparse_attention(q, k, v, cfg) with default arguments + autograd backward",
          "l2": "inputs larger than L2 (q+k+v+dO = 403 MB per GPU), no flush"}
     if sparsity is not None:
         c["block_sparsity"] = round(sparsity, 5)
@@ -393,13 +576,17 @@ def config_dict(world: int, sparsity=None):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-cfg4", action="store_true")
     ap.add_argument("--e2e-groups", type=int, default=6)
+    ap.add_argument("--ulysses-groups", type=int, default=5)
+    ap.add_argument("--lib", default=None, help="A/B: load this libspa2.so build instead of the in-tree one")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -410,13 +597,13 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        ref_steps = min(args.steps, 60)  # each step is a bounded CPU sample; keep the run to ~minutes
-        cpu = cpu_reference(ref_steps, min(args.warmup, 3))
-        line = {"metric": METRIC, "value": cpu["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": ref_steps,
-                "warmup": min(args.warmup, 3), "ms_per_step": cpu["full_job_ms"], "higher_is_better": True,
+        cpu = cpu_reference(args.steps, args.warmup, as_shipped=False)
+        line = {"metric": METRIC, "value": cpu["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": cpu["ms_per_step"], "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (Wan2.1-shaped, seeded)",
                 "config": config_dict(1), "impl": "reference",
-                "cpu_baseline": {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "cpu_baseline": {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample", "host_cores",
+                                                     "threadpool_info")},
                 "e2e": {"value": cpu["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
@@ -424,15 +611,22 @@ def main():
     import torch
     import torch.distributed as dist
 
+    if args.lib:
+        from paper_2602_13515_b200 import _lib
+
+        _lib.use_library(args.lib)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     try:
         r = gpu_arm(args, rank, world, dev)
+        c4 = None
+        if world > 1 and not args.no_cfg4:
+            c4 = cfg4_leg(args, rank, world, dev)
         cpu = None
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
-            cpu = cpu_reference(20, 2)
+            cpu = cpu_reference(1, 0)
         if rank == 0:
             value = world * dense_equiv_flops() / (r["ms_step"] * 1e-3) / 1e12
             line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -440,14 +634,17 @@ def main():
                     "vs_baseline": None, "dtype": "bf16",
                     "data": "synthetic (Wan2.1-shaped q/k/v: N(0,1) + per-block N(0,0.81) offsets, seeded)",
                     "config": config_dict(world, r["sparsity"]), "roofline": r["roofline"],
+                    "masker_roofline": r["masker_roofline"],
                     "gpu_launches": r["launches"], "clocks": r["clocks"],
                     "per_kernel_ms": {k.replace("spa2_", ""): round(v, 5) for k, v in r["per_kernel_ms"].items()}}
-            if "e2e" in r:
-                line["e2e"] = r["e2e"]
-            if "dense_baselines" in r:
-                line["dense_baselines"] = r["dense_baselines"]
+            for key in ("e2e", "dense_baselines", "secondary"):
+                if key in r:
+                    line[key] = r[key]
+            if c4 is not None:
+                line["cfg4"] = c4
             if cpu is not None:
-                line["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+                line["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample", "host_cores",
+                                                            "threadpool_info", "as_shipped", "ms_per_step")}
             print(json.dumps(line), flush=True)
     finally:
         if world > 1:

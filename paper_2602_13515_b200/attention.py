@@ -186,10 +186,13 @@ def _check_kernel_shape(q4: torch.Tensor) -> None:
         raise ValueError(f"GPU kernels support head dim d in {SUPPORTED_HEAD_DIMS}, got d={d}")
 
 
-def fwd(q4, k4, v4, lists: BlockLists, scale: float, counter: torch.Tensor | None = None):
-    """K4: returns (O [B,H,N,d] bf16, LSE [B,H,N] fp32)."""
+def fwd(q4, k4, v4, lists: BlockLists, scale: float, counter: torch.Tensor | None = None,
+        o: torch.Tensor | None = None):
+    """K4: returns (O [B,H,N,d] bf16, LSE [B,H,N] fp32).  ``o`` may be a preallocated strided
+    [B,H,N,d] view to write O into (e.g. a collective's send buffer)."""
     B, H, N, d = q4.shape
-    o = torch.empty((B, H, N, d), device=q4.device, dtype=q4.dtype)
+    if o is None:
+        o = torch.empty((B, H, N, d), device=q4.device, dtype=q4.dtype)
     lse = torch.empty((B, H, N), device=q4.device, dtype=torch.float32)
     st = torch.cuda.current_stream(q4.device)
     _lib.call("spa2_fwd", _lib.view4(q4), _lib.view4(k4), _lib.view4(v4), _lib.view4(o), _lib.ptr(lse),
@@ -198,12 +201,15 @@ def fwd(q4, k4, v4, lists: BlockLists, scale: float, counter: torch.Tensor | Non
     return o, lse
 
 
-def bwd(q4, k4, v4, o4, do4, lse, lists: BlockLists, scale: float):
-    """K5-K7: returns (dQ, dK, dV) bf16 [B,H,N,d]."""
+def bwd(q4, k4, v4, o4, do4, lse, lists: BlockLists, scale: float, dq=None, dk=None, dv=None):
+    """K5-K7: returns (dQ, dK, dV) bf16 [B,H,N,d] (optionally written into given strided views)."""
     B, H, N, d = q4.shape
-    dq = torch.empty((B, H, N, d), device=q4.device, dtype=q4.dtype)
-    dk = torch.empty_like(dq)
-    dv = torch.empty_like(dq)
+    if dq is None:
+        dq = torch.empty((B, H, N, d), device=q4.device, dtype=q4.dtype)
+    if dk is None:
+        dk = torch.empty((B, H, N, d), device=q4.device, dtype=q4.dtype)
+    if dv is None:
+        dv = torch.empty((B, H, N, d), device=q4.device, dtype=q4.dtype)
     delta = torch.empty((B, H, N), device=q4.device, dtype=torch.float32)
     st = torch.cuda.current_stream(q4.device)
     dt = _lib.DTYPE_CODES[q4.dtype]
@@ -256,7 +262,7 @@ def _host_finite(named) -> None:
 
 def _scan_finite(flag: torch.Tensor, *tensors: torch.Tensor) -> None:
     """K0: OR "has a NaN/Inf" of each bf16 [B,H,N,d] tensor into ``flag`` (no host sync)."""
-    st = torch.cuda.current_stream(flag.device)
+    st = torch.cuda.current_stream(tensors[0].device)
     for t in tensors:
         B, H, N, d = t.shape
         _lib.call("spa2_check_finite", _lib.view4(t), _lib.DTYPE_CODES[t.dtype], B, H, N, d, _lib.ptr(flag),
@@ -298,7 +304,7 @@ def _run(q4, k4, v4, bm: BlockMask, qb, counter, flag, check_finite, visit=None)
     ctr = torch.zeros((1,), device=q4.device, dtype=torch.int64) if counter is not None and native else None
     verdict = None
     if flag is not None:
-        verdict = finite_guard.submit(flag, "q, k or v", block=check_finite == "sync")
+        verdict = finite_guard.submit(flag, "q, k or v", block=check_finite == "sync", device=q4.device)
     o, lse = SparseAttentionFunction.apply(q4, k4, v4, lists, 1.0 / math.sqrt(d), ctr, verdict)
     if counter is not None:
         counter.count += int(ctr.item()) if native else bm.kept_blocks()
@@ -381,7 +387,7 @@ def attention_backward(q, k, v, bm: BlockMask, d_out, *, check_finite: bool | st
         raise ValueError(f"mask built for {bm.n_tokens} tokens, inputs have {N}")
     if flag is not None:
         _scan_finite(flag, q4, k4, v4, do4)
-        finite_guard.submit(flag, "q, k, v or d_out", block=check_finite == "sync")
+        finite_guard.submit(flag, "q, k, v or d_out", block=check_finite == "sync", device=q4.device)
     lists = mask_lists(bm, B, H, N)
     scale = 1.0 / math.sqrt(d)
     with torch.no_grad():

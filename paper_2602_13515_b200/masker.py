@@ -240,7 +240,7 @@ def pooled_map(q, k, cfg: SparsityConfig, *, check_finite: bool | str = True) ->
     flag = finite_guard.new_flag(qt.device) if check_finite else None
     probs = _pooled_probs(qt, kt, cfg.b_q, cfg.b_kv, flag)
     if flag is not None:
-        finite_guard.submit(flag, "q or k", block=qb.numpy or check_finite == "sync")
+        finite_guard.submit(flag, "q or k", block=qb.numpy or check_finite == "sync", device=qt.device)
     if qb.rank == 2:
         probs = probs[0, 0]
     if qb.numpy:

@@ -77,8 +77,10 @@ class FiniteGuard:
     """Deferred finiteness verdicts (the reference's ``ensure_finite``, numerics.py:29-32).
 
     The scans run on the GPU (K0 ``spa2_check_finite`` for v / dO, K1's pooling for q / k)
-    and set a device flag; the flag is copied to pinned host memory behind an event.  The
-    verdict is enforced
+    and store 1 into a flag that lives in pinned, device-mapped HOST memory (the kernels write
+    it over PCIe only when they find a NaN/Inf), so no copy is enqueued — a D2H copy on the
+    compute stream would queue behind bulk transfers on the copy engine.  An event recorded
+    after the scans says when the flag is final.  The verdict is enforced
 
     * immediately (``block=True``) for numpy callers, whose results are synchronised
       anyway, and for ``check_finite="sync"``;
@@ -95,15 +97,16 @@ class FiniteGuard:
 
     @staticmethod
     def new_flag(device: torch.device) -> torch.Tensor:
-        return torch.zeros((1,), device=device, dtype=torch.int32)
+        """A zeroed int32 flag in pinned host memory (UVA: the same pointer is valid in
+        kernels).  It stays referenced until its verdict is enforced, so the pinned block is
+        not recycled while a kernel may still write it."""
+        return torch.zeros((1,), dtype=torch.int32, pin_memory=True)
 
-    def submit(self, flag: torch.Tensor, what: str, block: bool) -> tuple:
-        """Register ``flag`` (set on the current stream) as the verdict on ``what``."""
-        host = torch.empty((1,), dtype=torch.int32, pin_memory=True)
-        host.copy_(flag, non_blocking=True)
+    def submit(self, flag: torch.Tensor, what: str, block: bool, device: torch.device | None = None) -> tuple:
+        """Register ``flag`` (written by kernels on the current stream) as the verdict on ``what``."""
         ev = torch.cuda.Event()
-        ev.record(torch.cuda.current_stream(flag.device))
-        entry = (ev, host, what)
+        ev.record(torch.cuda.current_stream(device))
+        entry = (ev, flag, what)
         if block:
             self._verify(entry)
         else:
