@@ -14,10 +14,11 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-KEYMAP = {"k_fwd": "spa2_fwd", "k_fwd3": "spa2_fwd", "k_dq": "spa2_bwd_dq", "k_dq3": "spa2_bwd_dq_delta",
-          "k_dq2": "spa2_bwd_dq", "k_pool_bf16_pipe": "spa2_pooled_scores:pool", "k_select": "spa2_select_scores", "k_dkdv": "spa2_bwd_dkdv", "k_dkdv5": "spa2_bwd_dkdv", "k_delta": "spa2_bwd_delta",
-          "k_pool": "spa2_pooled_map:pool", "k_scores": "spa2_pooled_map:scores",
-          "k_softmax_rows": "spa2_pooled_map:softmax", "k_select": "spa2_select"}
+KEYMAP = {"k_fwd": "spa2_fwd", "k_dq3": "spa2_bwd_dq_delta", "k_dkdv5": "spa2_bwd_dkdv", "k_delta": "spa2_bwd_delta",
+          "k_nonfinite_bf16": "spa2_check_finite", "k_pool_bf16_pipe": "spa2_pooled_scores:pool",
+          "k_pool": "spa2_pooled_map:pool", "k_scores": "spa2_pooled_scores:scores",
+          "k_softmax_rows": "spa2_pooled_map:softmax", "k_select": "spa2_select_scores"}
+PER_STEP = 10  # hot-path kernels of one bench step
 METRICS = {
     "gpu__time_duration.sum": "duration",
     "dram__bytes_read.sum": "dram_read",
@@ -89,7 +90,7 @@ def main():
     ll = read_launches(launches)
     ours = [x for x in ll if x[0].startswith("k_")]
     # the last step's kernels: the final len(recs) of our launches
-    step = ours[-13:] if len(ours) >= 13 else ours
+    step = ours[-PER_STEP:] if len(ours) >= PER_STEP else ours
     tot = sum(t for _, t in step) or 1.0
     kern = {}
     lines = [f"# ncu summary {tag}", "", "Workload: bench.py (Wan2.1-1.3B shape, B=1 H=12 N=32760 d=128, ~95% block "

@@ -22,7 +22,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2602_13515_b200 as spa  # noqa: E402
 from paper_2602_13515_b200 import attention as at  # noqa: E402
 from paper_2602_13515_b200 import masker as mk  # noqa: E402
-from paper_2602_13515_b200.synthetic import wan_like_qkv  # noqa: E402
+from paper_2602_13515_b200 import quality  # noqa: E402
+from paper_2602_13515_b200.synthetic import video_like_qkv, wan_like_qkv  # noqa: E402
 
 B, H, N, D = 1, 12, 32760, 128
 TARGETS = (0.80, 0.85, 0.90, 0.95, 0.97)
@@ -67,8 +68,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="profiles/sweep_r01")
     ap.add_argument("--s", type=float, default=0.9)
+    ap.add_argument("--video", action="store_true", help="correlated video-like inputs (synthetic.video_like_qkv)")
     args = ap.parse_args()
-    q, k, v = wan_like_qkv(B, H, N, D, args.s, seed=0)
+    if args.video:
+        q, k, v = video_like_qkv(B, H, N, D, args.s, seed=0)
+    else:
+        q, k, v = wan_like_qkv(B, H, N, D, args.s, seed=0)
     do = torch.randn_like(q)
     scale = 1.0 / math.sqrt(D)
     t_n = -(-N // 64)
@@ -89,18 +94,17 @@ def main():
             torch.nn.functional.scaled_dot_product_attention(qs, ks, vs).backward(do)
 
     t_dense_cudnn = timed(dense_cudnn, reps=3, warm=1)
-    pm = mk.PooledMap._trusted(mk._pooled_probs(q, k, 128, 64, False)[0], 128, 64, N)
+    pm = mk.PooledMap._trusted(mk._pooled_probs(q, k, 128, 64, None), 128, 64, N)
     rows = []
     for rule in ("top-k", "top-p", "hybrid"):
         for target in TARGETS:
             x = calibrate(rule, pm, target, t_n)
             bm = mask_for(rule, x, pm, t_n)
-            lists = at.mask_lists(bm, B, H, N)
-            _, lse = at.fwd(q, k, v, lists, scale)
-            recall = torch.exp(lse - lse_dense)
+            rep = quality.error_decomposition(q, k, v, bm)  # τ per row + relative-L1 error, no N×N
+            recall = rep.tau
 
             def step():
-                pm2 = mk.PooledMap._trusted(mk._pooled_probs(q, k, 128, 64, False)[0], 128, 64, N)
+                pm2 = mk.PooledMap._trusted(mk._pooled_probs(q, k, 128, 64, None), 128, 64, N)
                 bm2 = mask_for(rule, x, pm2, t_n)
                 l2 = at.build_lists(at._native_keep(bm2, B, H, N))
                 o2, lse2 = at.fwd(q, k, v, l2, scale)
@@ -110,7 +114,7 @@ def main():
             rows.append({"rule": rule, "param": round(x, 6), "target": target, "sparsity": round(bm.sparsity(), 4),
                          "recall_mean": round(float(recall.mean()), 4), "recall_p5": round(float(recall.flatten()
                          .kthvalue(max(1, recall.numel() // 20)).values), 4),
-                         "ms_fwd_bwd": round(t, 4), "speedup_vs_own_dense": round(t_dense_own / t, 2),
+                         "rel_l1_error": round(rep.aggregate, 4), "ms_fwd_bwd": round(t, 4), "speedup_vs_own_dense": round(t_dense_own / t, 2),
                          "speedup_vs_cudnn_dense": round(t_dense_cudnn / t, 2)})
             print(rows[-1], flush=True)
     meta = {"shape": dict(B=B, H=H, N=N, d=D), "offset_scale": args.s, "dense_own_ms": t_dense_own,
@@ -119,12 +123,16 @@ def main():
     os.makedirs(os.path.dirname(args.out) or ".", exist_ok=True)
     with open(args.out + ".json", "w") as f:
         json.dump({"meta": meta, "rows": rows}, f, indent=1)
-    lines = ["# Config 3: sparsity sweep (Wan2.1-1.3B shape, B=1 H=12 N=32760 d=128, synthetic s=%.2f)" % args.s, "",
+    lines = ["# Config 3: sparsity sweep (Wan2.1-1.3B shape, B=1 H=12 N=32760 d=128, %s synthetic s=%.2f)"
+             % ("video-like correlated" if args.video else "block-offset", args.s), "",
+             "Recall τ̄ and the relative-L1 error Σ|o − o_s|/Σ|o| from paper_2602_13515_b200.quality (dense and "
+             "sparse forwards, no N×N map; analysis.py:37-65, flowmatch.py:408-434).", "",
              f"Dense fwd+bwd: own kernels (all blocks) {t_dense_own:.2f} ms, cuDNN SDPA {t_dense_cudnn:.2f} ms.", "",
-             "| rule | param | block sparsity | mask recall (mean) | recall p5 | fwd+bwd ms (incl. masker) | "
-             "vs own dense | vs cuDNN dense |", "|---|---|---|---|---|---|---|---|"]
+             "| rule | param | block sparsity | mask recall τ̄ (mean) | recall p5 | rel. L1 error | fwd+bwd ms (incl. "
+             "masker) | vs own dense | vs cuDNN dense |", "|---|---|---|---|---|---|---|---|---|"]
     for r in rows:
         lines.append(f"| {r['rule']} | {r['param']} | {r['sparsity']} | {r['recall_mean']} | {r['recall_p5']} | "
+                     f"{r['rel_l1_error']} | "
                      f"{r['ms_fwd_bwd']} | {r['speedup_vs_own_dense']}x | {r['speedup_vs_cudnn_dense']}x |")
     with open(args.out + ".md", "w") as f:
         f.write("\n".join(lines) + "\n")
