@@ -31,6 +31,10 @@
 #include "ptx.cuh"
 #include "tma_host.h"
 
+#ifdef SPA2_TRACE
+__device__ unsigned long long g_spa2_trace[32 * SPA2_TRACE_SLOTS];  // kinds 0-15 dQ, 16-31 dK/dV
+#endif
+
 namespace spa2 {
 namespace {
 
@@ -355,9 +359,12 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
     cursor_init(c, p, p.T_m);
     if (warp == 1) {
       for (; c.valid; cursor_next(c, p, p.T_m)) {
+        SPA2_TR(9, c.g);
         if (c.t == 0) {
+          SPA2_TR(6, c.g);
           mbar_wait(qs_full, (uint32_t)c.it & 1u);
           if (c.it >= 1) mbar_wait(qd_free, (uint32_t)(c.it - 1) & 1u);
+          SPA2_TR(10, c.g);
           tc_fence_after();
 #pragma unroll
           for (int ks = 0; ks < HD / 16; ++ks) {
@@ -388,6 +395,7 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
                           dK + (uint64_t)((((ks * 16 / 64) * BKV * 128 + (ks * 16 % 64) * 2)) >> 4), idS, ks > 0 ? 1u : 0u);
         }
         mma_commit_w(&s_full[b]);
+        SPA2_TR(0, c.g);
         if (c.t == c.n - 1) mma_commit_w(qd_free);
       }
     } else {
@@ -395,13 +403,14 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
       // COMPLETE: it overwrites the TMEM columns dQ(g-2) reads dS from).  One warp issuing
       // both in the order dQ(g-2), dP(g) avoids that wait but measured 12 % slower.
       auto issue_dp = [&](const Cursor& cc) {
-        if (cc.t == 0) mbar_wait(qd_ready, (uint32_t)cc.it & 1u);
+        SPA2_TR(7, cc.g);
         const int b = cc.g & 1, sv = cc.g % NV;
         if (cc.g >= 2) mbar_wait(&dq_done[b], (uint32_t)((cc.g - 2) >> 1) & 1u);
         mbar_wait(&v_full[sv], (uint32_t)(cc.g / NV) & 1u);
-        tc_fence_after();
         const uint64_t dV = dV0 + (uint64_t)sv * KV16;
         const uint32_t sb = tbase + C::SDP_COL + (uint32_t)(b * 128) + 64u;
+        if (cc.t == 0) mbar_wait(qd_ready, (uint32_t)cc.it & 1u);
+        tc_fence_after();
 #ifdef SPA2_MMA_BATCH
         if constexpr (HD == 128) {
           mma_bf16_ts_k8_w<8u, 2ull, (uint64_t)(BKV * 128 / 16)>(sb, tbase + C::DO_COL, dV, idS, 0u);
@@ -414,10 +423,12 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
                           dV + (uint64_t)((((ks * 16 / 64) * BKV * 128 + (ks * 16 % 64) * 2)) >> 4), idS, ks > 0 ? 1u : 0u);
         }
         mma_commit_w(&dp_full[b]);
+        SPA2_TR(1, cc.g);
         mma_commit_w(&v_empty[sv]);
         if (cc.t == cc.n - 1) mma_commit_w(qd_free);
       };
       auto issue_dq = [&](const Cursor& cc) {
+        SPA2_TR(8, cc.g);
         const int b = cc.g & 1, sk = cc.g % NK;
         if (cc.t == 0 && cc.it >= 1) mbar_wait(acc_empty, (uint32_t)(cc.it - 1) & 1u);
         mbar_wait(&ds_full[b], (uint32_t)(cc.g >> 1) & 1u);
@@ -436,6 +447,7 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
                           (cc.t > 0 || ks > 0) ? 1u : 0u);
         }
         mma_commit_w(&dq_done[b]);
+        SPA2_TR(2, cc.g);
         mma_commit_w(&k_empty[sk]);
         if (cc.t == cc.n - 1) mma_commit_w(acc_full);
       };
@@ -477,6 +489,7 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
         if (t + 1 < m.n) j_next = __ldg(p.idx + m.beg + t + 1);
         const uint32_t sb = tbase + lane_off + C::SDP_COL + (uint32_t)(b * 128);
         mbar_wait(&s_full[b], (uint32_t)(g >> 1) & 1u);
+        if (warp == 2) SPA2_TR(3, g);
         tc_fence_after();
         uint32_t sr[CPT];
         if constexpr (CPT == 32) tmem_ld32(sb + (uint32_t)col0, sr);
@@ -505,6 +518,7 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
             if (col0 + c >= kv_tail) pv[c] = 0.f;
         }
         mbar_wait(&dp_full[b], (uint32_t)(g >> 1) & 1u);
+        if (warp == 2) SPA2_TR(4, g);
         tc_fence_after();
         uint32_t dr[CPT];
         if constexpr (CPT == 32) tmem_ld32(sb + 64u + (uint32_t)col0, dr);
@@ -520,6 +534,7 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
         if constexpr (CPT == 32) tmem_st16(sb + 64u + (uint32_t)col0, pk);  // dS over the dP columns read
         else tmem_st8(sb + 64u + (uint32_t)col0, pk);
         tmem_st_wait();
+        if (warp == 2) SPA2_TR(5, g);
         tc_fence_before();
         mbar_arrive(&ds_full[b]);
       }
@@ -736,7 +751,12 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
       // S (needs Q) and dP (needs dO) of tile g into TMEM buffer g&1, each as soon as its
       // operand has landed (Q and dO live in separate ring slots)
       for (; c.valid; cursor_next(c, p, p.T_n)) {
-        if (c.t == 0) mbar_wait(kv_full, (uint32_t)c.it & 1u);
+        SPA2_TR(25, c.g);
+        if (c.t == 0) {
+          SPA2_TR(22, c.g);
+          mbar_wait(kv_full, (uint32_t)c.it & 1u);
+          SPA2_TR(26, c.g);
+        }
         const uint32_t b = (uint32_t)(c.g & 1);
         if (c.g >= 2) mbar_wait(&sdp_read[b], (uint32_t)((c.g - 2) >> 1) & 1u);  // buffer b read out
         const int uq = 2 * c.g, ud = uq + 1;
@@ -776,6 +796,7 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
           }
         }
         mma_commit_w(&dp_full[b]);
+        SPA2_TR(16, c.g);
         mma_commit_w(&sl_empty[ud % NSL]);  // dP(g) no longer reads dO(g) once complete
         if (c.t == c.n - 1) mma_commit_w(kv_empty);  // K_j / V_j are only read by S and dP
       }
@@ -811,6 +832,7 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
           mma_bf16_w(acc + 64, dQm + (uint64_t)(ks * 128), dDSm + pbo + (uint64_t)(ks * 128), idT, (!first || ks > 0) ? 1u : 0u);
 #endif
         mma_commit_w(&ds_free[pb]);
+        SPA2_TR(18, c.g);
         mma_commit_w(&sl_empty[uq % NSL]);  // dKᵀ(g) was the other reader of Q(g)
         if (c.t == c.n - 1) mma_commit_w(&acc_full[c.it & 1]);
       }
@@ -842,6 +864,7 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
         float lse2_n = 0.f, dlt_n = 0.f;
         if (t + 1 < m.n) load_stats(t + 1, lse2_n, dlt_n);  // prefetch the next tile's row statistics
         mbar_wait(&s_full[b], (uint32_t)(g >> 1) & 1u);
+        if (warp == 2) SPA2_TR(19, g);
         tc_fence_after();
         uint32_t sr[CPT];
         if constexpr (CPT == 32) tmem_ld32(tbase + lane_off + C::S_COL + b * 64 + col0, sr);
@@ -873,6 +896,7 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
         fence_proxy_async_smem();
         mbar_arrive(&p_full[pb]);
         mbar_wait(&dp_full[b], (uint32_t)(g >> 1) & 1u);
+        if (warp == 2) SPA2_TR(20, g);
         tc_fence_after();
         uint32_t dr[CPT];
         if constexpr (CPT == 32) tmem_ld32(tbase + lane_off + C::DP_COL + b * 64 + col0, dr);
@@ -893,6 +917,7 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
           st_shared_v4(sDS + off, pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
         }
         fence_proxy_async_smem();
+        if (warp == 2) SPA2_TR(21, g);
         mbar_arrive(&ds_full[pb]);
         lse2 = lse2_n;
         dlt = dlt_n;
@@ -1136,3 +1161,14 @@ extern "C" int spa2_bwd(spa2_view q, spa2_view k, spa2_view v, spa2_view o, spa2
   return spa2_bwd_dkdv(q, k, v, dout, lse, delta, dk, dv, dtype, B, H, N, d, b_q, b_kv, col_ptr, col_idx, col_order,
                        scale, stream);
 }
+
+#ifdef SPA2_TRACE
+// diagnostic (trace builds only): copy and clear the pipeline trace of CTA 0
+extern "C" int spa2_trace_fetch(unsigned long long* host_dst) {
+  SPA2_CUDA_TRY(cudaDeviceSynchronize());
+  SPA2_CUDA_TRY(cudaMemcpyFromSymbol(host_dst, g_spa2_trace, sizeof(g_spa2_trace)));
+  static unsigned long long zeros[32 * SPA2_TRACE_SLOTS];
+  SPA2_CUDA_TRY(cudaMemcpyToSymbol(g_spa2_trace, zeros, sizeof(g_spa2_trace)));
+  return SPA2_OK;
+}
+#endif

@@ -51,6 +51,21 @@ __device__ __forceinline__ double to_f64<__nv_bfloat16>(__nv_bfloat16 x) {
 template <>
 __device__ __forceinline__ double to_f64<__half>(__half x) { return (double)__half2float(x); }
 
+// ---- diagnostic pipeline trace (compiled only with -DSPA2_TRACE, see tools/trace_bwd.py) ----
+// SPA2_TR(kind, idx): clock64 of event `kind` for tile / item `idx` of CTA 0, lane 0 of the
+// calling warp, into a per-translation-unit device array fetched by spa2_trace_fetch().
+#ifdef SPA2_TRACE
+#define SPA2_TRACE_SLOTS 2048
+#define SPA2_TR(kind, idx)                                                                             \
+  do {                                                                                                 \
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && (idx) < SPA2_TRACE_SLOTS)                        \
+      g_spa2_trace[(kind) * SPA2_TRACE_SLOTS + (idx)] = clock64();                                     \
+  } while (0)
+#else
+#define SPA2_TR(kind, idx) \
+  do {                     \
+  } while (0)
+#endif
 // ---- programmatic dependent launch (PDL) ---------------------------------------------
 // Hot-path kernels are launched with programmatic stream serialization: the next kernel's
 // CTAs may be scheduled (and run their prologue: barrier init, TMEM alloc, descriptor
