@@ -621,18 +621,25 @@ struct DkvRoles {
   static constexpr int CPT = 256 / EWW;          // S/dP columns per elementwise thread
 };
 
-template <int HD, int NSL_ = 5, int NPB_ = 1>
+#ifndef SPA2_DKDV_NSL
+#define SPA2_DKDV_NSL 5  // 32 KB Q / dO operand slots
+#endif
+#ifndef SPA2_DKDV_NKV
+#define SPA2_DKDV_NKV 1  // [K | V] item buffers (2: the next item's K/V load overlaps this item)
+#endif
+template <int HD, int NSL_ = SPA2_DKDV_NSL, int NPB_ = 1, int NKV_ = SPA2_DKDV_NKV>
 struct Dkv5Cfg {
   static constexpr int NSL = NSL_;  // 32 KB operand slots: Q(g) -> slot 2g mod NSL, dO(g) -> slot 2g+1 mod NSL
   static constexpr int NPB = NPB_;  // [P | dS] buffers
+  static constexpr int NKV = NKV_;  // [K | V] buffers: item it uses buffer it % NKV
   static constexpr int KV_BYTES = BKV * HD * 2;
   static constexpr int Q_BYTES = BQ * HD * 2;
   static constexpr int PB = BQ * BKV * 2;
-  static constexpr int OFF_KV = 0;                         // [K | V] of the current item
-  static constexpr int OFF_SL = 2 * KV_BYTES;              // [NSL] Q / dO operand slots
+  static constexpr int OFF_KV = 0;                         // [NKV][K | V]
+  static constexpr int OFF_SL = NKV * 2 * KV_BYTES;        // [NSL] Q / dO operand slots
   static constexpr int OFF_PDS = OFF_SL + NSL * Q_BYTES;   // [NPB][P | dS]
   static constexpr int OFF_BAR = OFF_PDS + NPB * 2 * PB;
-  static constexpr int NUM_BARS = 2 + 2 * NSL + 6 + 4 * NPB + 4;
+  static constexpr int NUM_BARS = 2 * NKV + 2 * NSL + 6 + 4 * NPB + 4;
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + kSmemAlignSlack;
   static constexpr uint32_t S_COL = 0, DP_COL = 128, ACC_COL = 256;
 };
@@ -642,7 +649,7 @@ struct Dkv5Cfg {
 // different warps (Q: S and dKᵀ, dO: dP and dVᵀ), so its slot is released by two commits, one
 // per issuer; the dVᵀ issuer also waits for dO(g) to land (P(g) existing only proves S(g)
 // finished).  P and dS share one smem buffer.
-template <int HD, int EWW, int NSL_ = 5, int NPB_ = 1>
+template <int HD, int EWW, int NSL_ = SPA2_DKDV_NSL, int NPB_ = 1>
 __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
     k_dkdv5(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
            const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO, const BwdParams p) {
@@ -655,9 +662,10 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* const smem = smem_align_1k(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
-  uint64_t* kv_full = bars;             // K/V of item `it` landed
-  uint64_t* kv_empty = kv_full + 1;     // last S/dP MMA of item `it` done: K/V slot reusable
-  uint64_t* sl_full = kv_empty + 1;     // [NSL] operand slot holds operand u (Q(g): u=2g, dO(g): u=2g+1)
+  constexpr int NKV = C::NKV;
+  uint64_t* kv_full = bars;             // [NKV] K/V of item `it` landed in buffer it % NKV
+  uint64_t* kv_empty = kv_full + NKV;   // [NKV] last S/dP MMA of item `it` done: K/V buffer reusable
+  uint64_t* sl_full = kv_empty + NKV;   // [NSL] operand slot holds operand u (Q(g): u=2g, dO(g): u=2g+1)
   uint64_t* sl_empty = sl_full + NSL;   // [NSL] both MMAs reading operand u are done
   uint64_t* s_full = sl_empty + NSL;    // [2] S of tile g in TMEM buffer g&1
   uint64_t* dp_full = s_full + 2;       // [2] dP of tile g
@@ -672,8 +680,10 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
 
   const int warp = (int)warp_id(), lane = (int)lane_id();
   if (threadIdx.x == 0) {
-    mbar_init(kv_full, 2);  // two producers: warp 0 (K, Q) and warp PROD2 (V, dO)
-    mbar_init(kv_empty, 1);
+    for (int s = 0; s < NKV; ++s) {
+      mbar_init(&kv_full[s], 2);  // two producers: warp 0 (K, Q) and warp PROD2 (V, dO)
+      mbar_init(&kv_empty[s], 1);
+    }
     for (int s = 0; s < NSL; ++s) {
       mbar_init(&sl_full[s], 1);
       mbar_init(&sl_empty[s], 2);  // released by the S/dP issuer AND the dVᵀ/dKᵀ issuer
@@ -717,9 +727,10 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
         const Item m = get_item(p, wi, p.T_n);
         if (m.n == 0) continue;
         const int hh = m.bh % p.H, bb = m.bh / p.H;
-        if (it >= 1) mbar_wait(kv_empty, (uint32_t)(it - 1) & 1u);
-        mbar_expect_tx(kv_full, C::KV_BYTES);
-        tma_load_5d(kv_dst, tmKV, kv_full, 0, m.blk * BKV, 0, hh, bb);
+        const int kb = it % NKV;
+        if (it >= NKV) mbar_wait(&kv_empty[kb], (uint32_t)((it - NKV) / NKV) & 1u);
+        mbar_expect_tx(&kv_full[kb], C::KV_BYTES);
+        tma_load_5d(kv_dst + kb * 2 * C::KV_BYTES, tmKV, &kv_full[kb], 0, m.blk * BKV, 0, hh, bb);
         for (int t = 0; t < m.n; ++t, ++g) {
           const int i = p.idx[m.beg + t];
           const int u = 2 * g + (second ? 1 : 0);  // operand index: Q(g) even, dO(g) odd
@@ -738,8 +749,7 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
     // smem) then dKᵀ += Q_iᵀ dS (after dS).  Warp-collective issue, warp-uniform descriptors.
     constexpr uint32_t idS = idesc_bf16(BQ, BKV, false, false);
     constexpr uint32_t idT = idesc_bf16(HD, BKV, true, true);
-    const uint64_t dK = sw128_desc(smem_u32(smem + C::OFF_KV), 16, 1024);
-    const uint64_t dV = dK + (uint64_t)(C::KV_BYTES >> 4);
+    const uint64_t dK0 = sw128_desc(smem_u32(smem + C::OFF_KV), 16, 1024);
     const uint64_t dSLk0 = sw128_desc(smem_u32(smem + C::OFF_SL), 16, 1024);        // K-major Q / dO slots
     const uint64_t dSLm0 = sw128_desc(smem_u32(smem + C::OFF_SL), BQ * 128, 1024);  // MN-major Q / dO slots
     const uint64_t dPm = sw128_desc(smem_u32(smem + C::OFF_PDS), BQ * 128, 1024);   // MN-major P
@@ -754,9 +764,11 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
         SPA2_TR(25, c.g);
         if (c.t == 0) {
           SPA2_TR(22, c.g);
-          mbar_wait(kv_full, (uint32_t)c.it & 1u);
+          mbar_wait(&kv_full[c.it % NKV], (uint32_t)(c.it / NKV) & 1u);
           SPA2_TR(26, c.g);
         }
+        const uint64_t dK = dK0 + (uint64_t)((c.it % NKV) * 2 * C::KV_BYTES >> 4);
+        const uint64_t dV = dK + (uint64_t)(C::KV_BYTES >> 4);
         const uint32_t b = (uint32_t)(c.g & 1);
         if (c.g >= 2) mbar_wait(&sdp_read[b], (uint32_t)((c.g - 2) >> 1) & 1u);  // buffer b read out
         const int uq = 2 * c.g, ud = uq + 1;
@@ -798,7 +810,7 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
         mma_commit_w(&dp_full[b]);
         SPA2_TR(16, c.g);
         mma_commit_w(&sl_empty[ud % NSL]);  // dP(g) no longer reads dO(g) once complete
-        if (c.t == c.n - 1) mma_commit_w(kv_empty);  // K_j / V_j are only read by S and dP
+        if (c.t == c.n - 1) mma_commit_w(&kv_empty[c.it % NKV]);  // K_j / V_j are only read by S and dP
       }
     } else {
       for (; c.valid; cursor_next(c, p, p.T_n)) {
