@@ -50,6 +50,10 @@ int spa2_probe_tmem_rate(int reps, int mode, int warps, int ctas, unsigned long 
 int spa2_probe_tma_rate2(const void* buf, long long rows, int box_rows, int chunks, int stages, int issuers,
                          int mode, int iters, int ctas, unsigned long long* cycles, void* stream);
 
+/* Diagnostic: fp32 reduction (mode 0, red.global.add.v4.f32) or store (mode 1) throughput of
+ * `ctas` CTAs each adding `tiles` 128x128 fp32 tiles into a rotating set of `nslots` tiles of dst. */
+int spa2_probe_red_rate(float* dst, int tiles, int nslots, int ctas, int mode, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

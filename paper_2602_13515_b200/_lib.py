@@ -77,6 +77,7 @@ DIAG_SIGNATURES = {
     "spa2_probe_mbar_latency": ([_I32, _I32, _I32, _P, _P], _I32),
     "spa2_probe_tmem_rate": ([_I32, _I32, _I32, _I32, _P, _P], _I32),
     "spa2_probe_tma_rate2": ([_P, ctypes.c_longlong, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P, _P], _I32),
+    "spa2_probe_red_rate": ([_P, _I32, _I32, _I32, _I32, _P], _I32),
 }
 
 # Kernels each entry point launches (for the bench's gpu_launches accounting).

@@ -676,3 +676,47 @@ extern "C" int spa2_probe_mbar_latency(int reps, int mode, int threads, unsigned
   SPA2_LAUNCH_CHECK();
   return SPA2_OK;
 }
+
+namespace spa2 {
+namespace {
+// fp32 reduction throughput into L2: each CTA adds `tiles` 128 x 128 fp32 tiles (one row of 128
+// floats = 512 B per thread, red.global.add.v4.f32) into a rotating set of `nslots` tiles of `dst`
+// (the access pattern of a dQ partial per kept tile in a fused backward).  mode 1: plain
+// st.global.v4 instead (store bandwidth reference).
+__global__ void __launch_bounds__(128) k_red_rate(float* __restrict__ dst, int tiles, int nslots, int mode) {
+  // mode 0/1: thread = row (the TMEM lane layout of a partial); mode 2: coalesced — each warp
+  // covers 512 contiguous bytes per instruction (a transposed / staged partial)
+  const int row = mode == 2 ? (threadIdx.x / 32) * 32 + 0 : threadIdx.x;
+  float v = 1.0f + 1e-3f * (float)threadIdx.x;
+  for (int t = 0; t < tiles; ++t) {
+    const int slot = (blockIdx.x * 7 + t * 13) % nslots;
+    if (mode == 2) {
+      float* base = dst + (int64_t)slot * 128 * 128;
+#pragma unroll 8
+      for (int i = 0; i < 32; ++i) {  // 128 threads x 16 B x 32 = 64 KB
+        float* p = base + (int64_t)(i * 128 + threadIdx.x) * 4;
+        asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v), "f"(v), "f"(v), "f"(v)
+                     : "memory");
+      }
+      continue;
+    }
+    float* p = dst + ((int64_t)slot * 128 + row) * 128;
+#pragma unroll 8
+    for (int c = 0; c < 128; c += 4) {
+      if (mode == 0)
+        asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p + c), "f"(v), "f"(v), "f"(v), "f"(v)
+                     : "memory");
+      else
+        asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p + c), "f"(v), "f"(v), "f"(v), "f"(v)
+                     : "memory");
+    }
+  }
+}
+}  // namespace
+}  // namespace spa2
+
+extern "C" int spa2_probe_red_rate(float* dst, int tiles, int nslots, int ctas, int mode, void* stream) {
+  spa2::k_red_rate<<<ctas, 128, 0, (cudaStream_t)stream>>>(dst, tiles, nslots, mode);
+  SPA2_LAUNCH_CHECK();
+  return SPA2_OK;
+}
