@@ -23,36 +23,46 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--rounds", type=int, default=5)
     args = ap.parse_args()
     N, D, H = 75600, 128, 40
     cfg = spa.SparsityConfig(0.03, 0.16, 128, 64)
     q, k, v = wan_like_qkv(1, H, N, D, 0.8, seed=40)
     do = torch.randn(q.shape, device="cuda", generator=torch.Generator(device="cuda").manual_seed(41)).to(q.dtype)
-    results = []
+    steps = {}
     for P in (1, 2, 4, 8):
         h = H // P
         qs, ks, vs, dos = (t[:, :h].contiguous() for t in (q, k, v, do))
 
-        def step():
+        def step(qs=qs, ks=ks, vs=vs, dos=dos):
             a, b, c = (t.detach().requires_grad_(True) for t in (qs, ks, vs))
             res = spa.sparse_attention(a, b, c, cfg)
             res.out.backward(dos)
             return res
 
-        res = step()
-        for _ in range(args.warmup):
-            step()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(args.steps):
-            step()
-        e1.record()
-        torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / args.steps
+        steps[P] = (h, step, step().mask_used.sparsity())
+    # the four per-rank workloads are timed in interleaved rounds (median over rounds), so every
+    # P sees the same clock / power state instead of one long run per P
+    times = {P: [] for P in steps}
+    for _ in range(args.rounds):
+        for P, (h, step, _) in steps.items():
+            for _ in range(args.warmup):
+                step()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(args.steps):
+                step()
+            e1.record()
+            torch.cuda.synchronize()
+            times[P].append(e0.elapsed_time(e1) / args.steps)
+    spa.check_pending()
+    results = []
+    for P, (h, _, sp) in steps.items():
+        ms = sorted(times[P])[len(times[P]) // 2]
         dense = 14 * h * N * N * D
-        results.append({"gpus": P, "heads_per_gpu": h, "ms_per_step": ms, "block_sparsity": res.mask_used.sparsity(),
-                        "dense_equiv_tflops_per_gpu": dense / ms / 1e9})
+        results.append({"gpus": P, "heads_per_gpu": h, "ms_per_step": ms, "block_sparsity": sp,
+                        "dense_equiv_tflops_per_gpu": dense / ms / 1e9, "rounds_ms": [round(t, 3) for t in times[P]]})
     base = results[0]["ms_per_step"]
     for r in results:
         r["speedup_vs_1gpu"] = base / r["ms_per_step"]
