@@ -28,7 +28,6 @@ import json
 import math
 import os
 import statistics
-import subprocess
 import sys
 import time
 
@@ -201,55 +200,65 @@ def cpu_reference(steps: int, warmup: int, w=WORKLOAD, as_shipped: bool = True):
 # clocks
 # ---------------------------------------------------------------------------------------
 class ClockSampler:
-    FIELDS = ["timestamp", "clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
-              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
-              "clocks_event_reasons.sw_power_cap"]
+    """SM clock and clock-event (throttle) reasons sampled DURING the timed region: NVML polled
+    every 2 ms from a background thread (the timed region of a 20-step run is ~30 ms, below
+    nvidia-smi's sampling period); nvidia-smi as the fallback when NVML is unavailable."""
+
     NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, device_uuid: str | None):
-        self.proc = None
-        self.path = os.path.join("/tmp", f"spa2_clocks_{os.getpid()}.csv")
-        cmd = ["nvidia-smi", f"--query-gpu={','.join(self.FIELDS)}", "--format=csv,noheader,nounits", "-lms", "100"]
-        if device_uuid:
-            cmd[1:1] = ["-i", device_uuid]
+    def __init__(self, device_index: int):
+        import threading
+
+        self.samples = []  # (t, sm_mhz, max_mhz, reasons bitmask)
+        self.stop_flag = False
+        self.err = None
         try:
-            self.fh = open(self.path, "w")
-            self.proc = subprocess.Popen(cmd, stdout=self.fh, stderr=subprocess.DEVNULL)
-        except Exception:
-            self.proc = None
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            uuid = None
+            try:
+                import torch
+
+                uuid = "GPU-" + str(torch.cuda.get_device_properties(device_index).uuid)
+                self.h = pynvml.nvmlDeviceGetHandleByUUID(uuid)
+            except Exception:
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.bits = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                         "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                         "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                         "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+        except Exception as e:  # pragma: no cover
+            self.nvml = None
+            self.err = str(e)[:120]
+            return
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.thread.start()
+
+    def _run(self):
+        nv = self.nvml
+        while not self.stop_flag:
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((time.time(), sm, rs))
+            except Exception as e:  # pragma: no cover
+                self.err = str(e)[:120]
+            time.sleep(0.002)
 
     def stop(self, t_start: float, t_end: float):
-        if self.proc is None:
-            return None
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        self.fh.close()
-        sm, mx, reasons, n_all = [], [], set(), 0
-        with open(self.path) as f:
-            for line in f:
-                parts = [p.strip() for p in line.split(",")]
-                if len(parts) != len(self.FIELDS):
-                    continue
-                n_all += 1
-                try:
-                    ts = _dt.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
-                except ValueError:
-                    continue
-                if not (t_start - 0.05 <= ts <= t_end + 0.05):
-                    continue
-                sm.append(float(parts[1]))
-                mx.append(float(parts[2]))
-                for name, val in zip(self.NAMES, parts[3:]):
-                    if val.lower() == "active":
-                        reasons.add(name)
-        os.unlink(self.path)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "samples_total": n_all}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if self.nvml is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "error": self.err}
+        self.stop_flag = True
+        self.thread.join(timeout=2)
+        win = [s for s in self.samples if t_start <= s[0] <= t_end]
+        if not win:  # a very short region: the samples closest to it
+            win = sorted(self.samples, key=lambda s: min(abs(s[0] - t_start), abs(s[0] - t_end)))[:3]
+        reasons = sorted({n for _, _, rs in win for n, bit in self.bits.items() if rs & bit})
+        return {"sm_mhz": statistics.median(s[1] for s in win) if win else None, "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(win), "source": "NVML, 2 ms polling"}
 
 
 # ---------------------------------------------------------------------------------------
@@ -331,13 +340,8 @@ def gpu_arm(args, rank: int, world: int, dev):
 
     # ---- the timed region: K steps back to back, no instrumentation between launches ----
     launches0 = _lib.STATS.launches
-    uuid = None
-    try:
-        uuid = "GPU-" + str(torch.cuda.get_device_properties(dev).uuid)
-    except Exception:
-        pass
-    sampler = ClockSampler(uuid)
-    time.sleep(0.6)  # nvidia-smi start-up
+    sampler = ClockSampler(dev.index if dev.index is not None else 0)
+    time.sleep(0.05)
     barrier()
     torch.cuda.synchronize()
     t_wall0 = time.time()

@@ -51,9 +51,9 @@ def main():
                 seen = {}
                 orig = spa.attention._run
 
-                def spy(q4, k4, v4, bm, qb, counter, visit=None):
+                def spy(q4, k4, v4, bm, *args, **kw):
                     seen.setdefault("sp", bm.sparsity())
-                    return orig(q4, k4, v4, bm, qb, counter, visit)
+                    return orig(q4, k4, v4, bm, *args, **kw)
                 spa.attention._run = spy
                 try:
                     student(x_t, t, text)
