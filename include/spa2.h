@@ -99,6 +99,9 @@ int spa2_select_scores(const double* scores, int64_t rows, int64_t t_n, int64_t 
  *   row_order int32 [bh*t_m], col_order int32 [bh*t_n]: rows/columns sorted by
  *            descending list length (longest-first launch order for load balance).
  * nnz <= bh*t_m*t_n; pass buffers of that size when nnz is unknown.
+ * keep values: 0 dropped, 1 kept; for masks on a 64-row query grid (b_q = 64) paired into
+ * 128-row query blocks: 2 = only the top half (rows 0-63) keeps the tile, 3 = only the
+ * bottom half; entries then carry (value - 1) in bits 30-31 (block index in bits 0-29).
  * scratch: int32 >= bh*(t_m + t_n) elements. */
 int spa2_build_lists(const uint8_t* keep, int64_t bh, int64_t t_m, int64_t t_n, int32_t* row_ptr,
                      int32_t* row_idx, int32_t* col_ptr, int32_t* col_idx, int32_t* row_order,
@@ -106,7 +109,9 @@ int spa2_build_lists(const uint8_t* keep, int64_t bh, int64_t t_m, int64_t t_n, 
 
 /* ---- K4: block-sparse forward ------------------------------------------------------
  * Replaces attention.sparse_attention_with_mask (attention.py:73-114).
- * q, k, v, o: bf16 [B,H,N,d], d in {64, 128}; b_q = 128; b_kv in {64}.
+ * q, k, v, o: bf16 [B,H,N,d], d in {64, 128}; b_kv = 64; b_q = 128 (lists from a 0/1 keep)
+ * or b_q = 64 (lists carrying half-block codes, see spa2_build_lists: rows of the half that
+ * does not keep a tile get P = 0 for it).  The same applies to the backward entry points.
  * lse: float32 [B*H, N], natural log (attention.py:113).  o/lse rows are written for
  * every query block (each row keeps >= 1 block, masker.py:78-79).
  * row_ptr/row_idx/row_order from spa2_build_lists; scale = 1/sqrt(d) (attention.py:86).

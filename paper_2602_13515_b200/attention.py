@@ -83,33 +83,56 @@ class BlockLists:
     col_idx: torch.Tensor
     col_order: torch.Tensor
     shape: tuple  # (B, H, T_m, T_n)
+    half: bool = False  # entries carry half-block codes (a b_q = 64·odd mask): kernels take b_q = 64
 
 
 def _native_keep(bm: BlockMask, B: int, H: int, N: int) -> torch.Tensor:
-    """keep at the kernel grid (128, 64) as uint8 [B, H, T_m, T_n] (exact refinement)."""
+    """keep at the kernel grid (128, 64) as uint8 codes [B, H, T_m, T_n]: 0 dropped, 1 kept.
+
+    Masks on coarser grids (b_q ∈ 128ℕ, b_kv ∈ 64ℕ) are refined exactly.  Masks with
+    b_q = 64·odd (e.g. the b_q = 64 of SURVEY §7) pair two 64-row mask rows per 128-row kernel
+    query block: code 1 = both halves keep the tile, 2 = only the top half (rows 0-63),
+    3 = only the bottom half — the kernels give the other half's rows P = 0 for that tile
+    (list entries carry the code in bits 30-31, see csrc/common.cuh)."""
     t_m, t_n = num_blocks(N, BQ), num_blocks(N, BKV)
     keep = bm.dev
     if keep.dim() == 2:
         keep = keep.view(1, 1, *keep.shape)
+    codes = None
     if (bm.b_q, bm.b_kv) != (BQ, BKV):
         if bm.b_q % BQ == 0 and bm.b_kv % BKV == 0:
             keep = keep.repeat_interleave(bm.b_q // BQ, dim=-2).repeat_interleave(bm.b_kv // BKV, dim=-1)
             keep = keep[..., :t_m, :t_n]
+        elif bm.b_q % (BQ // 2) == 0 and bm.b_kv % BKV == 0:
+            t_h = num_blocks(N, BQ // 2)  # 64-row halves
+            k64 = keep.repeat_interleave(bm.b_q // (BQ // 2), dim=-2).repeat_interleave(bm.b_kv // BKV, dim=-1)
+            k64 = k64[..., :t_h, :t_n]
+            if t_h % 2:  # the last query block has no bottom half inside N
+                k64 = torch.cat([k64, torch.zeros_like(k64[..., :1, :])], dim=-2)
+            top, bot = k64[..., 0::2, :], k64[..., 1::2, :]
+            codes = torch.where(top & bot, 1, torch.where(top, 2, torch.where(bot, 3, 0))).to(torch.uint8)
         elif bool(keep.all()):
             keep = torch.ones((*keep.shape[:2], t_m, t_n), device=keep.device, dtype=torch.bool)
         else:
-            raise ValueError(f"GPU kernels use b_q={BQ}, b_kv={BKV}; mask geometry (b_q={bm.b_q}, b_kv={bm.b_kv}) "
-                             "is not an exact multiple of it")
-    if keep.shape[0] != B or keep.shape[1] != H:
-        if keep.shape[0] == 1 and keep.shape[1] == 1:
-            keep = keep.expand(B, H, t_m, t_n)
+            raise ValueError(f"GPU kernels use b_q={BQ} (or 64), b_kv={BKV}; mask geometry (b_q={bm.b_q}, "
+                             f"b_kv={bm.b_kv}) is not a multiple of it")
+    if codes is None:
+        codes = keep.view(torch.uint8) if keep.dtype == torch.bool else keep.to(torch.uint8)
+    if codes.shape[0] != B or codes.shape[1] != H:
+        if codes.shape[0] == 1 and codes.shape[1] == 1:
+            codes = codes.expand(B, H, t_m, t_n)
         else:
-            raise ValueError(f"mask batch/head dims {tuple(keep.shape[:2])} do not match inputs ({B}, {H})")
-    return keep.contiguous().view(torch.uint8)
+            raise ValueError(f"mask batch/head dims {tuple(codes.shape[:2])} do not match inputs ({B}, {H})")
+    return codes.contiguous()
 
 
-def build_lists(keep_u8: torch.Tensor) -> BlockLists:
-    """K3 on a uint8 [B, H, T_m, T_n] keep tensor."""
+def _half_codes(bm: BlockMask) -> bool:
+    """True if the mask's query geometry is a 64-row multiple that is not a 128-row one."""
+    return (bm.b_q, bm.b_kv) != (BQ, BKV) and bm.b_q % BQ != 0 and bm.b_q % (BQ // 2) == 0 and bm.b_kv % BKV == 0
+
+
+def build_lists(keep_u8: torch.Tensor, half: bool = False) -> BlockLists:
+    """K3 on a uint8 [B, H, T_m, T_n] keep-code tensor (see ``_native_keep``)."""
     B, H, t_m, t_n = keep_u8.shape
     bh, dev = B * H, keep_u8.device
     cap = max(1, bh * t_m * t_n)
@@ -117,7 +140,7 @@ def build_lists(keep_u8: torch.Tensor) -> BlockLists:
     lists = BlockLists(
         row_ptr=torch.empty(bh * t_m + 1, **i32), row_idx=torch.empty(cap, **i32), row_order=torch.empty(bh * t_m, **i32),
         col_ptr=torch.empty(bh * t_n + 1, **i32), col_idx=torch.empty(cap, **i32), col_order=torch.empty(bh * t_n, **i32),
-        shape=(B, H, t_m, t_n))
+        shape=(B, H, t_m, t_n), half=half)
     scratch = torch.empty(bh * (t_m + t_n), **i32)
     st = torch.cuda.current_stream(dev)
     _lib.call("spa2_build_lists", _lib.ptr(keep_u8), bh, t_m, t_n, _lib.ptr(lists.row_ptr), _lib.ptr(lists.row_idx),
@@ -132,12 +155,14 @@ def _lists_with_order(bm: BlockMask, B: int, H: int, N: int, visit) -> BlockList
     reference; its order is then refined to the kernel grid (mask column j covers kernel
     columns j·(b_kv/64) ...).  Test-only: copies the mask to the host."""
     keep_u8 = _native_keep(bm, B, H, N)
-    base = build_lists(keep_u8)
+    base = build_lists(keep_u8, half=_half_codes(bm))
     t_m, t_n = keep_u8.shape[-2:]
     mk = bm.keep_numpy().astype(bool)
     mk = np.broadcast_to(mk.reshape((1, 1) + mk.shape[-2:]) if mk.ndim == 2 else mk, (B, H) + mk.shape[-2:])
     rq = bm.b_q // BQ if bm.b_q % BQ == 0 else None
     rk = bm.b_kv // BKV if bm.b_kv % BKV == 0 else None
+    half = rq is None and bm.b_q % (BQ // 2) == 0 and rk is not None  # b_q = 64·odd: two mask rows per block
+    codes = keep_u8.cpu().numpy()
     idx = []
     for b in range(B):
         for h in range(H):
@@ -149,6 +174,19 @@ def _lists_with_order(bm: BlockMask, B: int, H: int, N: int, visit) -> BlockList
                 return orders[i_m]
 
             for r in range(t_m):
+                if half:  # the union of the two halves' orders; entries carry the half code
+                    out, seen = [], set()
+                    for hrow in (2 * r, 2 * r + 1):
+                        i_m = hrow * (BQ // 2) // bm.b_q
+                        if hrow * (BQ // 2) >= N or i_m >= mk.shape[-2]:
+                            continue
+                        for j in order_of(i_m):
+                            for c in range(j * rk, min((j + 1) * rk, t_n)):
+                                if c not in seen:
+                                    seen.add(c)
+                                    out.append(c | ((int(codes[b, h, r, c]) - 1) << 30))
+                    idx.append(np.asarray(out, dtype=np.int64).astype(np.int32))
+                    continue
                 if rq is None or rk is None:  # all-ones mask of an arbitrary geometry
                     i_m = min(r * BQ // bm.b_q, mk.shape[-2] - 1)
                     order = order_of(i_m)
@@ -163,7 +201,8 @@ def _lists_with_order(bm: BlockMask, B: int, H: int, N: int, visit) -> BlockList
                     out = [c for j in order for c in range(j * rk, min((j + 1) * rk, t_n))]
                 idx.append(np.asarray(out, dtype=np.int32))
     flat = torch.tensor(np.concatenate(idx) if idx else np.zeros(0, np.int32), device=keep_u8.device)
-    return BlockLists(base.row_ptr, flat, base.row_order, base.col_ptr, base.col_idx, base.col_order, base.shape)
+    return BlockLists(base.row_ptr, flat, base.row_order, base.col_ptr, base.col_idx, base.col_order, base.shape,
+                      base.half)
 
 
 def mask_lists(bm: BlockMask, B: int, H: int, N: int) -> BlockLists:
@@ -171,7 +210,7 @@ def mask_lists(bm: BlockMask, B: int, H: int, N: int) -> BlockLists:
     key = ("lists", B, H, N)
     hit = bm._cache.get(key)
     if hit is None:
-        hit = build_lists(_native_keep(bm, B, H, N))
+        hit = build_lists(_native_keep(bm, B, H, N), half=_half_codes(bm))
         bm._cache[key] = hit
     return hit
 
@@ -196,8 +235,8 @@ def fwd(q4, k4, v4, lists: BlockLists, scale: float, counter: torch.Tensor | Non
     lse = torch.empty((B, H, N), device=q4.device, dtype=torch.float32)
     st = torch.cuda.current_stream(q4.device)
     _lib.call("spa2_fwd", _lib.view4(q4), _lib.view4(k4), _lib.view4(v4), _lib.view4(o), _lib.ptr(lse),
-              _lib.DTYPE_CODES[q4.dtype], B, H, N, d, BQ, BKV, _lib.ptr(lists.row_ptr), _lib.ptr(lists.row_idx),
-              _lib.ptr(lists.row_order), scale, _lib.ptr(counter), st.cuda_stream, stream_obj=st)
+              _lib.DTYPE_CODES[q4.dtype], B, H, N, d, BQ // 2 if lists.half else BQ, BKV, _lib.ptr(lists.row_ptr),
+              _lib.ptr(lists.row_idx), _lib.ptr(lists.row_order), scale, _lib.ptr(counter), st.cuda_stream, stream_obj=st)
     return o, lse
 
 
@@ -213,12 +252,13 @@ def bwd(q4, k4, v4, o4, do4, lse, lists: BlockLists, scale: float, dq=None, dk=N
     delta = torch.empty((B, H, N), device=q4.device, dtype=torch.float32)
     st = torch.cuda.current_stream(q4.device)
     dt = _lib.DTYPE_CODES[q4.dtype]
+    bq = BQ // 2 if lists.half else BQ  # b_q = 64 tells the kernels the lists carry half-block codes
     # δ = rowsum(dO ∘ O) is computed inside the dQ kernel (spa2_bwd_dq_delta)
     _lib.call("spa2_bwd_dq_delta", _lib.view4(q4), _lib.view4(k4), _lib.view4(v4), _lib.view4(o4), _lib.view4(do4),
-              _lib.ptr(lse), _lib.ptr(delta), _lib.view4(dq), dt, B, H, N, d, BQ, BKV, _lib.ptr(lists.row_ptr),
+              _lib.ptr(lse), _lib.ptr(delta), _lib.view4(dq), dt, B, H, N, d, bq, BKV, _lib.ptr(lists.row_ptr),
               _lib.ptr(lists.row_idx), _lib.ptr(lists.row_order), scale, st.cuda_stream, stream_obj=st)
     _lib.call("spa2_bwd_dkdv", _lib.view4(q4), _lib.view4(k4), _lib.view4(v4), _lib.view4(do4), _lib.ptr(lse),
-              _lib.ptr(delta), _lib.view4(dk), _lib.view4(dv), dt, B, H, N, d, BQ, BKV, _lib.ptr(lists.col_ptr),
+              _lib.ptr(delta), _lib.view4(dk), _lib.view4(dv), dt, B, H, N, d, bq, BKV, _lib.ptr(lists.col_ptr),
               _lib.ptr(lists.col_idx), _lib.ptr(lists.col_order), scale, st.cuda_stream, stream_obj=st)
     return dq, dk, dv
 

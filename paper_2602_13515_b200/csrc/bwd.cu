@@ -247,7 +247,7 @@ __device__ __forceinline__ uint32_t ds_col(int ks) {
   return (uint32_t)((16 * ks / CPT) * CPT + (16 * ks % CPT) / 2);
 }
 
-template <int HD, int EWW>
+template <int HD, int EWW, bool HALF = false>
 __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
     k_dq3(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
           const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO, const BwdParams p) {
@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
           const int s = g % ns;
           if (g >= ns) mbar_wait(&empty[s], ((uint32_t)(g / ns) + 1u) & 1u);
           mbar_expect_tx(&full[s], C::KV_BYTES);
-          tma_load_5d(ring + s * C::KV_BYTES, tmKV, &full[s], 0, p.idx[m.beg + t] * BKV, 0, hh, bb);
+          tma_load_5d(ring + s * C::KV_BYTES, tmKV, &full[s], 0, list_blk(p.idx[m.beg + t]) * BKV, 0, hh, bb);
         }
         ++it;
       }
@@ -482,11 +482,12 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
       }
       ++it;
       // key-block index of the next tile is loaded one tile ahead (off the critical path)
-      int j_next = __ldg(p.idx + m.beg);
+      int32_t e_next = __ldg(p.idx + m.beg);
       for (int t = 0; t < m.n; ++t, ++g) {
         const int b = g & 1;
-        const bool tail = kv_tail < BKV && j_next == p.T_n - 1;
-        if (t + 1 < m.n) j_next = __ldg(p.idx + m.beg + t + 1);
+        const bool tail = kv_tail < BKV && list_blk(e_next) == p.T_n - 1;
+        const bool dropped = HALF && list_row_dropped(e_next, row);  // b_q = 64 masks (warp-uniform)
+        if (t + 1 < m.n) e_next = __ldg(p.idx + m.beg + t + 1);
         const uint32_t sb = tbase + lane_off + C::SDP_COL + (uint32_t)(b * 128);
         mbar_wait(&s_full[b], (uint32_t)(g >> 1) & 1u);
         if (warp == 2) SPA2_TR(3, g);
@@ -516,6 +517,12 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
 #pragma unroll
           for (int c = 0; c < CPT; ++c)
             if (col0 + c >= kv_tail) pv[c] = 0.f;
+        }
+        if constexpr (HALF) {
+          if (dropped) {
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) pv[c] = 0.f;
+          }
         }
         mbar_wait(&dp_full[b], (uint32_t)(g >> 1) & 1u);
         if (warp == 2) SPA2_TR(4, g);
@@ -649,7 +656,7 @@ struct Dkv5Cfg {
 // different warps (Q: S and dKᵀ, dO: dP and dVᵀ), so its slot is released by two commits, one
 // per issuer; the dVᵀ issuer also waits for dO(g) to land (P(g) existing only proves S(g)
 // finished).  P and dS share one smem buffer.
-template <int HD, int EWW, int NSL_ = SPA2_DKDV_NSL, int NPB_ = 1>
+template <int HD, int EWW, bool HALF = false, int NSL_ = SPA2_DKDV_NSL, int NPB_ = 1>
 __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
     k_dkdv5(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
            const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO, const BwdParams p) {
@@ -732,7 +739,7 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
         mbar_expect_tx(&kv_full[kb], C::KV_BYTES);
         tma_load_5d(kv_dst + kb * 2 * C::KV_BYTES, tmKV, &kv_full[kb], 0, m.blk * BKV, 0, hh, bb);
         for (int t = 0; t < m.n; ++t, ++g) {
-          const int i = p.idx[m.beg + t];
+          const int i = list_blk(p.idx[m.beg + t]);
           const int u = 2 * g + (second ? 1 : 0);  // operand index: Q(g) even, dO(g) odd
           const int s = u % NSL;
           if (u >= NSL) mbar_wait(&sl_empty[s], ((uint32_t)(u / NSL) + 1u) & 1u);
@@ -864,8 +871,11 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
       if (m.n == 0) continue;
       const int64_t rowbase = (int64_t)m.bh * p.N;
       auto load_stats = [&](int t, float& lse2, float& dlt) {
-        const int tok = p.idx[m.beg + t] * BQ + row;
-        const bool valid = tok < p.N;
+        const int32_t e = p.idx[m.beg + t];
+        const int tok = list_blk(e) * BQ + row;
+        // rows outside the query block's range, or of a half that does not keep the tile (b_q = 64
+        // masks), get LSE = +inf: P = 0 and dS = 0
+        const bool valid = tok < p.N && !(HALF && list_row_dropped(e, row));
         lse2 = valid ? __ldg(p.lse + rowbase + tok) * kLog2e : INFINITY;
         dlt = valid ? __ldg(p.delta + rowbase + tok) : 0.f;
       };
@@ -1015,7 +1025,7 @@ template <int HD>
 int launch_attn_bwd(int which, const spa2_view& q, const spa2_view& k, const spa2_view& v, const spa2_view& dout,
                     const float* lse, const float* delta, const spa2_view& out0, const spa2_view* out1, int64_t B,
                     int64_t H, int64_t N, const int32_t* ptr, const int32_t* idx, const int32_t* order, float scale,
-                    cudaStream_t st, const FusedDelta* fd = nullptr) {
+                    cudaStream_t st, const FusedDelta* fd = nullptr, bool half = false) {
   const int64_t T_m = ceil_div(N, BQ), T_n = ceil_div(N, BKV);
   BwdMaps m;
   int rc;
@@ -1050,14 +1060,14 @@ int launch_attn_bwd(int which, const spa2_view& q, const spa2_view& k, const spa
   const unsigned grid = (unsigned)std::min<int64_t>(prm.num_items, num_sms());
   constexpr int EWW = 16;  // elementwise warps (4 per TMEM lane quarter); 8 measured slower
   if (which == 0) {
-    auto kern = k_dq3<HD, EWW>;
+    auto kern = half ? k_dq3<HD, EWW, true> : k_dq3<HD, EWW, false>;
     SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Dq3Cfg<HD>::SMEM));
     SPA2_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(Dq3Roles<EWW>::THREADS), Dq3Cfg<HD>::SMEM, st, m.q, m.k, m.v, m.dout,
                              prm));
   } else {
     prm.out1 = (__nv_bfloat16*)out1->ptr;
     prm.o1_sb = out1->sb, prm.o1_sh = out1->sh, prm.o1_sn = out1->sn;
-    auto kern = k_dkdv5<HD, EWW>;
+    auto kern = half ? k_dkdv5<HD, EWW, true> : k_dkdv5<HD, EWW, false>;
     SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Dkv5Cfg<HD>::SMEM));
     SPA2_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(DkvRoles<EWW>::THREADS), Dkv5Cfg<HD>::SMEM, st, m.q, m.k, m.v,
                              m.dout, prm));
@@ -1069,7 +1079,8 @@ int launch_attn_bwd(int which, const spa2_view& q, const spa2_view& k, const spa
 int check_bwd_args(int dtype, int64_t B, int64_t H, int64_t N, int64_t d, int64_t b_q, int64_t b_kv) {
   SPA2_REQUIRE(dtype == SPA2_BF16, SPA2_ERR_UNSUPPORTED, "bwd: only bf16 operands are supported");
   SPA2_REQUIRE(d == 64 || d == 128, SPA2_ERR_UNSUPPORTED, "bwd: head dim %lld not in {64, 128}", (long long)d);
-  SPA2_REQUIRE(b_q == BQ && b_kv == BKV, SPA2_ERR_UNSUPPORTED, "bwd: block sizes (%lld, %lld) != (128, 64)",
+  SPA2_REQUIRE((b_q == BQ || b_q == BQ / 2) && b_kv == BKV, SPA2_ERR_UNSUPPORTED,
+               "bwd: block sizes (%lld, %lld) not in {(128, 64), (64, 64)}",
                (long long)b_q, (long long)b_kv);
   SPA2_REQUIRE(B >= 1 && H >= 1 && N >= 1, SPA2_ERR_VALUE, "bwd: empty problem");
   SPA2_REQUIRE(N < (1ll << 31) && B * H * ceil_div(N, BKV) < (1ll << 31), SPA2_ERR_UNSUPPORTED, "bwd: too large");
@@ -1111,9 +1122,9 @@ extern "C" int spa2_bwd_dq(spa2_view q, spa2_view k, spa2_view v, spa2_view dout
   cudaStream_t st = (cudaStream_t)stream;
   if (d == 128)
     return launch_attn_bwd<128>(0, q, k, v, dout, lse, delta, dq, nullptr, B, H, N, row_ptr, row_idx, row_order,
-                                scale, st);
+                                scale, st, nullptr, b_q != BQ);
   return launch_attn_bwd<64>(0, q, k, v, dout, lse, delta, dq, nullptr, B, H, N, row_ptr, row_idx, row_order, scale,
-                             st);
+                             st, nullptr, b_q != BQ);
 }
 
 extern "C" int spa2_bwd_dq_delta(spa2_view q, spa2_view k, spa2_view v, spa2_view o, spa2_view dout,
@@ -1141,9 +1152,9 @@ extern "C" int spa2_bwd_dq_delta(spa2_view q, spa2_view k, spa2_view v, spa2_vie
                 dout.sn, delta};
   if (d == 128)
     return launch_attn_bwd<128>(0, q, k, v, dout, lse, delta, dq, nullptr, B, H, N, row_ptr, row_idx, row_order,
-                                scale, st, &fd);
+                                scale, st, &fd, b_q != BQ);
   return launch_attn_bwd<64>(0, q, k, v, dout, lse, delta, dq, nullptr, B, H, N, row_ptr, row_idx, row_order, scale,
-                             st, &fd);
+                             st, &fd, b_q != BQ);
 }
 
 extern "C" int spa2_bwd_dkdv(spa2_view q, spa2_view k, spa2_view v, spa2_view dout, const float* lse,
@@ -1157,8 +1168,9 @@ extern "C" int spa2_bwd_dkdv(spa2_view q, spa2_view k, spa2_view v, spa2_view do
   cudaStream_t st = (cudaStream_t)stream;
   if (d == 128)
     return launch_attn_bwd<128>(1, q, k, v, dout, lse, delta, dk, &dv, B, H, N, col_ptr, col_idx, col_order, scale,
-                                st);
-  return launch_attn_bwd<64>(1, q, k, v, dout, lse, delta, dk, &dv, B, H, N, col_ptr, col_idx, col_order, scale, st);
+                                st, nullptr, b_q != BQ);
+  return launch_attn_bwd<64>(1, q, k, v, dout, lse, delta, dk, &dv, B, H, N, col_ptr, col_idx, col_order, scale, st,
+                             nullptr, b_q != BQ);
 }
 
 extern "C" int spa2_bwd(spa2_view q, spa2_view k, spa2_view v, spa2_view o, spa2_view dout, const float* lse,

@@ -66,6 +66,15 @@ __device__ __forceinline__ double to_f64<__half>(__half x) { return (double)__ha
   do {                     \
   } while (0)
 #endif
+// ---- block-list entries -----------------------------------------------------------------
+// bits 0-29: block index; bits 30-31: which 64-row half of the 128-row query block keeps the
+// tile (masks with b_q = 64): 0 both, 1 the top half (rows 0-63) only, 2 the bottom half only.
+__device__ __forceinline__ int list_blk(int32_t e) { return e & 0x3FFFFFFF; }
+// true if query row `row` (0..127 within its query block) is NOT part of tile entry e
+__device__ __forceinline__ bool list_row_dropped(int32_t e, int row) {
+  const uint32_t code = (uint32_t)e >> 30;
+  return (code == 1u && row >= 64) || (code == 2u && row < 64);
+}
 // ---- programmatic dependent launch (PDL) ---------------------------------------------
 // Hot-path kernels are launched with programmatic stream serialization: the next kernel's
 // CTAs may be scheduled (and run their prologue: barrier init, TMEM alloc, descriptor

@@ -69,7 +69,7 @@ struct FwdParams {
   int64_t o_sb, o_sh, o_sn;
 };
 
-template <int HD, bool P_TMEM>
+template <int HD, bool P_TMEM, bool HALF>
 __global__ void __launch_bounds__(kFwdThreads, 2)
     k_fwd(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
           const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, const FwdParams p) {
@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
         const uint32_t ph = (uint32_t)(t / NS) & 1u;
         if (t >= NS) mbar_wait(&k_empty[s], ph ^ 1u);
         mbar_expect_tx(&k_full[s], C::KV_BYTES);
-        tma_load_5d(smem + C::OFF_K + s * C::KV_BYTES, &tmK, &k_full[s], 0, list[t] * BKV, 0, hh, bb);
+        tma_load_5d(smem + C::OFF_K + s * C::KV_BYTES, &tmK, &k_full[s], 0, list_blk(list[t]) * BKV, 0, hh, bb);
       }
     }
   } else if (warp == 6) {
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
         const uint32_t ph = (uint32_t)(t / NS) & 1u;
         if (t >= NS) mbar_wait(&v_empty[s], ph ^ 1u);
         mbar_expect_tx(&v_full[s], C::KV_BYTES);
-        tma_load_5d(smem + C::OFF_V + s * C::KV_BYTES, &tmV, &v_full[s], 0, list[t] * BKV, 0, hh, bb);
+        tma_load_5d(smem + C::OFF_V + s * C::KV_BYTES, &tmV, &v_full[s], 0, list_blk(list[t]) * BKV, 0, hh, bb);
       }
     }
   } else if (warp == 1) {
@@ -215,10 +215,13 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
     const int kv_tail = p.N - (p.T_n - 1) * BKV;  // valid columns of the last key block
     const float sl2 = p.scale_log2;
     float m = -INFINITY, l = 0.f;
-    int j_next = list[0];  // key-block index of the next tile, loaded one tile ahead
+    int32_t e_next = list[0];  // list entry of the next tile, loaded one tile ahead
     for (int t = 0; t < n; ++t) {
-      const bool tail = j_next == p.T_n - 1 && kv_tail < BKV;
-      if (t + 1 < n) j_next = list[t + 1];
+      const bool tail = list_blk(e_next) == p.T_n - 1 && kv_tail < BKV;
+      // b_q = 64 masks (HALF instantiation only): this row's half of the query block does not
+      // keep the tile (warp-uniform)
+      const bool dropped = HALF && list_row_dropped(e_next, row);
+      if (t + 1 < n) e_next = list[t + 1];
       const uint32_t s_col = tbase + lane_off + (uint32_t)((t & 1) * 64);
       mbar_wait(&s_full[t & 1], (uint32_t)(t >> 1) & 1u);
       tc_fence_after();
@@ -231,6 +234,12 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
 #pragma unroll
         for (int c = 0; c < 64; ++c)
           if (c >= kv_tail) sv[c] = -INFINITY;
+      }
+      if constexpr (HALF) {
+        if (dropped) {
+#pragma unroll
+          for (int c = 0; c < 64; ++c) sv[c] = -INFINITY;
+        }
       }
       float mx8[8];  // tree max: short dependency chains
 #pragma unroll
@@ -266,6 +275,12 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
       // (exp2_poly2) so the MUFU pipe (16/clk/SM) is not the limit of the two softmax CTAs
       uint32_t pk[32];
       float2 lsum = make_float2(0.f, 0.f);
+      if (dropped) {
+        // the tile contributes P = 0 to this row (its -inf scores minus a still -inf running
+        // max would give NaN if the row has not seen a kept tile yet)
+#pragma unroll
+        for (int c = 0; c < 32; ++c) pk[c] = 0u;
+      } else {
 #pragma unroll
       for (int c = 0; c < 32; ++c) {
         const float2 x = __ffma2_rn(make_float2(sv[2 * c], sv[2 * c + 1]), make_float2(sl2, sl2), make_float2(-m, -m));
@@ -278,6 +293,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
         }
         lsum = __fadd2_rn(lsum, e);
         pk[c] = pack_bf16(e.x, e.y);
+      }
       }
       l += lsum.x + lsum.y;
       if constexpr (P_TMEM) {
@@ -330,11 +346,11 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
   if (warp == 1) tmem_dealloc(tbase, 256);
 }
 
-template <int HD, bool P_TMEM>
+template <int HD, bool P_TMEM, bool HALF>
 int launch_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& to,
                const FwdParams& prm, unsigned grid, cudaStream_t st) {
   using C = FwdCfg<HD, P_TMEM>;
-  auto kern = k_fwd<HD, P_TMEM>;
+  auto kern = k_fwd<HD, P_TMEM, HALF>;
   SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
   kern<<<grid, kFwdThreads, C::SMEM, st>>>(tq, tk, tv, to, prm);
   SPA2_LAUNCH_CHECK();
@@ -360,7 +376,9 @@ extern "C" int spa2_fwd(spa2_view q, spa2_view k, spa2_view v, spa2_view o, floa
                         unsigned long long* block_counter, void* stream) {
   SPA2_REQUIRE(dtype == SPA2_BF16, SPA2_ERR_UNSUPPORTED, "fwd: only bf16 operands are supported");
   SPA2_REQUIRE(d == 64 || d == 128, SPA2_ERR_UNSUPPORTED, "fwd: head dim %lld not in {64, 128}", (long long)d);
-  SPA2_REQUIRE(b_q == BQ && b_kv == BKV, SPA2_ERR_UNSUPPORTED, "fwd: block sizes (%lld, %lld) != (128, 64)",
+  // b_q = 64: the row lists carry half-block codes (bits 30-31) from a b_q = 64 mask
+  SPA2_REQUIRE((b_q == BQ || b_q == BQ / 2) && b_kv == BKV, SPA2_ERR_UNSUPPORTED,
+               "fwd: block sizes (%lld, %lld) not in {(128, 64), (64, 64)}",
                (long long)b_q, (long long)b_kv);
   SPA2_REQUIRE(B >= 1 && H >= 1 && N >= 1, SPA2_ERR_VALUE, "fwd: empty problem");
   SPA2_REQUIRE(N < (1ll << 31) && B * H < (1ll << 31), SPA2_ERR_UNSUPPORTED, "fwd: problem too large");
@@ -390,6 +408,10 @@ extern "C" int spa2_fwd(spa2_view q, spa2_view k, spa2_view v, spa2_view o, floa
   prm.o_sn = o.sn;
   const unsigned grid = (unsigned)(B * H * T_m);
   cudaStream_t st = (cudaStream_t)stream;
-  if (d == 128) return launch_fwd<128, true>(tq, tk, tv, to, prm, grid, st);
-  return launch_fwd<64, true>(tq, tk, tv, to, prm, grid, st);
+  if (b_q == BQ) {
+    if (d == 128) return launch_fwd<128, true, false>(tq, tk, tv, to, prm, grid, st);
+    return launch_fwd<64, true, false>(tq, tk, tv, to, prm, grid, st);
+  }
+  if (d == 128) return launch_fwd<128, true, true>(tq, tk, tv, to, prm, grid, st);
+  return launch_fwd<64, true, true>(tq, tk, tv, to, prm, grid, st);
 }

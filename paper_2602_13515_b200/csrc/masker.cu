@@ -684,8 +684,10 @@ __global__ void __launch_bounds__(kColWarps * 32) k_fill(const uint8_t* __restri
     int off = col_ptr[bh * T_n + j];
     for (int x = 0; x < w; ++x) off += part[x][lane];
 #pragma unroll 8
-    for (int i = r0; i < r1; ++i)
-      if (base[(int64_t)i * T_n] != 0) col_idx[off++] = i;
+    for (int i = r0; i < r1; ++i) {
+      const int v = base[(int64_t)i * T_n];  // 1 = both query-block halves keep it, 2 top only, 3 bottom only
+      if (v != 0) col_idx[off++] = i | ((v - 1) << 30);
+    }
   } else {
     const int i = ((int)blockIdx.x - col_chunks) * kColWarps + w;
     if (i >= T_m) return;
@@ -693,9 +695,10 @@ __global__ void __launch_bounds__(kColWarps * 32) k_fill(const uint8_t* __restri
     int b = row_ptr[row];
     for (int j0 = 0; j0 < T_n; j0 += 32) {
       const int j = j0 + lane;
-      const bool f = j < T_n && keep[row * T_n + j] != 0;
+      const int v = j < T_n ? keep[row * T_n + j] : 0;
+      const bool f = v != 0;
       const unsigned m = __ballot_sync(0xffffffffu, f);
-      if (f) row_idx[b + __popc(m & ((1u << lane) - 1u))] = j;
+      if (f) row_idx[b + __popc(m & ((1u << lane) - 1u))] = j | ((v - 1) << 30);
       b += __popc(m);
     }
   }

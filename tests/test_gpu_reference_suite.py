@@ -252,9 +252,9 @@ def test_unsupported_head_dim_raises():  # d outside {64, 128} is
         at.dense_attention(np.zeros((4, 5)), np.zeros((4, 5)), np.zeros((4, 5)))
 
 
-def test_unsupported_block_geometry_raises():  # b_q = 64 is outside the kernels' grid
+def test_unsupported_block_geometry_raises():  # b_q not a multiple of 64
     q, k, v = rand_qkv(4, 256, 64)
-    bm = random_mask(4, 256, b_q=64, b_kv=64)
+    bm = random_mask(4, 256, b_q=32, b_kv=64)
     with pytest.raises(ValueError, match="b_q=128"):
         at.sparse_attention_with_mask(q, k, v, bm)
 
