@@ -309,6 +309,28 @@ def _scan_finite(flag: torch.Tensor, *tensors: torch.Tensor) -> None:
                   st.cuda_stream, stream_obj=st)
 
 
+_SIDE_STREAMS: dict = {}
+
+
+def _scan_finite_side(flag: torch.Tensor, *tensors: torch.Tensor) -> torch.cuda.Event:
+    """K0 on a per-device side stream, concurrent with the masker on the current stream (the
+    scan only feeds the host-side verdict, nothing on the GPU waits for it).  Returns the event
+    that marks its completion."""
+    dev = tensors[0].device
+    main = torch.cuda.current_stream(dev)
+    side = _SIDE_STREAMS.get(dev)
+    if side is None:
+        side = _SIDE_STREAMS[dev] = torch.cuda.Stream(dev)
+    side.wait_stream(main)
+    with torch.cuda.stream(side):
+        _scan_finite(flag, *tensors)
+        ev = torch.cuda.Event()
+        ev.record(side)
+    for t in tensors:
+        t.record_stream(side)
+    return ev
+
+
 def _prepare(q, k, v, check_finite):
     """attention.py:50-59: same shapes (ValueError), rank (ShapeError), finite
     (FloatingPointError; numpy inputs are checked on the host exactly as the reference does,
@@ -335,7 +357,7 @@ def _tma_ready(t: torch.Tensor) -> torch.Tensor:
     return t
 
 
-def _run(q4, k4, v4, bm: BlockMask, qb, counter, flag, check_finite, visit=None) -> AttentionOutput:
+def _run(q4, k4, v4, bm: BlockMask, qb, counter, flag, check_finite, visit=None, side_event=None) -> AttentionOutput:
     B, H, N, d = q4.shape
     if bm.n_tokens != N:
         raise ValueError(f"mask built for {bm.n_tokens} tokens, inputs have {N}")
@@ -344,7 +366,8 @@ def _run(q4, k4, v4, bm: BlockMask, qb, counter, flag, check_finite, visit=None)
     ctr = torch.zeros((1,), device=q4.device, dtype=torch.int64) if counter is not None and native else None
     verdict = None
     if flag is not None:
-        verdict = finite_guard.submit(flag, "q, k or v", block=check_finite == "sync", device=q4.device)
+        verdict = finite_guard.submit(flag, "q, k or v", block=check_finite == "sync", device=q4.device,
+                                      extra_event=side_event)
     o, lse = SparseAttentionFunction.apply(q4, k4, v4, lists, 1.0 / math.sqrt(d), ctr, verdict)
     if counter is not None:
         counter.count += int(ctr.item()) if native else bm.kept_blocks()
@@ -396,11 +419,10 @@ def sparse_attention(q, k, v, cfg: SparsityConfig, counter: BlockCounter | None 
     Finiteness: K1 checks q and k while pooling them, K0 scans v; no host sync for torch
     callers (``check_finite`` as in ``sparse_attention_with_mask``)."""
     q4, k4, v4, qb, flag = _prepare(q, k, v, check_finite)
-    if flag is not None:
-        _scan_finite(flag, v4)
+    side = _scan_finite_side(flag, v4) if flag is not None else None
     keep = _hybrid_mask_device(q4, k4, cfg, flag)
     bm = BlockMask._from_device(keep, cfg.b_q, cfg.b_kv, q4.shape[2], host=qb.numpy)
-    return _run(q4, k4, v4, bm, qb, counter, flag, check_finite)
+    return _run(q4, k4, v4, bm, qb, counter, flag, check_finite, side_event=side)
 
 
 def dense_attention(q, k, v, *, check_finite: bool | str = True) -> AttentionOutput:

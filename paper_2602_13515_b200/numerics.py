@@ -102,11 +102,13 @@ class FiniteGuard:
         not recycled while a kernel may still write it."""
         return torch.zeros((1,), dtype=torch.int32, pin_memory=True)
 
-    def submit(self, flag: torch.Tensor, what: str, block: bool, device: torch.device | None = None) -> tuple:
-        """Register ``flag`` (written by kernels on the current stream) as the verdict on ``what``."""
+    def submit(self, flag: torch.Tensor, what: str, block: bool, device: torch.device | None = None,
+               extra_event: torch.cuda.Event | None = None) -> tuple:
+        """Register ``flag`` (written by kernels on the current stream, and by those before
+        ``extra_event`` on a side stream) as the verdict on ``what``."""
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream(device))
-        entry = (ev, flag, what)
+        entry = (_Events(ev, extra_event), flag, what)
         if block:
             self._verify(entry)
         else:
@@ -142,6 +144,21 @@ class FiniteGuard:
         self._pending = keep
         if err is not None:
             raise err
+
+
+class _Events:
+    """Both events of a verdict (current stream, optional side stream) behave as one."""
+
+    def __init__(self, a: torch.cuda.Event, b: torch.cuda.Event | None):
+        self.a, self.b = a, b
+
+    def query(self) -> bool:
+        return self.a.query() and (self.b is None or self.b.query())
+
+    def synchronize(self) -> None:
+        self.a.synchronize()
+        if self.b is not None:
+            self.b.synchronize()
 
 
 finite_guard = FiniteGuard()
