@@ -276,6 +276,101 @@ __global__ void __launch_bounds__(256, 3) k_scores(const double* __restrict__ qb
 }
 constexpr int kScoresSmem = 2 * 2 * kSTI * kSTP * 8;
 
+// K1b on the fp64 tensor cores (default): DMMA m8n8k4 (mma.sync .f64).  CTA = 64 x 64 outputs,
+// 4 warps each owning 32 x 32 (4 x 4 DMMA tiles, 32 fp64 accumulators per thread); k chunks of
+// 32 staged by 16-byte cp.async into a 36-double pitch, so the fragment loads (8 rows x 4
+// consecutive k per DMMA operand) are conflict-free.  The fp64 FMA rate is the same as the
+// DFMA pipe's, but a DMMA needs 1 shared-memory wavefront per 256 FMAs instead of ~4, so the
+// kernel is no longer bound by the LSU (k_scores, 70 % L1 throughput).  Results differ from
+// k_scores only in fp64 summation order (<= 1e-16 relative; the map's tolerance is 1e-13).
+constexpr int kDmK = 32, kDmP = 36;
+constexpr int kDmSmem = 2 * 2 * 64 * kDmP * 8;
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(valid ? 16 : 0)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(128, 3) k_scores_dmma(const double* __restrict__ qbar,
+                                                        const double* __restrict__ kbar, int T_m, int T_n, int d,
+                                                        double inv_sqrt_d, double* __restrict__ s_out) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ double dm_smem[];  // [2 bufs][sq 64 x 36 | sk 64 x 36]
+  const int64_t bh = blockIdx.z;
+  const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
+  const double* qb = qbar + bh * (int64_t)T_m * d;
+  const double* kb = kbar + bh * (int64_t)T_n * d;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int wi = (warp >> 1) * 32, wj = (warp & 1) * 32;  // warp tile origin inside the CTA tile
+  const int fr = lane >> 2, fk = lane & 3;                // fragment row / k of this lane
+  auto load = [&](int c0, int buf) {
+    double* sq = dm_smem + buf * 2 * 64 * kDmP;
+    double* sk = sq + 64 * kDmP;
+    // 64 rows x 32 doubles per operand = 512 chunks of 16 B each; 128 threads x 4
+#pragma unroll
+    for (int e = threadIdx.x; e < 64 * (kDmK / 2); e += 128) {
+      const int rr = e / (kDmK / 2), cc = (e % (kDmK / 2)) * 2;
+      const int i = i0 + rr, j = j0 + rr, c = c0 + cc;
+      const bool vq = i < T_m && c < d, vk = j < T_n && c < d;
+      cp_async16(&sq[rr * kDmP + cc], vq ? qb + (int64_t)i * d + c : qb, vq);
+      cp_async16(&sk[rr * kDmP + cc], vk ? kb + (int64_t)j * d + c : kb, vk);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+  const int nch = (d + kDmK - 1) / kDmK;
+  load(0, 0);
+  for (int ch = 0; ch < nch; ++ch) {
+    if (ch + 1 < nch) {
+      load((ch + 1) * kDmK, (ch + 1) & 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const double* sq = dm_smem + (ch & 1) * 2 * 64 * kDmP;
+    const double* sk = sq + 64 * kDmP;
+#pragma unroll
+    for (int k0 = 0; k0 < kDmK; k0 += 4) {
+      double a[4], b[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) a[x] = sq[(wi + 8 * x + fr) * kDmP + k0 + fk];
+#pragma unroll
+      for (int y = 0; y < 4; ++y) b[y] = sk[(wj + 8 * y + fr) * kDmP + k0 + fk];
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                       : "+d"(acc[x][y][0]), "+d"(acc[x][y][1])
+                       : "d"(a[x]), "d"(b[y]));
+    }
+    __syncthreads();  // buffer (ch & 1) is refilled by the load issued in iteration ch + 1
+  }
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const int i = i0 + wi + 8 * x + fr;
+    if (i >= T_m) continue;
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      const int j = j0 + wj + 8 * y + fk * 2;
+      double* dst = s_out + (bh * T_m + i) * (int64_t)T_n + j;
+      if (j + 1 < T_n && ((T_n & 1) == 0)) {
+        *reinterpret_cast<double2*>(dst) = make_double2(acc[x][y][0] * inv_sqrt_d, acc[x][y][1] * inv_sqrt_d);
+      } else {
+        if (j < T_n) dst[0] = acc[x][y][0] * inv_sqrt_d;
+        if (j + 1 < T_n) dst[1] = acc[x][y][1] * inv_sqrt_d;
+      }
+    }
+  }
+}
+
 // K1c: in-place row softmax with max subtraction (numerics.py:46-52). One warp per row.
 __global__ void k_softmax_rows(double* __restrict__ p, int64_t rows, int T_n) {
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
@@ -763,10 +858,17 @@ static int pooled_map_impl(spa2_view q, spa2_view k, int dtype, int64_t B, int64
     default: SPA2_REQUIRE(false, SPA2_ERR_UNSUPPORTED, "pooled_map: unsupported dtype %d", dtype);
   }
   if (rc != SPA2_OK) return rc;
-  dim3 grid((unsigned)ceil_div(T_n, kSTJ), (unsigned)ceil_div(T_m, kSTI), (unsigned)BH);
-  SPA2_CUDA_TRY(cudaFuncSetAttribute(k_scores, cudaFuncAttributeMaxDynamicSharedMemorySize, kScoresSmem));
-  SPA2_CUDA_TRY(launch_pdl(k_scores, grid, dim3(256), kScoresSmem, st, qbar, kbar, (int)T_m, (int)T_n, (int)d,
-                           sqrt((double)d), probs));
+  if (d % 2 == 0) {  // 16-byte row chunks for cp.async (d is even for every supported head dim)
+    dim3 grid((unsigned)ceil_div(T_n, 64), (unsigned)ceil_div(T_m, 64), (unsigned)BH);
+    SPA2_CUDA_TRY(cudaFuncSetAttribute(k_scores_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, kDmSmem));
+    SPA2_CUDA_TRY(launch_pdl(k_scores_dmma, grid, dim3(128), kDmSmem, st, qbar, kbar, (int)T_m, (int)T_n, (int)d,
+                             1.0 / sqrt((double)d), probs));
+  } else {
+    dim3 grid((unsigned)ceil_div(T_n, kSTJ), (unsigned)ceil_div(T_m, kSTI), (unsigned)BH);
+    SPA2_CUDA_TRY(cudaFuncSetAttribute(k_scores, cudaFuncAttributeMaxDynamicSharedMemorySize, kScoresSmem));
+    SPA2_CUDA_TRY(launch_pdl(k_scores, grid, dim3(256), kScoresSmem, st, qbar, kbar, (int)T_m, (int)T_n, (int)d,
+                             sqrt((double)d), probs));
+  }
   SPA2_LAUNCH_CHECK();
   if (!softmax) return SPA2_OK;
   const int64_t rows = BH * T_m;

@@ -3,7 +3,7 @@
 #   bash tools/launch_list.sh [regex]
 mkdir -p gpurun_out
 ncu --metrics gpu__time_duration.sum --clock-control none ${1:+-k regex:"$1"} --csv --log-file gpurun_out/ll.csv \
-  python bench.py --steps 1 --warmup 3 --no-e2e --no-dense --no-cpu-baseline > /dev/null 2>&1
+  python bench.py --steps 1 --warmup 3 --no-e2e --no-dense --no-cpu-baseline --no-secondary ${LIB:+--lib $LIB} > /dev/null 2>&1
 python - <<'PY'
 import csv, collections
 rows = list(csv.reader(open("gpurun_out/ll.csv")))
