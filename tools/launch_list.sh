@@ -15,6 +15,7 @@ for r in rows[hi + 1:]:
         continue
     n = r[ik].split("(")[0].split("<")[0].split("::")[-1]
     d.setdefault(n, []).append(float(r[iv].replace(",", "")))
+import statistics
 for n, v in d.items():
-    print(f"{n:24s} n={len(v):3d} last={v[-1] / 1e3:8.1f} us")
+    print(f"{n:24s} n={len(v):3d} last={v[-1] / 1e3:8.1f} us  median={statistics.median(v) / 1e3:8.1f} us  min={min(v) / 1e3:8.1f} us")
 PY
