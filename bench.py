@@ -619,10 +619,16 @@ def main():
         from paper_2602_13515_b200 import _lib
 
         _lib.use_library(args.lib)
-    dev = torch.device("cuda", local)
+    dev = torch.device("cuda", local % max(1, torch.cuda.device_count()))  # ranks > GPUs: gloo test mode
     torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        # NCCL, one GPU per rank; SPA2_BENCH_BACKEND=gloo lets several ranks share one GPU to
+        # exercise the multi-rank code path (tests/test_gpu_bench_multirank.py; timings meaningless)
+        backend = os.environ.get("SPA2_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     try:
         r = gpu_arm(args, rank, world, dev)
         c4 = None
