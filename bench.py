@@ -626,9 +626,14 @@ def main():
         # exercise the multi-rank code path (tests/test_gpu_bench_multirank.py; timings meaningless)
         backend = os.environ.get("SPA2_BENCH_BACKEND", "nccl")
         if backend == "nccl":
+            # NCCL's init log (one "Init COMPLETE ... nranks N" line per rank) lets the driver count
+            # the ranks; limited to the INIT subsystem, and our JSON line is printed after teardown
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
+    line = None
     try:
         r = gpu_arm(args, rank, world, dev)
         c4 = None
@@ -655,10 +660,12 @@ def main():
             if cpu is not None:
                 line["cpu_baseline"] = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample", "host_cores",
                                                             "threadpool_info", "as_shipped", "ms_per_step")}
-            print(json.dumps(line), flush=True)
     finally:
         if world > 1:
             dist.destroy_process_group()
+    if line is not None:  # rank 0, last line of the output
+        sys.stderr.flush()
+        print(json.dumps(line), flush=True)
 
 
 if __name__ == "__main__":
