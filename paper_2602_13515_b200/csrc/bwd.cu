@@ -36,6 +36,9 @@ __device__ unsigned long long g_spa2_trace[32 * SPA2_TRACE_SLOTS];  // kinds 0-1
 #endif
 
 namespace spa2 {
+#ifdef SPA2_CTA_TIMES
+static __device__ unsigned long long g_spa2_cta[3 * SPA2_CTA_MAX * SPA2_CTA_SLOTS];  // [kind 0 fwd, 1 dQ, 2 dK/dV][cta][slot]
+#endif
 namespace {
 
 // Share of the elementwise exponentials computed by exp2_poly2 on the FMA pipe instead of
@@ -309,6 +312,7 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
   if (warp == 1) tmem_alloc(tmem_holder, 512);
   tc_fence_before();
   __syncthreads();
+  SPA2_CT(1, 0); SPA2_CT(1, 2); SPA2_CTC(1, 4);
   tc_fence_after();
   const uint32_t tbase = *tmem_holder;
   pdl_wait();  // everything above touched only this CTA's smem/TMEM
@@ -613,6 +617,7 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  SPA2_CT(1, 1); SPA2_CTC(1, 5);
   if (warp == 1) tmem_dealloc(tbase, 512);
 }
 
@@ -713,6 +718,7 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
   if (warp == 1) tmem_alloc(tmem_holder, 512);
   tc_fence_before();
   __syncthreads();
+  SPA2_CT(2, 0); SPA2_CT(2, 2); SPA2_CTC(2, 4);
   tc_fence_after();
   const uint32_t tbase = *tmem_holder;
   pdl_wait();  // everything above touched only this CTA's smem/TMEM
@@ -994,6 +1000,7 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  SPA2_CT(2, 1); SPA2_CTC(2, 5);
   if (warp == 1) tmem_dealloc(tbase, 512);
 }
 
@@ -1193,6 +1200,17 @@ extern "C" int spa2_trace_fetch(unsigned long long* host_dst) {
   SPA2_CUDA_TRY(cudaMemcpyFromSymbol(host_dst, g_spa2_trace, sizeof(g_spa2_trace)));
   static unsigned long long zeros[32 * SPA2_TRACE_SLOTS];
   SPA2_CUDA_TRY(cudaMemcpyToSymbol(g_spa2_trace, zeros, sizeof(g_spa2_trace)));
+  return SPA2_OK;
+}
+#endif
+
+#ifdef SPA2_CTA_TIMES
+// diagnostic (-DSPA2_CTA_TIMES builds only): copy and clear this unit's per-CTA timings
+extern "C" int spa2_cta_fetch_bwd(unsigned long long* host_dst) {
+  SPA2_CUDA_TRY(cudaDeviceSynchronize());
+  SPA2_CUDA_TRY(cudaMemcpyFromSymbol(host_dst, spa2::g_spa2_cta, sizeof(spa2::g_spa2_cta)));
+  static unsigned long long zeros[3 * SPA2_CTA_MAX * SPA2_CTA_SLOTS];
+  SPA2_CUDA_TRY(cudaMemcpyToSymbol(spa2::g_spa2_cta, zeros, sizeof(spa2::g_spa2_cta)));
   return SPA2_OK;
 }
 #endif

@@ -66,6 +66,53 @@ __device__ __forceinline__ double to_f64<__half>(__half x) { return (double)__ha
   do {                     \
   } while (0)
 #endif
+// ---- diagnostic per-CTA timing (compiled only with -DSPA2_CTA_TIMES, tools/cta_times.py) ----
+// SPA2_CT(kind, slot): thread 0 of the CTA stores globaltimer (slot 0 start of work, 1 end, 3
+// kernel entry, 4.. kernel-specific) or its SM id (slot 2) into a per-translation-unit device array fetched by spa2_cta_fetch_{fwd,bwd}().
+#ifdef SPA2_CTA_TIMES
+#define SPA2_CTA_MAX 4096
+#define SPA2_CTA_SLOTS 8
+#ifdef SPA2_CTA_CLOCK  // SM cycle counter instead of the global nanosecond timer
+#define SPA2_CTA_READ_TIMER(v) asm volatile("mov.u64 %0, %%clock64;" : "=l"(v))
+#else
+#define SPA2_CTA_READ_TIMER(v) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v))
+#endif
+#define SPA2_CT_IF(cond, kind, slot)                                                                  \
+  do {                                                                                                \
+    if ((cond) && blockIdx.x < SPA2_CTA_MAX) {                                                        \
+      unsigned long long v_;                                                                          \
+      if ((slot) == 2) {                                                                              \
+        unsigned s_;                                                                                  \
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(s_));                                               \
+        v_ = s_;                                                                                      \
+      } else {                                                                                        \
+        SPA2_CTA_READ_TIMER(v_);                                                                      \
+      }                                                                                               \
+      g_spa2_cta[((kind) * SPA2_CTA_MAX + blockIdx.x) * SPA2_CTA_SLOTS + (slot)] = v_;                \
+    }                                                                                                 \
+  } while (0)
+#else
+#define SPA2_CT_IF(cond, kind, slot) \
+  do {                               \
+  } while (0)
+#endif
+// thread 0 of the CTA / lane 0 of the calling warp; SPA2_CTC: the SM cycle counter instead
+#ifdef SPA2_CTA_TIMES
+#define SPA2_CTC(kind, slot)                                                                          \
+  do {                                                                                                \
+    if (threadIdx.x == 0 && blockIdx.x < SPA2_CTA_MAX) {                                              \
+      unsigned long long v_;                                                                          \
+      asm volatile("mov.u64 %0, %%clock64;" : "=l"(v_));                                             \
+      g_spa2_cta[((kind) * SPA2_CTA_MAX + blockIdx.x) * SPA2_CTA_SLOTS + (slot)] = v_;                \
+    }                                                                                                 \
+  } while (0)
+#else
+#define SPA2_CTC(kind, slot) \
+  do {                       \
+  } while (0)
+#endif
+#define SPA2_CT(kind, slot) SPA2_CT_IF(threadIdx.x == 0, kind, slot)
+#define SPA2_CTL(kind, slot) SPA2_CT_IF((threadIdx.x & 31) == 0, kind, slot)
 // ---- block-list entries -----------------------------------------------------------------
 // bits 0-29: block index; bits 30-31: which 64-row half of the 128-row query block keeps the
 // tile (masks with b_q = 64): 0 both, 1 the top half (rows 0-63) only, 2 the bottom half only.

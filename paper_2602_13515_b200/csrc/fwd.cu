@@ -27,6 +27,9 @@
 #include "tma_host.h"
 
 namespace spa2 {
+#ifdef SPA2_CTA_TIMES
+static __device__ unsigned long long g_spa2_cta[3 * SPA2_CTA_MAX * SPA2_CTA_SLOTS];  // [kind 0 fwd, 1 dQ, 2 dK/dV][cta][slot]
+#endif
 namespace {
 
 using namespace ptx;
@@ -75,6 +78,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
           const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, const FwdParams p) {
   using C = FwdCfg<HD, P_TMEM>;
   constexpr int NS = C::NS;
+  SPA2_CT(0, 3);
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* const smem = smem_align_1k(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
@@ -116,6 +120,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
   if (warp == 1) tmem_alloc(tmem_holder, 256);
   tc_fence_before();
   __syncthreads();
+  SPA2_CT(0, 0); SPA2_CT(0, 2);
   tc_fence_after();
   const uint32_t tbase = *tmem_holder;
 
@@ -204,7 +209,10 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
         }
         mma_commit_w(o_done);
         mma_commit_w(&v_empty[s]);
-        if (u == n - 1) mma_commit_w(o_final);
+        if (u == n - 1) {
+          mma_commit_w(o_final);
+          SPA2_CTL(0, 7);
+        }
       }
     }
   } else if (warp < 6) {
@@ -313,6 +321,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
     }
     // ---------------- epilogue ----------------
     mbar_wait(o_final, 0);
+    if (warp == 2) SPA2_CTL(0, 4);
     tc_fence_after();
     const float inv_l = 1.f / l;
     uint8_t* sO = smem + C::OFF_Q;  // Q is dead: every MMA has completed
@@ -339,11 +348,16 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
       tma_store_commit();
       if (p.counter) atomicAdd(p.counter, (unsigned long long)n);
       tma_store_wait_all();
+      SPA2_CT_IF(true, 0, 5);
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tbase, 256);
+  SPA2_CT(0, 1);
+  if (warp == 1) {
+    tmem_dealloc(tbase, 256);
+    SPA2_CTL(0, 6);
+  }
 }
 
 template <int HD, bool P_TMEM, bool HALF>
@@ -415,3 +429,14 @@ extern "C" int spa2_fwd(spa2_view q, spa2_view k, spa2_view v, spa2_view o, floa
   if (d == 128) return launch_fwd<128, true, true>(tq, tk, tv, to, prm, grid, st);
   return launch_fwd<64, true, true>(tq, tk, tv, to, prm, grid, st);
 }
+
+#ifdef SPA2_CTA_TIMES
+// diagnostic (-DSPA2_CTA_TIMES builds only): copy and clear this unit's per-CTA timings
+extern "C" int spa2_cta_fetch_fwd(unsigned long long* host_dst) {
+  SPA2_CUDA_TRY(cudaDeviceSynchronize());
+  SPA2_CUDA_TRY(cudaMemcpyFromSymbol(host_dst, spa2::g_spa2_cta, sizeof(spa2::g_spa2_cta)));
+  static unsigned long long zeros[3 * SPA2_CTA_MAX * SPA2_CTA_SLOTS];
+  SPA2_CUDA_TRY(cudaMemcpyToSymbol(spa2::g_spa2_cta, zeros, sizeof(spa2::g_spa2_cta)));
+  return SPA2_OK;
+}
+#endif

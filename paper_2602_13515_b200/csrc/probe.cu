@@ -226,7 +226,24 @@ __global__ void __launch_bounds__(128) k_mma_rate(int M, int N, int K, int a_mn,
       ta[ks] = tbase + 256u + (uint32_t)(kk * 8);
     }
     const uint64_t t0 = clock64();
-    if (a_tmem) {
+    if (a_tmem & 2) {  // weight-stationary form (tcgen05.mma.ws), A from TMEM (bit 0) or smem
+      const bool at = (a_tmem & 1) != 0;
+      for (int r = 0; r < reps; ++r) {
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+          if (at)
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                         "tcgen05.mma.ws.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tbase),
+                         "r"(ta[ks]), "l"(db[ks]), "r"(idesc), "r"(1u)
+                         : "memory");
+          else
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                         "tcgen05.mma.ws.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tbase),
+                         "l"(da[ks]), "l"(db[ks]), "r"(idesc), "r"(1u)
+                         : "memory");
+        }
+      }
+    } else if (a_tmem) {
       for (int r = 0; r < reps; ++r) {
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) mma_bf16_ts(tbase, ta[ks], db[ks], idesc, 1u);

@@ -20,6 +20,17 @@ CASES = [  # (name, m, n, k, a_mn, b_mn, a_tmem)
     ("PV      TS K/MN 128x64", 128, 64, 64, 0, 1, 1),
     ("PV      SS K/MN 128x128", 128, 128, 64, 0, 1, 0),
     ("M64     SS K/K  64x64", 64, 64, 128, 0, 0, 0),
+    ("M64     SS K/K  64x128", 64, 128, 128, 0, 0, 0),
+    ("M64     TS K/K  64x128", 64, 128, 128, 0, 0, 1),
+    ("M64     TS K/MN 64x128", 64, 128, 128, 0, 1, 1),
+    ("M64     TS K/K  64x256", 64, 256, 128, 0, 0, 1),
+    # weight-stationary form (tcgen05.mma.ws): a_tmem bit 1
+    ("WS M64  SS K/K  64x128", 64, 128, 128, 0, 0, 2),
+    ("WS M64  TS K/K  64x128", 64, 128, 128, 0, 0, 3),
+    ("WS M64  TS K/MN 64x128", 64, 128, 128, 0, 1, 3),
+    ("WS M64  TS K/K  64x64", 64, 64, 128, 0, 0, 3),
+    ("WS M128 TS K/K  128x64", 128, 64, 128, 0, 0, 3),
+    ("WS M128 SS K/K  128x64", 128, 64, 128, 0, 0, 2),
 ]
 
 def main():
@@ -27,7 +38,10 @@ def main():
     ctas = torch.cuda.get_device_properties(0).multi_processor_count
     out = torch.zeros(ctas, dtype=torch.int64, device="cuda")
     reps = 2000
+    only = sys.argv[1:]
     for name, m, n, k, amn, bmn, at in CASES:
+        if only and not any(o in name for o in only):
+            continue
         for c in (1, ctas):
             rc = lib.spa2_probe_mma_rate(m, n, k, amn, bmn, at, reps, c, _lib.ptr(out), torch.cuda.current_stream().cuda_stream)
             _lib.check_diag(rc, name)
