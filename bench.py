@@ -395,6 +395,54 @@ def gpu_arm(args, rank: int, world: int, dev):
                                                   else ", burst bf16 GEMM"),
                 "flops_per_launch": kflops[dom], "ms_per_launch": per_kernel_ms[dom],
                 "algorithmic": "Σ_kept c·r_i·c_j·d with c = 4 (fwd), 6 (dQ: S, dP, dQ), 8 (dK/dV: S, dP, dV, dK)"}
+    # ---- on-chip roofline of the dK/dV kernel ----
+    # Per kept 128x64 tile it issues four SS tcgen05 MMA groups with N = 64 (S, dP, dV^T, dK^T: 8
+    # K=16 steps each), whose operand fetch (6 KB per step) runs at ~128 B/clk/SM: ~50 cycles per
+    # step instead of the 32 of the tensor datapath, and not slowed by the kernel's TMA / STS / TMEM
+    # traffic (tools/smem_contend.py).  Its roofline is therefore the same MMA sequence issued back
+    # to back with no dependencies (libspa2_diag spa2_probe_dkdv_mix, one CTA per SM, as many tiles
+    # per CTA as the kernel's), timed right after the kernel: frac = probe time / kernel time.
+    onchip = None
+    try:
+        diag = _lib.load_diag()
+        st = torch.cuda.current_stream()
+        sc = 1.0 / math.sqrt(d)
+        bm_ = spa.BlockMask._trusted(keep, w["b_q"], w["b_kv"], N)
+        lists_ = at.mask_lists(bm_, B, H, N)
+        o_, lse_ = at.fwd(q, k, v, lists_, sc)
+        dq_, dk_, dv_ = at.bwd(q, k, v, o_, do, lse_, lists_, sc)
+        delta_ = torch.empty((B, H, N), device=dev, dtype=torch.float32)
+        _lib.call("spa2_bwd_dq_delta", _lib.view4(q), _lib.view4(k), _lib.view4(v), _lib.view4(o_), _lib.view4(do),
+                  _lib.ptr(lse_), _lib.ptr(delta_), _lib.view4(dq_), _lib.DTYPE_CODES[q.dtype], B, H, N, d, w["b_q"],
+                  w["b_kv"], _lib.ptr(lists_.row_ptr), _lib.ptr(lists_.row_idx), _lib.ptr(lists_.row_order), sc,
+                  st.cuda_stream, stream_obj=st)
+        n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+        tiles = int(keep.sum())
+        reps = -(-tiles // n_sm)
+        cyc = torch.zeros(n_sm, dtype=torch.int64, device=dev)
+
+        def kern():
+            _lib.call("spa2_bwd_dkdv", _lib.view4(q), _lib.view4(k), _lib.view4(v), _lib.view4(do), _lib.ptr(lse_),
+                      _lib.ptr(delta_), _lib.view4(dk_), _lib.view4(dv_), _lib.DTYPE_CODES[q.dtype], B, H, N, d,
+                      w["b_q"], w["b_kv"], _lib.ptr(lists_.col_ptr), _lib.ptr(lists_.col_idx),
+                      _lib.ptr(lists_.col_order), sc, st.cuda_stream, stream_obj=st)
+
+        def seq():
+            _lib.check_diag(diag.spa2_probe_dkdv_mix(reps, 0, n_sm, _lib.ptr(cyc), st.cuda_stream), "dkdv_mix")
+
+        t_k, t_s = [], []
+        for _ in range(5):  # interleaved, medians
+            t_k.append(_time(kern, 3, 1))
+            t_s.append(_time(seq, 3, 1))
+        t_k, t_s = sorted(t_k)[2], sorted(t_s)[2]
+        onchip = {"kernel": "spa2_bwd_dkdv", "bound": "tensor (SS N=64 operand fetch)",
+                  "ms_per_launch": t_k, "floor_ms": t_s, "frac": t_s / t_k, "tiles": tiles,
+                  "floor": "the kernel's own MMA sequence (S, dP K-major; dV^T, dK^T MN-major; 4 x 8 steps per kept "
+                           "tile, warp-batched issue as in the kernel) issued back to back on every SM, "
+                           f"{reps} tiles per SM, no data dependencies (profiles/clock_energy_r02.md)"}
+    except Exception as exc:  # diagnostics only: never fail the bench over it
+        onchip = {"unavailable": repr(exc)[:200]}
+
     # masker: HBM-bound.  K1 = pooling (reads Q and K once) + the fp64 pooled-score GEMM;
     # K0 = the finiteness scan of V (reads V once).
     qk_bytes = 2 * q.numel() * q.element_size()
@@ -416,7 +464,8 @@ def gpu_arm(args, rank: int, world: int, dev):
                       "pooling pass (per-kernel split in profiles/ncu_r02b.md)")
 
     out = {"ms_step": ms_step, "sparsity": sparsity, "clocks": clocks, "launches": launches,
-           "per_kernel_ms": per_kernel_ms, "roofline": roofline, "masker_roofline": masker, "kflops": kflops}
+           "per_kernel_ms": per_kernel_ms, "roofline": roofline, "masker_roofline": masker, "kflops": kflops,
+           "onchip_roofline": onchip}
 
     # ---- e2e through the public API with host buffers ----
     if not args.no_e2e:
@@ -443,8 +492,28 @@ def gpu_arm(args, rank: int, world: int, dev):
         spa.check_pending()
         e_step = _max_over_ranks(a.elapsed_time(b), world, dev) / n_e2e
         nbytes = q.numel() * q.element_size()
+        # the PCIe floor of the same traffic: 4 tensors in and 4 out per step, both directions at
+        # once (pinned buffers, two streams), nothing else running
+        s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        dev_bufs = [torch.empty_like(q) for _ in range(4)]
+
+        def duplex():
+            s_in.wait_stream(torch.cuda.current_stream())
+            s_out.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s_in):
+                for dst, src in zip(dev_bufs, (hq, hk, hv, hdo)):
+                    dst.copy_(src, non_blocking=True)
+            with torch.cuda.stream(s_out):
+                for dst, src in zip(outs, (q, k, v, do)):
+                    dst.copy_(src, non_blocking=True)
+            torch.cuda.current_stream().wait_stream(s_in)
+            torch.cuda.current_stream().wait_stream(s_out)
+
+        pcie_ms = _time(duplex, 5, 1)
+        del dev_bufs
         out["e2e"] = {"value": world * dense_equiv_flops() / (e_step * 1e-3) / 1e12, "unit": UNIT,
                       "h2d_bytes_per_step": 4 * nbytes, "d2h_bytes_per_step": 4 * nbytes, "ms_per_step": e_step,
+                      "pcie_duplex_copy_ms": pcie_ms, "frac_of_pcie_floor": pcie_ms / e_step,
                       "steps": n_e2e, "api": f"paper_2602_13515_b200.host.HostPipeline.fwd_bwd "
                                              f"({args.e2e_groups} head groups, H2D/compute/D2H overlapped)"}
 
@@ -655,7 +724,7 @@ def main():
                     "vs_baseline": None, "dtype": "bf16",
                     "data": "synthetic (Wan2.1-shaped q/k/v: N(0,1) + per-block N(0,0.81) offsets, seeded)",
                     "config": config_dict(world, r["sparsity"]), "roofline": r["roofline"],
-                    "masker_roofline": r["masker_roofline"],
+                    "masker_roofline": r["masker_roofline"], "onchip_roofline": r["onchip_roofline"],
                     "gpu_launches": r["launches"], "clocks": r["clocks"],
                     "per_kernel_ms": {k.replace("spa2_", ""): round(v, 5) for k, v in r["per_kernel_ms"].items()}}
             for key in ("e2e", "dense_baselines", "secondary"):

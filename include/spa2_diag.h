@@ -54,6 +54,22 @@ int spa2_probe_tma_rate2(const void* buf, long long rows, int box_rows, int chun
  * `ctas` CTAs each adding `tiles` 128x128 fp32 tiles into a rotating set of `nslots` tiles of dst. */
 int spa2_probe_red_rate(float* dst, int tiles, int nslots, int ctas, int mode, void* stream);
 
+/* SM clock probe (diagnostic): `ctas` CTAs each spin spin_ns nanoseconds of %globaltimer and
+ * store (clock64 cycles, nanoseconds) elapsed into out[2*cta], out[2*cta+1]; their ratio is
+ * the SM clock in GHz at that moment (e.g. right after a hot kernel on the same stream). */
+int spa2_probe_clock(int spin_ns, int ctas, unsigned long long* out, void* stream);
+
+/* Shared-memory contention probe (diagnostic): warp 0 times reps x 8 SS MMAs (M=128, N=64,
+ * K=16) while, by mode bits, 16 KB bulk copies from gsrc (>= 16 MB) (1), STS.128 stores (2),
+ * LDS.128 loads (4) or TMEM loads (8) run in other warps, (16) rotating the A operand over three
+ * tiles; out[4*cta] = MMA cycles, then bytes moved by each. */
+int spa2_probe_smem_contend(int reps, int mode, int ctas, const void* gsrc, unsigned long long* out, void* stream);
+
+/* dK/dV MMA mix probe (diagnostic): the four MMA groups of one K6 tile (S, dP K-major; dVᵀ, dKᵀ
+ * MN-major; M=128 N=64, 8 K=16 steps each) issued back to back by one thread, reps tiles;
+ * which = 0 all four, 1 S+dP only, 2 dVᵀ+dKᵀ only.  cycles[cta] = clock64 span. */
+int spa2_probe_dkdv_mix(int reps, int which, int ctas, unsigned long long* cycles, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -78,6 +78,9 @@ DIAG_SIGNATURES = {
     "spa2_probe_tmem_rate": ([_I32, _I32, _I32, _I32, _P, _P], _I32),
     "spa2_probe_tma_rate2": ([_P, ctypes.c_longlong, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P, _P], _I32),
     "spa2_probe_red_rate": ([_P, _I32, _I32, _I32, _I32, _P], _I32),
+    "spa2_probe_clock": ([_I32, _I32, _P, _P], _I32),
+    "spa2_probe_smem_contend": ([_I32, _I32, _I32, _P, _P, _P], _I32),
+    "spa2_probe_dkdv_mix": ([_I32, _I32, _I32, _P, _P], _I32),
 }
 
 # Kernels each entry point launches (for the bench's gpu_launches accounting).

@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
   if (warp == 1) tmem_alloc(tmem_holder, 512);
   tc_fence_before();
   __syncthreads();
-  SPA2_CT(1, 0); SPA2_CT(1, 2); SPA2_CTC(1, 4);
+  SPA2_CT(1, 0); SPA2_CT(1, 2); SPA2_CTC(1, 4); SPA2_CTC(1, 4);
   tc_fence_after();
   const uint32_t tbase = *tmem_holder;
   pdl_wait();  // everything above touched only this CTA's smem/TMEM
@@ -617,7 +617,7 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
-  SPA2_CT(1, 1); SPA2_CTC(1, 5);
+  SPA2_CT(1, 1); SPA2_CTC(1, 5); SPA2_CTC(1, 5);
   if (warp == 1) tmem_dealloc(tbase, 512);
 }
 
@@ -639,9 +639,31 @@ struct DkvRoles {
 #ifndef SPA2_DKDV_NKV
 #define SPA2_DKDV_NKV 1  // [K | V] item buffers (2: the next item's K/V load overlaps this item)
 #endif
-template <int HD, int NSL_ = SPA2_DKDV_NSL, int NPB_ = 1, int NKV_ = SPA2_DKDV_NKV>
+// Operand slots: Q and dO in separate pools, Q(g) in slot g mod NQ and dO(g) in slot
+// NQ + g mod (NSL-NQ).  Q is held from S(g) to dKᵀ(g), the tile's last MMA, dO only until dVᵀ(g),
+// so Q gets the larger pool; with one interleaved ring (NQ = 0: operand u = 2g + [dO] in slot
+// u mod NSL) dO(g+2) reused Q(g)'s slot and waited for dKᵀ(g).  Per-CTA cycles per kept tile
+// (tools/ab_cycles.sh): NQ 3 2139-2147, interleaved 2180, NQ 4 2445, NQ 2 slower.
+#ifndef SPA2_DKDV_NQ
+#define SPA2_DKDV_NQ 3
+#endif
+#ifndef SPA2_DKDV_NPB
+#define SPA2_DKDV_NPB 1  // [P | dS] smem buffers (2 with NSL = 4: 2362 cycles per tile vs 2180)
+#endif
+template <int HD, int NSL_ = SPA2_DKDV_NSL, int NPB_ = SPA2_DKDV_NPB, int NKV_ = SPA2_DKDV_NKV>
 struct Dkv5Cfg {
-  static constexpr int NSL = NSL_;  // 32 KB operand slots: Q(g) -> slot 2g mod NSL, dO(g) -> slot 2g+1 mod NSL
+  static constexpr int NSL = NSL_;  // 32 KB operand slots
+  static constexpr int NQ = SPA2_DKDV_NQ, ND = NSL - SPA2_DKDV_NQ;
+  static_assert(NQ == 0 || (NQ >= 1 && ND >= 1), "slot pools");
+  // slot and use count of operand `which` (0 = Q, 1 = dO) of tile g
+  __device__ static __forceinline__ int slot(int g, int which) {
+    if constexpr (NQ == 0) return (2 * g + which) % NSL;
+    else return which ? NQ + g % (ND > 0 ? ND : 1) : g % (NQ > 0 ? NQ : 1);
+  }
+  __device__ static __forceinline__ uint32_t use(int g, int which) {
+    if constexpr (NQ == 0) return (uint32_t)((2 * g + which) / NSL);
+    else return (uint32_t)(which ? g / (ND > 0 ? ND : 1) : g / (NQ > 0 ? NQ : 1));
+  }
   static constexpr int NPB = NPB_;  // [P | dS] buffers
   static constexpr int NKV = NKV_;  // [K | V] buffers: item it uses buffer it % NKV
   static constexpr int KV_BYTES = BKV * HD * 2;
@@ -661,7 +683,7 @@ struct Dkv5Cfg {
 // different warps (Q: S and dKᵀ, dO: dP and dVᵀ), so its slot is released by two commits, one
 // per issuer; the dVᵀ issuer also waits for dO(g) to land (P(g) existing only proves S(g)
 // finished).  P and dS share one smem buffer.
-template <int HD, int EWW, bool HALF = false, int NSL_ = SPA2_DKDV_NSL, int NPB_ = 1>
+template <int HD, int EWW, bool HALF = false, int NSL_ = SPA2_DKDV_NSL, int NPB_ = SPA2_DKDV_NPB>
 __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
     k_dkdv5(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
            const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmDO, const BwdParams p) {
@@ -718,7 +740,7 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
   if (warp == 1) tmem_alloc(tmem_holder, 512);
   tc_fence_before();
   __syncthreads();
-  SPA2_CT(2, 0); SPA2_CT(2, 2); SPA2_CTC(2, 4);
+  SPA2_CT(2, 0); SPA2_CT(2, 2); SPA2_CTC(2, 4); SPA2_CTC(2, 4);
   tc_fence_after();
   const uint32_t tbase = *tmem_holder;
   pdl_wait();  // everything above touched only this CTA's smem/TMEM
@@ -746,9 +768,9 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
         tma_load_5d(kv_dst + kb * 2 * C::KV_BYTES, tmKV, &kv_full[kb], 0, m.blk * BKV, 0, hh, bb);
         for (int t = 0; t < m.n; ++t, ++g) {
           const int i = list_blk(p.idx[m.beg + t]);
-          const int u = 2 * g + (second ? 1 : 0);  // operand index: Q(g) even, dO(g) odd
-          const int s = u % NSL;
-          if (u >= NSL) mbar_wait(&sl_empty[s], ((uint32_t)(u / NSL) + 1u) & 1u);
+          const int s = C::slot(g, second ? 1 : 0);
+          const uint32_t use = C::use(g, second ? 1 : 0);
+          if (use >= 1) mbar_wait(&sl_empty[s], (use + 1u) & 1u);
           mbar_expect_tx(&sl_full[s], C::Q_BYTES);
           tma_load_5d(smem + C::OFF_SL + s * C::Q_BYTES, tmR, &sl_full[s], 0, i * BQ, 0, hh, bb);
         }
@@ -784,10 +806,11 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
         const uint64_t dV = dK + (uint64_t)(C::KV_BYTES >> 4);
         const uint32_t b = (uint32_t)(c.g & 1);
         if (c.g >= 2) mbar_wait(&sdp_read[b], (uint32_t)((c.g - 2) >> 1) & 1u);  // buffer b read out
-        const int uq = 2 * c.g, ud = uq + 1;
-        mbar_wait(&sl_full[uq % NSL], (uint32_t)(uq / NSL) & 1u);
+        const int sq = C::slot(c.g, 0), sd = C::slot(c.g, 1);
+        mbar_wait(&sl_full[sq], C::use(c.g, 0) & 1u);
+        SPA2_TR(29, c.g);
         tc_fence_after();
-        const uint64_t dQ = dSLk0 + (uint64_t)(uq % NSL) * SLOT16, dDO = dSLk0 + (uint64_t)(ud % NSL) * SLOT16;
+        const uint64_t dQ = dSLk0 + (uint64_t)sq * SLOT16, dDO = dSLk0 + (uint64_t)sd * SLOT16;
 #ifdef SPA2_MMA_BATCH
         if constexpr (HD == 128) {
           mma_bf16_ss_k8_w<2ull, (uint64_t)(BQ * 128 / 16), 2ull, (uint64_t)(BKV * 128 / 16)>(tbase + C::S_COL + b * 64, dQ, dK,
@@ -803,8 +826,8 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
           }
         }
         mma_commit_w(&s_full[b]);
-        mma_commit_w(&sl_empty[uq % NSL]);  // S(g) no longer reads Q(g) once complete
-        mbar_wait(&sl_full[ud % NSL], (uint32_t)(ud / NSL) & 1u);
+        mma_commit_w(&sl_empty[sq]);  // S(g) no longer reads Q(g) once complete
+        mbar_wait(&sl_full[sd], C::use(c.g, 1) & 1u);
         tc_fence_after();
 #ifdef SPA2_MMA_BATCH
         if constexpr (HD == 128) {
@@ -822,21 +845,23 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
         }
         mma_commit_w(&dp_full[b]);
         SPA2_TR(16, c.g);
-        mma_commit_w(&sl_empty[ud % NSL]);  // dP(g) no longer reads dO(g) once complete
+        mma_commit_w(&sl_empty[sd]);  // dP(g) no longer reads dO(g) once complete
         if (c.t == c.n - 1) mma_commit_w(&kv_empty[c.it % NKV]);  // K_j / V_j are only read by S and dP
       }
     } else {
       for (; c.valid; cursor_next(c, p, p.T_n)) {
-        const int uq = 2 * c.g, ud = uq + 1;
+        const int sq = C::slot(c.g, 0), sd = C::slot(c.g, 1);
         const uint32_t acc = tbase + C::ACC_COL + (uint32_t)((c.it & 1) * 128);
-        const uint64_t dQm = dSLm0 + (uint64_t)(uq % NSL) * SLOT16, dDOm = dSLm0 + (uint64_t)(ud % NSL) * SLOT16;
+        const uint64_t dQm = dSLm0 + (uint64_t)sq * SLOT16, dDOm = dSLm0 + (uint64_t)sd * SLOT16;
         const bool first = c.t == 0;
         if (first && c.it >= 2) mbar_wait(&acc_empty[c.it & 1], ((uint32_t)(c.it >> 1) + 1u) & 1u);
         const int pb = c.g % NPB;
         const uint64_t pbo = (uint64_t)pb * 2 * PB16;
+        SPA2_TR(27, c.g);
         mbar_wait(&p_full[pb], (uint32_t)(c.g / NPB) & 1u);
         // dVᵀ reads dO(g): P(g) only proves S(g) finished, not that dO(g) has landed
-        mbar_wait(&sl_full[ud % NSL], (uint32_t)(ud / NSL) & 1u);
+        mbar_wait(&sl_full[sd], C::use(c.g, 1) & 1u);
+        SPA2_TR(17, c.g);
         tc_fence_after();
 #ifdef SPA2_MMA_BATCH
         mma_bf16_ss_k8_w<128ull, 512ull, 128ull, 512ull>(acc, dDOm, dPm + pbo, idT, first ? 0u : 1u);
@@ -846,8 +871,10 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
           mma_bf16_w(acc, dDOm + (uint64_t)(ks * 128), dPm + pbo + (uint64_t)(ks * 128), idT, (!first || ks > 0) ? 1u : 0u);
 #endif
         mma_commit_w(&p_free[pb]);
-        mma_commit_w(&sl_empty[ud % NSL]);  // dVᵀ(g) was the other reader of dO(g)
+        mma_commit_w(&sl_empty[sd]);  // dVᵀ(g) was the other reader of dO(g)
+
         mbar_wait(&ds_full[pb], (uint32_t)(c.g / NPB) & 1u);
+        SPA2_TR(28, c.g);
         tc_fence_after();
 #ifdef SPA2_MMA_BATCH
         mma_bf16_ss_k8_w<128ull, 512ull, 128ull, 512ull>(acc + 64, dQm, dDSm + pbo, idT, first ? 0u : 1u);
@@ -858,7 +885,7 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
 #endif
         mma_commit_w(&ds_free[pb]);
         SPA2_TR(18, c.g);
-        mma_commit_w(&sl_empty[uq % NSL]);  // dKᵀ(g) was the other reader of Q(g)
+        mma_commit_w(&sl_empty[sq]);  // dKᵀ(g) was the other reader of Q(g)
         if (c.t == c.n - 1) mma_commit_w(&acc_full[c.it & 1]);
       }
     }
@@ -914,7 +941,11 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
           pk[c] = pack_bf16(pv[2 * c], pv[2 * c + 1]);
         }
         const int pb = g % NPB;
+#ifdef SPA2_TRACE
+        if (warp == 2 && pk[CPT / 2 - 1] != 0xFFFFFFFFu) SPA2_TR(31, g);  // P computed (stamp after the math)
+#endif
         if (g >= NPB) mbar_wait(&p_free[pb], (uint32_t)((g - NPB) / NPB) & 1u);  // dV of tile g-NPB has read P
+        if (warp == 2) SPA2_TR(23, g);
         const uint32_t sP = smem_u32(smem + C::OFF_PDS) + (uint32_t)(pb * 2 * C::PB), sDS = sP + C::PB;
 #pragma unroll
         for (int u = 0; u < CPT / 8; ++u) {
@@ -925,6 +956,9 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
         mbar_arrive(&p_full[pb]);
         mbar_wait(&dp_full[b], (uint32_t)(g >> 1) & 1u);
         if (warp == 2) SPA2_TR(20, g);
+#ifdef SPA2_TRACE
+        if (warp == 2) SPA2_TR(30, g);  // (dP wait passed; kind 30 = same point, kept for the tool)
+#endif
         tc_fence_after();
         uint32_t dr[CPT];
         if constexpr (CPT == 32) tmem_ld32(tbase + lane_off + C::DP_COL + b * 64 + col0, dr);
@@ -939,6 +973,7 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
           pk[c] = pack_bf16(ds.x, ds.y);
         }
         if (g >= NPB) mbar_wait(&ds_free[pb], (uint32_t)((g - NPB) / NPB) & 1u);  // dK of tile g-NPB has read dS
+        if (warp == 2) SPA2_TR(24, g);
 #pragma unroll
         for (int u = 0; u < CPT / 8; ++u) {
           const uint32_t off = sw128_offset((uint32_t)row, col0 / 8 + (uint32_t)u);
@@ -1000,7 +1035,7 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
-  SPA2_CT(2, 1); SPA2_CTC(2, 5);
+  SPA2_CT(2, 1); SPA2_CTC(2, 5); SPA2_CTC(2, 5);
   if (warp == 1) tmem_dealloc(tbase, 512);
 }
 

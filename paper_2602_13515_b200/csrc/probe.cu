@@ -737,3 +737,271 @@ extern "C" int spa2_probe_red_rate(float* dst, int tiles, int nslots, int ctas, 
   SPA2_LAUNCH_CHECK();
   return SPA2_OK;
 }
+
+// ---- SM clock probe (diagnostic): the clock the SMs run at right now ----
+// Each CTA spins `spin_ns` of %globaltimer and records (Δclock64, Δglobaltimer); launched right
+// after a hot kernel on the same stream it reports the clock the power manager had settled on
+// for that kernel (the regulator reacts on a millisecond scale; NVML's samples are coarser).
+namespace spa2 {
+namespace {
+__global__ void k_probe_clock(int spin_ns, unsigned long long* out) {
+  if (threadIdx.x != 0) return;
+  unsigned long long g0, g1, c0, c1;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c0));
+  do {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+  } while (g1 - g0 < (unsigned long long)spin_ns);
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c1));
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+  out[2 * blockIdx.x] = c1 - c0;
+  out[2 * blockIdx.x + 1] = g1 - g0;
+}
+}  // namespace
+}  // namespace spa2
+
+extern "C" int spa2_probe_clock(int spin_ns, int ctas, unsigned long long* out, void* stream) {
+  SPA2_REQUIRE(spin_ns > 0 && ctas > 0 && out, SPA2_ERR_VALUE, "probe_clock: bad arguments");
+  spa2::k_probe_clock<<<ctas, 32, 0, (cudaStream_t)stream>>>(spin_ns, out);
+  SPA2_LAUNCH_CHECK();
+  return SPA2_OK;
+}
+
+// ---- shared-memory contention probe (diagnostic) ----
+// Does other traffic slow the tensor core's SS operand reads?  Warp 0 issues reps x 8 SS MMAs
+// M=128 N=64 K=16 (A 128x128 and B 64x128 bf16, K-major SW128, 6 KB of operands per MMA) and
+// times them; meanwhile, by `mode` bits, warps 1-2 stream 16 KB bulk copies global->smem (1),
+// warps 4-7 store STS.128 (2), warps 8-11 load LDS.128 (4), warps 4-7 instead load TMEM with
+// tcgen05.ld.32x32b.x32 from other columns (8, replaces 2), and (16) each rep's A operand rotates
+// over three 32 KB tiles.  out[cta*4 + {0,1,2,3}] = MMA cycles, bulk bytes, STS or TMEM bytes,
+// LDS bytes moved while the MMAs ran.
+namespace spa2 {
+namespace {
+__global__ void __launch_bounds__(384) k_smem_contend(int reps, int mode, const uint8_t* gsrc,
+                                                     unsigned long long* out) {
+  extern __shared__ uint8_t smem_dyn[];
+  __shared__ uint64_t bar_mma, bars[2];
+  __shared__ uint32_t tmem_base;
+  __shared__ volatile int stop;
+  __shared__ unsigned long long moved[3];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+  // [0, 96K) three A tiles | [96K, 112K) B | [112K, 144K) bulk | [144K, 160K) STS | [160K, 176K) LDS
+  for (int i = threadIdx.x; i < 114688 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(base)[i] = make_uint4(0x3f803f80u, 0x3f803f80u, 0x3f803f80u, 0x3f803f80u);
+  if (warp_id() == 0) tmem_alloc(&tmem_base, 512);
+  if (threadIdx.x == 32) {
+    mbar_init(&bar_mma, 1);
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    stop = 0;
+    moved[0] = moved[1] = moved[2] = 0;
+    fence_mbar_init();
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tmem_base;
+  const int warp = (int)warp_id();
+  if (warp == 0) {
+    if (lane_id() == 0) {
+      constexpr uint32_t idS = idesc_bf16(128, 64, false, false);
+      const uint64_t dA = sw128_desc(smem_u32(base), 16, 1024);
+      const uint64_t dB = sw128_desc(smem_u32(base + 98304), 16, 1024);
+      const bool rot = (mode & 16) != 0;
+      const uint64_t t0 = clock64();
+      for (int r = 0; r < reps; ++r) {
+        const uint64_t aoff = rot ? (uint64_t)(((r % 3) * 32768) >> 4) : 0ull;
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+          const uint64_t qo = (uint64_t)((((ks * 16) / 64) * 128 * 128 + ((ks * 16) % 64) * 2) >> 4);
+          const uint64_t ko = (uint64_t)((((ks * 16) / 64) * 64 * 128 + ((ks * 16) % 64) * 2) >> 4);
+          mma_bf16(tbase + (uint32_t)((r & 3) * 64), dA + aoff + qo, dB + ko, idS, ks > 0 ? 1u : 0u);
+        }
+      }
+      mma_commit(&bar_mma);
+      mbar_wait(&bar_mma, 0);
+      out[blockIdx.x * 4] = clock64() - t0;
+      stop = 1;
+    }
+  } else if ((warp == 1 || warp == 2) && (mode & 1)) {
+    if (lane_id() == 0) {
+      const int w = warp - 1;
+      uint8_t* dst = base + 114688 + w * 16384;
+      uint32_t ph = 0, x = 777u + (uint32_t)w;
+      unsigned long long n = 0;
+      while (!stop) {
+        x = x * 1664525u + 1013904223u;
+        mbar_expect_tx(&bars[w], 16384);
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(dst)),
+                     "l"(gsrc + (size_t)((x >> 8) % 1024) * 16384), "r"(16384), "r"(smem_u32(&bars[w]))
+                     : "memory");
+        mbar_wait(&bars[w], ph);
+        ph ^= 1u;
+        n += 16384;
+      }
+      atomicAdd(&moved[0], n);
+    }
+  } else if (warp >= 4 && warp < 8 && (mode & 8)) {
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    unsigned long long n = 0;
+    uint32_t acc = 0;
+    while (!stop) {
+      uint32_t r[32];
+      tmem_ld32(tbase + lane_off + 256u + (uint32_t)((n >> 7) & 3) * 32u, r);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) acc ^= r[i];
+      n += 128;
+    }
+    if (acc == 0x12345678u) n += 1;
+    atomicAdd(&moved[1], n);
+  } else if (warp >= 4 && warp < 8 && (mode & 2)) {
+    const uint32_t dst = smem_u32(base + 147456) + (uint32_t)((warp - 4) * 4096);
+    unsigned long long n = 0;
+    uint32_t v = threadIdx.x;
+    while (!stop) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        st_shared_v4(dst + (uint32_t)(((u * 32 + (int)lane_id()) * 16) & 4095), v, v + 1, v + 2, v + 3);
+        ++v;
+      }
+      n += 8 * 16;
+    }
+    atomicAdd(&moved[1], n);
+  } else if (warp >= 8 && (mode & 4)) {
+    const uint4* src = reinterpret_cast<const uint4*>(base + 163840 + (warp - 8) * 4096);
+    unsigned long long n = 0;
+    uint32_t acc = 0;
+    while (!stop) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        uint32_t x0, x1, x2, x3;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3)
+                     : "r"(smem_u32(src + ((u * 32 + (int)lane_id()) & 255))));
+        acc ^= x0 ^ x1 ^ x2 ^ x3;
+      }
+      n += 8 * 16;
+    }
+    if (acc == 0x12345678u) n += 1;  // keep the loads
+    atomicAdd(&moved[2], n);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    out[blockIdx.x * 4 + 1] = moved[0];
+    out[blockIdx.x * 4 + 2] = moved[1];
+    out[blockIdx.x * 4 + 3] = moved[2];
+  }
+  if (warp == 0) tmem_dealloc(tbase, 512);
+}
+}  // namespace
+}  // namespace spa2
+
+extern "C" int spa2_probe_smem_contend(int reps, int mode, int ctas, const void* gsrc, unsigned long long* out,
+                                       void* stream) {
+  const size_t smem = 180224 + 1024;
+  SPA2_CUDA_TRY(cudaFuncSetAttribute(spa2::k_smem_contend, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  spa2::k_smem_contend<<<ctas, 384, smem, (cudaStream_t)stream>>>(reps, mode, (const uint8_t*)gsrc, out);
+  SPA2_LAUNCH_CHECK();
+  return SPA2_OK;
+}
+
+// ---- dK/dV MMA mix probe (diagnostic): the K6 kernel's four MMA groups per tile in isolation ----
+// S = Q Kᵀ, dP = dO Vᵀ (M=128 N=64, K-major SW128 A and B), dVᵀ += dOᵀ P, dKᵀ += Qᵀ dS (M=128 N=64,
+// MN-major A and B), each 8 K=16 steps, with exactly the kernel's descriptors and its
+// warp-collective batched issue (mma_bf16_ss_k8_w), back to back without dependencies.
+// which: bits 0-1: 0 = all four per tile, 1 = S and dP only, 2 = dVᵀ and dKᵀ only; 32 = S only;
+// 64 = issue from a single thread (one MMA per asm block) instead of the warp batch.
+// cycles[cta] = clock64 span of reps tiles.
+namespace spa2 {
+namespace {
+__global__ void __launch_bounds__(128) k_dkdv_mix(int reps, int which, unsigned long long* cycles) {
+  extern __shared__ uint8_t smem_dyn[];
+  __shared__ uint64_t bar_mma;
+  __shared__ uint32_t tmem_base;
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+  for (int i = threadIdx.x; i < 131072 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(base)[i] = make_uint4(0x3f803f80u, 0x3f803f80u, 0x3f803f80u, 0x3f803f80u);
+  if (warp_id() == 0) tmem_alloc(&tmem_base, 512);
+  if (threadIdx.x == 32) {
+    mbar_init(&bar_mma, 1);
+    fence_mbar_init();
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tmem_base;
+  const bool single = (which & 64) != 0;
+  if (warp_id() == 0 && (!single || lane_id() == 0)) {
+    // [0,32K) Q | [32K,64K) dO | [64K,80K) K | [80K,96K) V | [96K,112K) P | [112K,128K) dS
+    constexpr uint32_t idS = idesc_bf16(128, 64, false, false);
+    constexpr uint32_t idT = idesc_bf16(128, 64, true, true);
+    const uint64_t dQk = sw128_desc(smem_u32(base), 16, 1024), dDOk = sw128_desc(smem_u32(base + 32768), 16, 1024);
+    const uint64_t dK = sw128_desc(smem_u32(base + 65536), 16, 1024), dV = sw128_desc(smem_u32(base + 81920), 16, 1024);
+    const uint64_t dQm = sw128_desc(smem_u32(base), 128 * 128, 1024), dDOm = sw128_desc(smem_u32(base + 32768), 128 * 128, 1024);
+    const uint64_t dPm = sw128_desc(smem_u32(base + 98304), 128 * 128, 1024), dDSm = sw128_desc(smem_u32(base + 114688), 128 * 128, 1024);
+    const int w2 = which & 3;
+    const uint64_t t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+      const uint32_t b = (uint32_t)(r & 1) * 64u;
+      if (w2 != 2) {
+        if (single) {
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks) {
+            const uint64_t qo = (uint64_t)((((ks * 16) / 64) * 128 * 128 + ((ks * 16) % 64) * 2) >> 4);
+            const uint64_t ko = (uint64_t)((((ks * 16) / 64) * 64 * 128 + ((ks * 16) % 64) * 2) >> 4);
+            mma_bf16(tbase + b, dQk + qo, dK + ko, idS, ks > 0 ? 1u : 0u);
+          }
+        } else {
+          mma_bf16_ss_k8_w<2ull, (uint64_t)(128 * 128 / 16), 2ull, (uint64_t)(64 * 128 / 16)>(tbase + b, dQk, dK, idS, 0u);
+        }
+        if (!(which & 32)) {
+          if (single) {
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+              const uint64_t qo = (uint64_t)((((ks * 16) / 64) * 128 * 128 + ((ks * 16) % 64) * 2) >> 4);
+              const uint64_t ko = (uint64_t)((((ks * 16) / 64) * 64 * 128 + ((ks * 16) % 64) * 2) >> 4);
+              mma_bf16(tbase + 128u + b, dDOk + qo, dV + ko, idS, ks > 0 ? 1u : 0u);
+            }
+          } else {
+            mma_bf16_ss_k8_w<2ull, (uint64_t)(128 * 128 / 16), 2ull, (uint64_t)(64 * 128 / 16)>(tbase + 128u + b, dDOk, dV,
+                                                                                              idS, 0u);
+          }
+        }
+      }
+      if (w2 != 1 && !(which & 32)) {
+        if (single) {
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks) mma_bf16(tbase + 256u, dDOm + (uint64_t)(ks * 128), dPm + (uint64_t)(ks * 128), idT, 1u);
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks) mma_bf16(tbase + 320u, dQm + (uint64_t)(ks * 128), dDSm + (uint64_t)(ks * 128), idT, 1u);
+        } else {
+          mma_bf16_ss_k8_w<128ull, 512ull, 128ull, 512ull>(tbase + 256u, dDOm, dPm, idT, 1u);
+          mma_bf16_ss_k8_w<128ull, 512ull, 128ull, 512ull>(tbase + 320u, dQm, dDSm, idT, 1u);
+        }
+      }
+    }
+    if (!single) {
+      mma_commit_w(&bar_mma);
+    } else {
+      mma_commit(&bar_mma);
+    }
+    mbar_wait(&bar_mma, 0);
+    if (lane_id() == 0) cycles[blockIdx.x] = clock64() - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp_id() == 0) tmem_dealloc(tbase, 512);
+}
+}  // namespace
+}  // namespace spa2
+
+extern "C" int spa2_probe_dkdv_mix(int reps, int which, int ctas, unsigned long long* cycles, void* stream) {
+  const size_t smem = 131072 + 1024;
+  SPA2_CUDA_TRY(cudaFuncSetAttribute(spa2::k_dkdv_mix, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  spa2::k_dkdv_mix<<<ctas, 128, smem, (cudaStream_t)stream>>>(reps, which, cycles);
+  SPA2_LAUNCH_CHECK();
+  return SPA2_OK;
+}
