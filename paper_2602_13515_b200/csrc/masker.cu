@@ -98,6 +98,17 @@ __global__ void __launch_bounds__(256) k_pool(spa2_view q, spa2_view k, int H, i
 // order into 8 float64 chains) with the row loads software-pipelined: the next 8 rows are in
 // flight while the current 8 are added, so twice the bytes are outstanding per thread.
 // ---------------------------------------------------------------------------------------
+// Streaming loads for the pooling pass (each byte of Q and K is read exactly once): not
+// allocating in L1 took K1 (pooling + scores) from 69.0 to 63.4 us at the bench shape
+// (tools/masker_time.py; the L2 prefetch-size hint made no difference).
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+#define POOL_LD(p) ld_stream(p)
 __global__ void __launch_bounds__(256) k_pool_bf16_pipe(spa2_view q, spa2_view k, int H, int N, int d, int b_q,
                                                         int b_kv, int T_m, int T_n, int64_t BH,
                                                         double* __restrict__ qbar, double* __restrict__ kbar,
@@ -130,11 +141,11 @@ __global__ void __launch_bounds__(256) k_pool_bf16_pipe(spa2_view q, spa2_view k
     for (int e = 0; e < 8; ++e) acc[e] = 0.0;
     uint4 cur[U], nxt[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) cur[u] = u < rows ? __ldg(base + u * rs) : make_uint4(0, 0, 0, 0);
+    for (int u = 0; u < U; ++u) cur[u] = u < rows ? POOL_LD(base + u * rs) : make_uint4(0, 0, 0, 0);
     for (int r0 = 0; r0 < rows; r0 += U) {
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        nxt[u] = (r0 + U + u < rows) ? __ldg(base + (int64_t)(r0 + U + u) * rs) : make_uint4(0, 0, 0, 0);
+        nxt[u] = (r0 + U + u < rows) ? POOL_LD(base + (int64_t)(r0 + U + u) * rs) : make_uint4(0, 0, 0, 0);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         if (r0 + u < rows) {
@@ -165,6 +176,7 @@ __global__ void __launch_bounds__(256) k_pool_bf16_pipe(spa2_view q, spa2_view k
 // a plain store, so the flag may live in mapped pinned host memory (no atomics over PCIe).
 // ---------------------------------------------------------------------------------------
 constexpr int kK0Unroll = 8;
+#define K0_LD(p) __ldg(p)  // (the streaming form of the pooling loads measured 3 % slower here)
 __global__ void __launch_bounds__(256) k_nonfinite_bf16(spa2_view x, int H, int N, int cpr_log2,
                                                         int32_t* __restrict__ nonfinite) {
   pdl_wait();
@@ -183,7 +195,7 @@ __global__ void __launch_bounds__(256) k_nonfinite_bf16(spa2_view x, int H, int 
 #pragma unroll
     for (int u = 0; u < kK0Unroll; ++u) {
       const int c = c0 + u * stride;
-      v[u] = c < chunks ? __ldg(reinterpret_cast<const uint4*>(base + (int64_t)(c >> cpr_log2) * x.sn + (c & cmask) * 8))
+      v[u] = c < chunks ? K0_LD(reinterpret_cast<const uint4*>(base + (int64_t)(c >> cpr_log2) * x.sn + (c & cmask) * 8))
                         : make_uint4(0, 0, 0, 0);
     }
 #pragma unroll
