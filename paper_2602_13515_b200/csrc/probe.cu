@@ -804,26 +804,28 @@ __global__ void __launch_bounds__(384) k_smem_contend(int reps, int mode, const 
   const uint32_t tbase = tmem_base;
   const int warp = (int)warp_id();
   if (warp == 0) {
-    if (lane_id() == 0) {
-      constexpr uint32_t idS = idesc_bf16(128, 64, false, false);
-      const uint64_t dA = sw128_desc(smem_u32(base), 16, 1024);
-      const uint64_t dB = sw128_desc(smem_u32(base + 98304), 16, 1024);
-      const bool rot = (mode & 16) != 0;
-      const uint64_t t0 = clock64();
+    // warp-collective batched issue exactly as in the kernels (one elect per 8-step group)
+    constexpr uint32_t idS = idesc_bf16(128, 64, false, false);
+    const uint64_t dA = sw128_desc(smem_u32(base), 16, 1024);
+    const uint64_t dB = sw128_desc(smem_u32(base + 98304), 16, 1024);
+    const bool rot = (mode & 16) != 0;
+    const bool ts = (mode & 32) != 0;  // A from TMEM columns [384, 448) (TS form, 32-cycle steps)
+    const uint64_t t0 = clock64();
+    if (ts) {
+      for (int r = 0; r < reps; ++r)
+        mma_bf16_ts_k8_w<8u, 2ull, (uint64_t)(64 * 128 / 16)>(tbase + (uint32_t)((r & 3) * 64), tbase + 384u, dB, idS, 0u);
+    } else {
       for (int r = 0; r < reps; ++r) {
         const uint64_t aoff = rot ? (uint64_t)(((r % 3) * 32768) >> 4) : 0ull;
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks) {
-          const uint64_t qo = (uint64_t)((((ks * 16) / 64) * 128 * 128 + ((ks * 16) % 64) * 2) >> 4);
-          const uint64_t ko = (uint64_t)((((ks * 16) / 64) * 64 * 128 + ((ks * 16) % 64) * 2) >> 4);
-          mma_bf16(tbase + (uint32_t)((r & 3) * 64), dA + aoff + qo, dB + ko, idS, ks > 0 ? 1u : 0u);
-        }
+        mma_bf16_ss_k8_w<2ull, (uint64_t)(128 * 128 / 16), 2ull, (uint64_t)(64 * 128 / 16)>(
+            tbase + (uint32_t)((r & 3) * 64), dA + aoff, dB, idS, 0u);
       }
-      mma_commit(&bar_mma);
-      mbar_wait(&bar_mma, 0);
-      out[blockIdx.x * 4] = clock64() - t0;
-      stop = 1;
     }
+    mma_commit_w(&bar_mma);
+    mbar_wait(&bar_mma, 0);
+    if (lane_id() == 0) out[blockIdx.x * 4] = clock64() - t0;
+    __syncwarp();
+    if (lane_id() == 0) stop = 1;
   } else if ((warp == 1 || warp == 2) && (mode & 1)) {
     if (lane_id() == 0) {
       const int w = warp - 1;

@@ -20,7 +20,8 @@ def main():
     reps = 4000
     names = {0: "MMA alone", 16: "A rotating (3 tiles)", 1: "+ bulk copies", 2: "+ STS.128", 4: "+ LDS.128",
              8: "+ TMEM loads", 3: "+ bulk + STS", 7: "+ bulk + STS + LDS", 8 | 16: "rot + TMEM loads",
-             1 | 2 | 16: "rot + bulk + STS", 1 | 8 | 16: "rot + bulk + TMEM"}
+             1 | 2 | 16: "rot + bulk + STS", 1 | 8 | 16: "rot + bulk + TMEM",
+             32: "TS MMA alone", 32 | 8: "TS + TMEM loads", 32 | 1 | 8: "TS + bulk + TMEM loads"}
     for mode, name in names.items():
         rc = lib.spa2_probe_smem_contend(reps, mode, ctas, _lib.ptr(src), _lib.ptr(out), torch.cuda.current_stream().cuda_stream)
         _lib.check_diag(rc, "smem_contend")
@@ -29,7 +30,7 @@ def main():
         cyc = o[0].item()
         per = cyc / (reps * 8)
         bpc = [o[i].item() / cyc for i in (1, 2, 3)]
-        mma_bpc = 6144 / per
+        mma_bpc = (2048 if mode & 32 else 6144) / per
         print(f"{name:22s} {per:6.1f} cyc per K=16 SS MMA ({mma_bpc:5.1f} B/clk operand reads)  "
               f"bulk {bpc[0]:5.1f}  STS/TMEM {bpc[1]:5.1f}  LDS {bpc[2]:5.1f} B/clk  total {mma_bpc + sum(bpc):6.1f} B/clk")
 
