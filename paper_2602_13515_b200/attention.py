@@ -86,7 +86,22 @@ class BlockLists:
     half: bool = False  # entries carry half-block codes (a b_q = 64·odd mask): kernels take b_q = 64
 
 
-def _native_keep(bm: BlockMask, B: int, H: int, N: int) -> torch.Tensor:
+def _mask_on(bm: BlockMask, device: torch.device | None) -> torch.Tensor:
+    """The mask's device keep tensor on ``device``: a host (numpy) mask is uploaded there (cached
+    per device); a CUDA mask must already live there (the kernels take raw device pointers)."""
+    keep = bm.dev
+    if device is None or keep.device == device:
+        return keep
+    if not bm.on_host:
+        raise ValueError(f"BlockMask is on {keep.device}, the inputs are on {device}")
+    key = ("dev", str(device))
+    hit = bm._cache.get(key)
+    if hit is None:
+        hit = bm._cache[key] = keep.to(device)
+    return hit
+
+
+def _native_keep(bm: BlockMask, B: int, H: int, N: int, device: torch.device | None = None) -> torch.Tensor:
     """keep at the kernel grid (128, 64) as uint8 codes [B, H, T_m, T_n]: 0 dropped, 1 kept.
 
     Masks on coarser grids (b_q ∈ 128ℕ, b_kv ∈ 64ℕ) are refined exactly.  Masks with
@@ -95,7 +110,7 @@ def _native_keep(bm: BlockMask, B: int, H: int, N: int) -> torch.Tensor:
     3 = only the bottom half — the kernels give the other half's rows P = 0 for that tile
     (list entries carry the code in bits 30-31, see csrc/common.cuh)."""
     t_m, t_n = num_blocks(N, BQ), num_blocks(N, BKV)
-    keep = bm.dev
+    keep = _mask_on(bm, device)
     if keep.dim() == 2:
         keep = keep.view(1, 1, *keep.shape)
     codes = None
@@ -149,12 +164,12 @@ def build_lists(keep_u8: torch.Tensor, half: bool = False) -> BlockLists:
     return lists
 
 
-def _lists_with_order(bm: BlockMask, B: int, H: int, N: int, visit) -> BlockLists:
+def _lists_with_order(bm: BlockMask, B: int, H: int, N: int, visit, device=None) -> BlockLists:
     """Row lists honouring the reference's ``_block_order`` test hook (attention.py:74-81,
     97-99), which is called with the MASK grid's row index and kept columns, as in the
     reference; its order is then refined to the kernel grid (mask column j covers kernel
     columns j·(b_kv/64) ...).  Test-only: copies the mask to the host."""
-    keep_u8 = _native_keep(bm, B, H, N)
+    keep_u8 = _native_keep(bm, B, H, N, device)
     base = build_lists(keep_u8, half=_half_codes(bm))
     t_m, t_n = keep_u8.shape[-2:]
     mk = bm.keep_numpy().astype(bool)
@@ -205,12 +220,13 @@ def _lists_with_order(bm: BlockMask, B: int, H: int, N: int, visit) -> BlockList
                       base.half)
 
 
-def mask_lists(bm: BlockMask, B: int, H: int, N: int) -> BlockLists:
-    """Block lists of ``bm`` for a [B, H, N, d] problem, cached on the (immutable) mask."""
-    key = ("lists", B, H, N)
+def mask_lists(bm: BlockMask, B: int, H: int, N: int, device: torch.device | None = None) -> BlockLists:
+    """Block lists of ``bm`` for a [B, H, N, d] problem on ``device`` (default: the mask's own),
+    cached on the (immutable) mask."""
+    key = ("lists", B, H, N, None if device is None else str(device))
     hit = bm._cache.get(key)
     if hit is None:
-        hit = build_lists(_native_keep(bm, B, H, N), half=_half_codes(bm))
+        hit = build_lists(_native_keep(bm, B, H, N, device), half=_half_codes(bm))
         bm._cache[key] = hit
     return hit
 
@@ -361,7 +377,8 @@ def _run(q4, k4, v4, bm: BlockMask, qb, counter, flag, check_finite, visit=None,
     B, H, N, d = q4.shape
     if bm.n_tokens != N:
         raise ValueError(f"mask built for {bm.n_tokens} tokens, inputs have {N}")
-    lists = mask_lists(bm, B, H, N) if visit is None else _lists_with_order(bm, B, H, N, visit)
+    lists = (mask_lists(bm, B, H, N, q4.device) if visit is None
+             else _lists_with_order(bm, B, H, N, visit, q4.device))
     native = (bm.b_q, bm.b_kv) == (BQ, BKV)
     ctr = torch.zeros((1,), device=q4.device, dtype=torch.int64) if counter is not None and native else None
     verdict = None
@@ -450,7 +467,7 @@ def attention_backward(q, k, v, bm: BlockMask, d_out, *, check_finite: bool | st
     if flag is not None:
         _scan_finite(flag, q4, k4, v4, do4)
         finite_guard.submit(flag, "q, k, v or d_out", block=check_finite == "sync", device=q4.device)
-    lists = mask_lists(bm, B, H, N)
+    lists = mask_lists(bm, B, H, N, q4.device)
     scale = 1.0 / math.sqrt(d)
     with torch.no_grad():
         o, lse = fwd(q4, k4, v4, lists, scale)

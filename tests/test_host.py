@@ -79,3 +79,23 @@ def test_require_device_fails_loudly_without_cuda():
         pytest.skip("GPU present")
     with pytest.raises(RuntimeError):
         mk.pooled_map([[0.0, 1.0]], [[0.0, 1.0]], mk.SparsityConfig(0.5, 0.5, 1, 1))
+
+
+def test_mask_device_placement():
+    """Masks follow the inputs' device: a host (numpy) mask is uploaded to it once per device;
+    a device mask on another device than the inputs is an error, not a silent copy."""
+    import types
+
+    import torch
+
+    from paper_2602_13515_b200 import attention as at
+
+    keep = torch.ones((2, 4), dtype=torch.bool)
+    host = types.SimpleNamespace(dev=keep, on_host=True, _cache={})
+    moved = at._mask_on(host, torch.device("meta"))
+    assert moved.device.type == "meta"
+    assert at._mask_on(host, torch.device("meta")) is moved  # cached per device
+    assert at._mask_on(host, torch.device("cpu")) is keep
+    dev_mask = types.SimpleNamespace(dev=keep, on_host=False, _cache={})
+    with pytest.raises(ValueError, match="inputs are on"):
+        at._mask_on(dev_mask, torch.device("meta"))
