@@ -410,6 +410,7 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
         SPA2_TR(7, cc.g);
         const int b = cc.g & 1, sv = cc.g % NV;
         if (cc.g >= 2) mbar_wait(&dq_done[b], (uint32_t)((cc.g - 2) >> 1) & 1u);
+        SPA2_TR(13, cc.g);
         mbar_wait(&v_full[sv], (uint32_t)(cc.g / NV) & 1u);
         const uint64_t dV = dV0 + (uint64_t)sv * KV16;
         const uint32_t sb = tbase + C::SDP_COL + (uint32_t)(b * 128) + 64u;
@@ -436,6 +437,7 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
         const int b = cc.g & 1, sk = cc.g % NK;
         if (cc.t == 0 && cc.it >= 1) mbar_wait(acc_empty, (uint32_t)(cc.it - 1) & 1u);
         mbar_wait(&ds_full[b], (uint32_t)(cc.g >> 1) & 1u);
+        SPA2_TR(12, cc.g);
         tc_fence_after();
         const uint64_t dKm = dKm0 + (uint64_t)sk * KV16;
         const uint32_t sb = tbase + C::SDP_COL + (uint32_t)(b * 128);
@@ -546,8 +548,21 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
         else tmem_st8(sb + 64u + (uint32_t)col0, pk);
         tmem_st_wait();
         if (warp == 2) SPA2_TR(5, g);
+#ifdef SPA2_TRACE
+        {  // trace builds: stamp the LAST elementwise warp to finish dS(g) (kind 11)
+          __shared__ uint32_t tr_cnt[2];
+          uint32_t old = 0;
+          if (lane == 0) old = atomicAdd(&tr_cnt[b], 1u);
+          old = __shfl_sync(0xffffffffu, old, 0);
+          if ((old % EWW) == EWW - 1) SPA2_TR(11, g);
+          tc_fence_before();
+          mbar_arrive(&ds_full[b]);
+          if ((old % EWW) == EWW - 1) SPA2_TR(14, g);
+        }
+#else
         tc_fence_before();
         mbar_arrive(&ds_full[b]);
+#endif
       }
     }
   } else if (warp < R::PROD2) {

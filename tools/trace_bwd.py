@@ -55,6 +55,17 @@ stat("EW: dP committed -> dP landed", e[4] - e[1])
 stat("EW: dP landed -> dS stored", e[5] - e[4])
 stat("EW: S landed -> dP landed", e[4] - e[3])
 stat("dQ: dS stored -> dQ committed", e[2] - e[5])
+last = ev[11, :n] - t0
+stat("EW: dS stored (warp 2) -> last warp's dS stored", last - e[5])
+stat("dQ: last warp's dS stored -> dQ committed", e[2] - last)
+e12, e13 = ev[12, :n] - t0, ev[13, :n] - t0
+stat("hop: last warp's dS stored -> dQ warp past ds_full wait", e12 - last)
+e14 = ev[14, :n] - t0
+stat("  of which: last warp's arrive instruction (release)", e14 - last)
+stat("  of which: arrive done -> dQ warp past wait", e12 - e14)
+stat("dQ warp: past wait -> dQ committed (issue)", e[2] - e12)
+stat("dP warp: past dq_done wait -> dP committed", e[1] - e13)
+stat("hop: dQ(g-2) committed -> dP warp past dq_done wait", e13[2:] - e[2][:-2])
 stat("dP(g) commit - dQ(g-2) commit", e[1][2:] - e[2][:-2])
 stat("S(g) commit - EW S landed(g-2)", e[0][2:] - e[3][:-2])
 stat("EW: dS stored(g) -> S landed(g+1)", e[3][1:] - e[5][:-1])
