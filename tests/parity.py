@@ -4,7 +4,7 @@ The GPU path computes on bf16 operands with fp32 accumulation (tensor cores) and
 bf16 O / dQ / dK / dV and fp32 LSE; the reference computes in float64 on the *same*
 bf16-representable inputs.  Stated tolerances (north_star: "max-abs/rel and cosine"),
 set to about twice the worst error measured over the whole GPU suite on a B200
-(tests/golden/parity_measured.json: out rel 5.6e-3, dq 6.8e-3, dk 5.9e-3, dv 4.9e-3,
+(tests/golden/parity_measured.json: out rel 5.6e-3, dq 7.0e-3, dk 5.9e-3, dv 4.9e-3,
 cosine >= 0.999993, LSE 1.9e-6 absolute):
 
   out       cosine >= 0.99998  and  max|Δ| <= 1.2e-2 · max|ref|
