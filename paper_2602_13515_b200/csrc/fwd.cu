@@ -37,7 +37,10 @@ using namespace ptx;
 constexpr int BQ = 128;
 constexpr int BKV = 64;
 constexpr int kFwdThreads = 224;  // + warp 6: second TMA producer (V)
-constexpr float kRescaleThreshold = 8.0f;  // log2 units: P entries stay <= 2^8
+#ifndef SPA2_FWD_RESCALE
+#define SPA2_FWD_RESCALE 8.0f
+#endif
+constexpr float kRescaleThreshold = SPA2_FWD_RESCALE;  // log2 units: P entries stay <= 2^8
 #ifndef SPA2_FWD1_POLY_PAIRS
 #define SPA2_FWD1_POLY_PAIRS 4  // exponential pairs (of 32 per row and tile) by FMA polynomial (forward span: 0: 295.8, 4: 291.9, 8: 296.4, 12: 295.7 us)
 #endif
