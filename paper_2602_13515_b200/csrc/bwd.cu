@@ -864,19 +864,22 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
         if (c.t == c.n - 1) mma_commit_w(&kv_empty[c.it % NKV]);  // K_j / V_j are only read by S and dP
       }
     } else {
-      for (; c.valid; cursor_next(c, p, p.T_n)) {
-        const int sq = C::slot(c.g, 0), sd = C::slot(c.g, 1);
-        const uint32_t acc = tbase + C::ACC_COL + (uint32_t)((c.it & 1) * 128);
-        const uint64_t dQm = dSLm0 + (uint64_t)sq * SLOT16, dDOm = dSLm0 + (uint64_t)sd * SLOT16;
-        const bool first = c.t == 0;
-        if (first && c.it >= 2) mbar_wait(&acc_empty[c.it & 1], ((uint32_t)(c.it >> 1) + 1u) & 1u);
-        const int pb = c.g % NPB;
+      // dVᵀ(g) += dO_iᵀ P (after P is in smem), then dKᵀ(g) += Q_iᵀ dS (after dS).  Issuing
+      // dVᵀ(g+1) before dKᵀ(g) measured 3 250 vs 2 152 cycles per tile (P(g+1) waits for dVᵀ(g),
+      // dS(g+1) for dKᵀ(g)).
+      auto issue_dv = [&](const Cursor& cc) {
+        const int sd = C::slot(cc.g, 1);
+        const uint32_t acc = tbase + C::ACC_COL + (uint32_t)((cc.it & 1) * 128);
+        const uint64_t dDOm = dSLm0 + (uint64_t)sd * SLOT16;
+        const bool first = cc.t == 0;
+        if (first && cc.it >= 2) mbar_wait(&acc_empty[cc.it & 1], ((uint32_t)(cc.it >> 1) + 1u) & 1u);
+        const int pb = cc.g % NPB;
         const uint64_t pbo = (uint64_t)pb * 2 * PB16;
-        SPA2_TR(27, c.g);
-        mbar_wait(&p_full[pb], (uint32_t)(c.g / NPB) & 1u);
+        SPA2_TR(27, cc.g);
+        mbar_wait(&p_full[pb], (uint32_t)(cc.g / NPB) & 1u);
         // dVᵀ reads dO(g): P(g) only proves S(g) finished, not that dO(g) has landed
-        mbar_wait(&sl_full[sd], C::use(c.g, 1) & 1u);
-        SPA2_TR(17, c.g);
+        mbar_wait(&sl_full[sd], C::use(cc.g, 1) & 1u);
+        SPA2_TR(17, cc.g);
         tc_fence_after();
 #ifdef SPA2_MMA_BATCH
         mma_bf16_ss_k8_w<128ull, 512ull, 128ull, 512ull>(acc, dDOm, dPm + pbo, idT, first ? 0u : 1u);
@@ -887,9 +890,16 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
 #endif
         mma_commit_w(&p_free[pb]);
         mma_commit_w(&sl_empty[sd]);  // dVᵀ(g) was the other reader of dO(g)
-
-        mbar_wait(&ds_full[pb], (uint32_t)(c.g / NPB) & 1u);
-        SPA2_TR(28, c.g);
+      };
+      auto issue_dk = [&](const Cursor& cc) {
+        const int sq = C::slot(cc.g, 0);
+        const uint32_t acc = tbase + C::ACC_COL + (uint32_t)((cc.it & 1) * 128);
+        const uint64_t dQm = dSLm0 + (uint64_t)sq * SLOT16;
+        const bool first = cc.t == 0;
+        const int pb = cc.g % NPB;
+        const uint64_t pbo = (uint64_t)pb * 2 * PB16;
+        mbar_wait(&ds_full[pb], (uint32_t)(cc.g / NPB) & 1u);
+        SPA2_TR(28, cc.g);
         tc_fence_after();
 #ifdef SPA2_MMA_BATCH
         mma_bf16_ss_k8_w<128ull, 512ull, 128ull, 512ull>(acc + 64, dQm, dDSm + pbo, idT, first ? 0u : 1u);
@@ -899,9 +909,13 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
           mma_bf16_w(acc + 64, dQm + (uint64_t)(ks * 128), dDSm + pbo + (uint64_t)(ks * 128), idT, (!first || ks > 0) ? 1u : 0u);
 #endif
         mma_commit_w(&ds_free[pb]);
-        SPA2_TR(18, c.g);
+        SPA2_TR(18, cc.g);
         mma_commit_w(&sl_empty[sq]);  // dKᵀ(g) was the other reader of Q(g)
-        if (c.t == c.n - 1) mma_commit_w(&acc_full[c.it & 1]);
+        if (cc.t == cc.n - 1) mma_commit_w(&acc_full[cc.it & 1]);
+      };
+      for (; c.valid; cursor_next(c, p, p.T_n)) {
+        issue_dv(c);
+        issue_dk(c);
       }
     }
   } else if (warp < R::EPI0) {
