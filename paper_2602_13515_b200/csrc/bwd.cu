@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
   if (warp == 1) tmem_alloc(tmem_holder, 512);
   tc_fence_before();
   __syncthreads();
-  SPA2_CT(1, 0); SPA2_CT(1, 2); SPA2_CTC(1, 4); SPA2_CTC(1, 4);
+  SPA2_CT(1, 0); SPA2_CT(1, 2); SPA2_CTC(1, 4);
   tc_fence_after();
   const uint32_t tbase = *tmem_holder;
   pdl_wait();  // everything above touched only this CTA's smem/TMEM
@@ -632,7 +632,7 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
-  SPA2_CT(1, 1); SPA2_CTC(1, 5); SPA2_CTC(1, 5);
+  SPA2_CT(1, 1); SPA2_CTC(1, 5);
   if (warp == 1) tmem_dealloc(tbase, 512);
 }
 
@@ -755,7 +755,7 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
   if (warp == 1) tmem_alloc(tmem_holder, 512);
   tc_fence_before();
   __syncthreads();
-  SPA2_CT(2, 0); SPA2_CT(2, 2); SPA2_CTC(2, 4); SPA2_CTC(2, 4);
+  SPA2_CT(2, 0); SPA2_CT(2, 2); SPA2_CTC(2, 4);
   tc_fence_after();
   const uint32_t tbase = *tmem_holder;
   pdl_wait();  // everything above touched only this CTA's smem/TMEM
@@ -1064,7 +1064,7 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
-  SPA2_CT(2, 1); SPA2_CTC(2, 5); SPA2_CTC(2, 5);
+  SPA2_CT(2, 1); SPA2_CTC(2, 5);
   if (warp == 1) tmem_dealloc(tbase, 512);
 }
 
