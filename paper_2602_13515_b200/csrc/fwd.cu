@@ -97,12 +97,6 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(o_final + 1);
 
   const int warp = (int)warp_id(), lane = (int)lane_id();
-  const int w = p.row_order ? p.row_order[blockIdx.x] : (int)blockIdx.x;
-  const int bh = w / p.T_m, qi = w % p.T_m;
-  const int hh = bh % p.H, bb = bh / p.H;
-  const int beg = p.row_ptr[w];
-  const int n = p.row_ptr[w + 1] - beg;
-  const int32_t* list = p.row_idx + beg;
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
@@ -126,6 +120,16 @@ __global__ void __launch_bounds__(kFwdThreads, 2)
   SPA2_CT(0, 0); SPA2_CT(0, 2);
   tc_fence_after();
   const uint32_t tbase = *tmem_holder;
+  // programmatic dependent launch: the setup above overlapped the list kernel's tail; the block
+  // lists (and q/k/v) are read only after it completes
+  pdl_wait();
+  pdl_trigger();
+  const int w = p.row_order ? p.row_order[blockIdx.x] : (int)blockIdx.x;
+  const int bh = w / p.T_m, qi = w % p.T_m;
+  const int hh = bh % p.H, bb = bh / p.H;
+  const int beg = p.row_ptr[w];
+  const int n = p.row_ptr[w + 1] - beg;
+  const int32_t* list = p.row_idx + beg;
 
   if (n == 0) {
     // A query block with no kept key block (rejected by BlockMask; reachable only through
@@ -369,7 +373,7 @@ int launch_fwd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& 
   using C = FwdCfg<HD, P_TMEM>;
   auto kern = k_fwd<HD, P_TMEM, HALF>;
   SPA2_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-  kern<<<grid, kFwdThreads, C::SMEM, st>>>(tq, tk, tv, to, prm);
+  SPA2_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(kFwdThreads), C::SMEM, st, tq, tk, tv, to, prm));
   SPA2_LAUNCH_CHECK();
   return SPA2_OK;
 }
