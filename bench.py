@@ -367,7 +367,7 @@ def gpu_arm(args, rank: int, world: int, dev):
     for _ in range(n_k):
         step()
     torch.cuda.synchronize()
-    per_kernel_ms = {n: (sum(a.elapsed_time(b) for a, b in lst) / len(lst) if lst else 0.0)
+    per_kernel_ms = {n: (statistics.median(a.elapsed_time(b) for a, b in lst) if lst else 0.0)
                      for n, lst in _lib.STATS.timing.items()}
     _lib.STATS.timing = None
 
