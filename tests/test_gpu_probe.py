@@ -46,3 +46,33 @@ def test_probe_tmem_cp_a_operand(n, k):
     torch.cuda.synchronize()
     want = a.float() @ b.float().t()
     assert (d - want).abs().max().item() <= 1e-3 * max(1.0, want.abs().max().item())
+
+
+def test_probe_rates_and_clock():
+    """The rate probes behind DESIGN §5 / bench.py's on-chip roofline run and report sane
+    numbers: an SS N=64 MMA step costs more than the 32-cycle datapath floor and a TS step
+    holds it; the dK/dV MMA sequence costs at least its 4 x 8 x 32-cycle floor per tile; the
+    SM clock probe reads a plausible clock."""
+    lib = _lib.load_diag()
+    st = torch.cuda.current_stream().cuda_stream
+    ctas = 4
+    src = torch.zeros(16 * 1024 * 1024 + 65536, dtype=torch.uint8, device="cuda")
+    out = torch.zeros(ctas * 4, dtype=torch.int64, device="cuda")
+    per = {}
+    for mode in (0, 32, 1 | 2 | 4):
+        _lib.check_diag(lib.spa2_probe_smem_contend(200, mode, ctas, _lib.ptr(src), _lib.ptr(out), st), "contend")
+        torch.cuda.synchronize()
+        per[mode] = out.view(ctas, 4)[:, 0].double().mean().item() / (200 * 8)
+    assert 40.0 < per[0] < 70.0, per  # SS N=64: operand fetch above the datapath rate
+    assert 28.0 < per[32] < 40.0, per  # TS N=64: at the 32-cycle floor
+    assert per[1 | 2 | 4] < 1.2 * per[0], per  # other shared-memory traffic barely slows it
+    cyc = torch.zeros(ctas, dtype=torch.int64, device="cuda")
+    _lib.check_diag(lib.spa2_probe_dkdv_mix(100, 0, ctas, _lib.ptr(cyc), st), "dkdv_mix")
+    torch.cuda.synchronize()
+    per_tile = cyc.double().mean().item() / 100
+    assert 1024 <= per_tile < 3000, per_tile
+    clk = torch.zeros(2 * ctas, dtype=torch.int64, device="cuda")
+    _lib.check_diag(lib.spa2_probe_clock(20000, ctas, _lib.ptr(clk), st), "clock")
+    torch.cuda.synchronize()
+    ghz = (clk.view(ctas, 2)[:, 0].double() / clk.view(ctas, 2)[:, 1].double()).median().item()
+    assert 0.3 < ghz < 2.5, ghz
