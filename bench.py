@@ -401,7 +401,7 @@ def gpu_arm(args, rank: int, world: int, dev):
     # step instead of the 32 of the tensor datapath, and not slowed by the kernel's TMA / STS / TMEM
     # traffic (tools/smem_contend.py).  Its roofline is therefore the same MMA sequence issued back
     # to back with no dependencies (libspa2_diag spa2_probe_dkdv_mix, one CTA per SM, as many tiles
-    # per CTA as the kernel's), timed right after the kernel: frac = probe time / kernel time.
+    # per CTA as the kernel's), timed interleaved with the kernel: frac = probe time / kernel time.
     onchip = None
     try:
         diag = _lib.load_diag()
@@ -439,7 +439,8 @@ def gpu_arm(args, rank: int, world: int, dev):
                   "ms_per_launch": t_k, "floor_ms": t_s, "frac": t_s / t_k, "tiles": tiles,
                   "floor": "the kernel's own MMA sequence (S, dP K-major; dV^T, dK^T MN-major; 4 x 8 steps per kept "
                            "tile, warp-batched issue as in the kernel) issued back to back on every SM, "
-                           f"{reps} tiles per SM, no data dependencies (profiles/clock_energy_r02.md)"}
+                           f"{reps} tiles per SM, no data dependencies (profiles/traces_r02.md, "
+                           "profiles/clock_energy_r02.md)"}
     except Exception as exc:  # diagnostics only: never fail the bench over it
         onchip = {"unavailable": repr(exc)[:200]}
 
