@@ -70,6 +70,10 @@ int spa2_probe_smem_contend(int reps, int mode, int ctas, const void* gsrc, unsi
  * which = 0 all four, 1 S+dP only, 2 dVᵀ+dKᵀ only.  cycles[cta] = clock64 span. */
 int spa2_probe_dkdv_mix(int reps, int which, int ctas, unsigned long long* cycles, void* stream);
 
+/* tcgen05.cp rate probe (diagnostic): per rep, 8 tcgen05.cp.128x256b (one 32 KB K-major tile
+ * into TMEM) and/or one 8-step SS MMA group (M=128, N=64), by mode bits 1 / 2; cycles[cta]. */
+int spa2_probe_cp_rate(int reps, int mode, int ctas, unsigned long long* cycles, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -81,6 +81,7 @@ DIAG_SIGNATURES = {
     "spa2_probe_clock": ([_I32, _I32, _P, _P], _I32),
     "spa2_probe_smem_contend": ([_I32, _I32, _I32, _P, _P, _P], _I32),
     "spa2_probe_dkdv_mix": ([_I32, _I32, _I32, _P, _P], _I32),
+    "spa2_probe_cp_rate": ([_I32, _I32, _I32, _P, _P], _I32),
 }
 
 # Kernels each entry point launches (for the bench's gpu_launches accounting).

@@ -1007,3 +1007,64 @@ extern "C" int spa2_probe_dkdv_mix(int reps, int which, int ctas, unsigned long 
   SPA2_LAUNCH_CHECK();
   return SPA2_OK;
 }
+
+// ---- tcgen05.cp rate probe (diagnostic): smem -> TMEM copies alone, SS MMAs alone, both ----
+// One warp issues, per rep, 8 tcgen05.cp.128x256b (a 32 KB K-major SW128 tile into TMEM
+// columns [256, 320)) and/or one 8-step SS MMA group (M=128, N=64, from other smem) into
+// columns [0, 64).  mode: 1 = copies only, 2 = MMAs only, 3 = both.  cycles[cta] = span.
+namespace spa2 {
+namespace {
+__global__ void __launch_bounds__(128) k_cp_rate(int reps, int mode, unsigned long long* cycles) {
+  extern __shared__ uint8_t smem_dyn[];
+  __shared__ uint64_t bar_mma;
+  __shared__ uint32_t tmem_base;
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+  for (int i = threadIdx.x; i < 98304 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(base)[i] = make_uint4(0x3f803f80u, 0x3f803f80u, 0x3f803f80u, 0x3f803f80u);
+  if (warp_id() == 0) tmem_alloc(&tmem_base, 512);
+  if (threadIdx.x == 32) {
+    mbar_init(&bar_mma, 1);
+    fence_mbar_init();
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tmem_base;
+  if (warp_id() == 0) {
+    // [0, 32K) copy source (K-major SW128 128 x 128) | [32K, 64K) MMA A | [64K, 80K) MMA B
+    const uint64_t dC = sw128_desc(smem_u32(base), 16, 1024);
+    const uint64_t dA = sw128_desc(smem_u32(base + 32768), 16, 1024);
+    const uint64_t dB = sw128_desc(smem_u32(base + 65536), 16, 1024);
+    constexpr uint32_t idS = idesc_bf16(128, 64, false, false);
+    const uint64_t t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+      if (mode & 1) {
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+          const uint64_t qo = (uint64_t)((((ks * 16) / 64) * 128 * 128 + ((ks * 16) % 64) * 2) >> 4);
+          tmem_cp_128x256b_w(tbase + 256u + (uint32_t)(ks * 8), dC + qo);
+        }
+      }
+      if (mode & 2)
+        mma_bf16_ss_k8_w<2ull, (uint64_t)(128 * 128 / 16), 2ull, (uint64_t)(64 * 128 / 16)>(
+            tbase + (uint32_t)((r & 1) * 64), dA, dB, idS, 0u);
+    }
+    mma_commit_w(&bar_mma);
+    mbar_wait(&bar_mma, 0);
+    if (lane_id() == 0) cycles[blockIdx.x] = clock64() - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp_id() == 0) tmem_dealloc(tbase, 512);
+}
+}  // namespace
+}  // namespace spa2
+
+extern "C" int spa2_probe_cp_rate(int reps, int mode, int ctas, unsigned long long* cycles, void* stream) {
+  const size_t smem = 98304 + 1024;
+  SPA2_CUDA_TRY(cudaFuncSetAttribute(spa2::k_cp_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  spa2::k_cp_rate<<<ctas, 128, smem, (cudaStream_t)stream>>>(reps, mode, cycles);
+  SPA2_LAUNCH_CHECK();
+  return SPA2_OK;
+}

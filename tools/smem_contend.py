@@ -46,6 +46,13 @@ def main():
         groups = 1 if which & 32 else (4 if (which & 3) == 0 else 2)
         print(f"{name:34s} {per:7.1f} cyc per tile ({per / groups:6.1f} per 8-step group, {per / groups / 8:5.1f} per K step)")
 
+    for mode, name in ((1, "tcgen05.cp 32 KB tile"), (2, "SS MMA group (8 x N=64)"), (3, "both, interleaved")):
+        _lib.check_diag(lib.spa2_probe_cp_rate(reps, mode, ctas, _lib.ptr(cyc), torch.cuda.current_stream().cuda_stream),
+                        "cp_rate")
+        torch.cuda.synchronize()
+        per = cyc.double().mean().item() / reps
+        print(f"{name:34s} {per:7.1f} cyc per rep" + (f" ({32768 / per:5.1f} B/clk)" if mode == 1 else ""))
+
 
 if __name__ == "__main__":
     main()
