@@ -444,25 +444,35 @@ def gpu_arm(args, rank: int, world: int, dev):
     except Exception as exc:  # diagnostics only: never fail the bench over it
         onchip = {"unavailable": repr(exc)[:200]}
 
-    # masker: HBM-bound.  K1 = pooling (reads Q and K once) + the fp64 pooled-score GEMM;
-    # K0 = the finiteness scan of V (reads V once).
-    qk_bytes = 2 * q.numel() * q.element_size()
-    hbm = peaks["hbm_gbs"]
-    # the masker's two HBM passes timed back to back (30 launches between two events, so launch
-    # overhead does not count): K0 reads V once; K1 reads Q and K once (pooling) and then runs the
-    # small fp64 pooled-score GEMM
+    # masker: HBM-bound passes.  K1a = block-mean pooling (reads Q and K once; the reference's
+    # block_mean_pool), K1 = K1a + the small fp64 pooled-score GEMM (what sparse_attention runs);
+    # K0 = the finiteness scan of V (reads V once).  Each timed over 30 back-to-back launches
+    # between two CUDA events, so launch overhead does not count.
     from paper_2602_13515_b200 import masker as mk_
 
+    qk_bytes = 2 * q.numel() * q.element_size()
+    hbm = peaks["hbm_gbs"]
     flag = torch.zeros((1,), dtype=torch.int32, pin_memory=True)
+    t_m_, t_n_ = -(-N // w["b_q"]), -(-N // w["b_kv"])
+    pool_ws = torch.empty(B * H * (t_m_ + t_n_) * d, device=dev, dtype=torch.float64)
+    st_ = torch.cuda.current_stream()
+
+    def k1a():
+        _lib.call("spa2_block_mean_pool", _lib.view4(q), _lib.view4(k), _lib.DTYPE_CODES[q.dtype], B, H, N, d,
+                  w["b_q"], w["b_kv"], _lib.ptr(pool_ws), _lib.ptr(pool_ws[B * H * t_m_ * d:]), None,
+                  st_.cuda_stream, stream_obj=st_)
+
     k0_ms = _time(lambda: at._scan_finite(flag, v), 30, 3)
+    k1a_ms = _time(k1a, 30, 3)
     k1_ms = _time(lambda: mk_._pooled_probs(q, k, w["b_q"], w["b_kv"], None, softmax=False), 30, 3)
     masker = {"bound": "hbm", "unit": "GB/s", "peak": hbm,
               "K0_finite_scan_v": {"bytes": qk_bytes // 2, "ms": k0_ms, "achieved": (qk_bytes // 2) / (k0_ms * 1e-3) / 1e9},
+              "K1a_block_mean_pool": {"bytes": qk_bytes, "ms": k1a_ms, "achieved": qk_bytes / (k1a_ms * 1e-3) / 1e9},
               "K1_pool_scores": {"bytes": qk_bytes, "ms": k1_ms, "achieved": qk_bytes / (k1_ms * 1e-3) / 1e9}}
-    for kk in ("K1_pool_scores", "K0_finite_scan_v"):
+    for kk in ("K1a_block_mean_pool", "K1_pool_scores", "K0_finite_scan_v"):
         masker[kk]["frac"] = masker[kk]["achieved"] / hbm
-    masker["note"] = ("back-to-back launches, CUDA events; K1's time includes the fp64 pooled-score GEMM after the "
-                      "pooling pass (per-kernel split in profiles/ncu_r02b.md)")
+    masker["note"] = ("K1a = the pooling pass alone (the HBM-bound part); K1 adds the fp64 pooled-score GEMM "
+                      "(tensor-core DMMA, ~20 us) that sparse_attention runs after it (profiles/ncu_r02c.md)")
 
     out = {"ms_step": ms_step, "sparsity": sparsity, "clocks": clocks, "launches": launches,
            "per_kernel_ms": per_kernel_ms, "roofline": roofline, "masker_roofline": masker, "kflops": kflops,

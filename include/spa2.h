@@ -66,6 +66,14 @@ int spa2_pooled_map(spa2_view q, spa2_view k, int dtype, int64_t B, int64_t H, i
                     int64_t d, int64_t b_q, int64_t b_kv, double* probs, double* workspace,
                     int32_t* nonfinite, void* stream);
 
+/* K1a alone: numerics.block_mean_pool (numerics.py:55-65) of q (b_q-row groups) and k (b_kv-row
+ * groups) into qbar float64 [B*H, T_m, d] and kbar float64 [B*H, T_n, d], with exactly
+ * spa2_pooled_map's pooling arithmetic (rows added in order in float64, ragged tail divided by
+ * its true count) and its non-finite flag.  The HBM-bound part of the masker. */
+int spa2_block_mean_pool(spa2_view q, spa2_view k, int dtype, int64_t B, int64_t H, int64_t N, int64_t d,
+                         int64_t b_q, int64_t b_kv, double* qbar, double* kbar, int32_t* nonfinite,
+                         void* stream);
+
 /* ---- K2: select --------------------------------------------------------------------
  * Replaces masker._descending_order/top_k_mask/top_p_row_count/top_p_mask/hybrid_mask
  * (masker.py:113-146).  Per row of `probs` (float64 [rows, t_n]): stable descending

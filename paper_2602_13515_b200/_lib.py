@@ -53,6 +53,7 @@ SIGNATURES = {
     "spa2_select": ([_P, _I64, _I64, _I64, _F64, _P, _P, _P], _I32),
     "spa2_check_finite": ([View, _I32, _I64, _I64, _I64, _I64, _P, _P], _I32),
     "spa2_pooled_scores": ([View, View, _I32, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P, _P, _P], _I32),
+    "spa2_block_mean_pool": ([View, View, _I32, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P, _P, _P], _I32),
     "spa2_select_scores": ([_P, _I64, _I64, _I64, _F64, _P, _P, _P], _I32),
     "spa2_build_lists": ([_P, _I64, _I64, _I64, _P, _P, _P, _P, _P, _P, _P, _P], _I32),
     "spa2_fwd": ([View, View, View, View, _P, _I32, _I64, _I64, _I64, _I64, _I64, _I64, _P, _P, _P, _F32, _P, _P],
@@ -85,7 +86,7 @@ DIAG_SIGNATURES = {
 }
 
 # Kernels each entry point launches (for the bench's gpu_launches accounting).
-KERNELS_PER_CALL = {"spa2_check_finite": 1, "spa2_pooled_map": 3, "spa2_select": 1, "spa2_pooled_scores": 2, "spa2_select_scores": 1, "spa2_build_lists": 3, "spa2_fwd": 1,
+KERNELS_PER_CALL = {"spa2_check_finite": 1, "spa2_block_mean_pool": 1, "spa2_pooled_map": 3, "spa2_select": 1, "spa2_pooled_scores": 2, "spa2_select_scores": 1, "spa2_build_lists": 3, "spa2_fwd": 1,
                     "spa2_bwd_delta": 1, "spa2_bwd_dq": 1, "spa2_bwd_dkdv": 1, "spa2_bwd": 2,
                     "spa2_bwd_dq_delta": 1}
 

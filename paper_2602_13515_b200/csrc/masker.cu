@@ -917,6 +917,29 @@ extern "C" int spa2_select(const double* probs, int64_t rows, int64_t t_n, int64
   return SPA2_OK;
 }
 
+extern "C" int spa2_block_mean_pool(spa2_view q, spa2_view k, int dtype, int64_t B, int64_t H, int64_t N, int64_t d,
+                                    int64_t b_q, int64_t b_kv, double* qbar, double* kbar, int32_t* nonfinite,
+                                    void* stream) {
+  SPA2_REQUIRE(B >= 1 && H >= 1 && N >= 1 && d >= 1, SPA2_ERR_VALUE,
+               "block_mean_pool: bad shape B=%lld H=%lld N=%lld d=%lld", (long long)B, (long long)H,
+               (long long)N, (long long)d);
+  SPA2_REQUIRE(b_q >= 1 && b_kv >= 1, SPA2_ERR_VALUE, "block sizes must be >= 1: b_q=%lld, b_kv=%lld",
+               (long long)b_q, (long long)b_kv);
+  SPA2_REQUIRE(q.ptr && k.ptr && qbar && kbar, SPA2_ERR_VALUE, "block_mean_pool: null pointer");
+  SPA2_REQUIRE(N < (1ll << 31), SPA2_ERR_UNSUPPORTED, "block_mean_pool: N too large");
+  SPA2_REQUIRE(kbar == qbar + B * H * ceil_div(N, b_q) * d, SPA2_ERR_VALUE,
+               "block_mean_pool: kbar must directly follow qbar (one workspace)");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t T_m = ceil_div(N, b_q), T_n = ceil_div(N, b_kv);
+  switch (dtype) {
+    case SPA2_BF16: return launch_pool<__nv_bfloat16>(q, k, B, H, N, d, b_q, b_kv, T_m, T_n, qbar, kbar, nonfinite, st);
+    case SPA2_F16: return launch_pool<__half>(q, k, B, H, N, d, b_q, b_kv, T_m, T_n, qbar, kbar, nonfinite, st);
+    case SPA2_F32: return launch_pool<float>(q, k, B, H, N, d, b_q, b_kv, T_m, T_n, qbar, kbar, nonfinite, st);
+    case SPA2_F64: return launch_pool<double>(q, k, B, H, N, d, b_q, b_kv, T_m, T_n, qbar, kbar, nonfinite, st);
+    default: SPA2_REQUIRE(false, SPA2_ERR_UNSUPPORTED, "block_mean_pool: unsupported dtype %d", dtype);
+  }
+}
+
 extern "C" int spa2_pooled_scores(spa2_view q, spa2_view k, int dtype, int64_t B, int64_t H, int64_t N, int64_t d,
                                   int64_t b_q, int64_t b_kv, double* scores, double* workspace, int32_t* nonfinite,
                                   void* stream) {

@@ -248,3 +248,23 @@ def test_cfg2_end_to_end_mask_disagreement():
                           "disagree_blocks": diff_blocks, "disagree_rows": diff_rows, "total_blocks": int(got.size),
                           "total_rows": int(got.shape[0] * got.shape[1])})
     assert diff_blocks <= 1e-4 * got.size, (diff_blocks, diff_rows)
+
+
+@pytest.mark.parametrize("n,d,b_q,b_kv", [(1000, 128, 128, 64), (777, 64, 128, 64), (300, 128, 64, 64), (4100, 128, 256, 128)])
+def test_block_mean_pool_entry_point(n, d, b_q, b_kv):
+    """spa2_block_mean_pool (K1a alone, the reference's numerics.block_mean_pool) equals the
+    oracle's float64 pooling bit for bit on bf16 inputs, ragged tails included."""
+    g = torch.Generator(device="cuda").manual_seed(n + d + b_q)
+    q = torch.randn(1, 2, n, d, device="cuda", generator=g).to(torch.bfloat16)
+    k = torch.randn(1, 2, n, d, device="cuda", generator=g).to(torch.bfloat16)
+    t_m, t_n = -(-n // b_q), -(-n // b_kv)
+    ws = torch.full((2 * (t_m + t_n) * d,), float("nan"), device="cuda", dtype=torch.float64)
+    st = torch.cuda.current_stream()
+    _lib.call("spa2_block_mean_pool", _lib.view4(q), _lib.view4(k), _lib.DTYPE_CODES[q.dtype], 1, 2, n, d, b_q, b_kv,
+              _lib.ptr(ws), _lib.ptr(ws[2 * t_m * d:]), None, st.cuda_stream, stream_obj=st)
+    torch.cuda.synchronize()
+    qbar = ws[:2 * t_m * d].view(2, t_m, d).cpu().numpy()
+    kbar = ws[2 * t_m * d:].view(2, t_n, d).cpu().numpy()
+    for h in range(2):
+        np.testing.assert_array_equal(qbar[h], oracle.masker.block_mean_pool(q[0, h].double().cpu().numpy(), b_q))
+        np.testing.assert_array_equal(kbar[h], oracle.masker.block_mean_pool(k[0, h].double().cpu().numpy(), b_kv))
