@@ -923,7 +923,7 @@ __global__ void __launch_bounds__(128) k_dkdv_mix(int reps, int which, unsigned 
   __shared__ uint64_t bar_mma;
   __shared__ uint32_t tmem_base;
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
-  for (int i = threadIdx.x; i < 131072 / 16; i += blockDim.x)
+  for (int i = threadIdx.x; i < 196608 / 16; i += blockDim.x)
     reinterpret_cast<uint4*>(base)[i] = make_uint4(0x3f803f80u, 0x3f803f80u, 0x3f803f80u, 0x3f803f80u);
   if (warp_id() == 0) tmem_alloc(&tmem_base, 512);
   if (threadIdx.x == 32) {
@@ -936,6 +936,63 @@ __global__ void __launch_bounds__(128) k_dkdv_mix(int reps, int which, unsigned 
   tc_fence_after();
   const uint32_t tbase = tmem_base;
   const bool single = (which & 64) != 0;
+  const bool ts = (which & 128) != 0;
+  __shared__ volatile int stop_flag;
+  __shared__ unsigned long long staged[4];
+  if (threadIdx.x == 0) stop_flag = 0;
+  __syncthreads();
+  if (warp_id() != 0 && (which & 256)) {
+    // Q / dO staging traffic as a TS-MMA K6 would add: each warp reads its 32 rows of a
+    // K-major SW128 128 x 128 tile (LDS.128, conflict-free) and stores them into TMEM columns
+    // [384, 448) of its lane quarter (tcgen05.st), until warp 0's MMA chain is done.
+    // region (bits 8192 / 16384): the Q tile S reads (default), the P tile dVᵀ reads, or
+    // [160K, 192K) which no MMA reads
+    const uint32_t row = (warp_id() & 3) * 32 + lane_id();
+    // (bit 32768: region at ((which >> 16) & 15) x 16 KB instead)
+    const uint32_t src = smem_u32(base) + ((which & 32768) ? (uint32_t)(((which >> 16) & 15) * 16384)
+                                           : (which & 8192) ? 98304u : (which & 16384) ? 163840u : 0u);
+    const uint32_t tq = tbase + ((uint32_t)((warp_id() & 3) * 32) << 16) + 384u;
+    unsigned long long n = 0;
+    while (!stop_flag) {
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        uint32_t r[32];
+        if (which & 4096) {  // shared-memory stores only (STS.128 of swizzled rows, like P / dS)
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            st_shared_v4(src + (uint32_t)(h * 16384) + sw128_offset(row, (uint32_t)u), (uint32_t)n, u, h, 1u);
+          n += 32 * 128;
+          continue;
+        }
+        if (which & 512) {  // TMEM stores only (register data, no shared-memory reads)
+#pragma unroll
+          for (int u = 0; u < 32; ++u) r[u] = (uint32_t)(n + u);
+        } else if (which & 1024) {  // shared-memory reads only (no TMEM stores)
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const uint4 v = ld_shared_v4(src + (uint32_t)(h * 16384) + sw128_offset(row, (uint32_t)u));
+            r[4 * u] = v.x; r[4 * u + 1] = v.y; r[4 * u + 2] = v.z; r[4 * u + 3] = v.w;
+          }
+          uint32_t x = 0;
+#pragma unroll
+          for (int u = 0; u < 32; ++u) x ^= r[u];
+          if (x == 0x12345678u) staged[0] = x;  // keep the loads
+          n += 32 * 128;
+          continue;
+        } else {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const uint4 v = ld_shared_v4(src + (uint32_t)(h * 16384) + sw128_offset(row, (uint32_t)u));
+            r[4 * u] = v.x; r[4 * u + 1] = v.y; r[4 * u + 2] = v.z; r[4 * u + 3] = v.w;
+          }
+        }
+        tmem_st32(tq + (uint32_t)(h * 32), r);
+        tmem_st_wait();
+        n += 32 * 128;
+      }
+    }
+    if (lane_id() == 0) staged[warp_id()] = n;
+  }
   if (warp_id() == 0 && (!single || lane_id() == 0)) {
     // [0,32K) Q | [32K,64K) dO | [64K,80K) K | [80K,96K) V | [96K,112K) P | [112K,128K) dS
     constexpr uint32_t idS = idesc_bf16(128, 64, false, false);
@@ -948,7 +1005,12 @@ __global__ void __launch_bounds__(128) k_dkdv_mix(int reps, int which, unsigned 
     const uint64_t t0 = clock64();
     for (int r = 0; r < reps; ++r) {
       const uint32_t b = (uint32_t)(r & 1) * 64u;
-      if (w2 != 2) {
+      if (w2 != 2 && ts) {
+        // S and dP as TS MMAs: A (Q / dO, K-major bf16 pairs) from TMEM columns 384 / 448
+        mma_bf16_ts_k8_w<8u, 2ull, (uint64_t)(64 * 128 / 16)>(tbase + b, tbase + 384u, dK, idS, 0u);
+        if (!(which & 32))
+          mma_bf16_ts_k8_w<8u, 2ull, (uint64_t)(64 * 128 / 16)>(tbase + 128u + b, tbase + 448u, dV, idS, 0u);
+      } else if (w2 != 2) {
         if (single) {
 #pragma unroll
           for (int ks = 0; ks < 8; ++ks) {
@@ -992,16 +1054,19 @@ __global__ void __launch_bounds__(128) k_dkdv_mix(int reps, int which, unsigned 
     }
     mbar_wait(&bar_mma, 0);
     if (lane_id() == 0) cycles[blockIdx.x] = clock64() - t0;
+    if (lane_id() == 0) stop_flag = 1;
   }
   tc_fence_before();
   __syncthreads();
+  if ((which & 256) && threadIdx.x == 0)
+    cycles[gridDim.x + blockIdx.x] = staged[1] + staged[2] + staged[3];  // bytes staged by warps 1-3
   if (warp_id() == 0) tmem_dealloc(tbase, 512);
 }
 }  // namespace
 }  // namespace spa2
 
 extern "C" int spa2_probe_dkdv_mix(int reps, int which, int ctas, unsigned long long* cycles, void* stream) {
-  const size_t smem = 131072 + 1024;
+  const size_t smem = 196608 + 1024;
   SPA2_CUDA_TRY(cudaFuncSetAttribute(spa2::k_dkdv_mix, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   spa2::k_dkdv_mix<<<ctas, 128, smem, (cudaStream_t)stream>>>(reps, which, cycles);
   SPA2_LAUNCH_CHECK();
