@@ -4,11 +4,15 @@ The GPU path computes on bf16 operands with fp32 accumulation (tensor cores) and
 bf16 O / dQ / dK / dV and fp32 LSE; the reference computes in float64 on the *same*
 bf16-representable inputs.  Stated tolerances (north_star: "max-abs/rel and cosine"),
 set to about twice the worst error measured over the whole GPU suite on a B200
-(tests/golden/parity_measured.json: out rel 5.6e-3, dq 7.0e-3, dk 5.9e-3, dv 4.9e-3,
-cosine >= 0.999993, LSE 1.9e-6 absolute):
+(tests/golden/parity_measured.json, 3 440 comparisons incl. the seeded geometry fuzz of
+tests/test_gpu_fuzz.py: out rel 6.2e-3, dq 1.08e-2, dk 6.1e-3, dv 5.6e-3; cosine >= 0.999995
+(out), 0.999985 (dq), 0.99999 (dk, dv); LSE 1.4e-6 absolute).  The dq worst cases are rows
+whose mass sits on one fully kept key block (the fuzz's "dense_column" pattern): dS = P ∘ (dP − δ)
+is then a small difference rounded to bf16 for the dQ MMA.
 
   out       cosine >= 0.99998  and  max|Δ| <= 1.2e-2 · max|ref|
-  dq/dk/dv  cosine >= 0.99998  and  max|Δ| <= 1.4e-2 · max|ref|
+  dq        cosine >= 0.99997  and  max|Δ| <= 2.2e-2 · max|ref|
+  dk/dv     cosine >= 0.99998  and  max|Δ| <= 1.4e-2 · max|ref|
   lse       max|Δ| <= 4e-6 · max(1, max|ref|)   (natural log units, fp32)
 """
 
@@ -16,7 +20,7 @@ import numpy as np
 
 TOL = {
     "out": (0.99998, 1.2e-2),
-    "dq": (0.99998, 1.4e-2),
+    "dq": (0.99997, 2.2e-2),
     "dk": (0.99998, 1.4e-2),
     "dv": (0.99998, 1.4e-2),
 }
