@@ -732,8 +732,44 @@ __global__ void __launch_bounds__(128) k_red_rate(float* __restrict__ dst, int t
 }  // namespace
 }  // namespace spa2
 
+// mode 3: the TMA bulk-reduce path a fused backward would use — each CTA holds one 64 KB fp32
+// partial in shared memory and adds it into a global tile with cp.reduce.async.bulk .add.f32 (four
+// 16 KB requests per tile from one elected thread, up to 4 tiles in flight).
+namespace spa2 {
+namespace {
+__global__ void __launch_bounds__(128) k_red_bulk(float* __restrict__ dst, int tiles, int nslots) {
+  extern __shared__ __align__(128) uint8_t smem_red[];
+  float* part = reinterpret_cast<float*>(smem_red);
+  for (int i = threadIdx.x; i < 128 * 128; i += blockDim.x) part[i] = 1.0f + 1e-3f * (float)(i & 127);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int t = 0; t < tiles; ++t) {
+      const int slot = (blockIdx.x * 7 + t * 13) % nslots;
+      float* base = dst + (int64_t)slot * 128 * 128;
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(base + c * 4096),
+                     "r"(smem_u32(part + c * 4096)), "r"(16384)
+                     : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  __syncthreads();
+}
+}  // namespace
+}  // namespace spa2
+
 extern "C" int spa2_probe_red_rate(float* dst, int tiles, int nslots, int ctas, int mode, void* stream) {
-  spa2::k_red_rate<<<ctas, 128, 0, (cudaStream_t)stream>>>(dst, tiles, nslots, mode);
+  if (mode == 3) {
+    const int smem = 128 * 128 * 4;
+    SPA2_CUDA_TRY(cudaFuncSetAttribute(spa2::k_red_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    spa2::k_red_bulk<<<ctas, 128, smem, (cudaStream_t)stream>>>(dst, tiles, nslots);
+  } else {
+    spa2::k_red_rate<<<ctas, 128, 0, (cudaStream_t)stream>>>(dst, tiles, nslots, mode);
+  }
   SPA2_LAUNCH_CHECK();
   return SPA2_OK;
 }

@@ -14,8 +14,9 @@ lib = _lib.load_diag()
 st = torch.cuda.current_stream().cuda_stream
 for nslots in (256, 3072):  # 16 MB (L2-resident) and 201 MB (the configs[1] dQ in fp32)
     dst = torch.zeros(nslots * 128 * 128, device="cuda")
-    for mode, name in ((0, "red.v4 row per thread"), (2, "red.v4 coalesced"), (1, "st.v4 row per thread")):
-        for ctas in (148, 296, 592):
+    for mode, name in ((0, "red.v4 row per thread"), (2, "red.v4 coalesced"), (1, "st.v4 row per thread"),
+                       (3, "TMA bulk reduce .add.f32")):
+        for ctas in ((148,) if mode == 3 else (148, 296, 592)):
             tiles = 64
             _lib.check_diag(lib.spa2_probe_red_rate(_lib.ptr(dst), tiles, nslots, ctas, mode, st), "red")
             torch.cuda.synchronize()
