@@ -50,8 +50,10 @@ int spa2_probe_tmem_rate(int reps, int mode, int warps, int ctas, unsigned long 
 int spa2_probe_tma_rate2(const void* buf, long long rows, int box_rows, int chunks, int stages, int issuers,
                          int mode, int iters, int ctas, unsigned long long* cycles, void* stream);
 
-/* Diagnostic: fp32 reduction (mode 0, red.global.add.v4.f32) or store (mode 1) throughput of
- * `ctas` CTAs each adding `tiles` 128x128 fp32 tiles into a rotating set of `nslots` tiles of dst. */
+/* Diagnostic: fp32 reduction (mode 0, red.global.add.v4.f32 one row per thread; 2, coalesced),
+ * store (mode 1) or TMA bulk reduction (mode 3, cp.reduce.async.bulk .add.f32 of a 64 KB shared-
+ * memory tile) throughput of `ctas` CTAs each adding `tiles` 128x128 fp32 tiles into a rotating
+ * set of `nslots` tiles of dst. */
 int spa2_probe_red_rate(float* dst, int tiles, int nslots, int ctas, int mode, void* stream);
 
 /* SM clock probe (diagnostic): `ctas` CTAs each spin spin_ns nanoseconds of %globaltimer and
@@ -67,7 +69,11 @@ int spa2_probe_smem_contend(int reps, int mode, int ctas, const void* gsrc, unsi
 
 /* dK/dV MMA mix probe (diagnostic): the four MMA groups of one K6 tile (S, dP K-major; dVᵀ, dKᵀ
  * MN-major; M=128 N=64, 8 K=16 steps each) issued back to back by one thread, reps tiles;
- * which = 0 all four, 1 S+dP only, 2 dVᵀ+dKᵀ only.  cycles[cta] = clock64 span. */
+ * which = 0 all four, 1 S+dP only, 2 dVᵀ+dKᵀ only; +32 S only, +64 single-thread issue, +128 S/dP
+ * as TS MMAs (A from TMEM); +256 three other warps add traffic while the chain runs: LDS.128 +
+ * tcgen05.st (default), +512 tcgen05.st only, +1024 LDS.128 only, +4096 STS.128 only, of the
+ * region at 0 (the Q tile), +8192 96 KB (the P tile), +16384 160 KB (no operand), or +32768 at
+ * ((which >> 16) & 15) x 16 KB.  cycles[cta] = clock64 span; cycles[ctas + cta] = bytes moved. */
 int spa2_probe_dkdv_mix(int reps, int which, int ctas, unsigned long long* cycles, void* stream);
 
 /* tcgen05.cp rate probe (diagnostic): per rep, 8 tcgen05.cp.128x256b (one 32 KB K-major tile
