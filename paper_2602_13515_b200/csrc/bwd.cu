@@ -932,21 +932,30 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
       const Item m = get_item(p, wi, p.T_n);
       if (m.n == 0) continue;
       const int64_t rowbase = (int64_t)m.bh * p.N;
-      auto load_stats = [&](int t, float& lse2, float& dlt) {
-        const int32_t e = p.idx[m.beg + t];
+      // row statistics of tile t+1 are loaded during tile t from the list entry loaded during tile
+      // t-1, and only consumed (scaled, selected) in tile t+1: no load result is waited for in
+      // the tile it is issued in (the dependent idx -> LSE load pair stalled these warps)
+      auto stats_raw = [&](int32_t e, float& lse_raw, float& dlt_raw, bool& valid) {
         const int tok = list_blk(e) * BQ + row;
         // rows outside the query block's range, or of a half that does not keep the tile (b_q = 64
         // masks), get LSE = +inf: P = 0 and dS = 0
-        const bool valid = tok < p.N && !(HALF && list_row_dropped(e, row));
-        lse2 = valid ? __ldg(p.lse + rowbase + tok) * kLog2e : INFINITY;
-        dlt = valid ? __ldg(p.delta + rowbase + tok) : 0.f;
+        valid = tok < p.N && !(HALF && list_row_dropped(e, row));
+        const int64_t off = rowbase + (valid ? tok : 0);
+        lse_raw = __ldg(p.lse + off);
+        dlt_raw = __ldg(p.delta + off);
       };
-      float lse2, dlt;
-      load_stats(0, lse2, dlt);
+      float lse_r, dlt_r;
+      bool vld;
+      stats_raw(__ldg(p.idx + m.beg), lse_r, dlt_r, vld);
+      int32_t e_nxt = m.n > 1 ? __ldg(p.idx + m.beg + 1) : 0;
       for (int t = 0; t < m.n; ++t, ++g) {
         const uint32_t b = (uint32_t)(g & 1);
-        float lse2_n = 0.f, dlt_n = 0.f;
-        if (t + 1 < m.n) load_stats(t + 1, lse2_n, dlt_n);  // prefetch the next tile's row statistics
+        const int32_t e_nn = t + 2 < m.n ? __ldg(p.idx + m.beg + t + 2) : 0;
+        float lse_rn = 0.f, dlt_rn = 0.f;
+        bool vld_n = false;
+        if (t + 1 < m.n) stats_raw(e_nxt, lse_rn, dlt_rn, vld_n);  // prefetch the next tile's row statistics
+        const float lse2 = vld ? lse_r * kLog2e : INFINITY;
+        const float dlt = vld ? dlt_r : 0.f;
         mbar_wait(&s_full[b], (uint32_t)(g >> 1) & 1u);
         if (warp == 2) SPA2_TR(19, g);
         tc_fence_after();
@@ -1011,8 +1020,10 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
         fence_proxy_async_smem();
         if (warp == 2) SPA2_TR(21, g);
         mbar_arrive(&ds_full[pb]);
-        lse2 = lse2_n;
-        dlt = dlt_n;
+        lse_r = lse_rn;
+        dlt_r = dlt_rn;
+        vld = vld_n;
+        e_nxt = e_nn;
       }
     }
   } else if (warp < R::PROD2) {
