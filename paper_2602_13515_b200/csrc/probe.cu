@@ -993,6 +993,15 @@ __global__ void __launch_bounds__(128) k_dkdv_mix(int reps, int which, unsigned 
 #pragma unroll 1
       for (int h = 0; h < 2; ++h) {
         uint32_t r[32];
+        if (which & 2048) {  // mbarrier polls (try_wait on a phase that never completes) at the region
+          if (lane_id() == 0 && warp_id() == 1 && h == 0 && n == 0) mbar_init(reinterpret_cast<uint64_t*>(base + (src - smem_u32(base))), 1);
+          __syncwarp();
+          uint32_t spins = 0;
+#pragma unroll 1
+          for (int i = 0; i < 64; ++i) spins += mbar_try_wait(src, 1u);
+          n += 64 + (spins & 0);  // counts polls, not bytes
+          continue;
+        }
         if (which & 4096) {  // shared-memory stores only (STS.128 of swizzled rows, like P / dS)
 #pragma unroll
           for (int u = 0; u < 8; ++u)
