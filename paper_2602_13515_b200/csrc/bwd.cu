@@ -49,7 +49,7 @@ namespace {
 #define SPA2_DQ_POLY_NUM 0
 #endif
 #ifndef SPA2_DKDV_POLY_NUM
-#define SPA2_DKDV_POLY_NUM 8
+#define SPA2_DKDV_POLY_NUM 4
 #endif
 #ifndef SPA2_DQ_NK
 #define SPA2_DQ_NK 4
