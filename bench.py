@@ -489,12 +489,12 @@ def gpu_arm(args, rank: int, world: int, dev):
         def e2e_step():
             pipe.fwd_bwd(hq, hk, hv, hdo, cfg, *outs)
 
-        for _ in range(2):
+        for _ in range(5):  # the host pipeline's pinned / device buffers and caches warm up
             e2e_step()
         # three back-to-back windows, the median reported (all listed): a rare host-side stall of
         # a few hundred ms (seen on the pool's boxes with the PCIe floor unchanged) would
         # otherwise dominate a single window (tools/e2e_sweep.py)
-        n_e2e = max(3, min(args.steps, 60) // 3)
+        n_e2e = max(10, min(args.steps, 60) // 3)
         windows = []
         for _ in range(3):
             barrier()
