@@ -209,6 +209,56 @@ __global__ void __launch_bounds__(256) k_delta(spa2_view o, spa2_view dout, floa
   if (part == 0 && row < rows_total) delta[row] = acc;
 }
 
+// δ of the 32 rows [row0, row0 + 32) of one query block, computed by one warp with k_delta's
+// thread layout and arithmetic (HD/8 lanes per row, one 16-byte chunk of O and dO each, the same
+// FMA chain and xor-butterfly), so the result is bit-identical to k_delta and row_delta, but every
+// load instruction reads whole rows (coalesced) instead of one row per thread, which made the fused
+// δ depend on L1 capacity.  Rows past N get δ = 0 in `sd` (if given) and are not stored to `gd`.
+template <int HD>
+__device__ __forceinline__ void warp_delta_rows(const __nv_bfloat16* o_blk, int64_t o_sn, const __nv_bfloat16* d_blk,
+                                                int64_t d_sn, int row0, int rows_valid, float* sd, float* gd) {
+  constexpr int TPR = HD / 8;        // lanes per row
+  constexpr int RPI = 32 / TPR;      // rows per warp instruction
+  const int lane = (int)(threadIdx.x & 31);
+  const int part = lane % TPR, sub = lane / TPR;
+#pragma unroll 1
+  for (int r = 0; r < 32; r += 4 * RPI) {
+    uint4 a[4], c[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int row = row0 + r + u * RPI + sub;
+      if (row < rows_valid) {
+        a[u] = __ldg(reinterpret_cast<const uint4*>(o_blk + (int64_t)row * o_sn + part * 8));
+        c[u] = __ldg(reinterpret_cast<const uint4*>(d_blk + (int64_t)row * d_sn + part * 8));
+      } else {
+        a[u] = make_uint4(0, 0, 0, 0);
+        c[u] = make_uint4(0, 0, 0, 0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a[u]);
+      const __nv_bfloat162* c2 = reinterpret_cast<const __nv_bfloat162*>(&c[u]);
+      float acc = 0.f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 x = __bfloat1622float2(a2[e]);
+        const float2 y = __bfloat1622float2(c2[e]);
+        acc = fmaf(x.x, y.x, acc);
+        acc = fmaf(x.y, y.y, acc);
+      }
+#pragma unroll
+      for (int off = TPR / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+      const int row = row0 + r + u * RPI + sub;
+      if (part == 0) {
+        const bool valid = row < rows_valid;
+        if (sd != nullptr) sd[row] = valid ? acc : 0.f;
+        if (valid) gd[row] = acc;
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------------------
 // K7 (default): dQ, persistent (one CTA per SM), with Q_i and dO_i RESIDENT IN TMEM.
 // Work item = query block i; tiles = its kept key blocks j.  Q_i and dO_i are staged once
@@ -237,7 +287,10 @@ struct Dq3Cfg {
   static constexpr int OFF_K = 2 * Q_BYTES;
   static constexpr int OFF_V = OFF_K + NK * KV_BYTES;
   static constexpr int OFF_DLT = OFF_V + NV * KV_BYTES;  // fused δ: float [2 items][128 rows]
-  static constexpr int OFF_BAR = OFF_DLT + 2 * BQ * 4;
+#ifndef SPA2_DQ_BAR_PAD
+#define SPA2_DQ_BAR_PAD 0
+#endif
+  static constexpr int OFF_BAR = OFF_DLT + 2 * BQ * 4 + SPA2_DQ_BAR_PAD;
   static constexpr int NUM_BARS = 4 + 2 * NK + 2 * NV + 2 * 5 + 2 + 2;
   static constexpr int SMEM = OFF_BAR + NUM_BARS * 8 + 16 + kSmemAlignSlack;
   static constexpr uint32_t Q_COL = 0, DO_COL = 64, SDP_COL = 128, ACC_COL = 384;  // S at +b*128, dP at +64
@@ -605,6 +658,7 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
       const int hh = m.bh % p.H, bb = m.bh / p.H;
       const int tok = m.blk * BQ + row;
       if (fused_delta) {
+#ifdef SPA2_DQ_ROW_DELTA  // one row per thread (L1-dependent loads)
         float dl = 0.f;
         if (tok < p.N) {
           dl = row_delta<HD>(p.o_in + bb * p.oi_sb + hh * p.oi_sh + (int64_t)tok * p.oi_sn,
@@ -615,6 +669,19 @@ __global__ void __launch_bounds__(Dq3Roles<EWW>::THREADS, 1)
           sdelta[(it & 1) * BQ + row] = dl;  // slot last read at the start of item it-2 (drained)
           mbar_arrive(&dlt_full[it & 1]);
         }
+#else
+        // this warp's 32 rows of the block, cooperatively (the smem slot was last read at the start
+        // of item it-2, which has been drained); rows of an empty list still get their global δ
+        const int64_t tok0 = (int64_t)m.blk * BQ;
+        warp_delta_rows<HD>(p.o_in + bb * p.oi_sb + hh * p.oi_sh + tok0 * p.oi_sn, p.oi_sn,
+                            p.do_in + bb * p.di_sb + hh * p.di_sh + tok0 * p.di_sn, p.di_sn, q4 * 32,
+                            (int)(p.N - tok0 < BQ ? p.N - tok0 : BQ), m.n > 0 ? sdelta + (it & 1) * BQ : nullptr,
+                            p.delta_out + (int64_t)m.bh * p.N + tok0);
+        if (m.n > 0) {
+          __syncwarp();
+          mbar_arrive(&dlt_full[it & 1]);
+        }
+#endif
       }
       if (m.n == 0) {
         if (tok < p.N) {
