@@ -52,10 +52,10 @@ namespace {
 #define SPA2_DKDV_POLY_NUM 4
 #endif
 #ifndef SPA2_DQ_NK
-#define SPA2_DQ_NK 4
+#define SPA2_DQ_NK 5
 #endif
 #ifndef SPA2_DQ_NV
-#define SPA2_DQ_NV 4
+#define SPA2_DQ_NV 5
 #endif
 using namespace ptx;
 
