@@ -1132,9 +1132,17 @@ __global__ void __launch_bounds__(DkvRoles<EWW>::THREADS, 1)
         const float mul = is_k ? p.scale : 1.f;
         const int rr = rows - (part & 1) * 32;
         if (own) {
+          // (these warps share their SM sub-partitions with the elementwise warps: keep the store
+          // loop lean — a running pointer, the full-block case without per-row predicates)
+          __nv_bfloat16* q = dst;
+          if (rr >= 32) {
 #pragma unroll
-          for (int r = 0; r < 32; ++r)
-            if (r < rr) dst[(int64_t)r * sn] = __float2bfloat16(__uint_as_float(r32[r]) * mul);
+            for (int r = 0; r < 32; ++r, q += sn) *q = __float2bfloat16(__uint_as_float(r32[r]) * mul);
+          } else {
+#pragma unroll
+            for (int r = 0; r < 32; ++r, q += sn)
+              if (r < rr) *q = __float2bfloat16(__uint_as_float(r32[r]) * mul);
+          }
         }
       }
       ++it;
