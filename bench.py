@@ -489,8 +489,17 @@ def gpu_arm(args, rank: int, world: int, dev):
         def e2e_step():
             pipe.fwd_bwd(hq, hk, hv, hdo, cfg, *outs)
 
-        for _ in range(5):  # the host pipeline's pinned / device buffers and caches warm up
-            e2e_step()
+        # untimed warm-up: the host pipeline's pinned / device buffers and caches, and the PCIe
+        # link, which the GPU runs at a lower speed when idle and only ramps up under sustained
+        # traffic (the first few hundred ms of host-buffer steps measured up to 2x slower on a
+        # fresh box, tools/e2e_sweep.py)
+        t_warm = time.perf_counter()
+        while True:
+            for _ in range(5):
+                e2e_step()
+            torch.cuda.synchronize()
+            if time.perf_counter() - t_warm > 1.0:
+                break
         # three back-to-back windows, the median reported (all listed): a rare host-side stall of
         # a few hundred ms (seen on the pool's boxes with the PCIe floor unchanged) would
         # otherwise dominate a single window (tools/e2e_sweep.py)
